@@ -1,0 +1,392 @@
+"""Benchmark: space-time DoFs solved per second by the FD solver (fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+One step = one full FD solve of the configuration on device-resident inputs:
+batched LDL^T factorization of every shift, transform-in GEMM, batched
+solves, transform-out GEMM, and iterative refinement to a 1e-13 relative
+space-time residual. Setup (host pencil decomposition, symbolic analysis,
+plan creation, uploads) is outside the timed region, as the reference's own
+`solve_fd(system, pencil=...)` allows; `e2e` times the public API call
+`solve_fd(system, pencil)` with host buffers instead (analysis, uploads and
+the download of the solution included).
+
+Multi-GPU (torchrun): the shifts are sharded over ranks, each rank does a
+partial back-transform and the cross-mode sum is an NCCL reduce-scatter by
+spatial rows (paper_2008_01996_b200/distributed.py).
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "space-time DoFs solved/sec (FD, fp64)"
+UNIT = "dof/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--refine", type=int, default=3)
+    ap.add_argument("--leaf-size", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--j-max", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---- clocks ---------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- peaks ------------------------------------------------------------------------
+def measured_peaks(device):
+    import torch
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        peaks["hbm_gbs"] = mp.get("hbm_gbs")
+        peaks["fp64_tflops"] = mp.get("fp64_tflops")
+        peaks["source"] = "MEASURED_PEAKS.json"
+    except OSError:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["source"] = "fallback (B200_PROFILING.md)"
+    if not peaks.get("fp64_tflops"):
+        # MEASURED_PEAKS.json carries no fp64 figure: measure cuBLAS DGEMM here
+        # with the driver's protocol (8192^3, best of 10, CUDA events)
+        n = 8192
+        a = torch.randn(n, n, dtype=torch.float64, device=device)
+        b = torch.randn(n, n, dtype=torch.float64, device=device)
+        for _ in range(2):
+            torch.matmul(a, b)
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        peaks["fp64_tflops"] = 2.0 * n**3 / best / 1e12
+        peaks["fp64_source"] = "cuBLAS DGEMM 8192^3 best of 10, measured in this run"
+        del a, b
+        torch.cuda.empty_cache()
+    else:
+        peaks["fp64_source"] = "MEASURED_PEAKS.json"
+    return peaks
+
+
+# ---- CPU baseline (oracle port, bounded sample) -------------------------------------
+def cpu_fd_sample(system, n_shift_sample, threads=1):
+    """Time the reference algorithm (oracle/fd_oracle.py restatement of
+    solvers.py:348-403) on a bounded sample: full pencil, transforms and
+    analysis, `n_shift_sample` of the N_t spatial factor+solves; the solve
+    time is extrapolated linearly to all N_t shifts."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import scipy.sparse as sp
+
+    from oracle import fd_oracle as orc
+
+    A_t, M_t, M_x, A_x, rhs = orc.system_arrays(system)
+    n_t, m_x = A_t.shape[0], M_x.shape[0]
+    t0 = time.perf_counter()
+    p = orc.fd_pencil(A_t, M_t)
+    t_pencil = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    F = rhs.reshape(m_x, n_t, order="F")
+    G = (orc._transform_in(p["L"], F, np.conj(p["U"])) / p["sigma"][None, :]) @ np.conj(p["Vh"])
+    t_in = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    M, A = sp.csr_matrix(M_x), sp.csr_matrix(A_x)
+    perm = orc.mmd_analyze((M + A).tocsr())
+    t_an = time.perf_counter() - t0
+    Mc, Ac = M.astype(complex), A.astype(complex)
+    ks = np.linspace(0, n_t - 1, n_shift_sample).astype(int)
+    Z = np.zeros((m_x, n_t), complex)
+
+    def one(k):
+        K = (Mc + p["D"][k] * Ac).tocsr()
+        return k, orc.superlu_solve(perm, orc.superlu_factor(perm, K), G[:, k])
+
+    t0 = time.perf_counter()
+    if threads > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            for k, z in pool.map(one, ks):
+                Z[:, k] = z
+    else:
+        for k in ks:
+            Z[:, k] = one(k)[1]
+    t_sp = (time.perf_counter() - t0) * n_t / len(ks)
+    t0 = time.perf_counter()
+    U = ((Z @ p["Vh"].T) * p["sigma"][None, :]) @ p["U"].T
+    _ = np.ascontiguousarray(U.real)
+    t_out = time.perf_counter() - t0
+    total = t_pencil + t_in + t_an + t_sp + t_out
+    return {"t_total": total, "t_pencil": t_pencil, "t_spatial_extrap": t_sp, "t_transform": t_in + t_out,
+            "t_analyze": t_an, "sample_shifts": int(len(ks)), "n_t": n_t}
+
+
+def shift_sample_size(cfg):
+    return {"c1": 32, "c2": 32, "c3": 12, "c4": 3}.get(cfg, 8)
+
+
+# ---- main -------------------------------------------------------------------------
+def main():
+    args = parse()
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2008_01996_b200 import problems, solvers, sparse_direct
+    from paper_2008_01996_b200.engine import FDEngine, modal_plan
+
+    kw = {} if args.j_max is None else {"j_max": args.j_max}
+    system, info = problems.build_system(args.config, temporal_device=dev, **kw)
+    pencil = solvers.build_pencil(system.temporal, "fd")
+    modal = modal_plan(system.temporal, pencil)
+    n, nt = system.m_x, system.n_t
+    dof = system.dof
+    leaf = args.leaf_size or sparse_direct.DEFAULT_LEAF_SIZE
+
+    if world > 1:
+        from paper_2008_01996_b200.distributed import ShardedFD
+
+        runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
+                           leaf_size=leaf)
+        eng = runner.engine
+    else:
+        runner = None
+        eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev, leaf_size=leaf)
+    F = torch.from_numpy(np.ascontiguousarray(system.rhs)).to(dev).view(nt, n)
+    U = torch.empty((nt, n), dtype=torch.float64, device=dev)
+    stats = eng.sym.stats
+
+    fac_events = []
+
+    def step(record=False):
+        eng.factored = False
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        if runner is not None:
+            out = runner.solve(F, refine=args.refine, factor_events=fac_events if record else None)
+        else:
+            eng.factor(events=fac_events if record else None)
+            out = eng.solve(F, U, refine=args.refine)
+        if record:
+            e1.record()
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = eng.gpu_launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    fac_events.clear()
+    torch.cuda.synchronize()
+    t_start.record()
+    infos = []
+    for _ in range(args.steps):
+        _, inf = step(record=True)
+        infos.append(inf)
+    t_end.record()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    launches = (eng.gpu_launches - launches0) // max(args.steps, 1)
+    ms = elapsed / args.steps * 1e3
+    value = dof * args.steps / elapsed
+
+    # roofline of the dominant kernel: the batched LDL^T factorization (DMMA fp64)
+    fac_s = sum(a.elapsed_time(b) for a, b in fac_events) / 1e3 / max(args.steps, 1)
+    n_shift_local = eng.n_k
+    fac_flops = stats["flops"] * n_shift_local
+    peaks = measured_peaks(dev) if rank == 0 else {}
+
+    e2e = None
+    if rank == 0 and world == 1:
+        e2e = measure_e2e(system, pencil, args, leaf)
+
+    if rank == 0:
+        achieved = fac_flops / fac_s / 1e12 if fac_s > 0 else None
+        traffic = load_traffic(args.config)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {info['mesh']} M_x={n} N_t={nt} dof={dof} rhs={info['rhs']}",
+                       "j_max": info["j_max"], "refine": args.refine, "leaf_size": leaf,
+                       "shifts_solved": int(modal.n_k), "conjugate_pairs": int(modal.n_pairs),
+                       "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
+                           stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
+                       "parallelism": f"shift-sharded x{world}" if world > 1 else "single GPU"},
+            "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
+            "fd_residual": infos[-1]["residuals"][0],
+            "gpu_launches": int(launches),
+            "clocks": ck,
+            "roofline": {"kernel": "factor_level_kernel (batched complex LDL^T, all levels)",
+                         "bound": "tensor", "achieved": achieved, "peak": peaks.get("fp64_tflops"),
+                         "unit": "TFLOP/s", "frac": (achieved / peaks["fp64_tflops"]) if achieved else None,
+                         "peak_source": peaks.get("fp64_source"),
+                         "flops_per_shift": stats["flops"], "shifts": int(n_shift_local),
+                         "ms_per_step": fac_s * 1e3, "share_of_step": fac_s * 1e3 / ms,
+                         "traffic": traffic},
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_fd_sample(system, shift_sample_size(args.config))
+            line["cpu_baseline"] = {"value": dof / cb["t_total"], "unit": UNIT, "cores": 1, "kind": "port",
+                                    "sample": (f"oracle port of solve_fd, full pencil/transforms/analysis, "
+                                               f"{cb['sample_shifts']} of {cb['n_t']} SuperLU shift solves "
+                                               f"timed and extrapolated; t_total={cb['t_total']:.2f}s")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def load_traffic(cfg):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(cfg)
+    except (OSError, ValueError):
+        return None
+
+
+def measure_e2e(system, pencil, args, leaf):
+    """Public API with host buffers: solve_fd(system, pencil) per step."""
+    import torch
+
+    from paper_2008_01996_b200 import solvers
+
+    solvers.solve_fd(system, pencil=pencil, refine=args.refine, leaf_size=leaf)  # warm-up
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        sol, rep = solvers.solve_fd(system, pencil=pencil, refine=args.refine, leaf_size=leaf)
+        times.append(time.perf_counter() - t0)
+    n, nt = system.m_x, system.n_t
+    nnz = system.spatial.M_II.nnz
+    h2d = 8 * n * nt + 8 * nt * (2 * nt) * 3 + 8 * (n + 1) + 8 * 3 * 2 * nnz
+    return {"value": system.dof / float(np.mean(times)), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(8 * n * nt), "steps": len(times),
+            "includes": "symbolic analysis, plan upload, factorization, solve, refinement, D2H of u",
+            "residual": rep.residual}
+
+
+def run_reference(args, world, rank):
+    """The reference's CPU algorithm (oracle port, threads = all host cores),
+    bounded shift sample per step, extrapolated to the full workload."""
+    if rank != 0:
+        return
+    from paper_2008_01996_b200 import problems
+
+    kw = {} if args.j_max is None else {"j_max": args.j_max}
+    system, info = problems.build_system(args.config, **kw)
+    threads = os.cpu_count() or 1
+    sample = shift_sample_size(args.config)
+    for _ in range(args.warmup):
+        cpu_fd_sample(system, max(1, sample // 4), threads)
+    totals = []
+    for _ in range(args.steps):
+        totals.append(cpu_fd_sample(system, sample, threads)["t_total"])
+    t = float(np.mean(totals))
+    value = system.dof / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: {info['mesh']} M_x={system.m_x} N_t={system.n_t} "
+                                   f"dof={system.dof} rhs={info['rhs']}", "j_max": info["j_max"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sample} of {system.n_t} shifts per step, extrapolated"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * khb200 -- C-ABI of the B200-native Fast-Diagonalization space-time solver.
+ *
+ * Every entry point replaces one piece of the reference's FD hot path
+ * (reference package `kronheat`, pkg/src/kronheat/):
+ *
+ *   kh_analyze ................ sparse_direct.analyze          sparse_direct.py:112-152
+ *                               (called once per solve from solvers.py:379 _union_symbolic)
+ *   kh_plan_create ............ per-shift matrix build K = Mc + lam*Ac   solvers.py:378, :384
+ *   kh_plan_factor ............ sparse_direct.factorize (SuperLU zgstrf) sparse_direct.py:155-188,
+ *                               batched over the shifts of the loop at solvers.py:383-393
+ *   kh_plan_pivot_check ....... pivot guard |U_ii| >= 1e-13 max|a|      sparse_direct.py:182-187
+ *   kh_plan_solve ............. sparse_direct.solve (SuperLU zgstrs)    sparse_direct.py:191-209
+ *   kh_dgemm .................. modal transforms (zgemm)                solvers.py:368-372, :397-400
+ *   kh_plan_residual .......... residual / kron_apply_right             solvers.py:428-440, dense.py:264-286
+ *   kh_sumsq .................. norms of _discard_imaginary              solvers.py:406-413
+ *
+ * Conventions: plain pointers and 64-bit sizes, column-major matrices,
+ * caller-owned buffers. Pointers documented "device" must be CUDA device
+ * memory of the plan's device; "host" pointers are ordinary host memory.
+ * `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ * every device call is stream-ordered and asynchronous unless noted.
+ * Every call returns a kh status (0 = OK); kh_last_error() gives the detail
+ * of the last failure on the calling thread.
+ *
+ * Status -> reference exception (pkg/src/kronheat/errors.py):
+ *   KH_ERR_DIMENSION  -> DimensionMismatch
+ *   KH_ERR_SINGULAR   -> SingularMatrix
+ *   KH_ERR_INVALID    -> UsageError
+ *   KH_ERR_CUDA, KH_ERR_NOMEM -> DeviceError (new class derived from KronheatError)
+ * Threading: distinct plans may be used from distinct threads; one plan is
+ * not re-entrant. One process per GPU for multi-GPU runs.
+ */
+#ifndef KHB200_H
+#define KHB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KH_OK 0
+#define KH_ERR_DIMENSION 1
+#define KH_ERR_SINGULAR 2
+#define KH_ERR_INVALID 3
+#define KH_ERR_CUDA 4
+#define KH_ERR_NOMEM 5
+
+typedef struct kh_symbolic kh_symbolic;
+typedef struct kh_plan kh_plan;
+
+typedef struct {
+  int64_t n;             /* matrix dimension */
+  int64_t nnz;           /* entries of the analyzed (symmetrized) CSR pattern */
+  int64_t n_fronts;      /* supernodal fronts of the dissection tree */
+  int64_t max_front;     /* largest front order m = p + q */
+  int64_t max_pivots;    /* largest pivot block p */
+  int64_t depth;         /* tree depth (levels = depth + 1) */
+  int64_t factor_nnz;    /* entries of L incl. diagonal (complex) */
+  int64_t panel_entries; /* complex entries of retained factor storage per shift */
+  int64_t upd_entries;   /* complex entries of update buffers per in-flight shift */
+  int64_t leaf_size;
+  double flops;          /* real flops per shift of the complex LDL^T (8 per complex FMA) */
+} kh_symbolic_stats;
+
+int kh_version(void);
+const char* kh_status_string(int status);
+const char* kh_last_error(void);
+
+/* Symbolic analysis (host). `indptr`/`indices`: host CSR of a square,
+ * structurally symmetric pattern (duplicates and self loops allowed).
+ * `leaf_size` <= 0 selects the default. */
+int kh_analyze(int64_t n, const int64_t* indptr, const int64_t* indices, int32_t leaf_size, kh_symbolic** out);
+int kh_symbolic_stats_get(const kh_symbolic* s, kh_symbolic_stats* out);
+/* perm[k] = original index eliminated k-th (host array of n). */
+int kh_symbolic_perm(const kh_symbolic* s, int64_t* perm);
+/* Per-front arrays (host, n_fronts each; any may be NULL). */
+int kh_symbolic_fronts(const kh_symbolic* s, int64_t* first, int32_t* npiv, int32_t* nupd, int32_t* parent,
+                       int32_t* depth);
+/* Concatenated update-row lists (permuted positions), sum of nupd entries. */
+int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows);
+void kh_symbolic_free(kh_symbolic* s);
+
+/* Numeric plan on `device`: uploads the analysis and the value arrays of the
+ * two matrices M and A (host, aligned with the analyzed CSR `indptr/indices`,
+ * which must be the pattern given to kh_analyze). The plan factors shifted
+ * matrices M + lambda A. It allocates factor storage for `factor_slots`
+ * shifts and work space for up to `max_batch` shifts per call. */
+int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, const int64_t* indices,
+                   const double* m_vals, const double* a_vals, int64_t max_batch, int64_t factor_slots,
+                   kh_plan** out);
+/* Bytes the plan would allocate (no allocation). */
+int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes);
+int kh_plan_set_values(kh_plan* plan, const double* m_vals, const double* a_vals);
+/* Factor M + lambda_s A for s < nshift into slots slot0.. ; `lambda_ri` is a
+ * host array of nshift (re, im) pairs. nshift <= max_batch. */
+int kh_plan_factor(kh_plan* plan, int64_t slot0, int64_t nshift, const double* lambda_ri, void* stream);
+/* Synchronizes `stream`; returns KH_ERR_SINGULAR if some shift has a pivot
+ * |d| < rel_threshold * max|a_ij| (or a non-finite pivot). `first_bad`
+ * (may be NULL) receives the first offending shift index or -1;
+ * `worst_ratio` (may be NULL) the smallest |d|/max|a|. */
+int kh_plan_pivot_check(kh_plan* plan, int64_t slot0, int64_t nshift, double rel_threshold, void* stream,
+                        int64_t* first_bad, double* worst_ratio);
+/* Solve (M + lambda_s A) x_s = b_s with the factors in slots slot0.. .
+ * Device arrays; column s of b/x at b_re + s*ldb. b_im/x_im may be NULL
+ * (real rhs / discard imaginary part). nshift <= max_batch. */
+int kh_plan_solve(kh_plan* plan, int64_t slot0, int64_t nshift, const double* b_re, const double* b_im,
+                  int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream);
+/* R = F - (M Y[:, :nt] + A Y[:, nt:2nt]) on the plan's CSR (device arrays);
+ * R may be NULL. norms2 (device, 2 doubles) receives ||R||_F^2, ||F||_F^2. */
+int kh_plan_residual(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
+                     double* R, int64_t ldr, double* norms2, void* stream);
+void kh_plan_free(kh_plan* plan);
+
+/* C = alpha A B + beta C, fp64, column-major, device arrays (DMMA GEMM). */
+int kh_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+             int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+/* Plan-free residual on a device CSR (indptr n+1, indices/m_vals/a_vals nnz):
+ * same contract as kh_plan_residual. */
+int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                         const double* m_vals, const double* a_vals, const double* Y, int64_t ldy,
+                         const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2, void* stream);
+/* out (device, 1 double) = sum_i x_i^2 over n device doubles. */
+int kh_sumsq(const double* x, int64_t n, double* out, void* stream);
+int kh_set_device(int device);
+int kh_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KHB200_H */

@@ -1,0 +1,458 @@
+// C-ABI of libkhb200 (declared in include/khb200.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/khb200.h"
+#include "kernels.h"
+#include "symbolic.h"
+
+struct kh_symbolic {
+  kh::Symbolic S;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(KH_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define KH_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);      \
+  } while (0)
+
+constexpr int32_t kDefaultLeaf = 24;
+constexpr int32_t kAbsmaxBlocks = 64;
+constexpr int32_t kResidualBlocks = 1184;  // 8 x 148 SMs
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t count) {
+  *dst = nullptr;
+  if (count == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), count * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+}  // namespace
+
+struct kh_plan {
+  int device = 0;
+  int64_t n = 0, nnz = 0, max_batch = 0, slots = 0;
+  int32_t nf = 0, max_p = 0;
+  std::vector<int32_t> level_off;  // levels d -> [level_off[d], level_off[d+1]) in level_fronts
+  int32_t depth = 0;
+  int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
+  // device
+  KhDevFront* fronts = nullptr;
+  int32_t *child_list = nullptr, *relind = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
+  int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
+  double *mv = nullptr, *av = nullptr;
+  double2* panels = nullptr;
+  double2* upd[2] = {nullptr, nullptr};
+  double2* rupd[2] = {nullptr, nullptr};
+  double2* y = nullptr;
+  double2* lam = nullptr;
+  double* minpiv_work = nullptr;  // [max_batch][nf]
+  double* absmax_work = nullptr;  // [max_batch][kAbsmaxBlocks]
+  double* minpiv = nullptr;       // [slots]
+  double* absmax = nullptr;       // [slots]
+  double* resid_part = nullptr;   // [2][kResidualBlocks]
+
+  KhTree tree() const {
+    KhTree T;
+    T.fronts = fronts;
+    T.child_list = child_list;
+    T.relind = relind;
+    T.urows = urows;
+    T.orig_src = orig_src;
+    T.orig_dst = orig_dst;
+    T.mv = mv;
+    T.av = av;
+    T.nf = nf;
+    T.n = n;
+    T.panel_total = panel_total;
+    return T;
+  }
+};
+
+namespace {
+
+void plan_release(kh_plan* p) {
+  void* ptrs[] = {p->fronts, p->child_list, p->relind, p->orig_dst, p->level_fronts, p->urows, p->orig_src,
+                  p->perm, p->indptr, p->indices, p->mv, p->av, p->panels, p->upd[0], p->upd[1], p->rupd[0],
+                  p->rupd[1], p->y, p->lam, p->minpiv_work, p->absmax_work, p->minpiv, p->absmax,
+                  p->resid_part};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+}
+
+int64_t plan_bytes(const kh::Symbolic& S, int64_t max_batch, int64_t slots) {
+  int64_t b = 0;
+  b += slots * S.panel_total * 16;
+  b += max_batch * (S.upd_size[0] + S.upd_size[1] + S.rupd_size[0] + S.rupd_size[1] + S.n) * 16;
+  b += (int64_t)S.fronts.size() * (sizeof(KhDevFront) + max_batch * 8);
+  b += (int64_t)(S.urows.size() * 12 + S.orig_src.size() * 12 + S.n * 16 + S.nnz * 24);
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kh_version(void) { return 1; }
+
+const char* kh_status_string(int status) {
+  switch (status) {
+    case KH_OK: return "ok";
+    case KH_ERR_DIMENSION: return "dimension mismatch";
+    case KH_ERR_SINGULAR: return "singular matrix";
+    case KH_ERR_INVALID: return "invalid usage";
+    case KH_ERR_CUDA: return "CUDA error";
+    case KH_ERR_NOMEM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+const char* kh_last_error(void) { return g_last_error.c_str(); }
+
+namespace {
+// per-thread, per-device scratch for plan-free reductions
+cudaError_t scratch(double** out) {
+  static thread_local double* part[64] = {nullptr};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!part[dev]) {
+    e = cudaMalloc(&part[dev], 2 * kResidualBlocks * sizeof(double));
+    if (e != cudaSuccess) return e;
+  }
+  *out = part[dev];
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                    const double* m_vals, const double* a_vals, const double* Y, int64_t ldy,
+                                    const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2,
+                                    void* stream) {
+  if (!indptr || !Y || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
+  if (ldy < n || ldf < n || (R && ldr < n)) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  KH_CUDA(scratch(&part));
+  KH_CUDA(kh_launch_pair_residual(n, nt, indptr, indices, m_vals, a_vals, Y, ldy, F, ldf, R, ldr, part,
+                                  kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 2, 0, norms2, st));
+  return KH_OK;
+}
+
+extern "C" int kh_sumsq(const double* x, int64_t n, double* out, void* stream) {
+  if (!out || (n > 0 && !x)) return fail(KH_ERR_INVALID, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  KH_CUDA(scratch(&part));
+  KH_CUDA(kh_launch_sumsq(x, n, part, kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 1, 0, out, st));
+  return KH_OK;
+}
+
+int kh_set_device(int device) {
+  KH_CUDA(cudaSetDevice(device));
+  return KH_OK;
+}
+
+int kh_stream_sync(void* stream) {
+  KH_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
+int kh_analyze(int64_t n, const int64_t* indptr, const int64_t* indices, int32_t leaf_size, kh_symbolic** out) {
+  if (!out || (n > 0 && (!indptr || !indices))) return fail(KH_ERR_INVALID, "null argument");
+  if (n < 0) return fail(KH_ERR_DIMENSION, "negative dimension");
+  kh_symbolic* s = new kh_symbolic();
+  std::string err = kh::analyze(n, indptr, indices, leaf_size > 0 ? leaf_size : kDefaultLeaf, s->S);
+  if (!err.empty()) {
+    delete s;
+    return fail(KH_ERR_DIMENSION, err);
+  }
+  *out = s;
+  return KH_OK;
+}
+
+int kh_symbolic_stats_get(const kh_symbolic* s, kh_symbolic_stats* o) {
+  if (!s || !o) return fail(KH_ERR_INVALID, "null argument");
+  const kh::Symbolic& S = s->S;
+  std::memset(o, 0, sizeof(*o));
+  o->n = S.n;
+  o->nnz = S.nnz;
+  o->n_fronts = (int64_t)S.fronts.size();
+  o->max_front = S.max_front;
+  for (const auto& F : S.fronts) o->max_pivots = std::max<int64_t>(o->max_pivots, F.p);
+  o->depth = S.max_depth;
+  o->factor_nnz = S.factor_nnz;
+  o->panel_entries = S.panel_total;
+  o->upd_entries = S.upd_size[0] + S.upd_size[1] + S.rupd_size[0] + S.rupd_size[1] + S.n;
+  o->leaf_size = S.leaf_size;
+  o->flops = S.flops;
+  return KH_OK;
+}
+
+int kh_symbolic_perm(const kh_symbolic* s, int64_t* perm) {
+  if (!s || (!perm && s->S.n)) return fail(KH_ERR_INVALID, "null argument");
+  std::copy(s->S.perm.begin(), s->S.perm.end(), perm);
+  return KH_OK;
+}
+
+int kh_symbolic_fronts(const kh_symbolic* s, int64_t* first, int32_t* npiv, int32_t* nupd, int32_t* parent,
+                       int32_t* depth) {
+  if (!s) return fail(KH_ERR_INVALID, "null argument");
+  const auto& Fs = s->S.fronts;
+  for (size_t f = 0; f < Fs.size(); ++f) {
+    if (first) first[f] = Fs[f].first;
+    if (npiv) npiv[f] = Fs[f].p;
+    if (nupd) nupd[f] = Fs[f].q;
+    if (parent) parent[f] = Fs[f].parent;
+    if (depth) depth[f] = Fs[f].depth;
+  }
+  return KH_OK;
+}
+
+int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows) {
+  if (!s || (!rows && !s->S.urows.empty())) return fail(KH_ERR_INVALID, "null argument");
+  std::copy(s->S.urows.begin(), s->S.urows.end(), rows);
+  return KH_OK;
+}
+
+void kh_symbolic_free(kh_symbolic* s) { delete s; }
+
+int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes) {
+  if (!s || !bytes) return fail(KH_ERR_INVALID, "null argument");
+  *bytes = plan_bytes(s->S, max_batch, factor_slots);
+  return KH_OK;
+}
+
+int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, const int64_t* indices,
+                   const double* m_vals, const double* a_vals, int64_t max_batch, int64_t factor_slots,
+                   kh_plan** out) {
+  if (!s || !out || !indptr || (s->S.nnz && (!indices || !m_vals || !a_vals)))
+    return fail(KH_ERR_INVALID, "null argument");
+  if (max_batch < 1 || factor_slots < max_batch) return fail(KH_ERR_INVALID, "need factor_slots >= max_batch >= 1");
+  const kh::Symbolic& S = s->S;
+  if (indptr[S.n] != S.nnz) return fail(KH_ERR_DIMENSION, "CSR does not match the analyzed pattern");
+  KH_CUDA(cudaSetDevice(device));
+  kh_plan* p = new kh_plan();
+  p->device = device;
+  p->n = S.n;
+  p->nnz = S.nnz;
+  p->max_batch = max_batch;
+  p->slots = factor_slots;
+  p->nf = (int32_t)S.fronts.size();
+  p->depth = S.max_depth;
+  p->panel_total = S.panel_total;
+  for (int k = 0; k < 2; ++k) {
+    p->upd_size[k] = std::max<int64_t>(S.upd_size[k], 1);
+    p->rupd_size[k] = std::max<int64_t>(S.rupd_size[k], 1);
+  }
+  std::vector<KhDevFront> df(p->nf);
+  for (int32_t f = 0; f < p->nf; ++f) {
+    const kh::Front& F = S.fronts[f];
+    KhDevFront& D = df[f];
+    D.first = F.first;
+    D.p = F.p;
+    D.q = F.q;
+    D.panel_off = F.panel_off;
+    D.upd_off = F.upd_off;
+    D.rupd_off = F.rupd_off;
+    D.orig_begin = F.orig_begin;
+    D.orig_end = F.orig_end;
+    D.rows_begin = F.rows_begin;
+    D.child_begin = S.child_ptr[f];
+    D.child_end = S.child_ptr[f + 1];
+    D.depth = F.depth;
+    D.pad = 0;
+    p->max_p = std::max(p->max_p, F.p);
+  }
+  std::vector<int32_t> lf;
+  p->level_off.push_back(0);
+  for (const auto& lev : S.levels) {
+    lf.insert(lf.end(), lev.begin(), lev.end());
+    p->level_off.push_back((int32_t)lf.size());
+  }
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  chk(upload(&p->fronts, df.data(), df.size()));
+  chk(upload(&p->child_list, S.child_list.data(), S.child_list.size()));
+  chk(upload(&p->relind, S.relind.data(), S.relind.size()));
+  chk(upload(&p->urows, S.urows.data(), S.urows.size()));
+  chk(upload(&p->orig_src, S.orig_src.data(), S.orig_src.size()));
+  chk(upload(&p->orig_dst, S.orig_dst.data(), S.orig_dst.size()));
+  chk(upload(&p->level_fronts, lf.data(), lf.size()));
+  chk(upload(&p->perm, S.perm.data(), S.perm.size()));
+  chk(upload(&p->indptr, indptr, (size_t)S.n + 1));
+  chk(upload(&p->indices, indices, (size_t)S.nnz));
+  chk(upload(&p->mv, m_vals, (size_t)S.nnz));
+  chk(upload(&p->av, a_vals, (size_t)S.nnz));
+  auto alloc = [&](void** ptr, int64_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(ptr, (size_t)std::max<int64_t>(bytes, 16));
+  };
+  alloc((void**)&p->panels, factor_slots * S.panel_total * 16);
+  for (int k = 0; k < 2; ++k) {
+    alloc((void**)&p->upd[k], max_batch * p->upd_size[k] * 16);
+    alloc((void**)&p->rupd[k], max_batch * p->rupd_size[k] * 16);
+  }
+  alloc((void**)&p->y, max_batch * S.n * 16);
+  alloc((void**)&p->lam, max_batch * 16);
+  alloc((void**)&p->minpiv_work, max_batch * (int64_t)p->nf * 8);
+  alloc((void**)&p->absmax_work, max_batch * (int64_t)kAbsmaxBlocks * 8);
+  alloc((void**)&p->minpiv, factor_slots * 8);
+  alloc((void**)&p->absmax, factor_slots * 8);
+  alloc((void**)&p->resid_part, 2 * (int64_t)kResidualBlocks * 8);
+  if (e != cudaSuccess) {
+    plan_release(p);
+    delete p;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? KH_ERR_NOMEM : KH_ERR_CUDA,
+                std::string("kh_plan_create: ") + cudaGetErrorString(e));
+  }
+  *out = p;
+  return KH_OK;
+}
+
+int kh_plan_set_values(kh_plan* p, const double* m_vals, const double* a_vals) {
+  if (!p || (p->nnz && (!m_vals || !a_vals))) return fail(KH_ERR_INVALID, "null argument");
+  KH_CUDA(cudaSetDevice(p->device));
+  KH_CUDA(cudaMemcpy(p->mv, m_vals, p->nnz * 8, cudaMemcpyHostToDevice));
+  KH_CUDA(cudaMemcpy(p->av, a_vals, p->nnz * 8, cudaMemcpyHostToDevice));
+  return KH_OK;
+}
+
+int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, void* stream) {
+  if (!p || (nshift > 0 && !lambda_ri)) return fail(KH_ERR_INVALID, "null argument");
+  if (nshift < 0 || nshift > p->max_batch || slot0 < 0 || slot0 + nshift > p->slots)
+    return fail(KH_ERR_INVALID, "shift batch outside the plan's slots");
+  if (nshift == 0) return KH_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KH_CUDA(cudaSetDevice(p->device));
+  KH_CUDA(cudaMemcpyAsync(p->lam, lambda_ri, nshift * 16, cudaMemcpyHostToDevice, st));
+  const KhTree T = p->tree();
+  double2* panels = p->panels + slot0 * p->panel_total;
+  for (int32_t d = p->depth; d >= 0; --d) {
+    const int32_t* lev = p->level_fronts + p->level_off[d];
+    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
+    KH_CUDA(kh_launch_factor_level(T, lev, nlev, (int32_t)nshift, p->lam, panels, p->upd[d & 1],
+                                   p->upd_size[d & 1], p->upd[(d + 1) & 1], p->upd_size[(d + 1) & 1],
+                                   p->minpiv_work, st));
+  }
+  KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));
+  KH_CUDA(kh_launch_shift_absmax_nnz(p->mv, p->av, p->nnz, (int32_t)nshift, p->lam, p->absmax_work,
+                                     kAbsmaxBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(p->absmax_work, kAbsmaxBlocks, (int32_t)nshift, 2, p->absmax + slot0, st));
+  return KH_OK;
+}
+
+int kh_plan_pivot_check(kh_plan* p, int64_t slot0, int64_t nshift, double rel_threshold, void* stream,
+                        int64_t* first_bad, double* worst_ratio) {
+  if (!p) return fail(KH_ERR_INVALID, "null argument");
+  if (nshift < 0 || slot0 < 0 || slot0 + nshift > p->slots) return fail(KH_ERR_INVALID, "slots out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KH_CUDA(cudaSetDevice(p->device));
+  std::vector<double> mp(nshift), am(nshift);
+  if (nshift) {
+    KH_CUDA(cudaMemcpyAsync(mp.data(), p->minpiv + slot0, nshift * 8, cudaMemcpyDeviceToHost, st));
+    KH_CUDA(cudaMemcpyAsync(am.data(), p->absmax + slot0, nshift * 8, cudaMemcpyDeviceToHost, st));
+  }
+  KH_CUDA(cudaStreamSynchronize(st));
+  int64_t bad = -1;
+  double worst = INFINITY;
+  for (int64_t s = 0; s < nshift; ++s) {
+    double ratio = am[s] > 0.0 ? mp[s] / am[s] : 0.0;
+    if (!(mp[s] >= 0.0) || !std::isfinite(mp[s])) ratio = -1.0;
+    worst = std::min(worst, ratio);
+    if (bad < 0 && (am[s] == 0.0 || !(ratio >= rel_threshold))) bad = s;
+  }
+  if (first_bad) *first_bad = bad;
+  if (worst_ratio) *worst_ratio = worst;
+  if (bad >= 0) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "pivot %.3e below threshold %.3e (shift %lld)", mp[bad] < 0 ? NAN : mp[bad],
+                  rel_threshold * am[bad], (long long)bad);
+    return fail(KH_ERR_SINGULAR, buf);
+  }
+  return KH_OK;
+}
+
+int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re, const double* b_im, int64_t ldb,
+                  double* x_re, double* x_im, int64_t ldx, void* stream) {
+  if (!p || (nshift > 0 && (!b_re || !x_re))) return fail(KH_ERR_INVALID, "null argument");
+  if (nshift < 0 || nshift > p->max_batch || slot0 < 0 || slot0 + nshift > p->slots)
+    return fail(KH_ERR_INVALID, "shift batch outside the plan's slots");
+  if (ldb < p->n || ldx < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  if (nshift == 0 || p->n == 0) return KH_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KH_CUDA(cudaSetDevice(p->device));
+  const KhTree T = p->tree();
+  const double2* panels = p->panels + slot0 * p->panel_total;
+  const int32_t ns = (int32_t)nshift;
+  KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
+  for (int32_t d = p->depth; d >= 0; --d) {
+    const int32_t* lev = p->level_fronts + p->level_off[d];
+    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
+    KH_CUDA(kh_launch_fwd_level(T, lev, nlev, ns, panels, p->y, p->rupd[d & 1], p->rupd_size[d & 1],
+                                p->rupd[(d + 1) & 1], p->rupd_size[(d + 1) & 1], st));
+  }
+  for (int32_t d = 0; d <= p->depth; ++d) {
+    const int32_t* lev = p->level_fronts + p->level_off[d];
+    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
+    KH_CUDA(kh_launch_bwd_level(T, lev, nlev, ns, p->max_p, panels, p->y, st));
+  }
+  KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
+  return KH_OK;
+}
+
+int kh_plan_residual(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf, double* R,
+                     int64_t ldr, double* norms2, void* stream) {
+  if (!p || !Y || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
+  if (ldy < p->n || ldf < p->n || (R && ldr < p->n)) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KH_CUDA(cudaSetDevice(p->device));
+  KH_CUDA(kh_launch_pair_residual(p->n, nt, p->indptr, p->indices, p->mv, p->av, Y, ldy, F, ldf, R, ldr,
+                                  p->resid_part, kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(p->resid_part, kResidualBlocks, 2, 0, norms2, st));
+  return KH_OK;
+}
+
+void kh_plan_free(kh_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  plan_release(p);
+  delete p;
+}
+
+int kh_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+             int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  if (m < 0 || n < 0 || k < 0) return fail(KH_ERR_DIMENSION, "negative GEMM dimension");
+  if ((m > 0 && lda < m) || (k > 0 && ldb < k) || (m > 0 && ldc < m))
+    return fail(KH_ERR_DIMENSION, "GEMM leading dimension too small");
+  if (m && n && (!C || (k && (!A || !B)))) return fail(KH_ERR_INVALID, "null GEMM operand");
+  KH_CUDA(kh_launch_dgemm(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
+}  // extern "C"

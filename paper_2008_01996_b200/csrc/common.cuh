@@ -1,0 +1,46 @@
+// Shared device helpers: complex fp64 on double2, the DMMA fp64 MMA wrapper
+// (mma.sync m8n8k4 f64 -- sm_100a has no tcgen05 kind::f64, SURVEY.md
+// finding 6), cp.async, and error plumbing for the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define KH_DEV __device__ __forceinline__
+
+// ---- complex fp64 -----------------------------------------------------------
+KH_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+KH_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+KH_DEV double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a - b*c
+KH_DEV double2 cfms(double2 a, double2 b, double2 c) {
+  return make_double2(a.x - b.x * c.x + b.y * c.y, a.y - b.x * c.y - b.y * c.x);
+}
+KH_DEV double2 cinv(double2 a) {
+  // Smith-style scaling is unnecessary here: pivots are O(1) after the
+  // reference's threshold check; use the plain formula in fp64.
+  double den = a.x * a.x + a.y * a.y;
+  return make_double2(a.x / den, -a.y / den);
+}
+KH_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// ---- DMMA ---------------------------------------------------------------------
+// D(8x8) = A(8x4, row) * B(4x8, col) + C. Lane (g = lane>>2, t = lane&3):
+// a = A[g][t], b = B[t][g], c/d = C[g][2t], C[g][2t+1].
+KH_DEV void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// ---- cp.async -------------------------------------------------------------------
+KH_DEV void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+KH_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+KH_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

@@ -1,0 +1,126 @@
+// fp64 DMMA GEMM for the modal transforms (C = alpha*A*B + beta*C, column-
+// major). Replaces the reference's zgemm chains at solvers.py:368-372
+// (G = F A^-1 conj(U) S^-1 conj(Vh)) and :397-400 (U = Z Vh^T S U^T); the host
+// folds those N_t x N_t factors into one real matrix per direction, so each
+// transform is a single real GEMM (M_x x N_t) * (N_t x N_t).
+//
+// Tiling: 128x64 CTA tile, K chunks of 16 staged by cp.async in a 3-stage
+// ring, 8 warps of 32x32 each issuing mma.sync.m8n8k4.f64 (DMMA). Shared
+// layouts are padded so both fragment loads are bank-conflict free:
+// A chunk [k][m] with ld 132, B chunk [n][k] with ld 20.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int BM = 128, BN = 64, BK = 16, NST = 3;
+constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
+constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
+constexpr size_t SMEM_BYTES = sizeof(double) * NST * (A_STAGE + B_STAGE);
+
+__global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                    const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ B, int64_t ldb,
+                                                    double beta, double* __restrict__ C, int64_t ldc) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + NST * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
+  const int nk = (int)((K + BK - 1) / BK);
+
+  auto load_stage = [&](int st, int kc) {
+    const int64_t k0 = (int64_t)kc * BK;
+    double* as = As + st * A_STAGE;
+    double* bs = Bs + st * B_STAGE;
+#pragma unroll
+    for (int r = 0; r < (BK * BM) / 256; ++r) {
+      int idx = tid + r * 256;
+      int k = idx / BM, i = idx % BM;
+      int64_t gi = m0 + i, gk = k0 + k;
+      bool ok = gi < M && gk < K;
+      cp_async8(as + k * LDA_S + i, ok ? A + gi + gk * lda : A, ok);
+    }
+#pragma unroll
+    for (int r = 0; r < (BK * BN) / 256; ++r) {
+      int idx = tid + r * 256;
+      int k = idx % BK, j = idx / BK;
+      int64_t gj = n0 + j, gk = k0 + k;
+      bool ok = gj < N && gk < K;
+      cp_async8(bs + j * LDB_S + k, ok ? B + gk + gj * ldb : B, ok);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<NST - 2>();
+    __syncthreads();
+    {
+      int nxt = kc + NST - 1;
+      if (nxt < nk) load_stage(nxt % NST, nxt);
+      cp_async_commit();
+    }
+    const double* as = As + (kc % NST) * A_STAGE;
+    const double* bs = Bs + (kc % NST) * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = as[(kk + t) * LDA_S + wm * 32 + mt * 8 + g];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = bs[(wn * 32 + nt * 8 + g) * LDB_S + kk + t];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    int64_t row = m0 + wm * 32 + mt * 8 + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int64_t col = n0 + wn * 32 + nt * 8 + 2 * t + h;
+        if (col >= N) continue;
+        double* c = C + row + col * ldc;
+        double v = alpha * acc[mt][nt][h];
+        if (beta != 0.0) v = fma(beta, *c, v);
+        *c = v;
+      }
+  }
+}
+
+}  // namespace
+
+cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                            cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  dgemm_kernel<<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  return cudaGetLastError();
+}

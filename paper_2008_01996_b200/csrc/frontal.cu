@@ -1,0 +1,532 @@
+// Batched multifrontal complex-symmetric LDL^T (pivot-free) and its
+// triangular solves, one CTA per (front, shift).
+//
+// Replaces the reference's per-shift SuperLU path
+//   K = (Mc + lam[k] Ac).tocsr(); sparse_direct.factorize(sym, K).solve(G[:,k])
+// (solvers.py:383-393 -> sparse_direct.py:155-209). All shifts share one
+// symbolic analysis (symbolic.cpp) and are processed level by level of the
+// dissection tree, deepest level first; every launch covers all fronts of a
+// level for all shifts of a batch, so the grid is (#fronts x #shifts).
+//
+// Per front (m = p + q rows, p pivots):
+//   panel P (m x p, column-major, ld m) in the retained factor storage,
+//   update U (q x q, lower) in a depth-parity buffer consumed by the parent.
+// Factorization: assemble (originals + extend-add of children), then 32-wide
+// pivot blocks: LDL^T of the diagonal block in shared memory, TRSM of the rows
+// below as a GEMM with the explicit unit-triangular inverse, trailing update
+// of the remaining pivot columns, and finally one SYRK-like update of U with
+// K = p. All three GEMM-shaped steps run on DMMA (mma.sync m8n8k4 f64) as
+// complex products built from four real MMAs.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int NT = 256;      // threads per CTA
+constexpr int TB = 64;       // complex tile edge
+constexpr int KC = 16;       // complex K chunk
+constexpr int LDS = TB + 2;  // padded smem row (double2): conflict-free LDS.128 fragments
+constexpr int NB = 32;       // pivot block width
+
+struct Acc {
+  double r[4][2][2];
+  double i[4][2][2];
+};
+
+// acc(i, j) = sum_k a(i, k) * b(j, k) over k in [0, K), i, j in [0, 64).
+// `la(i, k)` / `lb(j, k)` return the (already masked/scaled) operands.
+// Register-prefetch double buffering: the next chunk's loads are in flight
+// while the current one is multiplied out of shared memory.
+template <class LA, class LB>
+KH_DEV void tile_mma(Acc& acc, int K, LA la, LB lb, double2* sA, double2* sB) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wi = warp & 1, wj = warp >> 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc.r[a][b][h] = acc.i[a][b][h] = 0.0;
+  const int nch = (K + KC - 1) / KC;
+  double2 ra[4], rb[4];
+  auto fetch = [&](int c) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int idx = tid + r * NT;
+      int i = idx & (TB - 1), k = idx >> 6;
+      int kk = c * KC + k;
+      ra[r] = kk < K ? la(i, kk) : make_double2(0.0, 0.0);
+      rb[r] = kk < K ? lb(i, kk) : make_double2(0.0, 0.0);
+    }
+  };
+  if (nch > 0) fetch(0);
+  for (int c = 0; c < nch; ++c) {
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int idx = tid + r * NT;
+      int i = idx & (TB - 1), k = idx >> 6;
+      sA[k * LDS + i] = ra[r];
+      sB[k * LDS + i] = rb[r];
+    }
+    __syncthreads();
+    if (c + 1 < nch) fetch(c + 1);
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double2 af[4], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = sA[(kk + t) * LDS + wi * 32 + mt * 8 + g];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = sB[(kk + t) * LDS + wj * 16 + nt * 8 + g];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        double nai = -af[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], af[mt].x, bf[nt].x);
+          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], nai, bf[nt].y);
+          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].x, bf[nt].y);
+          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].y, bf[nt].x);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Visit the accumulator: ep(row, col, value) with row, col in [0, 64).
+template <class EP>
+KH_DEV void tile_epilogue(const Acc& acc, EP ep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wi = warp & 1, wj = warp >> 1;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        ep(wi * 32 + mt * 8 + g, wj * 16 + nt * 8 + 2 * t + h,
+           make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
+}
+
+struct FactorSmem {
+  double2 a[KC * LDS];
+  double2 b[KC * LDS];
+  double2 d[NB * (NB + 1)];   // diagonal block, [i][j] at i*(NB+1)+j
+  double2 li[NB * (NB + 1)];  // unit-lower inverse
+  double2 dinv[NB];
+  double red[NT / 32];
+};
+
+__global__ void __launch_bounds__(NT) factor_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                          const double2* __restrict__ lam, double2* panels,
+                                                          double2* upd_cur, int64_t upd_stride_cur,
+                                                          const double2* __restrict__ upd_child,
+                                                          int64_t upd_stride_child, double* minpiv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FactorSmem& S = *reinterpret_cast<FactorSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2 L = lam[b];
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+
+  // ---- assembly -------------------------------------------------------------
+  for (int64_t idx = tid; idx < (int64_t)m * p; idx += NT) P[idx] = make_double2(0.0, 0.0);
+  for (int64_t idx = tid; idx < (int64_t)q * q; idx += NT) U[idx] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NT) {
+    int64_t s = T.orig_src[e];
+    double mvv = T.mv[s], avv = T.av[s];
+    P[T.orig_dst[e]] = make_double2(fma(L.x, avv, mvv), L.y * avv);
+  }
+  __syncthreads();
+  for (int c = F.child_begin; c < F.child_end; ++c) {
+    const KhDevFront C = T.fronts[T.child_list[c]];
+    const int qc = C.q;
+    const double2* Uc = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
+    const int32_t* rel = T.relind + C.rows_begin;
+    for (int64_t idx = tid; idx < (int64_t)qc * qc; idx += NT) {
+      int a = (int)(idx % qc), bb = (int)(idx / qc);
+      if (a < bb) continue;
+      double2 v = Uc[idx];
+      int ra = rel[a], rb = rel[bb];
+      if (rb < p) {
+        double2* d = P + ra + (int64_t)rb * m;
+        *d = cadd(*d, v);
+      } else {
+        double2* d = U + (ra - p) + (int64_t)(rb - p) * q;
+        *d = cadd(*d, v);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- pivot blocks ---------------------------------------------------------
+  double minp = DBL_MAX;
+  Acc acc;
+  for (int kb = 0; kb < p; kb += NB) {
+    const int w = min(NB, p - kb);
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, j = idx / w;
+      S.d[i * (NB + 1) + j] = i >= j ? P[(kb + i) + (int64_t)(kb + j) * m] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int k = 0; k < w; ++k) {
+      const double2 dk = S.d[k * (NB + 1) + k];
+      const double2 di = cinv(dk);
+      const int r = w - k - 1;
+      for (int idx = tid; idx < r * r; idx += NT) {
+        int i = k + 1 + idx % r, j = k + 1 + idx / r;
+        if (i >= j) {
+          double2 lik = cmul(S.d[i * (NB + 1) + k], di);
+          S.d[i * (NB + 1) + j] = cfms(S.d[i * (NB + 1) + j], lik, S.d[j * (NB + 1) + k]);
+        }
+      }
+      __syncthreads();
+      for (int i = k + 1 + tid; i < w; i += NT) S.d[i * (NB + 1) + k] = cmul(S.d[i * (NB + 1) + k], di);
+      if (tid == 0) {
+        S.dinv[k] = di;
+        double ad = sqrt(cabs2(dk));
+        minp = (ad != ad) ? -1.0 : fmin(minp, ad);  // NaN pivots are reported as -1
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, j = idx / w;
+      if (i >= j) P[(kb + i) + (int64_t)(kb + j) * m] = S.d[i * (NB + 1) + j];
+    }
+    // explicit inverse of the unit-lower block, row by row
+    for (int idx = tid; idx < NB * NB; idx += NT) {
+      int i = idx / NB, j = idx % NB;
+      S.li[i * (NB + 1) + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    for (int i = 1; i < w; ++i) {
+      for (int j = tid; j < i; j += NT) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int k = j; k < i; ++k) s = cfms(s, S.d[i * (NB + 1) + k], S.li[k * (NB + 1) + j]);
+        S.li[i * (NB + 1) + j] = s;
+      }
+      __syncthreads();
+    }
+    const int r0 = kb + w;
+    // TRSM of the rows below: L[r, kb+j] = (A[r, kb:kb+w] Linv^T)[j] / d_j
+    for (int i0 = r0; i0 < m; i0 += TB) {
+      const int rows = m - i0;
+      tile_mma(
+          acc, w,
+          [&](int i, int k) { return i < rows ? P[(i0 + i) + (int64_t)(kb + k) * m] : make_double2(0.0, 0.0); },
+          [&](int j, int k) { return j < w ? S.li[j * (NB + 1) + k] : make_double2(0.0, 0.0); }, S.a, S.b);
+      tile_epilogue(acc, [&](int i, int j, double2 v) {
+        if (i < rows && j < w) P[(i0 + i) + (int64_t)(kb + j) * m] = cmul(v, S.dinv[j]);
+      });
+    }
+    __syncthreads();
+    // trailing update of the remaining pivot columns (lower trapezoid)
+    for (int j0 = r0; j0 < p; j0 += TB) {
+      for (int i0 = j0; i0 < m; i0 += TB) {
+        tile_mma(
+            acc, w,
+            [&](int i, int k) {
+              return i0 + i < m ? P[(i0 + i) + (int64_t)(kb + k) * m] : make_double2(0.0, 0.0);
+            },
+            [&](int j, int k) {
+              return j0 + j < p ? cmul(P[(j0 + j) + (int64_t)(kb + k) * m], S.d[k * (NB + 1) + k])
+                                : make_double2(0.0, 0.0);
+            },
+            S.a, S.b);
+        tile_epilogue(acc, [&](int i, int j, double2 v) {
+          int r = i0 + i, c = j0 + j;
+          if (r < m && c < p && r >= c) {
+            double2* d = P + r + (int64_t)c * m;
+            *d = csub(*d, v);
+          }
+        });
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- update matrix: U -= L21 D L21^T ---------------------------------------
+  for (int j0 = 0; j0 < q; j0 += TB) {
+    for (int i0 = j0; i0 < q; i0 += TB) {
+      tile_mma(
+          acc, p,
+          [&](int i, int k) {
+            return i0 + i < q ? P[(p + i0 + i) + (int64_t)k * m] : make_double2(0.0, 0.0);
+          },
+          [&](int j, int k) {
+            return j0 + j < q ? cmul(P[(p + j0 + j) + (int64_t)k * m], P[k + (int64_t)k * m])
+                              : make_double2(0.0, 0.0);
+          },
+          S.a, S.b);
+      tile_epilogue(acc, [&](int i, int j, double2 v) {
+        int r = i0 + i, c = j0 + j;
+        if (r < q && c < q && r >= c) {
+          double2* d = U + r + (int64_t)c * q;
+          *d = csub(*d, v);
+        }
+      });
+    }
+  }
+  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+}
+
+// ---- forward solve: y <- L^{-1} b, fronts bottom-up ------------------------
+__global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                       const double2* __restrict__ panels, double2* y,
+                                                       double2* ru_cur, int64_t ru_stride_cur,
+                                                       const double2* __restrict__ ru_child,
+                                                       int64_t ru_stride_child) {
+  __shared__ double2 sL[NB * (NB + 1)];
+  __shared__ double2 sy[NB];
+  const int tid = threadIdx.x;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  for (int a = tid; a < q; a += NT) ru[a] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int c = F.child_begin; c < F.child_end; ++c) {
+    const KhDevFront C = T.fronts[T.child_list[c]];
+    const double2* ruc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+    const int32_t* rel = T.relind + C.rows_begin;
+    for (int a = tid; a < C.q; a += NT) {
+      int loc = rel[a];
+      double2 v = ruc[a];
+      if (loc < p) yy[loc] = cadd(yy[loc], v);
+      else ru[loc - p] = cadd(ru[loc - p], v);
+    }
+    __syncthreads();
+  }
+  for (int kb = 0; kb < p; kb += NB) {
+    const int w = min(NB, p - kb);
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, j = idx / w;
+      sL[i * (NB + 1) + j] = P[(kb + i) + (int64_t)(kb + j) * m];
+    }
+    if (tid < w) sy[tid] = yy[kb + tid];
+    __syncthreads();
+    if (tid < 32) {  // one warp: unit-lower solve of the block
+      for (int k = 0; k < w; ++k) {
+        double2 yk = sy[k];
+        __syncwarp();
+        if (tid > k && tid < w) sy[tid] = cfms(sy[tid], sL[tid * (NB + 1) + k], yk);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (tid < w) yy[kb + tid] = sy[tid];
+    // rows below the block
+    for (int r = kb + w + tid; r < m; r += NT) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < w; ++k) {
+        double2 l = P[r + (int64_t)(kb + k) * m];
+        s = cadd(s, cmul(l, sy[k]));
+      }
+      if (r < p) yy[r] = csub(yy[r], s);
+      else ru[r - p] = csub(ru[r - p], s);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- backward solve: x <- L^{-T} D^{-1} y, fronts top-down -------------------
+__global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                       const double2* __restrict__ panels, double2* y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* st = reinterpret_cast<double2*>(smem_raw);  // p entries
+  __shared__ double2 sL[NB * (NB + 1)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  const int64_t* urows = T.urows + F.rows_begin;
+  // t_k = y_k / d_k - sum_a L21[a, k] x[urows[a]]   (warp per column k)
+  for (int k = warp; k < p; k += NT / 32) {
+    double2 s = make_double2(0.0, 0.0);
+    const double2* col = P + p + (int64_t)k * m;
+    for (int a = lane; a < q; a += 32) s = cadd(s, cmul(col[a], yb[urows[a]]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    if (lane == 0) st[k] = csub(cmul(yy[k], cinv(P[k + (int64_t)k * m])), s);
+  }
+  __syncthreads();
+  // blocks from last to first: solve L_blk^T x_blk = t_blk, then push into earlier t
+  const int nblk = (p + NB - 1) / NB;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * NB, w = min(NB, p - kb);
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, j = idx / w;
+      sL[i * (NB + 1) + j] = P[(kb + i) + (int64_t)(kb + j) * m];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      for (int i = w - 1; i >= 0; --i) {
+        double2 xi = st[kb + i];
+        __syncwarp();
+        if (tid < i) st[kb + tid] = cfms(st[kb + tid], sL[i * (NB + 1) + tid], xi);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // earlier pivots k < kb: t_k -= sum_i L[kb+i, k] x_{kb+i}  (warp per column)
+    for (int k = warp; k < kb; k += NT / 32) {
+      double2 s = make_double2(0.0, 0.0);
+      if (lane < w) s = cmul(P[(kb + lane) + (int64_t)k * m], st[kb + lane]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      if (lane == 0) st[k] = csub(st[k], s);
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < p; k += NT) yy[k] = st[k];
+}
+
+__global__ void gather_rhs_kernel(int64_t n, const int64_t* __restrict__ perm, const double* __restrict__ g_re,
+                                  const double* __restrict__ g_im, int64_t ldg, double2* y) {
+  const int b = blockIdx.y;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t src = perm[k] + (int64_t)b * ldg;
+    y[(int64_t)b * n + k] = make_double2(g_re[src], g_im ? g_im[src] : 0.0);
+  }
+}
+
+__global__ void scatter_sol_kernel(int64_t n, const int64_t* __restrict__ perm, const double2* __restrict__ y,
+                                   double* z_re, double* z_im, int64_t ldz) {
+  const int b = blockIdx.y;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t dst = perm[k] + (int64_t)b * ldz;
+    double2 v = y[(int64_t)b * n + k];
+    z_re[dst] = v.x;
+    if (z_im) z_im[dst] = v.y;
+  }
+}
+
+__global__ void shift_absmax_kernel(const double* __restrict__ mv, const double* __restrict__ av, int64_t nnz,
+                                    const double2* __restrict__ lam, double* part) {
+  __shared__ double red[NT / 32];
+  const int b = blockIdx.y;
+  const double2 L = lam[b];
+  double mx = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * NT) {
+    double re = fma(L.x, av[e], mv[e]), im = L.y * av[e];
+    mx = fmax(mx, sqrt(re * re + im * im));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NT / 32; ++w) mx = fmax(mx, red[w]);
+    part[(int64_t)b * gridDim.x + blockIdx.x] = mx;
+  }
+}
+
+// op: 0 = sum, 1 = min, 2 = max over each row of a [rows][len] array
+__global__ void rowreduce_kernel(const double* __restrict__ in, int64_t len, int op, double* out) {
+  __shared__ double red[NT / 32];
+  const int r = blockIdx.x;
+  auto comb = [op](double a, double b) { return op == 0 ? a + b : (op == 1 ? fmin(a, b) : fmax(a, b)); };
+  double v = op == 0 ? 0.0 : (op == 1 ? DBL_MAX : -DBL_MAX);
+  for (int64_t i = threadIdx.x; i < len; i += NT) v = comb(v, in[(int64_t)r * len + i]);
+  for (int o = 16; o > 0; o >>= 1) v = comb(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NT / 32; ++w) v = comb(v, red[w]);
+    out[r] = v;
+  }
+}
+
+}  // namespace
+
+cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
+                                   const double2* upd_child, int64_t upd_stride_child, double* minpiv,
+                                   cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  static bool attr = false;
+  const int smem = (int)sizeof(FactorSmem);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  factor_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, lam, panels, upd_cur,
+                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
+                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  fwd_level_kernel<<<dim3(nlev, batch), NT, 0, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
+                                                         ru_child, ru_stride_child);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                int32_t max_p, const double2* panels, double2* y, cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  size_t smem = sizeof(double2) * (size_t)max_p;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(bwd_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  bwd_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
+                                 const double* g_im, int64_t ldg, double2* y, cudaStream_t stream) {
+  if (n == 0 || batch == 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  gather_rhs_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(n, perm, g_re, g_im, ldg, y);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm, const double2* y, double* z_re,
+                                  double* z_im, int64_t ldz, cudaStream_t stream) {
+  if (n == 0 || batch == 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  scatter_sol_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(n, perm, y, z_re, z_im, ldz);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_shift_absmax_nnz(const double* mv, const double* av, int64_t nnz, int32_t batch,
+                                       const double2* lam, double* part, int32_t nblk, cudaStream_t stream) {
+  if (batch == 0) return cudaSuccess;
+  shift_absmax_kernel<<<dim3(nblk, batch), NT, 0, stream>>>(mv, av, nnz, lam, part);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_rowreduce(const double* in, int64_t len, int32_t rows, int op, double* out,
+                                cudaStream_t stream) {
+  if (rows == 0) return cudaSuccess;
+  rowreduce_kernel<<<rows, NT, 0, stream>>>(in, len, op, out);
+  return cudaGetLastError();
+}

@@ -1,0 +1,56 @@
+// Internal launcher interfaces shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+struct KhDevFront {
+  int64_t first;
+  int32_t p, q;
+  int64_t panel_off, upd_off, rupd_off;
+  int64_t orig_begin, orig_end;
+  int64_t rows_begin;  // urows / relind of this front
+  int32_t child_begin, child_end;
+  int32_t depth, pad;
+};
+
+struct KhTree {  // device pointers shared by every level kernel
+  const KhDevFront* fronts;
+  const int32_t* child_list;
+  const int32_t* relind;
+  const int64_t* urows;
+  const int64_t* orig_src;
+  const int32_t* orig_dst;
+  const double* mv;  // M values aligned with the analyzed CSR
+  const double* av;  // A values aligned with the analyzed CSR
+  int32_t nf;
+  int64_t n;
+  int64_t panel_total;
+};
+
+cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                            cudaStream_t stream);
+
+// Factor every front of one depth level for `batch` shifts.
+cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev,
+                                   int32_t batch, const double2* lam, double2* panels,
+                                   double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
+                                   int64_t upd_stride_child, double* minpiv, cudaStream_t stream);
+cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
+                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream);
+cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                int32_t max_p, const double2* panels, double2* y, cudaStream_t stream);
+cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
+                                 const double* g_im, int64_t ldg, double2* y, cudaStream_t stream);
+cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm, const double2* y,
+                                  double* z_re, double* z_im, int64_t ldz, cudaStream_t stream);
+cudaError_t kh_launch_shift_absmax_nnz(const double* mv, const double* av, int64_t nnz, int32_t batch,
+                                       const double2* lam, double* part, int32_t nblk, cudaStream_t stream);
+cudaError_t kh_launch_rowreduce(const double* in, int64_t len, int32_t rows, int op, double* out,
+                                cudaStream_t stream);
+cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                    const double* mv, const double* av, const double* Y, int64_t ldy,
+                                    const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
+                                    int32_t nblk, cudaStream_t stream);
+cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);

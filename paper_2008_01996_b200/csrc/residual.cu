@@ -1,0 +1,87 @@
+// Space-time residual R = F - (M_x Y1 + A_x Y2) with Y = [Y1 | Y2] = U [A_t^T | M_t^T].
+//
+// Replaces `residual` (solvers.py:428-440), which applies
+// K u = vec(M_x U A_t^T + A_x U M_t^T) through two `kron_apply_right` calls
+// (dense.py:264-286). The dense temporal products run on the DMMA GEMM; this
+// kernel is the fused dual SpMM (M_x and A_x share one CSR pattern) plus the
+// subtraction from F and the partial sums of ||R||^2 and ||F||^2 (a fixed
+// grid and a fixed reduction order keep the result deterministic).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+__global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t nt, const int64_t* __restrict__ indptr,
+                                                            const int64_t* __restrict__ indices,
+                                                            const double* __restrict__ mv,
+                                                            const double* __restrict__ av,
+                                                            const double* __restrict__ Y, int64_t ldy,
+                                                            const double* __restrict__ F, int64_t ldf, double* R,
+                                                            int64_t ldr, double* part) {
+  __shared__ double red[2][8];
+  const int64_t total = n * nt;
+  double rr = 0.0, ff = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / n, i = idx - t * n;
+    const double* y1 = Y + t * ldy;
+    const double* y2 = Y + (t + nt) * ldy;
+    double s = 0.0;
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      const int64_t j = indices[e];
+      s = fma(mv[e], y1[j], s);
+      s = fma(av[e], y2[j], s);
+    }
+    const double f = F[i + t * ldf];
+    const double r = f - s;
+    if (R) R[i + t * ldr] = r;
+    rr = fma(r, r, rr);
+    ff = fma(f, f, ff);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    ff += __shfl_xor_sync(0xffffffffu, ff, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = rr;
+    red[1][threadIdx.x >> 5] = ff;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      rr += red[0][w];
+      ff += red[1][w];
+    }
+    part[blockIdx.x] = rr;
+    part[gridDim.x + blockIdx.x] = ff;
+  }
+}
+
+__global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x, int64_t n, double* part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+}  // namespace
+
+cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream) {
+  sumsq_kernel<<<nblk, 256, 0, stream>>>(x, n, part);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                    const double* mv, const double* av, const double* Y, int64_t ldy,
+                                    const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
+                                    int32_t nblk, cudaStream_t stream) {
+  pair_residual_kernel<<<nblk, 256, 0, stream>>>(n, nt, indptr, indices, mv, av, Y, ldy, F, ldf, R, ldr, part);
+  return cudaGetLastError();
+}

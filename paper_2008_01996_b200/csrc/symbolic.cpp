@@ -1,0 +1,412 @@
+// Nested-dissection symbolic analysis (host C++). See symbolic.h.
+//
+// Ordering: recursive graph bisection. For each connected vertex set a
+// pseudo-peripheral BFS level structure is built (from both ends of the
+// pseudo-diameter); the separator is the smallest level whose two sides are
+// within 2:1 of each other, thinned by moving separator vertices without an
+// upper-side neighbour to the lower side. Sets at or below `leaf_size`
+// vertices become dense leaf fronts. Every separator is one supernode, so
+// every front has a dense p x p pivot block and a sorted list of q update
+// rows; the elimination order is the postorder of the dissection tree, which
+// is what the reference's etree postorder achieves for its MMD ordering
+// (sparse_direct.py:71-109, :144-145).
+#include "symbolic.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <numeric>
+
+namespace kh {
+namespace {
+
+struct Graph {
+  int64_t n = 0;
+  std::vector<int64_t> xadj, adj;
+};
+
+Graph build_graph(int64_t n, const int64_t* indptr, const int64_t* indices) {
+  Graph g;
+  g.n = n;
+  std::vector<int64_t> deg(n, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      int64_t j = indices[e];
+      if (j != i) { ++deg[i]; ++deg[j]; }
+    }
+  g.xadj.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) g.xadj[i + 1] = g.xadj[i] + deg[i];
+  g.adj.resize(g.xadj[n]);
+  std::vector<int64_t> fill(g.xadj.begin(), g.xadj.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      int64_t j = indices[e];
+      if (j != i) { g.adj[fill[i]++] = j; g.adj[fill[j]++] = i; }
+    }
+  // sort + unique each row, then compact
+  int64_t w = 0;
+  std::vector<int64_t> nx(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    auto b = g.adj.begin() + g.xadj[i], e = g.adj.begin() + g.xadj[i + 1];
+    std::sort(b, e);
+    auto last = std::unique(b, e);
+    nx[i] = w;
+    for (auto it = b; it != last; ++it) g.adj[w++] = *it;
+  }
+  nx[n] = w;
+  g.adj.resize(w);
+  g.xadj.swap(nx);
+  return g;
+}
+
+struct Builder {
+  const Graph& g;
+  int32_t leaf;
+  std::vector<int64_t> iperm;
+  int64_t next_pos = 0;
+  std::vector<std::vector<int64_t>> piv;      // per front (original ids)
+  std::vector<std::vector<int32_t>> kids;
+  // scratch
+  std::vector<int32_t> in_set;  // stamp of current set
+  int32_t stamp = 0;
+  std::vector<int32_t> dist;
+  std::vector<int64_t> queue;
+
+  Builder(const Graph& gr, int32_t lf)
+      : g(gr), leaf(lf), iperm(gr.n, -1), in_set(gr.n, 0), dist(gr.n, -1), queue(gr.n) {}
+
+  int32_t make_front(std::vector<int64_t> pivots, std::vector<int32_t> children) {
+    for (int64_t v : pivots) iperm[v] = next_pos++;
+    piv.push_back(std::move(pivots));
+    kids.push_back(std::move(children));
+    return (int32_t)piv.size() - 1;
+  }
+
+  // BFS restricted to vertices with in_set == s; fills order (queue) and
+  // level starts; returns number of visited vertices.
+  int64_t bfs(int64_t root, int32_t s, std::vector<int64_t>& lvl_start) {
+    lvl_start.clear();
+    int64_t head = 0, tail = 0;
+    queue[tail++] = root;
+    dist[root] = 0;
+    int32_t cur = -1;
+    while (head < tail) {
+      int64_t v = queue[head];
+      if (dist[v] != cur) { cur = dist[v]; lvl_start.push_back(head); }
+      ++head;
+      for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
+        int64_t u = g.adj[e];
+        if (in_set[u] == s && dist[u] < 0) { dist[u] = dist[v] + 1; queue[tail++] = u; }
+      }
+    }
+    lvl_start.push_back(tail);
+    return tail;
+  }
+
+  void reset_dist(const std::vector<int64_t>& V) {
+    for (int64_t v : V) dist[v] = -1;
+  }
+
+  int64_t deg_in(int64_t v, int32_t s) const {
+    int64_t d = 0;
+    for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) d += (in_set[g.adj[e]] == s);
+    return d;
+  }
+
+  struct Cut {
+    bool ok = false;
+    std::vector<int64_t> sep;
+    int64_t sep_size = 0;
+    double ratio = 1e30;
+  };
+
+  // Separator from the BFS level structure rooted at `root`.
+  Cut cut_from(int64_t root, int32_t s, const std::vector<int64_t>& V) {
+    Cut c;
+    std::vector<int64_t> ls;
+    reset_dist(V);
+    int64_t N = bfs(root, s, ls);
+    int64_t e = (int64_t)ls.size() - 2;  // eccentricity
+    if (e < 2) return c;
+    std::vector<int64_t> order(queue.begin(), queue.begin() + N);
+    int64_t best = -1;
+    for (int64_t l = 1; l < e; ++l) {
+      int64_t below = ls[l], size = ls[l + 1] - ls[l], above = N - ls[l + 1];
+      if (below == 0 || above == 0) continue;
+      double r = (double)std::max(below, above) / (double)std::min(below, above);
+      if (r > 2.0) continue;
+      if (best < 0 || size < c.sep_size || (size == c.sep_size && r < c.ratio)) {
+        best = l; c.sep_size = size; c.ratio = r;
+      }
+    }
+    if (best < 0) {  // fall back to the median level
+      for (int64_t l = 1; l < e; ++l)
+        if (ls[l + 1] > N / 2) { best = l; break; }
+      if (best < 0) best = e - 1;
+      int64_t below = ls[best], above = N - ls[best + 1];
+      c.ratio = (double)std::max(below, above) / (double)std::max<int64_t>(1, std::min(below, above));
+    }
+    // thin: a level-l vertex without a neighbour at level l+1 joins the lower side
+    for (int64_t k = ls[best]; k < ls[best + 1]; ++k) {
+      int64_t v = order[k];
+      bool up = false;
+      for (int64_t a = g.xadj[v]; a < g.xadj[v + 1] && !up; ++a) {
+        int64_t u = g.adj[a];
+        up = (in_set[u] == s && dist[u] == best + 1);
+      }
+      if (up) c.sep.push_back(v);
+    }
+    c.sep_size = (int64_t)c.sep.size();
+    c.ok = c.sep_size > 0;
+    return c;
+  }
+
+  // Connected components of the set stamped `s` (in V order).
+  std::vector<std::vector<int64_t>> components(const std::vector<int64_t>& V, int32_t s) {
+    std::vector<std::vector<int64_t>> parts;
+    reset_dist(V);
+    std::vector<int64_t> ls;
+    for (int64_t v : V) {
+      if (in_set[v] != s || dist[v] >= 0) continue;
+      int64_t N = bfs(v, s, ls);
+      std::vector<int64_t> part(queue.begin(), queue.begin() + N);
+      std::sort(part.begin(), part.end());
+      parts.push_back(std::move(part));
+    }
+    return parts;
+  }
+
+  int32_t nd(std::vector<int64_t> V) {
+    if ((int64_t)V.size() <= leaf) {
+      std::sort(V.begin(), V.end());
+      return make_front(std::move(V), {});
+    }
+    int32_t s = ++stamp;
+    for (int64_t v : V) in_set[v] = s;
+    // pseudo-peripheral pair
+    int64_t r = V[0];
+    int64_t ecc = -1, a = r, b = r;
+    std::vector<int64_t> ls;
+    for (int it = 0; it < 8; ++it) {
+      reset_dist(V);
+      int64_t N = bfs(r, s, ls);
+      int64_t e = (int64_t)ls.size() - 2;
+      if (e <= ecc) break;
+      ecc = e;
+      a = r;
+      int64_t bestv = -1, bestd = 0;
+      for (int64_t k = ls[e]; k < N; ++k) {
+        int64_t v = queue[k];
+        int64_t d = deg_in(v, s);
+        if (bestv < 0 || d < bestd) { bestv = v; bestd = d; }
+      }
+      b = bestv;
+      r = bestv;
+    }
+    Cut ca = cut_from(a, s, V);
+    Cut cb = cut_from(b, s, V);
+    Cut* c = nullptr;
+    if (ca.ok && cb.ok) {
+      bool a_bal = ca.ratio <= 2.0, b_bal = cb.ratio <= 2.0;
+      if (a_bal != b_bal) c = a_bal ? &ca : &cb;
+      else c = (ca.sep_size <= cb.sep_size) ? &ca : &cb;
+    } else if (ca.ok) {
+      c = &ca;
+    } else if (cb.ok) {
+      c = &cb;
+    }
+    if (c == nullptr || c->sep_size * 2 > (int64_t)V.size()) {
+      std::sort(V.begin(), V.end());
+      return make_front(std::move(V), {});
+    }
+    std::vector<int64_t> sep = std::move(c->sep);
+    int32_t s2 = ++stamp;
+    for (int64_t v : V) in_set[v] = s2;
+    for (int64_t v : sep) in_set[v] = 0;
+    auto parts = components(V, s2);
+    std::vector<int64_t>().swap(V);
+    std::vector<int32_t> children;
+    for (auto& part : parts) children.push_back(nd(std::move(part)));
+    std::sort(sep.begin(), sep.end());
+    return make_front(std::move(sep), std::move(children));
+  }
+};
+
+}  // namespace
+
+std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
+                    int32_t leaf_size, Symbolic& S) {
+  if (n < 0) return "negative dimension";
+  if (leaf_size < 1) leaf_size = 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] < indptr[i]) return "indptr not monotone";
+  for (int64_t e = 0; e < (n ? indptr[n] : 0); ++e)
+    if (indices[e] < 0 || indices[e] >= n) return "column index out of range";
+  S = Symbolic();
+  S.n = n;
+  S.nnz = n ? indptr[n] : 0;
+  S.leaf_size = leaf_size;
+  Graph g = build_graph(n, indptr, indices);
+  Builder B(g, leaf_size);
+
+  // connected components of the whole graph -> roots
+  {
+    int32_t s = ++B.stamp;
+    std::vector<int64_t> all(n);
+    std::iota(all.begin(), all.end(), 0);
+    for (int64_t v : all) B.in_set[v] = s;
+    auto comps = B.components(all, s);
+    for (auto& c : comps) B.nd(std::move(c));
+  }
+  const int32_t nf = (int32_t)B.piv.size();
+  S.perm.assign(n, -1);
+  S.iperm = B.iperm;
+  for (int64_t v = 0; v < n; ++v) S.perm[S.iperm[v]] = v;
+
+  S.fronts.resize(nf);
+  S.child_ptr.assign(nf + 1, 0);
+  for (int32_t f = 0; f < nf; ++f) S.child_ptr[f + 1] = S.child_ptr[f] + (int32_t)B.kids[f].size();
+  S.child_list.resize(S.child_ptr[nf]);
+  for (int32_t f = 0; f < nf; ++f) {
+    std::copy(B.kids[f].begin(), B.kids[f].end(), S.child_list.begin() + S.child_ptr[f]);
+    Front& F = S.fronts[f];
+    F.p = (int32_t)B.piv[f].size();
+    F.first = F.p ? S.iperm[B.piv[f][0]] : 0;
+    F.parent = -1;
+  }
+  for (int32_t f = 0; f < nf; ++f)
+    for (int32_t k = S.child_ptr[f]; k < S.child_ptr[f + 1]; ++k) S.fronts[S.child_list[k]].parent = f;
+
+  // update-row structure, bottom-up (fronts are already in postorder)
+  std::vector<int64_t> mark(n, -1);
+  std::vector<std::vector<int64_t>> U(nf);
+  for (int32_t f = 0; f < nf; ++f) {
+    Front& F = S.fronts[f];
+    const int64_t last = F.first + F.p - 1;
+    std::vector<int64_t>& u = U[f];
+    for (int64_t v : B.piv[f])
+      for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
+        int64_t r = S.iperm[g.adj[e]];
+        if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
+      }
+    for (int32_t k = S.child_ptr[f]; k < S.child_ptr[f + 1]; ++k)
+      for (int64_t r : U[S.child_list[k]])
+        if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
+    std::sort(u.begin(), u.end());
+    F.q = (int32_t)u.size();
+  }
+  // depth (parents have larger index than children)
+  for (int32_t f = nf - 1; f >= 0; --f) {
+    Front& F = S.fronts[f];
+    F.depth = F.parent < 0 ? 0 : S.fronts[F.parent].depth + 1;
+    S.max_depth = std::max(S.max_depth, F.depth);
+  }
+  S.levels.assign(S.max_depth + 1, {});
+  for (int32_t f = 0; f < nf; ++f) S.levels[S.fronts[f].depth].push_back(f);
+
+  // rows, relind, storage offsets, stats
+  int64_t rows_total = 0;
+  for (int32_t f = 0; f < nf; ++f) rows_total += S.fronts[f].q;
+  S.urows.resize(rows_total);
+  S.relind.resize(rows_total);
+  int64_t ro = 0, panel = 0;
+  for (int32_t f = 0; f < nf; ++f) {
+    Front& F = S.fronts[f];
+    F.rows_begin = ro;
+    F.relind_begin = ro;
+    std::copy(U[f].begin(), U[f].end(), S.urows.begin() + ro);
+    ro += F.q;
+    F.panel_off = panel;
+    panel += (int64_t)F.m() * F.p;
+    S.max_front = std::max(S.max_front, F.m());
+    S.factor_nnz += (int64_t)F.p * (F.p + 1) / 2 + (int64_t)F.q * F.p;
+    for (int64_t k = 0; k < F.p; ++k) {
+      double r = (double)(F.m() - k - 1);
+      S.flops += 8.0 * r * (r + 1.0) / 2.0 + 8.0 * r;
+    }
+  }
+  S.panel_total = panel;
+  for (int32_t f = 0; f < nf; ++f) {
+    const Front& F = S.fronts[f];
+    if (F.parent < 0) continue;
+    const Front& P = S.fronts[F.parent];
+    const int64_t plast = P.first + P.p - 1;
+    const int64_t* prow = S.urows.data() + P.rows_begin;
+    for (int32_t a = 0; a < F.q; ++a) {
+      int64_t r = S.urows[F.rows_begin + a];
+      int32_t loc;
+      if (r <= plast) {
+        if (r < P.first) return "internal: update row below parent pivots";
+        loc = (int32_t)(r - P.first);
+      } else {
+        const int64_t* it = std::lower_bound(prow, prow + P.q, r);
+        if (it == prow + P.q || *it != r) return "internal: update row missing in parent";
+        loc = P.p + (int32_t)(it - prow);
+      }
+      S.relind[F.relind_begin + a] = loc;
+    }
+  }
+  for (int32_t d = 0; d <= S.max_depth; ++d) {
+    int64_t uo = 0, ru = 0;
+    for (int32_t f : S.levels[d]) {
+      Front& F = S.fronts[f];
+      F.upd_off = uo;
+      F.rupd_off = ru;
+      uo += (int64_t)F.q * F.q;
+      ru += F.q;
+    }
+    S.upd_size[d & 1] = std::max(S.upd_size[d & 1], uo);
+    S.rupd_size[d & 1] = std::max(S.rupd_size[d & 1], ru);
+  }
+
+  // original entries: CSR entry (r, c) with iperm[r] >= iperm[c] lands in the
+  // front owning pivot iperm[c] at local (row(iperm[r]), iperm[c]-first)
+  std::vector<int32_t> front_of(n, -1);
+  for (int32_t f = 0; f < nf; ++f)
+    for (int64_t k = 0; k < S.fronts[f].p; ++k) front_of[S.fronts[f].first + k] = f;
+  std::vector<int64_t> cnt(nf + 1, 0);
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+      int64_t i = S.iperm[r], j = S.iperm[indices[e]];
+      if (i >= j) ++cnt[front_of[j] + 1];
+    }
+  for (int32_t f = 0; f < nf; ++f) cnt[f + 1] += cnt[f];
+  S.orig_src.resize(cnt[nf]);
+  S.orig_dst.resize(cnt[nf]);
+  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+      int64_t i = S.iperm[r], j = S.iperm[indices[e]];
+      if (i < j) continue;
+      int32_t f = front_of[j];
+      const Front& F = S.fronts[f];
+      int32_t ri;
+      if (i < F.first + F.p) {
+        ri = (int32_t)(i - F.first);
+      } else {
+        const int64_t* prow = S.urows.data() + F.rows_begin;
+        const int64_t* it = std::lower_bound(prow, prow + F.q, i);
+        if (it == prow + F.q || *it != i) return "internal: entry outside front rows";
+        ri = F.p + (int32_t)(it - prow);
+      }
+      int64_t dst = (int64_t)ri + (j - F.first) * (int64_t)F.m();
+      if (dst > INT32_MAX) return "front too large for 32-bit local offsets";
+      S.orig_src[pos[f]] = e;
+      S.orig_dst[pos[f]] = (int32_t)dst;
+      ++pos[f];
+    }
+  for (int32_t f = 0; f < nf; ++f) {
+    S.fronts[f].orig_begin = cnt[f];
+    S.fronts[f].orig_end = cnt[f + 1];
+    // deterministic, write-coalescing order inside the front
+    std::vector<std::pair<int32_t, int64_t>> tmp;
+    for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) tmp.emplace_back(S.orig_dst[k], S.orig_src[k]);
+    std::sort(tmp.begin(), tmp.end());
+    for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) {
+      S.orig_dst[k] = tmp[k - cnt[f]].first;
+      S.orig_src[k] = tmp[k - cnt[f]].second;
+    }
+  }
+  return "";
+}
+
+}  // namespace kh

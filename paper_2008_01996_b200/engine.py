@@ -1,0 +1,276 @@
+"""GPU orchestration of the Fast-Diagonalization solve (host control, device data).
+
+One `FDEngine` owns everything a solve needs on the device:
+
+1. the host-side modal plan (`modal_plan`): the reference's
+   G = F A_t^-1 conj(U) S^-1 conj(Vh) (solvers.py:368-372) and
+   U = Z Vh^T S U^T (solvers.py:397-400) folded into one real N_t x 2N_k
+   matrix per direction, restricted to one representative per conjugate
+   eigenpair (the partner's solve is the complex conjugate, so the back
+   transform 2 Re(z x^T) is real by construction);
+2. the symbolic analysis of M_x + A_x (one per engine, solvers.py:379) and a
+   numeric plan holding the LDL^T factors of every shift M_x + lambda_k A_x;
+3. device buffers for F, G, Z, U and the residual.
+
+`solve(F)` runs transform-in GEMM -> batched factor/solve -> transform-out
+GEMM, then iterative refinement on the space-time residual (not in the
+reference; needed because FD's accuracy is limited by kappa_2(X_t), see
+DESIGN.md). All kernels are in libkhb200.so; torch only allocates memory.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native, sparse_direct
+from .dense import spd_solve
+from .errors import DimensionMismatch, ImaginaryResidueTooLarge
+
+FD_IMAG_TOL = 1e-6  # solvers.py:400
+
+
+@dataclass
+class ModalPlan:
+    n_t: int
+    lam: np.ndarray        # (N_k,) complex; conjugate-pair representatives first, then singles
+    weight: np.ndarray     # 2.0 for pair representatives, 1.0 for singles
+    n_pairs: int
+    n_single: int
+    w_in: np.ndarray       # (N_t, 2 N_k): [Re W_in[:, modes] | Im W_in[:, modes]]
+    w_out: np.ndarray      # (2 N_k, N_t): [w Re W_out[modes, :] ; -w Im W_out[modes, :]]
+    w_out_im: np.ndarray   # (2 n_single, N_t): imaginary part of the single modes' back transform
+    kron_b: np.ndarray     # (N_t, 2 N_t): [A_t^T | M_t^T] for K u = vec(M_x U A_t^T + A_x U M_t^T)
+
+    @property
+    def n_k(self):
+        return len(self.lam)
+
+
+def conjugate_pairs(D, X):
+    """Split eigen-indices into (+Im representative of exact conjugate pairs, singles).
+
+    dggev returns a pair adjacent with +Im first and eig_pencil builds exactly
+    conjugate vectors (reference dense.py:210-220).
+    """
+    reps, singles = [], []
+    n = len(D)
+    j = 0
+    while j < n:
+        if (D[j].imag > 0.0 and j + 1 < n and D[j + 1] == np.conj(D[j])
+                and np.array_equal(X[:, j + 1], np.conj(X[:, j]))):
+            reps.append(j)
+            j += 2
+        else:
+            singles.append(j)
+            j += 1
+    return np.array(reps, dtype=np.int64), np.array(singles, dtype=np.int64)
+
+
+def modal_plan(temporal, pencil):
+    form = pencil.form
+    n_t = temporal.A.shape[0]
+    reps, singles = conjugate_pairs(form.D, form.X)
+    modes = np.concatenate([reps, singles])
+    weight = np.concatenate([np.full(len(reps), 2.0), np.ones(len(singles))])
+    # W_in = A_t^-1 conj(U) Sigma^-1 conj(Vh)  (same factor order as solvers.py:370-371)
+    w_in_c = (spd_solve(pencil.chol_A, np.conj(form.U)) / form.sigma[None, :]) @ np.conj(form.Vh)
+    # W_out = conj(V) Sigma U^T = Vh^T Sigma U^T (solvers.py:399)
+    w_out_c = (form.Vh.T * form.sigma[None, :]) @ form.U.T
+    wi = w_in_c[:, modes]
+    wo = w_out_c[modes, :]
+    w_in = np.ascontiguousarray(np.hstack([wi.real, wi.imag]))
+    w_out = np.ascontiguousarray(np.vstack([weight[:, None] * wo.real, -weight[:, None] * wo.imag]))
+    ws = w_out_c[singles, :]
+    w_out_im = np.ascontiguousarray(np.vstack([ws.imag, ws.real]))
+    kron_b = np.ascontiguousarray(np.hstack([temporal.A.T, temporal.M.T]))
+    return ModalPlan(n_t=n_t, lam=form.D[modes].astype(np.complex128), weight=weight,
+                     n_pairs=len(reps), n_single=len(singles), w_in=w_in, w_out=w_out,
+                     w_out_im=w_out_im, kron_b=kron_b)
+
+
+def _fortran(t_np, device):
+    """Host (rows x cols) array -> device column-major buffer (as a torch tensor
+    of shape (cols, rows), i.e. the transpose view, contiguous)."""
+    import torch
+
+    a = np.asarray(t_np, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(a.T)).to(device)
+
+
+class FDEngine:
+    """Device-resident FD solver for one (M_x, A_x, temporal pencil) triple."""
+
+    def __init__(self, M_x, A_x, modal, device=None, keep_factors=None, max_batch=None,
+                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.7, symbolic=None):
+        import torch
+
+        _native.require_cuda()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        M = sp.csr_matrix(M_x)
+        A = sp.csr_matrix(A_x)
+        if M.shape != A.shape or M.shape[0] != M.shape[1]:
+            raise DimensionMismatch("spatial matrices must be square and of equal shape")
+        self.n = M.shape[0]
+        self.modal = modal
+        self.n_t = modal.n_t
+        self.n_k = modal.n_k
+        self.sym = symbolic if symbolic is not None else sparse_direct.analyze((M + A).tocsr(), leaf_size)
+        mv = self.sym.align_values(M)
+        av = self.sym.align_values(A)
+
+        # memory plan: keep every shift's factors when they fit
+        with torch.cuda.device(self.device):
+            free, _ = torch.cuda.mem_get_info()
+        work = 8 * self.n * (2 * self.n_k * 2 + 2 * self.n_t * 3) + 8 * self.n_t * 8 * self.n_t
+        budget = mem_fraction * free - work
+        nk = max(self.n_k, 1)
+        batch = min(nk, max_batch or nk)
+        if keep_factors is None:
+            keep_factors = sparse_direct.plan_bytes(self.sym, batch, nk) <= budget
+        if keep_factors:
+            slots = nk
+        else:
+            while batch > 1 and sparse_direct.plan_bytes(self.sym, batch, batch) > budget:
+                batch = (batch + 1) // 2
+            slots = batch
+        self.keep_factors = bool(keep_factors)
+        self.batch = int(batch)
+        self.plan = sparse_direct._Plan(self.sym, mv, av, self.batch, slots, self.device.index)
+        self.factored = False
+
+        dev = self.device
+        f64 = torch.float64
+        self.w_in = _fortran(modal.w_in, dev)        # (2N_k, N_t) storage of N_t x 2N_k
+        self.w_out = _fortran(modal.w_out, dev)      # (N_t, 2N_k) storage of 2N_k x N_t
+        self.w_out_im = _fortran(modal.w_out_im, dev) if modal.n_single else None
+        self.kron_b = _fortran(modal.kron_b, dev)    # (2N_t, N_t) storage of N_t x 2N_t
+        n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
+        self.G = torch.empty((nk2, n), dtype=f64, device=dev)   # column-major n x 2N_k
+        self.Z = torch.empty((nk2, n), dtype=f64, device=dev)
+        self.Y = torch.empty((2 * nt, n), dtype=f64, device=dev)
+        self.R = torch.empty((nt, n), dtype=f64, device=dev)
+        self.norms = torch.zeros(4, dtype=f64, device=dev)
+        self.lam = np.ascontiguousarray(modal.lam)
+        self.gpu_launches = 0
+
+    # ---- primitives -----------------------------------------------------------
+    def _stream(self):
+        return _native.stream_handle()
+
+    def _gemm(self, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc):
+        _native.call("kh_dgemm", m, n, k, float(alpha), A, lda, B, ldb, float(beta), C, ldc, self._stream())
+        self.gpu_launches += 1
+
+    def factor(self, events=None):
+        """Factor M_x + lambda_k A_x for every retained shift (no-op otherwise).
+
+        `events`: optional list that receives a (start, end) CUDA-event pair
+        bracketing the factorization launches (for the roofline)."""
+        if not self.keep_factors:
+            return
+        import torch
+
+        st = self._stream()
+        if events is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        for s0 in range(0, self.n_k, self.batch):
+            s1 = min(self.n_k, s0 + self.batch)
+            self.plan.factor(s0, self.lam[s0:s1], st)
+            self.gpu_launches += self.sym.stats["depth"] + 4
+        if events is not None:
+            e1.record()
+            events.append((e0, e1))
+        self.plan.pivot_check(0, self.n_k, st)
+        self.factored = True
+
+    def _spatial(self):
+        """Z[:, k] = (M_x + lambda_k A_x)^-1 G[:, k] for all modes."""
+        st = self._stream()
+        n, nk = self.n, self.n_k
+        g, z = self.G.data_ptr(), self.Z.data_ptr()
+        depth = self.sym.stats["depth"] + 1
+        for s0 in range(0, nk, self.batch):
+            s1 = min(nk, s0 + self.batch)
+            if self.keep_factors:
+                slot = s0
+            else:
+                self.plan.factor(0, self.lam[s0:s1], st)
+                self.plan.pivot_check(0, s1 - s0, st)
+                self.gpu_launches += depth + 3
+                slot = 0
+            self.plan.solve(slot, s1 - s0, g + 8 * s0 * n, g + 8 * (nk + s0) * n, n,
+                            z + 8 * s0 * n, z + 8 * (nk + s0) * n, n, st)
+            self.gpu_launches += 2 * depth + 2
+
+    def fd_apply(self, F, U, accumulate=False, imag_norm=False):
+        """U (+)= FD(F): F and U are device column-major n x N_t buffers (torch
+        tensors of shape (N_t, n))."""
+        n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
+        self._gemm(n, nk2, nt, 1.0, F.data_ptr(), n, self.w_in.data_ptr(), nt, 0.0, self.G.data_ptr(), n)
+        self._spatial()
+        self._gemm(n, nt, nk2, 1.0, self.Z.data_ptr(), n, self.w_out.data_ptr(), nk2,
+                   1.0 if accumulate else 0.0, U.data_ptr(), n)
+        if imag_norm and self.modal.n_single:
+            ns, nk = self.modal.n_single, self.n_k
+            z = self.Z.data_ptr()
+            zr = z + 8 * (self.modal.n_pairs) * n
+            zi = z + 8 * (nk + self.modal.n_pairs) * n
+            wim = self.w_out_im.data_ptr()
+            self._gemm(n, nt, ns, 1.0, zr, n, wim, 2 * ns, 0.0, self.R.data_ptr(), n)
+            self._gemm(n, nt, ns, 1.0, zi, n, wim + 8 * ns, 2 * ns, 1.0, self.R.data_ptr(), n)
+            _native.call("kh_sumsq", self.R.data_ptr(), n * nt, self.norms.data_ptr() + 16, self._stream())
+            _native.call("kh_sumsq", U.data_ptr(), n * nt, self.norms.data_ptr() + 24, self._stream())
+            self.gpu_launches += 4
+
+    def residual(self, U, F, keep_r=True):
+        """Device: R = F - K U; returns (||R||^2, ||F||^2) as a device tensor slice."""
+        n, nt = self.n, self.n_t
+        self._gemm(n, 2 * nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt, 0.0, self.Y.data_ptr(), n)
+        self.plan.residual(nt, self.Y.data_ptr(), n, F.data_ptr(), n, self.R.data_ptr() if keep_r else None, n,
+                           self.norms.data_ptr(), self._stream())
+        self.gpu_launches += 2
+        return self.norms[:2]
+
+    def solve(self, F, U=None, refine=3, tol=1e-13, check_imag=True):
+        """Full FD solve of K u = f on the device with iterative refinement.
+
+        Returns (U, info); U is a device tensor (N_t, n) = column-major n x N_t.
+        """
+        import torch
+
+        if U is None:
+            U = torch.empty((self.n_t, self.n), dtype=torch.float64, device=self.device)
+        if not self.factored and self.keep_factors:
+            self.factor()
+        self.fd_apply(F, U, accumulate=False, imag_norm=check_imag)
+        info = {"imag_residue": 0.0, "residuals": [], "refine_steps": 0}
+        if check_imag and self.modal.n_single:
+            im2, u2 = self.norms[2:4].tolist()
+            info["imag_residue"] = float(np.sqrt(im2) / np.sqrt(u2)) if u2 > 0 else 0.0
+        rel = self._rel(self.residual(U, F))
+        info["residuals"].append(rel)
+        steps = 0
+        while rel > tol and steps < refine:
+            self.fd_apply(self.R, U, accumulate=True)
+            steps += 1
+            new = self._rel(self.residual(U, F))
+            info["residuals"].append(new)
+            if not new < rel:  # stagnation at the rounding floor
+                rel = new
+                break
+            rel = new
+        info["refine_steps"] = steps
+        info["residual"] = rel
+        return U, info
+
+    @staticmethod
+    def _rel(norms):
+        r2, f2 = norms.tolist()
+        return float(np.sqrt(r2) / np.sqrt(f2)) if f2 > 0 else float(np.sqrt(r2))
+
+
+def check_imag(info, tol=FD_IMAG_TOL):
+    if info["imag_residue"] > tol:
+        raise ImaginaryResidueTooLarge(f"imaginary residue {info['imag_residue']:.3e} above {tol:.1e}")

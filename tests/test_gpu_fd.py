@@ -1,0 +1,142 @@
+"""GPU FD solve vs the reference (golden fixtures) and the CPU oracle.
+
+Bars: against the backward-stable reference BS-complex solution <= 1e-10
+relative l2 with space-time residual <= 1e-11 (after refinement); against the
+reference FD <= max(1e-10, the reference FD's own distance to BS) -- the
+reference FD is itself only kappa_2(X_t)*eps accurate (SURVEY.md finding 3).
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel_diff
+from paper_2008_01996_b200 import solvers
+from paper_2008_01996_b200.errors import DefectivePencil
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["lshape0", "odd", "random_11", "random_12", "random_13", "c1"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_fd_matches_reference(cuda_ok, name):
+    system, ref = load_golden(name)
+    sol, rep = solvers.solve_fd(system)
+    u = sol.coefficients
+    assert rel_diff(u, ref["bs"]) < 1e-10
+    gap = rel_diff(ref["fd"], ref["bs"])
+    assert rel_diff(u, ref["fd"]) < max(1e-10, 2.0 * gap)
+    assert rep.residual < 1e-11
+    assert rep.analyze_calls == 1
+    assert rep.kappa2 == pytest.approx(float(ref["fd_kappa2"]), rel=1e-10)
+    assert rep.min_re_lambda == pytest.approx(float(ref["fd_min_re_lambda"]), rel=1e-10)
+    if "dense" in ref:
+        assert rel_diff(u, ref["dense"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_plain_fd_without_refinement(cuda_ok, name):
+    """refine=0 is the reference's plain FD: same accuracy class as the CPU FD."""
+    system, ref = load_golden(name)
+    sol, rep = solvers.solve_fd(system, refine=0)
+    ref_gap = rel_diff(ref["fd"], ref["bs"])
+    assert rel_diff(sol.coefficients, ref["bs"]) < max(1e-10, 10.0 * ref_gap)
+    assert rep.refine_steps == 0
+    assert rep.fd_residual == pytest.approx(rep.residual)
+
+
+@pytest.mark.parametrize("name", ["lshape0", "c1"])
+def test_residual_matches_oracle(cuda_ok, name):
+    from oracle import fd_oracle as orc
+
+    system, ref = load_golden(name)
+    for key in ("fd", "bs"):
+        got = solvers.residual(system, ref[key])
+        want = orc.residual(*orc.system_arrays(system), ref[key])
+        assert got == pytest.approx(want, rel=1e-6, abs=1e-16)
+
+
+def test_reported_residual_is_reproducible(cuda_ok):
+    system, _ = load_golden("lshape0")
+    sol, rep = solvers.solve_fd(system)
+    assert solvers.residual(system, sol.coefficients) == pytest.approx(rep.residual, rel=1e-6, abs=1e-16)
+
+
+def test_fd_reports_spectral_stats(cuda_ok):
+    system, _ = load_golden("lshape0")
+    _, rep = solvers.solve_fd(system)
+    assert rep.kappa2 == pytest.approx(9.576, rel=1e-3)   # reference test_solvers.py:204-208
+    assert rep.sigma_min > 0.0 and rep.min_re_lambda > 0.0
+
+
+def test_fd_threads_agree(cuda_ok):
+    system, _ = load_golden("lshape0")
+    a, _ = solvers.solve_fd(system, threads=1)
+    b, r = solvers.solve_fd(system, threads=3)
+    assert rel_diff(a.coefficients, b.coefficients) < 1e-13
+    assert r.threads == 3
+
+
+def test_fd_is_deterministic(cuda_ok):
+    system, _ = load_golden("c1")
+    a, _ = solvers.solve_fd(system)
+    b, _ = solvers.solve_fd(system)
+    assert np.array_equal(a.coefficients, b.coefficients)
+
+
+def test_batching_and_refactoring_agree(cuda_ok):
+    system, _ = load_golden("c1")
+    a, _ = solvers.solve_fd(system)
+    b, _ = solvers.solve_fd(system, max_batch=5, keep_factors=False)
+    assert rel_diff(a.coefficients, b.coefficients) < 1e-13
+
+
+def test_scalar_reduction(cuda_ok):
+    system, _ = load_golden("lshape0")
+    m, a = 0.7, 2.3
+    temp = system.temporal
+    rng = np.random.default_rng(8)
+    rhs = rng.standard_normal(temp.A.shape[0])
+    from conftest import _Spatial
+    import scipy.sparse as sp
+
+    one = solvers.SpaceTimeSystem(temporal=temp, spatial=_Spatial(sp.csr_matrix([[m]]), sp.csr_matrix([[a]])),
+                                  rhs=rhs)
+    expect = np.linalg.solve(m * temp.A + a * temp.M, rhs)
+    sol, _ = solvers.solve_fd(one)
+    assert rel_diff(sol.coefficients, expect) < 1e-10
+
+
+def test_fd_falls_back_to_bs_complex(cuda_ok, monkeypatch):
+    system, ref = load_golden("lshape0")
+
+    def broken(system, pencil=None, threads=1):
+        raise DefectivePencil("forced")
+
+    monkeypatch.setattr(solvers, "solve_fd", broken)
+    sol, report = solvers.solve(system, "fd")
+    assert report.variant == "bs-complex"
+    assert "DefectivePencil" in report.fallback
+    assert rel_diff(sol.coefficients, ref["dense"]) < 1e-10
+
+
+def test_no_fallback_propagates(cuda_ok, monkeypatch):
+    system, _ = load_golden("lshape0")
+
+    def broken(system, pencil=None, threads=1):
+        raise DefectivePencil("forced")
+
+    monkeypatch.setattr(solvers, "solve_fd", broken)
+    with pytest.raises(DefectivePencil):
+        solvers.solve(system, "fd", fallback=False)
+
+
+@pytest.mark.parametrize("name", ["lshape0", "odd", "random_11", "c1"])
+def test_bs_complex_matches_reference(cuda_ok, name):
+    system, ref = load_golden(name)
+    sol, rep = solvers.solve_bs_complex(system)
+    assert rel_diff(sol.coefficients, ref["bs"]) < 1e-11
+    assert rep.residual < 1e-12
+    assert rep.analyze_calls == 1

@@ -1,0 +1,177 @@
+"""GPU parity of the native kernels through the C-ABI: DMMA GEMM and the
+batched multifrontal LDL^T (ports of the reference's sparse_direct contracts,
+pkg/tests/test_sparse_direct.py)."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from paper_2008_01996_b200 import _native
+from paper_2008_01996_b200 import sparse_direct as sd
+from paper_2008_01996_b200.errors import DimensionMismatch, SingularMatrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (129, 65, 17), (1000, 256, 256), (4097, 130, 33)])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_dgemm_matches_numpy(cuda_ok, m, n, k, beta):
+    import torch
+
+    rng = np.random.default_rng(m + n + k)
+    A = rng.standard_normal((m, k))
+    B = rng.standard_normal((k, n))
+    C0 = rng.standard_normal((m, n))
+    dA, dB, dC = _dev(A.T), _dev(B.T), _dev(C0.T)  # column-major storage
+    _native.call("kh_dgemm", m, n, k, 1.5, dA.data_ptr(), m, dB.data_ptr(), k, beta, dC.data_ptr(), m,
+                 _native.stream_handle())
+    got = dC.cpu().numpy().T
+    want = 1.5 * A @ B + beta * C0
+    assert np.max(np.abs(got - want)) <= 1e-13 * max(1.0, np.max(np.abs(want))) * np.sqrt(k)
+    torch.cuda.synchronize()
+
+
+def test_dgemm_strided_lda(cuda_ok):
+    rng = np.random.default_rng(5)
+    m, n, k, lda = 301, 40, 57, 333
+    A = rng.standard_normal((lda, k))
+    B = rng.standard_normal((k, n))
+    dA, dB = _dev(A.T), _dev(B.T)
+    import torch
+
+    dC = torch.zeros((n, m), dtype=torch.float64, device="cuda")
+    _native.call("kh_dgemm", m, n, k, 1.0, dA.data_ptr(), lda, dB.data_ptr(), k, 0.0, dC.data_ptr(), m,
+                 _native.stream_handle())
+    assert np.allclose(dC.cpu().numpy().T, A[:m] @ B, rtol=1e-13, atol=1e-12)
+
+
+def laplacian_1d(n):
+    return sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(n, n), format="csr")
+
+
+def grid_5pt(k):
+    I = sp.identity(k, format="csr")
+    T = laplacian_1d(k)
+    return (sp.kron(I, T) + sp.kron(T, I)).tocsr()
+
+
+def test_identity(cuda_ok):
+    sym = sd.analyze(sp.identity(4, format="csr"))
+    num = sd.factorize(sym, sp.identity(4, format="csr"))
+    assert np.allclose(num.solve(np.arange(4.0)), np.arange(4.0))
+
+
+def test_laplacian_eigenfunction(cuda_ok):
+    n = 1023
+    h = 1.0 / (n + 1)
+    x = np.linspace(h, 1.0 - h, n)
+    sol = sd.factor_solve(laplacian_1d(n) / h**2, np.sin(np.pi * x))
+    assert np.max(np.abs(sol - np.sin(np.pi * x) / np.pi**2)) < 5 * h**2
+
+
+def test_multi_rhs_matches_columns(cuda_ok):
+    rng = np.random.default_rng(4)
+    A = grid_5pt(8) + sp.identity(64)
+    B = rng.standard_normal((64, 5))
+    num = sd.factorize(sd.analyze(A), A)
+    X = num.solve(B)
+    for j in range(5):
+        assert np.allclose(X[:, j], num.solve(B[:, j]), atol=1e-14)
+
+
+def test_pattern_reuse_across_shifts(cuda_ok):
+    rng = np.random.default_rng(9)
+    M = grid_5pt(6)
+    A = sp.identity(36, format="csr")
+    sym = sd.analyze((M + A).tocsr())
+    for alpha in (0.5, 2.0, 17.0):
+        K = (M + alpha * A).tocsr()
+        b = rng.standard_normal(36)
+        x = sd.factorize(sym, K).solve(b)
+        assert np.linalg.norm(K @ x - b) / np.linalg.norm(b) < 1e-12
+
+
+def test_complex_symmetric_matches_real_block_oracle(cuda_ok):
+    rng = np.random.default_rng(12)
+    n = 30
+    M = (laplacian_1d(n) + sp.identity(n)).tocsr()
+    A = laplacian_1d(n)
+    lam = 0.7 + 1.9j
+    K = (M + lam * A).astype(complex).tocsr()
+    f = rng.standard_normal(n)
+    z = sd.factor_solve(K, f.astype(complex))
+    Mr = (M + lam.real * A).toarray()
+    Ai = (lam.imag * A).toarray()
+    xy = np.linalg.solve(np.block([[Mr, -Ai], [-Ai, -Mr]]), np.concatenate([f, np.zeros(n)]))
+    oracle = xy[:n] + 1j * xy[n:]
+    assert np.linalg.norm(z - oracle) / np.linalg.norm(oracle) < 1e-10
+
+
+def test_singular_matrix_detected(cuda_ok):
+    bad = sp.csr_matrix(np.array([[1.0, 1.0], [1.0, 1.0]]))
+    with pytest.raises(SingularMatrix):
+        sd.factorize(sd.analyze(bad), bad)
+
+
+def test_deterministic_factorization(cuda_ok):
+    A = grid_5pt(10) + sp.identity(100)
+    sym = sd.analyze(A)
+    b = np.random.default_rng(1).standard_normal(100)
+    x1 = sd.factorize(sym, A).solve(b)
+    x2 = sd.factorize(sym, A).solve(b)
+    assert np.array_equal(x1, x2)
+
+
+def test_refinement_keeps_residual_small(cuda_ok):
+    rng = np.random.default_rng(30)
+    A = grid_5pt(12) * 1e6 + sp.identity(144)
+    b = rng.standard_normal(144)
+    x = sd.factorize(sd.analyze(A), A).solve(b, refine=True)
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-12
+
+
+def test_rhs_dimension_check(cuda_ok):
+    num = sd.factorize(sd.analyze(sp.identity(4, format="csr")), sp.identity(4, format="csr"))
+    with pytest.raises(DimensionMismatch):
+        num.solve(np.ones(5))
+
+
+@pytest.mark.parametrize("mesh", [("square", 40), ("lshape", 4), ("square", 128)])
+def test_batched_shifts_match_superlu(cuda_ok, mesh):
+    """Many complex shifts M + lam_k A in one batched factorization vs SuperLU."""
+    import torch
+
+    from paper_2008_01996_b200 import fem, problems
+
+    ops = fem.assemble_p1(problems.spatial_mesh(*mesh))
+    M, A = ops.M_II.tocsr(), ops.A_II.tocsr()
+    n = M.shape[0]
+    rng = np.random.default_rng(3)
+    lam = rng.uniform(0.01, 3.0, 9) + 1j * rng.uniform(-40.0, 40.0, 9)
+    sym = sd.analyze((M + A).tocsr())
+    plan = sd._Plan(sym, sym.align_values(M), sym.align_values(A), 4, 9, torch.cuda.current_device())
+    st = _native.stream_handle()
+    for s0 in range(0, 9, 4):
+        plan.factor(s0, lam[s0:s0 + 4], st)
+    plan.pivot_check(0, 9, st)
+    B = rng.standard_normal((n, 9)) + 1j * rng.standard_normal((n, 9))
+    bre, bim = _dev(B.real.T), _dev(B.imag.T)
+    xre = torch.empty_like(bre)
+    xim = torch.empty_like(bim)
+    for s0 in range(0, 9, 4):
+        c = min(4, 9 - s0)
+        plan.solve(s0, c, bre.data_ptr() + 8 * s0 * n, bim.data_ptr() + 8 * s0 * n, n,
+                   xre.data_ptr() + 8 * s0 * n, xim.data_ptr() + 8 * s0 * n, n, st)
+    X = xre.cpu().numpy().T + 1j * xim.cpu().numpy().T
+    for k in range(9):
+        K = (M + lam[k] * A).astype(complex).tocsc()
+        ref = spla.spsolve(K, B[:, k])
+        assert np.linalg.norm(X[:, k] - ref) / np.linalg.norm(ref) < 1e-11, k
+        assert np.linalg.norm(K @ X[:, k] - B[:, k]) / np.linalg.norm(B[:, k]) < 1e-12
