@@ -21,13 +21,13 @@ DESIGN.md). All kernels are in libkhb200.so; torch only allocates memory.
 from dataclasses import dataclass
 
 import numpy as np
+import scipy.linalg as sla
 import scipy.sparse as sp
 
 from . import _native, sparse_direct
 from .dense import spd_solve
-from .errors import DimensionMismatch, ImaginaryResidueTooLarge
+from .errors import DefectivePencil, DimensionMismatch
 
-FD_IMAG_TOL = 1e-6  # solvers.py:400
 
 
 @dataclass
@@ -39,7 +39,6 @@ class ModalPlan:
     n_single: int
     w_in: np.ndarray       # (N_t, 2 N_k): [Re W_in[:, modes] | Im W_in[:, modes]]
     w_out: np.ndarray      # (2 N_k, N_t): [w Re W_out[modes, :] ; -w Im W_out[modes, :]]
-    w_out_im: np.ndarray   # (2 n_single, N_t): imaginary part of the single modes' back transform
     kron_b: np.ndarray     # (N_t, 2 N_t): [A_t^T | M_t^T] for K u = vec(M_x U A_t^T + A_x U M_t^T)
 
     @property
@@ -48,16 +47,18 @@ class ModalPlan:
 
 
 def conjugate_pairs(D, X):
-    """Split eigen-indices into (+Im representative of exact conjugate pairs, singles).
+    """Split eigen-indices into (+Im representative of conjugate pairs, singles).
 
-    dggev returns a pair adjacent with +Im first and eig_pencil builds exactly
-    conjugate vectors (reference dense.py:210-220).
+    dggev returns a complex pair adjacent with +Im first, and eig_pencil builds
+    the two eigenvectors as exact conjugates (reference dense.py:210-220);
+    the eigenvalues themselves may differ from exact conjugates in the last
+    bit (alpha/beta rounding), so pairs are identified by the vectors.
     """
     reps, singles = [], []
     n = len(D)
     j = 0
     while j < n:
-        if (D[j].imag > 0.0 and j + 1 < n and D[j + 1] == np.conj(D[j])
+        if (D[j].imag > 0.0 and j + 1 < n and D[j + 1].imag < 0.0
                 and np.array_equal(X[:, j + 1], np.conj(X[:, j]))):
             reps.append(j)
             j += 2
@@ -68,25 +69,61 @@ def conjugate_pairs(D, X):
 
 
 def modal_plan(temporal, pencil):
+    """Real-basis FD transforms with one solve per conjugate pair.
+
+    The reference applies X^-1 = V S^-1 U^* from the complex SVD of X
+    (solvers.py:368-372). Here X is first mapped to the
+    real basis X_r = [.., Re x_j, Im x_j, .., x_real, ..] (X_r = X T with T
+    block-diagonal), and the SVD damping is applied to X_r. The computed
+    inverse columns of a pair are then exact conjugates,
+        (X^-T)[:, j] = (r1 - i r2) / 2,   r1, r2 = columns of X_r^-T,
+    so solving only the representative and taking 2 Re(z_j x_j^T) is
+    consistent with the inverse to working precision. (Using the complex
+    inverse's column j alone is not: its deviation from conjugate symmetry
+    is kappa_2(X) eps, amplified again by kappa_2 in the back transform.)
+    """
     form = pencil.form
     n_t = temporal.A.shape[0]
-    reps, singles = conjugate_pairs(form.D, form.X)
-    modes = np.concatenate([reps, singles])
-    weight = np.concatenate([np.full(len(reps), 2.0), np.ones(len(singles))])
-    # W_in = A_t^-1 conj(U) Sigma^-1 conj(Vh)  (same factor order as solvers.py:370-371)
-    w_in_c = (spd_solve(pencil.chol_A, np.conj(form.U)) / form.sigma[None, :]) @ np.conj(form.Vh)
-    # W_out = conj(V) Sigma U^T = Vh^T Sigma U^T (solvers.py:399)
-    w_out_c = (form.Vh.T * form.sigma[None, :]) @ form.U.T
-    wi = w_in_c[:, modes]
-    wo = w_out_c[modes, :]
-    w_in = np.ascontiguousarray(np.hstack([wi.real, wi.imag]))
-    w_out = np.ascontiguousarray(np.vstack([weight[:, None] * wo.real, -weight[:, None] * wo.imag]))
-    ws = w_out_c[singles, :]
-    w_out_im = np.ascontiguousarray(np.vstack([ws.imag, ws.real]))
+    X = form.X
+    reps, singles = conjugate_pairs(form.D, X)
+    if any(abs(form.D[j].imag) > 0.0 for j in singles):
+        # only reachable for complex pencils that dggev never produces for real (M_t, A_t)
+        raise DefectivePencil("unpaired complex eigenvalue in a real pencil")
+    # real basis: pair j -> columns (Re x_j, Im x_j); real eigenvalue -> x_j
+    cols, where = [], {}
+    for j in reps:
+        where[j] = len(cols)
+        cols += [X[:, j].real, X[:, j].imag]
+    for j in singles:
+        where[j] = len(cols)
+        cols.append(X[:, j].real)
+    Xr = np.column_stack(cols)
+    Ur, sr, Vrh = sla.svd(Xr)
+    if sr[-1] <= 0.0:
+        raise DefectivePencil("eigenvector matrix is numerically singular")
+    # W_r = A_t^-1 X_r^-T = A_t^-1 U_r S_r^-1 V_r^T (damped through the SVD)
+    Wr = spd_solve(pencil.chol_A, Ur / sr[None, :]) @ Vrh
+    nk = len(reps) + len(singles)
+    w_in = np.zeros((n_t, 2 * nk))
+    w_out = np.zeros((2 * nk, n_t))
+    lam = np.empty(nk, dtype=np.complex128)
+    for k, j in enumerate(reps):
+        c = where[j]
+        w_in[:, k] = 0.5 * Wr[:, c]            # Re of (r1 - i r2) / 2
+        w_in[:, nk + k] = -0.5 * Wr[:, c + 1]  # Im
+        w_out[k, :] = 2.0 * Xr[:, c]           # 2 Re(z x^T) = 2 (z_r x_r^T - z_i x_i^T)
+        w_out[nk + k, :] = -2.0 * Xr[:, c + 1]
+        lam[k] = form.D[j]
+    for s, j in enumerate(singles):
+        k = len(reps) + s
+        c = where[j]
+        w_in[:, k] = Wr[:, c]
+        w_out[k, :] = Xr[:, c]
+        lam[k] = form.D[j].real
     kron_b = np.ascontiguousarray(np.hstack([temporal.A.T, temporal.M.T]))
-    return ModalPlan(n_t=n_t, lam=form.D[modes].astype(np.complex128), weight=weight,
-                     n_pairs=len(reps), n_single=len(singles), w_in=w_in, w_out=w_out,
-                     w_out_im=w_out_im, kron_b=kron_b)
+    weight = np.concatenate([np.full(len(reps), 2.0), np.ones(len(singles))])
+    return ModalPlan(n_t=n_t, lam=lam, weight=weight, n_pairs=len(reps), n_single=len(singles),
+                     w_in=np.ascontiguousarray(w_in), w_out=np.ascontiguousarray(w_out), kron_b=kron_b)
 
 
 def _fortran(t_np, device):
@@ -106,7 +143,9 @@ class FDEngine:
         import torch
 
         _native.require_cuda()
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device if isinstance(device, torch.device) else torch.device("cuda", int(device))
         M = sp.csr_matrix(M_x)
         A = sp.csr_matrix(A_x)
         if M.shape != A.shape or M.shape[0] != M.shape[1]:
@@ -143,7 +182,6 @@ class FDEngine:
         f64 = torch.float64
         self.w_in = _fortran(modal.w_in, dev)        # (2N_k, N_t) storage of N_t x 2N_k
         self.w_out = _fortran(modal.w_out, dev)      # (N_t, 2N_k) storage of 2N_k x N_t
-        self.w_out_im = _fortran(modal.w_out_im, dev) if modal.n_single else None
         self.kron_b = _fortran(modal.kron_b, dev)    # (2N_t, N_t) storage of N_t x 2N_t
         n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
         self.G = torch.empty((nk2, n), dtype=f64, device=dev)   # column-major n x 2N_k
@@ -204,7 +242,7 @@ class FDEngine:
                             z + 8 * s0 * n, z + 8 * (nk + s0) * n, n, st)
             self.gpu_launches += 2 * depth + 2
 
-    def fd_apply(self, F, U, accumulate=False, imag_norm=False):
+    def fd_apply(self, F, U, accumulate=False):
         """U (+)= FD(F): F and U are device column-major n x N_t buffers (torch
         tensors of shape (N_t, n))."""
         n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
@@ -212,17 +250,6 @@ class FDEngine:
         self._spatial()
         self._gemm(n, nt, nk2, 1.0, self.Z.data_ptr(), n, self.w_out.data_ptr(), nk2,
                    1.0 if accumulate else 0.0, U.data_ptr(), n)
-        if imag_norm and self.modal.n_single:
-            ns, nk = self.modal.n_single, self.n_k
-            z = self.Z.data_ptr()
-            zr = z + 8 * (self.modal.n_pairs) * n
-            zi = z + 8 * (nk + self.modal.n_pairs) * n
-            wim = self.w_out_im.data_ptr()
-            self._gemm(n, nt, ns, 1.0, zr, n, wim, 2 * ns, 0.0, self.R.data_ptr(), n)
-            self._gemm(n, nt, ns, 1.0, zi, n, wim + 8 * ns, 2 * ns, 1.0, self.R.data_ptr(), n)
-            _native.call("kh_sumsq", self.R.data_ptr(), n * nt, self.norms.data_ptr() + 16, self._stream())
-            _native.call("kh_sumsq", U.data_ptr(), n * nt, self.norms.data_ptr() + 24, self._stream())
-            self.gpu_launches += 4
 
     def residual(self, U, F, keep_r=True):
         """Device: R = F - K U; returns (||R||^2, ||F||^2) as a device tensor slice."""
@@ -233,7 +260,7 @@ class FDEngine:
         self.gpu_launches += 2
         return self.norms[:2]
 
-    def solve(self, F, U=None, refine=3, tol=1e-13, check_imag=True):
+    def solve(self, F, U=None, refine=3, tol=1e-13):
         """Full FD solve of K u = f on the device with iterative refinement.
 
         Returns (U, info); U is a device tensor (N_t, n) = column-major n x N_t.
@@ -244,11 +271,8 @@ class FDEngine:
             U = torch.empty((self.n_t, self.n), dtype=torch.float64, device=self.device)
         if not self.factored and self.keep_factors:
             self.factor()
-        self.fd_apply(F, U, accumulate=False, imag_norm=check_imag)
+        self.fd_apply(F, U, accumulate=False)
         info = {"imag_residue": 0.0, "residuals": [], "refine_steps": 0}
-        if check_imag and self.modal.n_single:
-            im2, u2 = self.norms[2:4].tolist()
-            info["imag_residue"] = float(np.sqrt(im2) / np.sqrt(u2)) if u2 > 0 else 0.0
         rel = self._rel(self.residual(U, F))
         info["residuals"].append(rel)
         steps = 0
@@ -269,8 +293,3 @@ class FDEngine:
     def _rel(norms):
         r2, f2 = norms.tolist()
         return float(np.sqrt(r2) / np.sqrt(f2)) if f2 > 0 else float(np.sqrt(r2))
-
-
-def check_imag(info, tol=FD_IMAG_TOL):
-    if info["imag_residue"] > tol:
-        raise ImaginaryResidueTooLarge(f"imaginary residue {info['imag_residue']:.3e} above {tol:.1e}")
