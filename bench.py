@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--j-max", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
@@ -287,7 +288,7 @@ def main():
     peaks = measured_peaks(dev) if rank == 0 else {}
 
     e2e = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_e2e:
         e2e = measure_e2e(system, pencil, args, leaf)
 
     if rank == 0:

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,11 +55,14 @@ struct kh_plan {
   int64_t n = 0, nnz = 0, max_batch = 0, slots = 0;
   int32_t nf = 0, max_p = 0;
   std::vector<int32_t> level_off;  // levels d -> [level_off[d], level_off[d+1]) in level_fronts
+  std::vector<int32_t> cls_off;    // 4 per level: class starts (m<=32, m<=64, large) relative to level_off[d]
+  std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
+  int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
   KhDevFront* fronts = nullptr;
-  int32_t *child_list = nullptr, *relind = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
+  int32_t *child_list = nullptr, *relind = nullptr, *cmap = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
   int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
   double *mv = nullptr, *av = nullptr;
   double2* panels = nullptr;
@@ -77,6 +81,7 @@ struct kh_plan {
     T.fronts = fronts;
     T.child_list = child_list;
     T.relind = relind;
+    T.cmap = cmap;
     T.urows = urows;
     T.orig_src = orig_src;
     T.orig_dst = orig_dst;
@@ -95,7 +100,7 @@ void plan_release(kh_plan* p) {
   void* ptrs[] = {p->fronts, p->child_list, p->relind, p->orig_dst, p->level_fronts, p->urows, p->orig_src,
                   p->perm, p->indptr, p->indices, p->mv, p->av, p->panels, p->upd[0], p->upd[1], p->rupd[0],
                   p->rupd[1], p->y, p->lam, p->minpiv_work, p->absmax_work, p->minpiv, p->absmax,
-                  p->resid_part};
+                  p->resid_part, p->tasks, p->cmap};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -105,7 +110,7 @@ int64_t plan_bytes(const kh::Symbolic& S, int64_t max_batch, int64_t slots) {
   b += slots * S.panel_total * 16;
   b += max_batch * (S.upd_size[0] + S.upd_size[1] + S.rupd_size[0] + S.rupd_size[1] + S.n) * 16;
   b += (int64_t)S.fronts.size() * (sizeof(KhDevFront) + max_batch * 8);
-  b += (int64_t)(S.urows.size() * 12 + S.orig_src.size() * 12 + S.n * 16 + S.nnz * 24);
+  b += (int64_t)(S.urows.size() * 12 + S.cmap.size() * 4 + S.orig_src.size() * 12 + S.n * 16 + S.nnz * 24);
   return b;
 }
 
@@ -283,15 +288,42 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     D.rows_begin = F.rows_begin;
     D.child_begin = S.child_ptr[f];
     D.child_end = S.child_ptr[f + 1];
+    D.cmap_begin = F.cmap_begin;
     D.depth = F.depth;
     D.pad = 0;
     p->max_p = std::max(p->max_p, F.p);
   }
+  // each level's fronts grouped by kernel class: m <= 32, m <= 64 (register-
+  // resident kernels), larger (tiled DMMA kernel); KH_SMALL_MAX caps the
+  // register-resident classes (0 disables them, for A/B measurements)
+  int small_max = 64;
+  if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
   std::vector<int32_t> lf;
   p->level_off.push_back(0);
   for (const auto& lev : S.levels) {
-    lf.insert(lf.end(), lev.begin(), lev.end());
+    const int32_t base = (int32_t)lf.size();
+    for (int c = 0; c < 3; ++c) {
+      p->cls_off.push_back((int32_t)lf.size() - base);
+      for (int32_t f : lev) {
+        const int32_t m = S.fronts[f].m();
+        const int cls = (m <= 32 && small_max >= 32) ? 0 : ((m <= 64 && small_max >= 64) ? 1 : 2);
+        if (cls == c) lf.push_back(f);
+      }
+    }
+    p->cls_off.push_back((int32_t)lf.size() - base);
     p->level_off.push_back((int32_t)lf.size());
+  }
+  // Schur-update tasks: lower 64x64 tiles of U for every large front, per level
+  std::vector<int32_t> tasks;
+  p->task_off.push_back(0);
+  for (size_t d = 0; d < S.levels.size(); ++d) {
+    for (int32_t k = p->level_off[d] + p->cls_off[4 * d + 2]; k < p->level_off[d + 1]; ++k) {
+      const int32_t f = lf[k];
+      const int32_t nt = (S.fronts[f].q + 63) / 64;
+      for (int32_t jt = 0; jt < nt; ++jt)
+        for (int32_t it = jt; it < nt; ++it) tasks.insert(tasks.end(), {f, it, jt});
+    }
+    p->task_off.push_back((int32_t)(tasks.size() / 3));
   }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) {
@@ -300,10 +332,12 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   chk(upload(&p->fronts, df.data(), df.size()));
   chk(upload(&p->child_list, S.child_list.data(), S.child_list.size()));
   chk(upload(&p->relind, S.relind.data(), S.relind.size()));
+  chk(upload(&p->cmap, S.cmap.data(), S.cmap.size()));
   chk(upload(&p->urows, S.urows.data(), S.urows.size()));
   chk(upload(&p->orig_src, S.orig_src.data(), S.orig_src.size()));
   chk(upload(&p->orig_dst, S.orig_dst.data(), S.orig_dst.size()));
   chk(upload(&p->level_fronts, lf.data(), lf.size()));
+  chk(upload(&p->tasks, tasks.data(), tasks.size()));
   chk(upload(&p->perm, S.perm.data(), S.perm.size()));
   chk(upload(&p->indptr, indptr, (size_t)S.n + 1));
   chk(upload(&p->indices, indices, (size_t)S.nnz));
@@ -355,9 +389,16 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
   double2* panels = p->panels + slot0 * p->panel_total;
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
-    KH_CUDA(kh_launch_factor_level(T, lev, nlev, (int32_t)nshift, p->lam, panels, p->upd[d & 1],
-                                   p->upd_size[d & 1], p->upd[(d + 1) & 1], p->upd_size[(d + 1) & 1],
+    const int32_t* co = p->cls_off.data() + 4 * d;
+    double2 *uc = p->upd[d & 1], *uch = p->upd[(d + 1) & 1];
+    const int64_t sc = p->upd_size[d & 1], sch = p->upd_size[(d + 1) & 1];
+    const int32_t ns = (int32_t)nshift;
+    KH_CUDA(kh_launch_factor_small(32, T, lev + co[0], co[1] - co[0], ns, p->lam, panels, uc, sc, uch, sch,
+                                   p->minpiv_work, st));
+    KH_CUDA(kh_launch_factor_small(64, T, lev + co[1], co[2] - co[1], ns, p->lam, panels, uc, sc, uch, sch,
+                                   p->minpiv_work, st));
+    KH_CUDA(kh_launch_factor_level(T, lev + co[2], co[3] - co[2], p->tasks + 3 * p->task_off[d],
+                                   p->task_off[d + 1] - p->task_off[d], ns, p->lam, panels, uc, sc, uch, sch,
                                    p->minpiv_work, st));
   }
   KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));

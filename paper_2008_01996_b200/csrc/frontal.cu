@@ -113,20 +113,186 @@ KH_DEV void tile_epilogue(const Acc& acc, EP ep) {
            make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
 }
 
-struct FactorSmem {
+// Original entries of the front's pivot columns: store(local_offset, value)
+// with value = M_ij + lambda A_ij. Four entries per thread are in flight at
+// once (the index -> value loads are dependent, so batching hides latency).
+template <int NTH, class ST>
+KH_DEV void scatter_originals(const KhTree& T, const KhDevFront& F, double2 L, ST store) {
+  for (int64_t e0 = F.orig_begin + threadIdx.x; e0 < F.orig_end; e0 += 4 * NTH) {
+    int64_t s[4];
+    int d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = e0 + (int64_t)u * NTH;
+      s[u] = e < F.orig_end ? T.orig_src[e] : -1;
+      d[u] = e < F.orig_end ? T.orig_dst[e] : 0;
+    }
+    double mv[4], av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      mv[u] = s[u] >= 0 ? T.mv[s[u]] : 0.0;
+      av[u] = s[u] >= 0 ? T.av[s[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s[u] >= 0) store(d[u], make_double2(fma(L.x, av[u], mv[u]), L.y * av[u]));
+  }
+}
+
+// ---- pull assembly ------------------------------------------------------------
+// A parent entry (r, c) (parent-local rows, r >= c) is the sum over children
+// k of U_k[ci + cj*q_k] with ci = cmap_k[r], cj = cmap_k[c] when both are
+// present. Gathering instead of scattering needs no zeroing pass and no
+// read-modify-write, keeps many independent loads in flight, and fixes the
+// summation order (bitwise-deterministic factors).
+constexpr int MAXC = 8;  // children cached in shared memory; more are read from global
+
+struct ChildRef {
+  const double2* U;
+  const int32_t* cmap;
+  int q;
+};
+
+struct Kids {
+  ChildRef c[MAXC];
+  int n;
+};
+
+KH_DEV void load_kids(const KhTree& T, const KhDevFront& F, const double2* upd_child, int64_t stride_child, int b,
+                      Kids& K) {
+  if (threadIdx.x == 0) K.n = F.child_end - F.child_begin;
+  if (threadIdx.x < MAXC && threadIdx.x < F.child_end - F.child_begin) {
+    const KhDevFront C = T.fronts[T.child_list[F.child_begin + threadIdx.x]];
+    K.c[threadIdx.x] = {upd_child + (int64_t)b * stride_child + C.upd_off, T.cmap + C.cmap_begin, C.q};
+  }
+}
+
+KH_DEV ChildRef kid(const KhTree& T, const KhDevFront& F, const double2* upd_child, int64_t stride_child, int b,
+                    const Kids& K, int k) {
+  if (k < MAXC) return K.c[k];
+  const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+  return {upd_child + (int64_t)b * stride_child + C.upd_off, T.cmap + C.cmap_begin, C.q};
+}
+
+// Extend-add of one child's update matrix (lower triangle, q_c x q_c, ld q_c):
+// add(parent_row, parent_col, value). A warp walks a column so the reads of
+// U_c and relind are contiguous; distinct (a, b) map to distinct targets.
+template <int NTH, class AD>
+KH_DEV void extend_add_child(const double2* __restrict__ Uc, int qc, const int32_t* __restrict__ rel, AD add) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NTH / 32;
+  for (int bb = warp; bb < qc; bb += NW) {
+    const int rb = rel[bb];
+    const double2* colp = Uc + (int64_t)bb * qc;
+    for (int a0 = bb + lane; a0 < qc; a0 += 64) {
+      const int a1 = a0 + 32;
+      const bool ok1 = a1 < qc;
+      const double2 v0 = colp[a0];
+      const int r0 = rel[a0];
+      const double2 v1 = ok1 ? colp[a1] : make_double2(0.0, 0.0);
+      const int r1 = ok1 ? rel[a1] : 0;
+      add(r0, rb, v0);
+      if (ok1) add(r1, rb, v1);
+    }
+  }
+}
+
+// One pipeline stage of the cp.async tile engine: 16 K-columns of A and B
+// (64 rows each, [k][row] with the conflict-free pad) and the 16 pivots d_k.
+struct CpStage {
   double2 a[KC * LDS];
   double2 b[KC * LDS];
+  double2 d[KC];
+};
+
+// acc(i, j) = sum_{k<K} A[i + k*lda] * d_k * B[j + k*ldb]   (i < rowsA, j < rowsB)
+// with d_k = D[k * ldd] (the pivots on the panel diagonal). Two-stage
+// cp.async ring: the next chunk streams in while DMMA consumes the current
+// one; out-of-range rows and k are zero-filled by the copy itself. The
+// pivot scaling is applied to the B fragments in registers.
+KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t lda, int rowsA,
+                        const double2* __restrict__ B, int64_t ldb, int rowsB, const double2* __restrict__ D,
+                        int64_t ldd, CpStage* st) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wi = warp & 1, wj = warp >> 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc.r[a][b][h] = acc.i[a][b][h] = 0.0;
+  const int nch = (K + KC - 1) / KC;
+  auto load = [&](int s, int c) {
+    CpStage& S = st[s];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + r * NT;
+      const int i = idx & (TB - 1), k = idx >> 6;
+      const int kk = c * KC + k;
+      const bool okk = kk < K;
+      const bool oa = okk && i < rowsA, ob = okk && i < rowsB;
+      cp_async16(&S.a[k * LDS + i], oa ? A + i + (int64_t)kk * lda : A, oa);
+      cp_async16(&S.b[k * LDS + i], ob ? B + i + (int64_t)kk * ldb : B, ob);
+    }
+    if (tid < KC) {
+      const int kk = c * KC + tid;
+      cp_async16(&S.d[tid], kk < K ? D + (int64_t)kk * ldd : D, kk < K);
+    }
+  };
+  if (nch > 0) load(0, 0);
+  cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) load((c + 1) & 1, c + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const CpStage& S = st[c & 1];
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double2 af[4], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = S.a[(kk + t) * LDS + wi * 32 + mt * 8 + g];
+      const double2 dk = S.d[kk + t];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = cmul(S.b[(kk + t) * LDS + wj * 16 + nt * 8 + g], dk);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double nai = -af[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], af[mt].x, bf[nt].x);
+          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], nai, bf[nt].y);
+          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].x, bf[nt].y);
+          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].y, bf[nt].x);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+struct FactorSmem {
+  CpStage st[2];
   double2 d[NB * (NB + 1)];   // diagonal block, [i][j] at i*(NB+1)+j
   double2 li[NB * (NB + 1)];  // unit-lower inverse
   double2 dinv[NB];
-  double red[NT / 32];
 };
 
-__global__ void __launch_bounds__(NT) factor_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
-                                                          const double2* __restrict__ lam, double2* panels,
-                                                          double2* upd_cur, int64_t upd_stride_cur,
-                                                          const double2* __restrict__ upd_child,
-                                                          int64_t upd_stride_child, double* minpiv) {
+// Panel kernel for fronts with m > 64 (one CTA per (front, shift)):
+// assembly of P (m x p) and U (q x q), then a left-looking blocked LDL^T of
+// the m x p panel. For pivot block [kb, kb+w): the block column is first
+// updated with all earlier columns in one long-K DMMA product
+//   P[kb:, kb:kb+w] -= L[kb:, :kb] D L[kb:kb+w, :kb]^T,
+// then the w x w diagonal block is factored in shared memory and the rows
+// below are solved against it (TRSM as a GEMM with the unit-lower inverse).
+// The Schur complement U -= L21 D L21^T is left to schur_update_kernel.
+__global__ void __launch_bounds__(NT, 2) factor_panel_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                             const double2* __restrict__ lam, double2* panels,
+                                                             double2* upd_cur, int64_t upd_stride_cur,
+                                                             const double2* __restrict__ upd_child,
+                                                             int64_t upd_stride_child, double* minpiv) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FactorSmem& S = *reinterpret_cast<FactorSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -136,44 +302,59 @@ __global__ void __launch_bounds__(NT) factor_level_kernel(KhTree T, const int32_
   const int p = F.p, q = F.q, m = p + q;
   const double2 L = lam[b];
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  (void)upd_cur;
+  (void)upd_stride_cur;
+  (void)q;
 
-  // ---- assembly -------------------------------------------------------------
-  for (int64_t idx = tid; idx < (int64_t)m * p; idx += NT) P[idx] = make_double2(0.0, 0.0);
-  for (int64_t idx = tid; idx < (int64_t)q * q; idx += NT) U[idx] = make_double2(0.0, 0.0);
+  // ---- assembly of P (pull children, then add the originals) --------------------
+  // The strict upper triangle of the pivot block is never read, so it is not
+  // written; U is assembled by schur_update_kernel.
+  __shared__ Kids kids;
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
   __syncthreads();
-  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NT) {
-    int64_t s = T.orig_src[e];
-    double mvv = T.mv[s], avv = T.av[s];
-    P[T.orig_dst[e]] = make_double2(fma(L.x, avv, mvv), L.y * avv);
-  }
-  __syncthreads();
-  for (int c = F.child_begin; c < F.child_end; ++c) {
-    const KhDevFront C = T.fronts[T.child_list[c]];
-    const int qc = C.q;
-    const double2* Uc = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
-    const int32_t* rel = T.relind + C.rows_begin;
-    for (int64_t idx = tid; idx < (int64_t)qc * qc; idx += NT) {
-      int a = (int)(idx % qc), bb = (int)(idx / qc);
-      if (a < bb) continue;
-      double2 v = Uc[idx];
-      int ra = rel[a], rb = rel[bb];
-      if (rb < p) {
-        double2* d = P + ra + (int64_t)rb * m;
-        *d = cadd(*d, v);
-      } else {
-        double2* d = U + (ra - p) + (int64_t)(rb - p) * q;
-        *d = cadd(*d, v);
+  for (int c = 0; c < p; ++c) {
+    for (int r0 = c + tid; r0 < m; r0 += 4 * NT) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = make_double2(0.0, 0.0);
+      for (int k = 0; k < kids.n; ++k) {
+        const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+        const int cj = C.cmap[c];
+        if (cj < 0) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + u * NT;
+          const int ci = r < m ? C.cmap[r] : -1;
+          if (ci >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
+        }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r0 + u * NT < m) P[(r0 + u * NT) + (int64_t)c * m] = v[u];
     }
-    __syncthreads();
   }
+  __syncthreads();
+  scatter_originals<NT>(T, F, L, [&](int d, double2 v) { P[d] = cadd(P[d], v); });
+  __syncthreads();
 
-  // ---- pivot blocks ---------------------------------------------------------
+  // ---- left-looking pivot blocks ----------------------------------------------
   double minp = DBL_MAX;
   Acc acc;
   for (int kb = 0; kb < p; kb += NB) {
     const int w = min(NB, p - kb);
+    if (kb > 0) {
+      for (int i0 = kb; i0 < m; i0 += TB) {
+        tile_mma_cp(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, S.st);
+        tile_epilogue(acc, [&](int i, int j, double2 v) {
+          const int r = i0 + i;
+          if (r < m && j < w && r >= kb + j) {
+            double2* d = P + r + (int64_t)(kb + j) * m;
+            *d = csub(*d, v);
+          }
+        });
+      }
+      __syncthreads();
+    }
     for (int idx = tid; idx < w * w; idx += NT) {
       int i = idx % w, j = idx / w;
       S.d[i * (NB + 1) + j] = i >= j ? P[(kb + i) + (int64_t)(kb + j) * m] : make_double2(0.0, 0.0);
@@ -217,64 +398,149 @@ __global__ void __launch_bounds__(NT) factor_level_kernel(KhTree T, const int32_
       }
       __syncthreads();
     }
-    const int r0 = kb + w;
     // TRSM of the rows below: L[r, kb+j] = (A[r, kb:kb+w] Linv^T)[j] / d_j
-    for (int i0 = r0; i0 < m; i0 += TB) {
+    for (int i0 = kb + w; i0 < m; i0 += TB) {
       const int rows = m - i0;
       tile_mma(
           acc, w,
           [&](int i, int k) { return i < rows ? P[(i0 + i) + (int64_t)(kb + k) * m] : make_double2(0.0, 0.0); },
-          [&](int j, int k) { return j < w ? S.li[j * (NB + 1) + k] : make_double2(0.0, 0.0); }, S.a, S.b);
+          [&](int j, int k) { return j < w ? S.li[j * (NB + 1) + k] : make_double2(0.0, 0.0); }, S.st[0].a,
+          S.st[0].b);
       tile_epilogue(acc, [&](int i, int j, double2 v) {
         if (i < rows && j < w) P[(i0 + i) + (int64_t)(kb + j) * m] = cmul(v, S.dinv[j]);
       });
     }
     __syncthreads();
-    // trailing update of the remaining pivot columns (lower trapezoid)
-    for (int j0 = r0; j0 < p; j0 += TB) {
-      for (int i0 = j0; i0 < m; i0 += TB) {
-        tile_mma(
-            acc, w,
-            [&](int i, int k) {
-              return i0 + i < m ? P[(i0 + i) + (int64_t)(kb + k) * m] : make_double2(0.0, 0.0);
-            },
-            [&](int j, int k) {
-              return j0 + j < p ? cmul(P[(j0 + j) + (int64_t)(kb + k) * m], S.d[k * (NB + 1) + k])
-                                : make_double2(0.0, 0.0);
-            },
-            S.a, S.b);
-        tile_epilogue(acc, [&](int i, int j, double2 v) {
-          int r = i0 + i, c = j0 + j;
-          if (r < m && c < p && r >= c) {
-            double2* d = P + r + (int64_t)c * m;
-            *d = csub(*d, v);
-          }
-        });
+  }
+  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+}
+
+// Schur complement of the large fronts of one level: one CTA per 64 x 64
+// lower tile of U, per shift: U[i0:, j0:] -= L21[i0:, :] D L21[j0:, :]^T
+// (K = p). Tasks are (front, tile row, tile col) triples built on the host.
+__global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                             const double2* __restrict__ panels, double2* upd_cur,
+                                                             int64_t upd_stride_cur,
+                                                             const double2* __restrict__ upd_child,
+                                                             int64_t upd_stride_child) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+  __shared__ Kids kids;
+  const int32_t f = tasks[3 * blockIdx.x];
+  const int i0 = tasks[3 * blockIdx.x + 1] * TB, j0 = tasks[3 * blockIdx.x + 2] * TB;
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  Acc acc;
+  tile_mma_cp(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
+  // U = (children's contributions, pulled) - L21 D L21^T
+  tile_epilogue(acc, [&](int i, int j, double2 v) {
+    const int r = i0 + i, c = j0 + j;
+    if (r < q && c < q && r >= c) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < kids.n; ++k) {
+        const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+        const int ci = C.cmap[p + r], cj = C.cmap[p + c];
+        if (ci >= 0 && cj >= 0) s = cadd(s, C.U[ci + (int64_t)cj * C.q]);
+      }
+      U[r + (int64_t)c * q] = csub(s, v);
+    }
+  });
+}
+
+// ---- small fronts (m <= MS): register-resident right-looking LDL^T ----------
+// The front is assembled in shared memory, then held in registers: thread t
+// owns row i = t % MS at columns j = t / MS + 4c. Pivot k costs one barrier:
+// the owners of column k publish it to a double-buffered shared column and
+// every thread applies the rank-1 update to its entries. The trailing
+// q x q block left in registers after p pivots is the update matrix U.
+template <int MS>
+__global__ void __launch_bounds__(MS * 4) factor_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                              const double2* __restrict__ lam, double2* panels,
+                                                              double2* upd_cur, int64_t upd_stride_cur,
+                                                              const double2* __restrict__ upd_child,
+                                                              int64_t upd_stride_child, double* minpiv) {
+  constexpr int NTH = MS * 4, NC = MS / 4, NPK = MS * (MS + 1) / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sO = reinterpret_cast<double2*>(smem_raw);  // originals, packed lower triangle
+  double2(*col)[MS] = reinterpret_cast<double2(*)[MS]>(sO + NPK);
+  __shared__ Kids kids;
+  const int tid = threadIdx.x;
+  const int i = tid % MS, jg = tid / MS;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2 L = lam[b];
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  auto pk = [](int r, int c) { return c * MS - (c * (c - 1)) / 2 + (r - c); };
+
+  for (int idx = tid; idx < NPK; idx += NTH) sO[idx] = make_double2(0.0, 0.0);
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  __syncthreads();
+  scatter_originals<NTH>(T, F, L, [&](int d, double2 v) { sO[pk(d % m, d / m)] = v; });
+  __syncthreads();
+  // registers <- originals + pulled children contributions
+  double2 a[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = jg + 4 * c;
+    a[c] = (i < m && j <= i) ? sO[pk(i, j)] : make_double2(0.0, 0.0);
+  }
+  for (int k = 0; k < kids.n; ++k) {
+    const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+    const int ci = i < m ? C.cmap[i] : -1;
+    if (ci < 0) continue;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int j = jg + 4 * c;
+      if (j <= i) {
+        const int cj = C.cmap[j];
+        if (cj >= 0) a[c] = cadd(a[c], C.U[ci + cj * C.q]);
       }
     }
-    __syncthreads();
   }
 
-  // ---- update matrix: U -= L21 D L21^T ---------------------------------------
-  for (int j0 = 0; j0 < q; j0 += TB) {
-    for (int i0 = j0; i0 < q; i0 += TB) {
-      tile_mma(
-          acc, p,
-          [&](int i, int k) {
-            return i0 + i < q ? P[(p + i0 + i) + (int64_t)k * m] : make_double2(0.0, 0.0);
-          },
-          [&](int j, int k) {
-            return j0 + j < q ? cmul(P[(p + j0 + j) + (int64_t)k * m], P[k + (int64_t)k * m])
-                              : make_double2(0.0, 0.0);
-          },
-          S.a, S.b);
-      tile_epilogue(acc, [&](int i, int j, double2 v) {
-        int r = i0 + i, c = j0 + j;
-        if (r < q && c < q && r >= c) {
-          double2* d = U + r + (int64_t)c * q;
-          *d = csub(*d, v);
+  // pivot k = 4c + r lives in register slot c of the threads with jg == r;
+  // c is a compile-time index so the front never leaves the register file
+  double minp = DBL_MAX;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+#pragma unroll 1
+    for (int r = 0; r < 4; ++r) {
+      const int k = 4 * c + r;
+      if (k < p) {
+        double2* buf = col[k & 1];
+        if (jg == r) buf[i] = a[c];
+        __syncthreads();
+        const double2 dk = buf[k];
+        const double2 di = cinv(dk);
+        if (i > k && i < m) {
+          const double2 li = cmul(buf[i], di);
+#pragma unroll
+          for (int c2 = c; c2 < NC; ++c2) {
+            const int j = jg + 4 * c2;
+            if (j > k && j <= i) a[c2] = cfms(a[c2], li, buf[j]);
+          }
+          if (jg == r) a[c] = li;
         }
-      });
+        if (tid == 0) {
+          double ad = sqrt(cabs2(dk));
+          minp = (ad != ad) ? -1.0 : fmin(minp, ad);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = jg + 4 * c;
+    if (i < m && j <= i) {
+      if (j < p) P[i + (int64_t)j * m] = a[c];
+      else U[(i - p) + (int64_t)(j - p) * q] = a[c];
     }
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
@@ -296,20 +562,36 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* yy = y + (int64_t)b * T.n + F.first;
   double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
-  for (int a = tid; a < q; a += NT) ru[a] = make_double2(0.0, 0.0);
-  __syncthreads();
-  for (int c = F.child_begin; c < F.child_end; ++c) {
-    const KhDevFront C = T.fronts[T.child_list[c]];
-    const double2* ruc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
-    const int32_t* rel = T.relind + C.rows_begin;
-    for (int a = tid; a < C.q; a += NT) {
-      int loc = rel[a];
-      double2 v = ruc[a];
-      if (loc < p) yy[loc] = cadd(yy[loc], v);
-      else ru[loc - p] = cadd(ru[loc - p], v);
-    }
-    __syncthreads();
+  // pull the children's rhs updates (fixed child order: deterministic)
+  __shared__ const double2* kru[MAXC];
+  __shared__ const int32_t* kcm[MAXC];
+  const int nk = F.child_end - F.child_begin;
+  if (tid < MAXC && tid < nk) {
+    const KhDevFront C = T.fronts[T.child_list[F.child_begin + tid]];
+    kru[tid] = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+    kcm[tid] = T.cmap + C.cmap_begin;
   }
+  __syncthreads();
+  for (int r = tid; r < m; r += NT) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int k = 0; k < nk; ++k) {
+      const double2* rc;
+      const int32_t* cm;
+      if (k < MAXC) {
+        rc = kru[k];
+        cm = kcm[k];
+      } else {
+        const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+        rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+        cm = T.cmap + C.cmap_begin;
+      }
+      const int ci = cm[r];
+      if (ci >= 0) v = cadd(v, rc[ci]);
+    }
+    if (r < p) yy[r] = cadd(yy[r], v);
+    else ru[r - p] = v;
+  }
+  __syncthreads();
   for (int kb = 0; kb < p; kb += NB) {
     const int w = min(NB, p - kb);
     for (int idx = tid; idx < w * w; idx += NT) {
@@ -331,6 +613,7 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
     // rows below the block
     for (int r = kb + w + tid; r < m; r += NT) {
       double2 s = make_double2(0.0, 0.0);
+#pragma unroll 8
       for (int k = 0; k < w; ++k) {
         double2 l = P[r + (int64_t)(kb + k) * m];
         s = cadd(s, cmul(l, sy[k]));
@@ -361,6 +644,7 @@ __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* 
   for (int k = warp; k < p; k += NT / 32) {
     double2 s = make_double2(0.0, 0.0);
     const double2* col = P + p + (int64_t)k * m;
+#pragma unroll 4
     for (int a = lane; a < q; a += 32) s = cadd(s, cmul(col[a], yb[urows[a]]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -461,20 +745,27 @@ __global__ void rowreduce_kernel(const double* __restrict__ in, int64_t len, int
 
 }  // namespace
 
-cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
-                                   const double2* upd_child, int64_t upd_stride_child, double* minpiv,
-                                   cudaStream_t stream) {
+cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, const int32_t* tasks,
+                                   int32_t ntasks, int32_t batch, const double2* lam, double2* panels,
+                                   double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
+                                   int64_t upd_stride_child, double* minpiv, cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   static bool attr = false;
   const int smem = (int)sizeof(FactorSmem);
+  const int smem_s = (int)(2 * sizeof(CpStage));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(factor_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  factor_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, lam, panels, upd_cur,
+  factor_panel_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, lam, panels, upd_cur,
                                                                upd_stride_cur, upd_child, upd_stride_child, minpiv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || ntasks == 0) return e;
+  schur_update_kernel<<<dim3(ntasks, batch), NT, smem_s, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
+                                                                   upd_child, upd_stride_child);
   return cudaGetLastError();
 }
 
@@ -528,5 +819,30 @@ cudaError_t kh_launch_rowreduce(const double* in, int64_t len, int32_t rows, int
                                 cudaStream_t stream) {
   if (rows == 0) return cudaSuccess;
   rowreduce_kernel<<<rows, NT, 0, stream>>>(in, len, op, out);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
+                                   const double2* upd_child, int64_t upd_stride_child, double* minpiv,
+                                   cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  dim3 grid(nlev, batch);
+  constexpr int s32 = (32 * 33 / 2 + 2 * 32) * 16, s64 = (64 * 65 / 2 + 2 * 64) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(factor_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (ms == 32) {
+    factor_small_kernel<32><<<grid, 128, s32, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur,
+                                                        upd_child, upd_stride_child, minpiv);
+  } else if (ms == 64) {
+    factor_small_kernel<64><<<grid, 256, s64, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur,
+                                                        upd_child, upd_stride_child, minpiv);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }

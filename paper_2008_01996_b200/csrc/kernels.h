@@ -9,6 +9,7 @@ struct KhDevFront {
   int64_t panel_off, upd_off, rupd_off;
   int64_t orig_begin, orig_end;
   int64_t rows_begin;  // urows / relind of this front
+  int64_t cmap_begin;  // pull map over the parent's rows (see symbolic.h)
   int32_t child_begin, child_end;
   int32_t depth, pad;
 };
@@ -17,6 +18,7 @@ struct KhTree {  // device pointers shared by every level kernel
   const KhDevFront* fronts;
   const int32_t* child_list;
   const int32_t* relind;
+  const int32_t* cmap;
   const int64_t* urows;
   const int64_t* orig_src;
   const int32_t* orig_dst;
@@ -32,8 +34,10 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
                             cudaStream_t stream);
 
 // Factor every front of one depth level for `batch` shifts.
-cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev,
-                                   int32_t batch, const double2* lam, double2* panels,
+// Large fronts (m > 64): panel kernel, then the Schur update over `tasks`
+// ((front, tile row, tile col) triples of the level).
+cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, const int32_t* tasks,
+                                   int32_t ntasks, int32_t batch, const double2* lam, double2* panels,
                                    double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
                                    int64_t upd_stride_child, double* minpiv, cudaStream_t stream);
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
@@ -54,3 +58,8 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
                                     int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);
+// Register-resident factorization of fronts with m <= ms (ms = 32 or 64).
+cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
+                                   const double2* upd_child, int64_t upd_stride_child, double* minpiv,
+                                   cudaStream_t stream);

@@ -345,6 +345,21 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       S.relind[F.relind_begin + a] = loc;
     }
   }
+  // pull maps: for child c of P, cmap[c][r] = a with relind_c[a] = r (r < m_P), else -1
+  {
+    int64_t tot = 0;
+    for (int32_t f = 0; f < nf; ++f) {
+      Front& F = S.fronts[f];
+      F.cmap_begin = tot;
+      if (F.parent >= 0) tot += S.fronts[F.parent].m();
+    }
+    S.cmap.assign(tot, -1);
+    for (int32_t f = 0; f < nf; ++f) {
+      const Front& F = S.fronts[f];
+      if (F.parent < 0) continue;
+      for (int32_t a = 0; a < F.q; ++a) S.cmap[F.cmap_begin + S.relind[F.relind_begin + a]] = a;
+    }
+  }
   for (int32_t d = 0; d <= S.max_depth; ++d) {
     int64_t uo = 0, ru = 0;
     for (int32_t f : S.levels[d]) {

@@ -24,6 +24,7 @@ struct Front {
   int64_t panel_off;    // complex offset of the m x p panel in per-shift factor storage
   int64_t upd_off;      // complex offset of the q x q update in its depth-parity buffer
   int64_t rupd_off;     // complex offset of the q rhs-update in its depth-parity buffer
+  int64_t cmap_begin;   // into Symbolic::cmap: parent's m local rows -> this front's update index or -1
   int32_t m() const { return p + q; }
 };
 
@@ -37,6 +38,7 @@ struct Symbolic {
   std::vector<int32_t> child_list;
   std::vector<int64_t> urows;      // update-row positions per front
   std::vector<int32_t> relind;     // child update row -> parent local row
+  std::vector<int32_t> cmap;       // inverse of relind per child, over the parent's m rows (-1 = absent)
   std::vector<int64_t> orig_src;   // CSR entry index
   std::vector<int32_t> orig_dst;   // local (row + col*m) inside the front panel
   std::vector<std::vector<int32_t>> levels;  // levels[d] = fronts at depth d
