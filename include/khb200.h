@@ -121,6 +121,8 @@ int kh_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int
 int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
                          const double* m_vals, const double* a_vals, const double* Y, int64_t ldy,
                          const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2, void* stream);
+/* y += alpha x over n device doubles (refinement update of a row shard). */
+int kh_daxpy(int64_t n, double alpha, const double* x, double* y, void* stream);
 /* out (device, 1 double) = sum_i x_i^2 over n device doubles. */
 int kh_sumsq(const double* x, int64_t n, double* out, void* stream);
 int kh_set_device(int device);

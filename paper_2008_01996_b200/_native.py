@@ -71,6 +71,7 @@ SIGNATURES = {
     "kh_plan_free": (None, [_vp]),
     "kh_dgemm": (ctypes.c_int, [_i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp]),
     "kh_sumsq": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
+    "kh_daxpy": (ctypes.c_int, [_i64, _dbl, _vp, _vp, _vp]),
     "kh_csr_pair_residual": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                                             _vp, _vp]),
     "kh_set_device": (ctypes.c_int, [ctypes.c_int]),

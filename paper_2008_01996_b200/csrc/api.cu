@@ -166,6 +166,12 @@ extern "C" int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
   return KH_OK;
 }
 
+extern "C" int kh_daxpy(int64_t n, double alpha, const double* x, double* y, void* stream) {
+  if (n > 0 && (!x || !y)) return fail(KH_ERR_INVALID, "null argument");
+  KH_CUDA(kh_launch_daxpy(n, alpha, x, y, static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
 extern "C" int kh_sumsq(const double* x, int64_t n, double* out, void* stream) {
   if (!out || (n > 0 && !x)) return fail(KH_ERR_INVALID, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

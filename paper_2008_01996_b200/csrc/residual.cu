@@ -6,6 +6,8 @@
 // kernel is the fused dual SpMM (M_x and A_x share one CSR pattern) plus the
 // subtraction from F and the partial sums of ||R||^2 and ||F||^2 (a fixed
 // grid and a fixed reduction order keep the result deterministic).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,7 +73,20 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x
   }
 }
 
+__global__ void __launch_bounds__(256) daxpy_kernel(int64_t n, double alpha, const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(alpha, x[i], y[i]);
+}
+
 }  // namespace
+
+cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  daxpy_kernel<<<blocks, 256, 0, stream>>>(n, alpha, x, y);
+  return cudaGetLastError();
+}
 
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream) {
   sumsq_kernel<<<nblk, 256, 0, stream>>>(x, n, part);

@@ -1,0 +1,198 @@
+"""Multi-GPU FD: shifts sharded over ranks, back transform finished by a
+reduce-scatter by spatial rows (BASELINE.json north star).
+
+One process per GPU (torchrun). Rank r owns a contiguous block of the N_k
+modal shifts (conjugate-pair representatives first). Per FD application:
+
+1. G_r = F W_in[:, modes_r]              local DMMA GEMM (F is resident on every rank)
+2. Z_r = (M_x + lambda_k A_x)^-1 G_r      local batched LDL^T solves
+3. P_r[c] = Z_r[rows_c, :] W_out[modes_r, :]   partial back transform, written
+                                          directly in row-chunk layout (chunk c =
+                                          spatial rows of rank c, column-major)
+4. U_shard = sum_r P_r[rank]              NCCL reduce-scatter (the cross-mode sum)
+
+Refinement needs K u: Y_shard = U_shard [A_t^T | M_t^T] is row-local; the
+Y shards are all-gathered and every rank forms the full residual
+R = F - (M_x Y1 + A_x Y2) (a cheap SpMM) so that step 1 of the next
+application again has all spatial rows. Norms are then identical on every
+rank, so the refinement loop takes the same branch everywhere.
+
+The device work is behind `ops` (default: the FDEngine kernels); the
+collectives are plain torch.distributed calls, so the same driver runs on
+NCCL/GPU and, in tests, on gloo/CPU with an emulated `ops`.
+"""
+
+import math
+
+import numpy as np
+
+from .engine import ModalPlan
+
+
+def shard_range(n_items, world, rank):
+    """Balanced contiguous block [k0, k1) of n_items for `rank`."""
+    base, extra = divmod(n_items, world)
+    k0 = rank * base + min(rank, extra)
+    return k0, k0 + base + (1 if rank < extra else 0)
+
+
+def row_chunk(n, world):
+    """Rows per chunk of the reduce-scatter (last chunk padded)."""
+    return max(1, math.ceil(n / world))
+
+
+def restrict_modal(modal, k0, k1):
+    nk = modal.n_k
+    cols = np.r_[k0:k1, nk + k0:nk + k1]
+    n_pairs = int(np.clip(modal.n_pairs - k0, 0, k1 - k0))
+    return ModalPlan(n_t=modal.n_t, lam=modal.lam[k0:k1].copy(), weight=modal.weight[k0:k1].copy(),
+                     n_pairs=n_pairs, n_single=(k1 - k0) - n_pairs,
+                     w_in=np.ascontiguousarray(modal.w_in[:, cols]),
+                     w_out=np.ascontiguousarray(modal.w_out[cols, :]), kron_b=modal.kron_b)
+
+
+class EngineOps:
+    """Device primitives of one rank on top of FDEngine (libkhb200 kernels)."""
+
+    def __init__(self, engine):
+        self.e = engine
+
+    def factor(self, events=None):
+        self.e.factored = False
+        self.e.factor(events=events)
+
+    def apply_local(self, F):
+        """G = F W_in_local; Z = solves (stays in the engine)."""
+        e = self.e
+        n, nt, nk2 = e.n, e.n_t, 2 * e.n_k
+        if nk2:
+            e._gemm(n, nk2, nt, 1.0, F.data_ptr(), n, e.w_in.data_ptr(), nt, 0.0, e.G.data_ptr(), n)
+            e._spatial()
+
+    def out_chunk(self, r0, rows, dst, ldd):
+        """dst (rows x N_t, ld ldd) = Z[r0:r0+rows, :] W_out_local."""
+        e = self.e
+        nk2 = 2 * e.n_k
+        if nk2 == 0:
+            dst.zero_()
+            return
+        e._gemm(rows, e.n_t, nk2, 1.0, e.Z.data_ptr() + 8 * r0, e.n, e.w_out.data_ptr(), nk2, 0.0,
+                dst.data_ptr(), ldd)
+
+    def y_shard(self, U_shard, rows, ld, dst):
+        """dst (rows x 2N_t, ld) = U_shard [A_t^T | M_t^T]."""
+        e = self.e
+        e._gemm(rows, 2 * e.n_t, e.n_t, 1.0, U_shard.data_ptr(), ld, e.kron_b.data_ptr(), e.n_t, 0.0,
+                dst.data_ptr(), ld)
+
+    def residual_full(self, Y, F):
+        """R (engine buffer) = F - (M Y1 + A Y2); returns (R, rel residual)."""
+        e = self.e
+        e.plan.residual(e.n_t, Y.data_ptr(), e.n, F.data_ptr(), e.n, e.R.data_ptr(), e.n, e.norms.data_ptr(),
+                        e._stream())
+        return e.R, e._rel(e.norms[:2])
+
+    def axpy_(self, y, x):
+        from . import _native
+
+        _native.call("kh_daxpy", y.numel(), 1.0, x.data_ptr(), y.data_ptr(), self.e._stream())
+
+
+class ShardedFD:
+    """FD over `world` ranks of torch.distributed (row-sharded result)."""
+
+    def __init__(self, M_x, A_x, modal, rank, world, device=None, leaf_size=None, ops=None, group=None,
+                 engine_kwargs=None):
+        import torch
+
+        self.rank, self.world, self.group = rank, world, group
+        self.k0, self.k1 = shard_range(modal.n_k, world, rank)
+        self.local = restrict_modal(modal, self.k0, self.k1)
+        self.n = M_x.shape[0]
+        self.n_t = modal.n_t
+        self.rp = row_chunk(self.n, world)
+        if ops is None:
+            from . import sparse_direct
+            from .engine import FDEngine
+
+            kw = dict(engine_kwargs or {})
+            if leaf_size is not None:
+                kw["leaf_size"] = leaf_size
+            else:
+                kw.setdefault("leaf_size", sparse_direct.DEFAULT_LEAF_SIZE)
+            self.engine = FDEngine(M_x, A_x, self.local, device=device, **kw)
+            ops = EngineOps(self.engine)
+            dev = self.engine.device
+        else:
+            self.engine = getattr(ops, "engine", None)
+            dev = getattr(ops, "device", torch.device("cpu"))
+        self.ops = ops
+        f64 = torch.float64
+        g, rp, nt = world, self.rp, self.n_t
+        self.P = torch.zeros((g, nt, rp), dtype=f64, device=dev)     # partial chunks, col-major rp x N_t each
+        self.U = torch.zeros((nt, rp), dtype=f64, device=dev)        # this rank's rows of u
+        self.D = torch.zeros((nt, rp), dtype=f64, device=dev)        # correction shard
+        self.Ys = torch.zeros((2 * nt, rp), dtype=f64, device=dev)
+        self.Yall = torch.zeros((g, 2 * nt, rp), dtype=f64, device=dev)
+        self.Y = torch.zeros((2 * nt, self.n), dtype=f64, device=dev)  # col-major n x 2N_t
+        self.gpu_launches = 0
+
+    def rows(self, c):
+        r0 = c * self.rp
+        return r0, max(0, min(self.n, r0 + self.rp) - r0)
+
+    def _apply(self, F, out):
+        """out (this rank's rows) = FD(F), F full (col-major n x N_t)."""
+        import torch.distributed as dist
+
+        self.ops.apply_local(F)
+        for c in range(self.world):
+            r0, rows = self.rows(c)
+            if rows < self.rp:
+                self.P[c].zero_()
+            if rows:
+                self.ops.out_chunk(r0, rows, self.P[c], self.rp)
+        dist.reduce_scatter_tensor(out.view(-1), self.P.view(-1), group=self.group)
+
+    def _residual(self):
+        import torch.distributed as dist
+
+        r0, rows = self.rows(self.rank)
+        if rows:
+            self.ops.y_shard(self.U, rows, self.rp, self.Ys)
+        dist.all_gather_into_tensor(self.Yall.view(-1), self.Ys.view(-1), group=self.group)
+        # chunked (g, 2N_t, rp) -> column-major n x 2N_t
+        self.Y.copy_(self.Yall.permute(1, 0, 2).reshape(2 * self.n_t, self.world * self.rp)[:, :self.n])
+        return self.ops.residual_full(self.Y, self._F)
+
+    def solve(self, F, refine=3, tol=1e-13, factor_events=None):
+        """Returns (U_shard, info): U_shard is (N_t, rp) = column-major rows
+        [rank*rp, rank*rp + rows) of u."""
+        self._F = F
+        self.ops.factor(factor_events)
+        self._apply(F, self.U)
+        R, rel = self._residual()
+        info = {"residuals": [rel], "refine_steps": 0, "imag_residue": 0.0}
+        steps = 0
+        while rel > tol and steps < refine:
+            self._apply(R, self.D)
+            self.ops.axpy_(self.U, self.D)
+            steps += 1
+            R, new = self._residual()
+            info["residuals"].append(new)
+            stalled = not new < rel
+            rel = new
+            if stalled:
+                break
+        info["refine_steps"] = steps
+        info["residual"] = rel
+        return self.U, info
+
+    def gather(self):
+        """Full u (column-major n x N_t as an (N_t, n) tensor) on every rank."""
+        import torch
+        import torch.distributed as dist
+
+        allU = torch.zeros((self.world, self.n_t, self.rp), dtype=self.U.dtype, device=self.U.device)
+        dist.all_gather_into_tensor(allU.view(-1), self.U.view(-1), group=self.group)
+        return allU.permute(1, 0, 2).reshape(self.n_t, self.world * self.rp)[:, :self.n].contiguous()
