@@ -58,6 +58,17 @@ struct kh_plan {
   std::vector<int32_t> cls_off;    // 4 per level: class starts (m<=32, m<=64, large) relative to level_off[d]
   std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
+  // large-front schedule: per level an assembly list and per 32-wide pivot
+  // block the diag / left-looking / TRSM lists (offsets into btasks, int32s)
+  struct KbInfo {
+    int32_t diag_off, diag_n, lupd_off, lupd_n, trsm_off, trsm_n;
+  };
+  struct BigLevel {
+    int32_t asm_off, asm_n, kb_off, nkb;
+  };
+  std::vector<BigLevel> big;
+  std::vector<KbInfo> kbinfo;
+  int32_t* btasks = nullptr;
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -100,7 +111,7 @@ void plan_release(kh_plan* p) {
   void* ptrs[] = {p->fronts, p->child_list, p->relind, p->orig_dst, p->level_fronts, p->urows, p->orig_src,
                   p->perm, p->indptr, p->indices, p->mv, p->av, p->panels, p->upd[0], p->upd[1], p->rupd[0],
                   p->rupd[1], p->y, p->lam, p->minpiv_work, p->absmax_work, p->minpiv, p->absmax,
-                  p->resid_part, p->tasks, p->cmap};
+                  p->resid_part, p->tasks, p->cmap, p->btasks};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -331,6 +342,47 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     }
     p->task_off.push_back((int32_t)(tasks.size() / 3));
   }
+  std::vector<int32_t> bt;
+  for (size_t d = 0; d < S.levels.size(); ++d) {
+    std::vector<int32_t> large(lf.begin() + p->level_off[d] + p->cls_off[4 * d + 2], lf.begin() + p->level_off[d + 1]);
+    kh_plan::BigLevel L{};
+    L.asm_off = (int32_t)bt.size();
+    int32_t nkb = 0;
+    for (int32_t f : large) {
+      const kh::Front& F = S.fronts[f];
+      for (int32_t idx0 = 0; idx0 < F.m() * F.p; idx0 += KH_ASM_CHUNK) bt.insert(bt.end(), {f, idx0});
+      nkb = std::max(nkb, (F.p + 31) / 32);
+    }
+    L.asm_n = ((int32_t)bt.size() - L.asm_off) / 2;
+    L.kb_off = (int32_t)p->kbinfo.size();
+    L.nkb = nkb;
+    for (int32_t kbi = 0; kbi < nkb; ++kbi) {
+      const int32_t kb = 32 * kbi;
+      kh_plan::KbInfo K{};
+      K.diag_off = (int32_t)bt.size();
+      for (int32_t f : large)
+        if (S.fronts[f].p > kb) bt.push_back(f);
+      K.diag_n = (int32_t)bt.size() - K.diag_off;
+      K.lupd_off = (int32_t)bt.size();
+      if (kb > 0)
+        for (int32_t f : large) {
+          const kh::Front& F = S.fronts[f];
+          if (F.p <= kb) continue;
+          for (int32_t i0 = (kb / 64) * 64; i0 < F.m(); i0 += 64) bt.insert(bt.end(), {f, i0});
+        }
+      K.lupd_n = ((int32_t)bt.size() - K.lupd_off) / 2;
+      K.trsm_off = (int32_t)bt.size();
+      for (int32_t f : large) {
+        const kh::Front& F = S.fronts[f];
+        if (F.p <= kb) continue;
+        const int32_t start = kb + std::min(32, F.p - kb);
+        for (int32_t i0 = (start / 64) * 64; i0 < F.m(); i0 += 64) bt.insert(bt.end(), {f, i0});
+      }
+      K.trsm_n = ((int32_t)bt.size() - K.trsm_off) / 2;
+      p->kbinfo.push_back(K);
+    }
+    p->big.push_back(L);
+  }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t x) {
     if (e == cudaSuccess) e = x;
@@ -344,6 +396,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   chk(upload(&p->orig_dst, S.orig_dst.data(), S.orig_dst.size()));
   chk(upload(&p->level_fronts, lf.data(), lf.size()));
   chk(upload(&p->tasks, tasks.data(), tasks.size()));
+  chk(upload(&p->btasks, bt.data(), bt.size()));
   chk(upload(&p->perm, S.perm.data(), S.perm.size()));
   chk(upload(&p->indptr, indptr, (size_t)S.n + 1));
   chk(upload(&p->indices, indices, (size_t)S.nnz));
@@ -403,9 +456,17 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
                                    p->minpiv_work, st));
     KH_CUDA(kh_launch_factor_small(64, T, lev + co[1], co[2] - co[1], ns, p->lam, panels, uc, sc, uch, sch,
                                    p->minpiv_work, st));
-    KH_CUDA(kh_launch_factor_level(T, lev + co[2], co[3] - co[2], p->tasks + 3 * p->task_off[d],
-                                   p->task_off[d + 1] - p->task_off[d], ns, p->lam, panels, uc, sc, uch, sch,
-                                   p->minpiv_work, st));
+    const kh_plan::BigLevel& B = p->big[d];
+    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
+    for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
+      const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
+      const int kb = 32 * kbi;
+      if (kb > 0) KH_CUDA(kh_launch_big_lupdate(T, p->btasks + K.lupd_off, K.lupd_n, kb, ns, panels, st));
+      KH_CUDA(kh_launch_big_diag(T, p->btasks + K.diag_off, K.diag_n, kb, ns, panels, p->minpiv_work, st));
+      KH_CUDA(kh_launch_big_trsm(T, p->btasks + K.trsm_off, K.trsm_n, kb, ns, panels, st));
+    }
+    KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
+                            sc, uch, sch, st));
   }
   KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));
   KH_CUDA(kh_launch_shift_absmax_nnz(p->mv, p->av, p->nnz, (int32_t)nshift, p->lam, p->absmax_work,
@@ -458,16 +519,20 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   const double2* panels = p->panels + slot0 * p->panel_total;
   const int32_t ns = (int32_t)nshift;
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
+  // fronts with m <= 64 (classes 0 and 1) use the warp-per-front kernels
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
-    KH_CUDA(kh_launch_fwd_level(T, lev, nlev, ns, panels, p->y, p->rupd[d & 1], p->rupd_size[d & 1],
-                                p->rupd[(d + 1) & 1], p->rupd_size[(d + 1) & 1], st));
+    const int32_t* co = p->cls_off.data() + 4 * d;
+    double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
+    const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
+    KH_CUDA(kh_launch_fwd_small(T, lev, co[2], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(kh_launch_fwd_level(T, lev + co[2], co[3] - co[2], ns, panels, p->y, rc, sc, rch, sch, st));
   }
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t nlev = p->level_off[d + 1] - p->level_off[d];
-    KH_CUDA(kh_launch_bwd_level(T, lev, nlev, ns, p->max_p, panels, p->y, st));
+    const int32_t* co = p->cls_off.data() + 4 * d;
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[2], ns, panels, p->y, st));
+    KH_CUDA(kh_launch_bwd_level(T, lev + co[2], co[3] - co[2], ns, p->max_p, panels, p->y, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
   return KH_OK;

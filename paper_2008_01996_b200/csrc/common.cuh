@@ -18,10 +18,10 @@ KH_DEV double2 cfms(double2 a, double2 b, double2 c) {
   return make_double2(a.x - b.x * c.x + b.y * c.y, a.y - b.x * c.y - b.y * c.x);
 }
 KH_DEV double2 cinv(double2 a) {
-  // Smith-style scaling is unnecessary here: pivots are O(1) after the
-  // reference's threshold check; use the plain formula in fp64.
-  double den = a.x * a.x + a.y * a.y;
-  return make_double2(a.x / den, -a.y / den);
+  // One IEEE reciprocal instead of two divisions. Smith-style scaling is
+  // unnecessary: pivots passing the reference's threshold check are O(1).
+  const double r = 1.0 / (a.x * a.x + a.y * a.y);
+  return make_double2(a.x * r, -a.y * r);
 }
 KH_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 

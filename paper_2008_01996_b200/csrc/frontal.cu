@@ -205,14 +205,23 @@ struct CpStage {
   double2 d[KC];
 };
 
-// acc(i, j) = sum_{k<K} A[i + k*lda] * d_k * B[j + k*ldb]   (i < rowsA, j < rowsB)
-// with d_k = D[k * ldd] (the pivots on the panel diagonal). Two-stage
-// cp.async ring: the next chunk streams in while DMMA consumes the current
-// one; out-of-range rows and k are zero-filled by the copy itself. The
+// acc(i, j) = sum_{k<K} A[i + k*lda] * s_k * B(j, k)   (i < rowsA, j < rowsB)
+// on a 64 x (16 NWJ) tile computed by 2 x NWJ warps (64 NWJ threads).
+//  MODE_SCALED: B(j, k) = B[j + k*ldb], s_k = d_k = D[k*ldd] (the pivots on the
+//               panel diagonal): Schur complements and left-looking updates.
+//  MODE_TRSM:   B(j, k) = B[k + j*ldb] for k < j, else 0, s_k = 1: the strictly
+//               lower unit-triangular inverse stored transposed in the upper
+//               triangle of a factored 32 x 32 diagonal block.
+// Two-stage cp.async ring: the next chunk streams in while DMMA consumes the
+// current one; out-of-range operands are zero-filled by the copy itself. The
 // pivot scaling is applied to the B fragments in registers.
+constexpr int MODE_SCALED = 0, MODE_TRSM = 1;
+
+template <int NWJ, int MODE>
 KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t lda, int rowsA,
                         const double2* __restrict__ B, int64_t ldb, int rowsB, const double2* __restrict__ D,
                         int64_t ldd, CpStage* st) {
+  constexpr int NTH = 64 * NWJ, TN = 16 * NWJ;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wi = warp & 1, wj = warp >> 1;
@@ -226,16 +235,27 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
   auto load = [&](int s, int c) {
     CpStage& S = st[s];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * NT;
+    for (int r = 0; r < (TB * KC) / NTH; ++r) {
+      const int idx = tid + r * NTH;
       const int i = idx & (TB - 1), k = idx >> 6;
       const int kk = c * KC + k;
-      const bool okk = kk < K;
-      const bool oa = okk && i < rowsA, ob = okk && i < rowsB;
+      const bool oa = kk < K && i < rowsA;
       cp_async16(&S.a[k * LDS + i], oa ? A + i + (int64_t)kk * lda : A, oa);
-      cp_async16(&S.b[k * LDS + i], ob ? B + i + (int64_t)kk * ldb : B, ob);
     }
-    if (tid < KC) {
+#pragma unroll
+    for (int r = 0; r < (TN * KC) / NTH; ++r) {
+      const int idx = tid + r * NTH;
+      const int j = idx % TN, k = idx / TN;
+      const int kk = c * KC + k;
+      if (MODE == MODE_SCALED) {
+        const bool ob = kk < K && j < rowsB;
+        cp_async16(&S.b[k * LDS + j], ob ? B + j + (int64_t)kk * ldb : B, ob);
+      } else {
+        const bool ob = kk < K && j < rowsB && kk < j;
+        cp_async16(&S.b[k * LDS + j], ob ? B + kk + (int64_t)j * ldb : B, ob);
+      }
+    }
+    if (MODE == MODE_SCALED && tid < KC) {
       const int kk = c * KC + tid;
       cp_async16(&S.d[tid], kk < K ? D + (int64_t)kk * ldd : D, kk < K);
     }
@@ -253,9 +273,11 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
       double2 af[4], bf[2];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) af[mt] = S.a[(kk + t) * LDS + wi * 32 + mt * 8 + g];
-      const double2 dk = S.d[kk + t];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = cmul(S.b[(kk + t) * LDS + wj * 16 + nt * 8 + g], dk);
+      for (int nt = 0; nt < 2; ++nt) {
+        bf[nt] = S.b[(kk + t) * LDS + wj * 16 + nt * 8 + g];
+        if (MODE == MODE_SCALED) bf[nt] = cmul(bf[nt], S.d[kk + t]);
+      }
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
         const double nai = -af[mt].y;
@@ -271,6 +293,51 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
     __syncthreads();
   }
   cp_async_wait<0>();
+}
+
+KH_DEV double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// One warp factors the w x w (w <= 32) diagonal block at B (column-major, ld
+// m) in registers: lane i holds row i, pivot k is broadcast by shuffles, so
+// the block costs no CTA barriers. Writes L (unit lower) and D back to B, a
+// row-major copy to sd (ld NB+1) and 1/d_k to dinv. Returns min |d_k| on
+// lane 0 (-1 if a pivot is not finite).
+KH_DEV double warp_ldlt_block(double2* B, int64_t m, int w, double2* sd, double2* dinv) {
+  const int lane = threadIdx.x & 31;
+  double2 a[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+    a[j] = (lane < w && j <= lane) ? B[lane + (int64_t)j * m] : make_double2(0.0, 0.0);
+  double minp = DBL_MAX;
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    if (k < w) {
+      const double2 dk = shfl2(a[k], k);
+      const double2 di = cinv(dk);
+      const double2 lik = cmul(a[k], di);
+#pragma unroll
+      for (int j = k + 1; j < NB; ++j) {
+        const double2 ajk = shfl2(a[k], j);
+        if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
+      }
+      if (lane > k && lane < w) a[k] = lik;
+      if (lane == 0) {
+        dinv[k] = di;
+        const double ad = sqrt(cabs2(dk));
+        minp = (ad != ad) ? -1.0 : fmin(minp, ad);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+    if (lane < w && j <= lane) {
+      B[lane + (int64_t)j * m] = a[j];
+      sd[lane * (NB + 1) + j] = a[j];
+    }
+  __syncwarp();
+  return minp;
 }
 
 struct FactorSmem {
@@ -312,25 +379,32 @@ __global__ void __launch_bounds__(NT, 2) factor_panel_kernel(KhTree T, const int
   __shared__ Kids kids;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
   __syncthreads();
-  for (int c = 0; c < p; ++c) {
-    for (int r0 = c + tid; r0 < m; r0 += 4 * NT) {
-      double2 v[4];
+  {
+    // flat walk over the m x p panel, 8 independent entries per thread in flight
+    const int total = m * p;
+    for (int base = tid; base < total; base += 8 * NT) {
+      int rr[8], cc[8];
+      double2 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = make_double2(0.0, 0.0);
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * NT;
+        cc[u] = idx / m;
+        rr[u] = idx - cc[u] * m;
+        v[u] = make_double2(0.0, 0.0);
+      }
       for (int k = 0; k < kids.n; ++k) {
         const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-        const int cj = C.cmap[c];
-        if (cj < 0) continue;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int r = r0 + u * NT;
-          const int ci = r < m ? C.cmap[r] : -1;
-          if (ci >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
+        for (int u = 0; u < 8; ++u) {
+          if (base + u * NT < total && rr[u] >= cc[u]) {
+            const int ci = C.cmap[rr[u]], cj = C.cmap[cc[u]];
+            if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
+          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (r0 + u * NT < m) P[(r0 + u * NT) + (int64_t)c * m] = v[u];
+      for (int u = 0; u < 8; ++u)
+        if (base + u * NT < total && rr[u] >= cc[u]) P[base + u * NT] = v[u];
     }
   }
   __syncthreads();
@@ -344,7 +418,7 @@ __global__ void __launch_bounds__(NT, 2) factor_panel_kernel(KhTree T, const int
     const int w = min(NB, p - kb);
     if (kb > 0) {
       for (int i0 = kb; i0 < m; i0 += TB) {
-        tile_mma_cp(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, S.st);
+        tile_mma_cp<4, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, S.st);
         tile_epilogue(acc, [&](int i, int j, double2 v) {
           const int r = i0 + i;
           if (r < m && j < w && r >= kb + j) {
@@ -355,35 +429,11 @@ __global__ void __launch_bounds__(NT, 2) factor_panel_kernel(KhTree T, const int
       }
       __syncthreads();
     }
-    for (int idx = tid; idx < w * w; idx += NT) {
-      int i = idx % w, j = idx / w;
-      S.d[i * (NB + 1) + j] = i >= j ? P[(kb + i) + (int64_t)(kb + j) * m] : make_double2(0.0, 0.0);
+    if (tid < 32) {
+      const double mp = warp_ldlt_block(P + kb + (int64_t)kb * m, m, w, S.d, S.dinv);
+      if (tid == 0) minp = fmin(minp, mp);  // -1 (non-finite pivot) is sticky
     }
     __syncthreads();
-    for (int k = 0; k < w; ++k) {
-      const double2 dk = S.d[k * (NB + 1) + k];
-      const double2 di = cinv(dk);
-      const int r = w - k - 1;
-      for (int idx = tid; idx < r * r; idx += NT) {
-        int i = k + 1 + idx % r, j = k + 1 + idx / r;
-        if (i >= j) {
-          double2 lik = cmul(S.d[i * (NB + 1) + k], di);
-          S.d[i * (NB + 1) + j] = cfms(S.d[i * (NB + 1) + j], lik, S.d[j * (NB + 1) + k]);
-        }
-      }
-      __syncthreads();
-      for (int i = k + 1 + tid; i < w; i += NT) S.d[i * (NB + 1) + k] = cmul(S.d[i * (NB + 1) + k], di);
-      if (tid == 0) {
-        S.dinv[k] = di;
-        double ad = sqrt(cabs2(dk));
-        minp = (ad != ad) ? -1.0 : fmin(minp, ad);  // NaN pivots are reported as -1
-      }
-      __syncthreads();
-    }
-    for (int idx = tid; idx < w * w; idx += NT) {
-      int i = idx % w, j = idx / w;
-      if (i >= j) P[(kb + i) + (int64_t)(kb + j) * m] = S.d[i * (NB + 1) + j];
-    }
     // explicit inverse of the unit-lower block, row by row
     for (int idx = tid; idx < NB * NB; idx += NT) {
       int i = idx / NB, j = idx % NB;
@@ -435,7 +485,7 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
   Acc acc;
-  tile_mma_cp(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
+  tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
   // U = (children's contributions, pulled) - L21 D L21^T
   tile_epilogue(acc, [&](int i, int j, double2 v) {
     const int r = i0 + i, c = j0 + j;
@@ -447,6 +497,184 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
         if (ci >= 0 && cj >= 0) s = cadd(s, C.U[ci + (int64_t)cj * C.q]);
       }
       U[r + (int64_t)c * q] = csub(s, v);
+    }
+  });
+}
+
+// ---- large fronts, level-synchronous batched kernels ------------------------------
+// For the fronts with m > 64 of one level, the factorization is a sequence of
+// launches, each covering every (front, shift) of the level at once:
+//   big_assemble   (front, 2048-entry chunk): P = pulled children + originals
+//   for each 32-wide pivot block kb:
+//     big_lupdate  (front, 64-row tile): P[:, kb:kb+w] -= L[:, :kb] D L[kb:kb+w, :kb]^T   (DMMA, K = kb)
+//     big_diag     warp per (front, shift): LDL^T of the w x w diagonal block in shared
+//                  memory; L and D in place, L^-1 (strict part) transposed into the
+//                  otherwise unused upper triangle of the block
+//     big_trsm     (front, 64-row tile): L[r, kb:kb+w] = (A[r, kb:kb+w] L^-T) D^-1   (DMMA)
+//   schur_update   (front, 64x64 tile of U): U = pulled children - L21 D L21^T       (DMMA)
+// Tasks are int32 pairs (front, index) prepared on the host per level and block.
+constexpr int ASM_CHUNK = 2048;
+
+__global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                          const double2* __restrict__ lam, double2* panels,
+                                                          const double2* __restrict__ upd_child,
+                                                          int64_t upd_stride_child) {
+  __shared__ Kids kids;
+  const int tid = threadIdx.x;
+  const int32_t f = tasks[2 * blockIdx.x];
+  const int idx0 = tasks[2 * blockIdx.x + 1];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q;
+  const int total = min(m * p, idx0 + ASM_CHUNK);
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  __syncthreads();
+  int rr[ASM_CHUNK / NT], cc[ASM_CHUNK / NT];
+  double2 v[ASM_CHUNK / NT];
+#pragma unroll
+  for (int u = 0; u < ASM_CHUNK / NT; ++u) {
+    const int idx = idx0 + tid + u * NT;
+    cc[u] = idx / m;
+    rr[u] = idx - cc[u] * m;
+    v[u] = make_double2(0.0, 0.0);
+  }
+  for (int k = 0; k < kids.n; ++k) {
+    const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+#pragma unroll
+    for (int u = 0; u < ASM_CHUNK / NT; ++u) {
+      if (idx0 + tid + u * NT < total && rr[u] >= cc[u]) {
+        const int ci = C.cmap[rr[u]], cj = C.cmap[cc[u]];
+        if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < ASM_CHUNK / NT; ++u)
+    if (idx0 + tid + u * NT < total && rr[u] >= cc[u]) P[idx0 + tid + u * NT] = v[u];
+  __syncthreads();
+  // originals whose (sorted) destinations fall into this chunk
+  int64_t lo = F.orig_begin, hi = F.orig_end;
+  {
+    int64_t a = lo, z = hi;
+    while (a < z) {
+      const int64_t mid = (a + z) >> 1;
+      if (T.orig_dst[mid] < idx0) a = mid + 1;
+      else z = mid;
+    }
+    lo = a;
+    z = hi;
+    while (a < z) {
+      const int64_t mid = (a + z) >> 1;
+      if (T.orig_dst[mid] < total) a = mid + 1;
+      else z = mid;
+    }
+    hi = a;
+  }
+  const double2 L = lam[b];
+  for (int64_t e = lo + tid; e < hi; e += NT) {
+    const int64_t s = T.orig_src[e];
+    const int d = T.orig_dst[e];
+    P[d] = cadd(P[d], make_double2(fma(L.x, T.av[s], T.mv[s]), L.y * T.av[s]));
+  }
+}
+
+__global__ void __launch_bounds__(128) big_lupdate_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
+                                                          double2* panels) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+  const int32_t f = tasks[2 * blockIdx.x];
+  const int i0 = tasks[2 * blockIdx.x + 1];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  Acc acc;
+  tile_mma_cp<2, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, st);
+  tile_epilogue(acc, [&](int i, int j, double2 v) {
+    const int r = i0 + i, c = kb + j;
+    if (r < m && j < w && r >= c) {
+      double2* d = P + r + (int64_t)c * m;
+      *d = csub(*d, v);
+    }
+  });
+}
+
+// One warp per (front, shift): factor the w x w diagonal block at kb.
+constexpr int DIAG_WARPS = 4;
+__global__ void __launch_bounds__(32 * DIAG_WARPS) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
+                                                                   int nfr, int kb, double2* panels,
+                                                                   double* minpiv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int idx = blockIdx.x * DIAG_WARPS + wid;
+  if (idx >= nfr) return;
+  double2* S = reinterpret_cast<double2*>(smem_raw) + wid * NB * (NB + 1);  // row-major, ld NB+1
+  const int32_t f = fronts[idx];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
+  double2* B = panels + (int64_t)b * T.panel_total + F.panel_off + kb + (int64_t)kb * m;
+  // load: lane = column j (coalesced along rows i)
+  for (int j = 0; j < w; ++j)
+    if (lane < w) S[lane * (NB + 1) + j] = lane >= j ? B[lane + (int64_t)j * m] : make_double2(0.0, 0.0);
+  __syncwarp();
+  double minp = DBL_MAX;
+  for (int k = 0; k < w; ++k) {
+    const double2 dk = S[k * (NB + 1) + k];
+    const double2 di = cinv(dk);
+    if (lane > k && lane < w) {
+      const double2 lik = cmul(S[lane * (NB + 1) + k], di);
+      for (int j = k + 1; j <= lane; ++j)
+        S[lane * (NB + 1) + j] = cfms(S[lane * (NB + 1) + j], lik, S[j * (NB + 1) + k]);
+    }
+    __syncwarp();
+    if (lane > k && lane < w) S[lane * (NB + 1) + k] = cmul(S[lane * (NB + 1) + k], di);
+    const double ad = sqrt(cabs2(dk));
+    minp = (ad != ad) ? -1.0 : fmin(minp, ad);
+    __syncwarp();
+  }
+  // write L (strict lower) and D back
+  for (int j = 0; j < w; ++j)
+    if (lane < w && lane >= j) B[lane + (int64_t)j * m] = S[lane * (NB + 1) + j];
+  // L^-1: lane j computes column j (x_j = 1, x_i = -sum_{k=j}^{i-1} L[i][k] x_k),
+  // keeping x_i in the free upper triangle of its own row of S, then stores
+  // Linv[i][j] (i > j) transposed at block position (j, i)
+  if (lane < w) {
+    double2* x = S + lane * (NB + 1);
+    for (int i = lane + 1; i < w; ++i) {
+      double2 s = make_double2(-S[i * (NB + 1) + lane].x, -S[i * (NB + 1) + lane].y);
+      for (int k = lane + 1; k < i; ++k) s = cfms(s, S[i * (NB + 1) + k], x[k]);
+      x[i] = s;
+    }
+    for (int i = lane + 1; i < w; ++i) B[lane + (int64_t)i * m] = x[i];
+  }
+  if (lane == 0) {
+    double* mp = minpiv + (int64_t)b * T.nf + f;
+    *mp = kb == 0 ? minp : fmin(*mp, minp);
+  }
+}
+
+__global__ void __launch_bounds__(128) big_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
+                                                       double2* panels) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+  const int32_t f = tasks[2 * blockIdx.x];
+  const int i0 = tasks[2 * blockIdx.x + 1];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  const double2* Bk = P + kb + (int64_t)kb * m;
+  Acc acc;
+  // acc = sum_{k<j} A[r, kb+k] Linv[j][k]; the unit diagonal term is added below
+  tile_mma_cp<2, MODE_TRSM>(acc, w, P + i0 + (int64_t)kb * m, m, m - i0, Bk, m, w, nullptr, 0, st);
+  tile_epilogue(acc, [&](int i, int j, double2 v) {
+    const int r = i0 + i;
+    if (r < m && r >= kb + w && j < w) {
+      double2* d = P + r + (int64_t)(kb + j) * m;
+      const double2 dj = Bk[j + (int64_t)j * m];
+      *d = cmul(cadd(v, *d), cinv(dj));
     }
   });
 }
@@ -625,6 +853,94 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
   }
 }
 
+// ---- warp-per-front solves for fronts with m <= 64 ------------------------------
+// Lane l owns front rows l and l + 32. No block barriers: pivots are broadcast
+// with shuffles and every column of the panel is read with one coalesced load.
+KH_DEV double2 warp_sum2(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+                                                        const double2* __restrict__ panels, double2* y, double2* ru_cur,
+                                                        int64_t ru_stride_cur, const double2* __restrict__ ru_child,
+                                                        int64_t ru_stride_child) {
+  const int lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (idx >= nlev) return;
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[level_fronts[idx]];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  const int r0 = lane, r1 = lane + 32;
+  double2 x0 = make_double2(0.0, 0.0), x1 = make_double2(0.0, 0.0);
+  for (int c = F.child_begin; c < F.child_end; ++c) {
+    const KhDevFront C = T.fronts[T.child_list[c]];
+    const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+    const int32_t* cm = T.cmap + C.cmap_begin;
+    const int c0 = r0 < m ? cm[r0] : -1;
+    const int c1 = r1 < m ? cm[r1] : -1;
+    if (c0 >= 0) x0 = cadd(x0, rc[c0]);
+    if (c1 >= 0) x1 = cadd(x1, rc[c1]);
+  }
+  if (r0 < p) x0 = cadd(x0, yy[r0]);
+  if (r1 < p) x1 = cadd(x1, yy[r1]);
+  for (int k = 0; k < p; ++k) {
+    const double2 l0 = (r0 > k && r0 < m) ? P[r0 + (int64_t)k * m] : make_double2(0.0, 0.0);
+    const double2 l1 = (r1 > k && r1 < m) ? P[r1 + (int64_t)k * m] : make_double2(0.0, 0.0);
+    const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
+    x0 = cfms(x0, l0, yk);
+    x1 = cfms(x1, l1, yk);
+  }
+  if (r0 < p) yy[r0] = x0;
+  else if (r0 < m) ru[r0 - p] = x0;
+  if (r1 < p) yy[r1] = x1;
+  else if (r1 < m) ru[r1 - p] = x1;
+}
+
+__global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+                                                        const double2* __restrict__ panels, double2* y) {
+  const int lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (idx >= nlev) return;
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[level_fronts[idx]];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  const int64_t* urows = T.urows + F.rows_begin;
+  // solution values of the update rows (already final: ancestors are done)
+  const double2 xu0 = lane < q ? yb[urows[lane]] : make_double2(0.0, 0.0);
+  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : make_double2(0.0, 0.0);
+  // lane k (and k+32) owns pivot k: t_k = y_k / d_k - sum_a L21[a, k] xu[a].
+  // Row form: xu[a] is broadcast and every lane updates its own t_k, so there
+  // is no reduction on the dependency chain; the strided panel reads hit L1
+  // (a front's panel is a few tens of KB and every line is reused).
+  const int k0 = lane, k1 = lane + 32;
+  double2 t0 = k0 < p ? cmul(yy[k0], cinv(P[k0 + (int64_t)k0 * m])) : make_double2(0.0, 0.0);
+  double2 t1 = k1 < p ? cmul(yy[k1], cinv(P[k1 + (int64_t)k1 * m])) : make_double2(0.0, 0.0);
+  for (int a = 0; a < q; ++a) {
+    const double2 xa = shfl2(a < 32 ? xu0 : xu1, a & 31);
+    if (k0 < p) t0 = cfms(t0, P[p + a + (int64_t)k0 * m], xa);
+    if (k1 < p) t1 = cfms(t1, P[p + a + (int64_t)k1 * m], xa);
+  }
+  // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for j < i
+  for (int i = p - 1; i > 0; --i) {
+    const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
+    if (k0 < i) t0 = cfms(t0, P[i + (int64_t)k0 * m], xi);
+    if (k1 < i) t1 = cfms(t1, P[i + (int64_t)k1 * m], xi);
+  }
+  if (k0 < p) yy[k0] = t0;
+  if (k1 < p) yy[k1] = t1;
+}
+
 // ---- backward solve: x <- L^{-T} D^{-1} y, fronts top-down -------------------
 __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                        const double2* __restrict__ panels, double2* y) {
@@ -745,6 +1061,68 @@ __global__ void rowreduce_kernel(const double* __restrict__ in, int64_t len, int
 
 }  // namespace
 
+cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+                                   const double2* lam, double2* panels, const double2* upd_child,
+                                   int64_t upd_stride_child, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_child, upd_stride_child);
+  return cudaGetLastError();
+}
+
+static cudaError_t set_smem_once(const void* fn, int bytes, bool& done) {
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = (e == cudaSuccess);
+  return e;
+}
+
+cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
+                                  double2* panels, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  static bool done = false;
+  const int smem = (int)(2 * sizeof(CpStage));
+  cudaError_t e = set_smem_once((const void*)big_lupdate_kernel, smem, done);
+  if (e != cudaSuccess) return e;
+  big_lupdate_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t nfr, int kb, int32_t batch,
+                               double2* panels, double* minpiv, cudaStream_t stream) {
+  if (nfr == 0 || batch == 0) return cudaSuccess;
+  static bool done = false;
+  const int smem = DIAG_WARPS * NB * (NB + 1) * (int)sizeof(double2);
+  cudaError_t e = set_smem_once((const void*)big_diag_kernel, smem, done);
+  if (e != cudaSuccess) return e;
+  big_diag_kernel<<<dim3((nfr + DIAG_WARPS - 1) / DIAG_WARPS, batch), 32 * DIAG_WARPS, smem, stream>>>(
+      T, fronts, nfr, kb, panels, minpiv);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
+                               double2* panels, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  static bool done = false;
+  const int smem = (int)(2 * sizeof(CpStage));
+  cudaError_t e = set_smem_once((const void*)big_trsm_kernel, smem, done);
+  if (e != cudaSuccess) return e;
+  big_trsm_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+                            const double2* panels, double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
+                            int64_t upd_stride_child, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  static bool done = false;
+  const int smem = (int)(2 * sizeof(CpStage));
+  cudaError_t e = set_smem_once((const void*)schur_update_kernel, smem, done);
+  if (e != cudaSuccess) return e;
+  schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
+                                                                 upd_child, upd_stride_child);
+  return cudaGetLastError();
+}
+
 cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, const int32_t* tasks,
                                    int32_t ntasks, int32_t batch, const double2* lam, double2* panels,
                                    double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
@@ -766,6 +1144,22 @@ cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts,
   if (e != cudaSuccess || ntasks == 0) return e;
   schur_update_kernel<<<dim3(ntasks, batch), NT, smem_s, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
                                                                    upd_child, upd_stride_child);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
+                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  fwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y, ru_cur,
+                                                                    ru_stride_cur, ru_child, ru_stride_child);
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
+                                const double2* panels, double2* y, cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  bwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y);
   return cudaGetLastError();
 }
 
