@@ -36,6 +36,11 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 constexpr int32_t kDefaultLeaf = 24;
+// fronts with m <= kClassMax[c] use the register-resident kernels; the rest
+// ("large", class kSmallClasses) the level-synchronous DMMA kernels
+constexpr int kSmallClasses = 3;
+constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64};
+constexpr int kClsStride = kSmallClasses + 2;
 constexpr int32_t kAbsmaxBlocks = 64;
 constexpr int32_t kResidualBlocks = 1184;  // 8 x 148 SMs
 
@@ -55,7 +60,10 @@ struct kh_plan {
   int64_t n = 0, nnz = 0, max_batch = 0, slots = 0;
   int32_t nf = 0, max_p = 0;
   std::vector<int32_t> level_off;  // levels d -> [level_off[d], level_off[d+1]) in level_fronts
-  std::vector<int32_t> cls_off;    // 4 per level: class starts (m<=32, m<=64, large) relative to level_off[d]
+  // kClsStride per level: starts of the front classes (m <= 32, 48, 64, large)
+  // relative to level_off[d], plus the end
+  std::vector<int32_t> cls_off;
+  const int32_t* classes(int32_t d) const { return cls_off.data() + kClsStride * d; }
   std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   // large-front schedule: per level an assembly list and per 32-wide pivot
@@ -317,15 +325,17 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
   std::vector<int32_t> lf;
   p->level_off.push_back(0);
+  auto front_class = [&](int32_t m) {
+    for (int c = 0; c < kSmallClasses; ++c)
+      if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
+    return kSmallClasses;  // large
+  };
   for (const auto& lev : S.levels) {
     const int32_t base = (int32_t)lf.size();
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c <= kSmallClasses; ++c) {
       p->cls_off.push_back((int32_t)lf.size() - base);
-      for (int32_t f : lev) {
-        const int32_t m = S.fronts[f].m();
-        const int cls = (m <= 32 && small_max >= 32) ? 0 : ((m <= 64 && small_max >= 64) ? 1 : 2);
-        if (cls == c) lf.push_back(f);
-      }
+      for (int32_t f : lev)
+        if (front_class(S.fronts[f].m()) == c) lf.push_back(f);
     }
     p->cls_off.push_back((int32_t)lf.size() - base);
     p->level_off.push_back((int32_t)lf.size());
@@ -334,7 +344,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   std::vector<int32_t> tasks;
   p->task_off.push_back(0);
   for (size_t d = 0; d < S.levels.size(); ++d) {
-    for (int32_t k = p->level_off[d] + p->cls_off[4 * d + 2]; k < p->level_off[d + 1]; ++k) {
+    for (int32_t k = p->level_off[d] + p->classes(d)[kSmallClasses]; k < p->level_off[d + 1]; ++k) {
       const int32_t f = lf[k];
       const int32_t nt = (S.fronts[f].q + 63) / 64;
       for (int32_t jt = 0; jt < nt; ++jt)
@@ -344,13 +354,14 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   }
   std::vector<int32_t> bt;
   for (size_t d = 0; d < S.levels.size(); ++d) {
-    std::vector<int32_t> large(lf.begin() + p->level_off[d] + p->cls_off[4 * d + 2], lf.begin() + p->level_off[d + 1]);
+    std::vector<int32_t> large(lf.begin() + p->level_off[d] + p->classes(d)[kSmallClasses],
+                               lf.begin() + p->level_off[d + 1]);
     kh_plan::BigLevel L{};
     L.asm_off = (int32_t)bt.size();
     int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
-      for (int32_t idx0 = 0; idx0 < F.m() * F.p; idx0 += KH_ASM_CHUNK) bt.insert(bt.end(), {f, idx0});
+      for (int32_t idx0 = 0; idx0 < F.m() * F.p + F.q * F.q; idx0 += KH_ASM_CHUNK) bt.insert(bt.end(), {f, idx0});
       nkb = std::max(nkb, (F.p + 31) / 32);
     }
     L.asm_n = ((int32_t)bt.size() - L.asm_off) / 2;
@@ -448,16 +459,15 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
   double2* panels = p->panels + slot0 * p->panel_total;
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->cls_off.data() + 4 * d;
+    const int32_t* co = p->classes(d);
     double2 *uc = p->upd[d & 1], *uch = p->upd[(d + 1) & 1];
     const int64_t sc = p->upd_size[d & 1], sch = p->upd_size[(d + 1) & 1];
     const int32_t ns = (int32_t)nshift;
-    KH_CUDA(kh_launch_factor_small(32, T, lev + co[0], co[1] - co[0], ns, p->lam, panels, uc, sc, uch, sch,
-                                   p->minpiv_work, st));
-    KH_CUDA(kh_launch_factor_small(64, T, lev + co[1], co[2] - co[1], ns, p->lam, panels, uc, sc, uch, sch,
-                                   p->minpiv_work, st));
+    for (int c = 0; c < kSmallClasses; ++c)
+      KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
+                                     uch, sch, p->minpiv_work, st));
     const kh_plan::BigLevel& B = p->big[d];
-    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
+    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uc, sc, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
       const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
       const int kb = 32 * kbi;
@@ -519,20 +529,21 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   const double2* panels = p->panels + slot0 * p->panel_total;
   const int32_t ns = (int32_t)nshift;
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
-  // fronts with m <= 64 (classes 0 and 1) use the warp-per-front kernels
+  // fronts with m <= 64 (the small classes) use the warp-per-front kernels
+  constexpr int L = kSmallClasses;
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->cls_off.data() + 4 * d;
+    const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    KH_CUDA(kh_launch_fwd_small(T, lev, co[2], ns, panels, p->y, rc, sc, rch, sch, st));
-    KH_CUDA(kh_launch_fwd_level(T, lev + co[2], co[3] - co[2], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[L + 1] - co[L], ns, panels, p->y, rc, sc, rch, sch, st));
   }
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->cls_off.data() + 4 * d;
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[2], ns, panels, p->y, st));
-    KH_CUDA(kh_launch_bwd_level(T, lev + co[2], co[3] - co[2], ns, p->max_p, panels, p->y, st));
+    const int32_t* co = p->classes(d);
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, st));
+    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[L + 1] - co[L], ns, p->max_p, panels, p->y, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
   return KH_OK;

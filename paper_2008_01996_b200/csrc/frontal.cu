@@ -483,20 +483,17 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   const int p = F.p, q = F.q, m = p + q;
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
-  load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  (void)kids;
+  (void)upd_child;
+  (void)upd_stride_child;
   Acc acc;
   tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
-  // U = (children's contributions, pulled) - L21 D L21^T
+  // U holds the pulled children's contributions (big_assemble): U -= L21 D L21^T
   tile_epilogue(acc, [&](int i, int j, double2 v) {
     const int r = i0 + i, c = j0 + j;
     if (r < q && c < q && r >= c) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int k = 0; k < kids.n; ++k) {
-        const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-        const int ci = C.cmap[p + r], cj = C.cmap[p + c];
-        if (ci >= 0 && cj >= 0) s = cadd(s, C.U[ci + (int64_t)cj * C.q]);
-      }
-      U[r + (int64_t)c * q] = csub(s, v);
+      double2* d = U + r + (int64_t)c * q;
+      *d = csub(*d, v);
     }
   });
 }
@@ -513,30 +510,41 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
 //     big_trsm     (front, 64-row tile): L[r, kb:kb+w] = (A[r, kb:kb+w] L^-T) D^-1   (DMMA)
 //   schur_update   (front, 64x64 tile of U): U = pulled children - L21 D L21^T       (DMMA)
 // Tasks are int32 pairs (front, index) prepared on the host per level and block.
-constexpr int ASM_CHUNK = 2048;
+constexpr int ASM_CHUNK = KH_ASM_CHUNK;
 
 __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                           const double2* __restrict__ lam, double2* panels,
+                                                          double2* upd_cur, int64_t upd_stride_cur,
                                                           const double2* __restrict__ upd_child,
                                                           int64_t upd_stride_child) {
+  // index space of a front: [0, m*p) = panel P (column-major m x p), then
+  // [m*p, m*p + q*q) = update block U (column-major q x q); lower parts only
   __shared__ Kids kids;
   const int tid = threadIdx.x;
   const int32_t f = tasks[2 * blockIdx.x];
   const int idx0 = tasks[2 * blockIdx.x + 1];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q;
-  const int total = min(m * p, idx0 + ASM_CHUNK);
+  const int p = F.p, q = F.q, m = p + q, np = m * p;
+  const int total = min(np + q * q, idx0 + ASM_CHUNK);
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
   __syncthreads();
-  int rr[ASM_CHUNK / NT], cc[ASM_CHUNK / NT];
+  int rr[ASM_CHUNK / NT], cc[ASM_CHUNK / NT];  // front-local row / column
   double2 v[ASM_CHUNK / NT];
 #pragma unroll
   for (int u = 0; u < ASM_CHUNK / NT; ++u) {
     const int idx = idx0 + tid + u * NT;
-    cc[u] = idx / m;
-    rr[u] = idx - cc[u] * m;
+    if (idx < np) {
+      cc[u] = idx / m;
+      rr[u] = idx - cc[u] * m;
+    } else {
+      const int w = idx - np;
+      cc[u] = w / max(q, 1);
+      rr[u] = p + (w - cc[u] * q);
+      cc[u] += p;
+    }
     v[u] = make_double2(0.0, 0.0);
   }
   for (int k = 0; k < kids.n; ++k) {
@@ -550,8 +558,14 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
     }
   }
 #pragma unroll
-  for (int u = 0; u < ASM_CHUNK / NT; ++u)
-    if (idx0 + tid + u * NT < total && rr[u] >= cc[u]) P[idx0 + tid + u * NT] = v[u];
+  for (int u = 0; u < ASM_CHUNK / NT; ++u) {
+    const int idx = idx0 + tid + u * NT;
+    if (idx < total && rr[u] >= cc[u]) {
+      if (idx < np) P[idx] = v[u];
+      else U[idx - np] = v[u];
+    }
+  }
+  if (idx0 >= np) return;  // chunk lies in U: no original entries
   __syncthreads();
   // originals whose (sorted) destinations fall into this chunk
   int64_t lo = F.orig_begin, hi = F.orig_end;
@@ -751,6 +765,7 @@ __global__ void __launch_bounds__(MS * 4) factor_small_kernel(KhTree T, const in
           const double2 li = cmul(buf[i], di);
 #pragma unroll
           for (int c2 = c; c2 < NC; ++c2) {
+            if (4 * c2 >= m) break;  // uniform: slots beyond the front order are dead
             const int j = jg + 4 * c2;
             if (j > k && j <= i) a[c2] = cfms(a[c2], li, buf[j]);
           }
@@ -1062,10 +1077,11 @@ __global__ void rowreduce_kernel(const double* __restrict__ in, int64_t len, int
 }  // namespace
 
 cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
-                                   const double2* lam, double2* panels, const double2* upd_child,
-                                   int64_t upd_stride_child, cudaStream_t stream) {
+                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
+                                   const double2* upd_child, int64_t upd_stride_child, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_child, upd_stride_child);
+  big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_cur, upd_stride_cur,
+                                                              upd_child, upd_stride_child);
   return cudaGetLastError();
 }
 
@@ -1222,21 +1238,29 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   dim3 grid(nlev, batch);
-  constexpr int s32 = (32 * 33 / 2 + 2 * 32) * 16, s64 = (64 * 65 / 2 + 2 * 64) * 16;
+  auto smem = [](int s) { return (s * (s + 1) / 2 + 2 * s) * 16; };
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(factor_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+    cudaError_t e =
+        cudaFuncSetAttribute(factor_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem(64));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (ms == 32) {
-    factor_small_kernel<32><<<grid, 128, s32, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur,
-                                                        upd_child, upd_stride_child, minpiv);
-  } else if (ms == 64) {
-    factor_small_kernel<64><<<grid, 256, s64, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur,
-                                                        upd_child, upd_stride_child, minpiv);
-  } else {
-    return cudaErrorInvalidValue;
+  switch (ms) {
+    case 32:
+      factor_small_kernel<32><<<grid, 128, smem(32), stream>>>(T, level_fronts, lam, panels, upd_cur,
+                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
+      break;
+    case 48:
+      factor_small_kernel<48><<<grid, 192, smem(48), stream>>>(T, level_fronts, lam, panels, upd_cur,
+                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
+      break;
+    case 64:
+      factor_small_kernel<64><<<grid, 256, smem(64), stream>>>(T, level_fronts, lam, panels, upd_cur,
+                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
+      break;
+    default:
+      return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
