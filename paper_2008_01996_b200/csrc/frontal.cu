@@ -18,6 +18,7 @@
 // K = p. All three GEMM-shaped steps run on DMMA (mma.sync m8n8k4 f64) as
 // complex products built from four real MMAs.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -693,6 +694,155 @@ __global__ void __launch_bounds__(128) big_trsm_kernel(KhTree T, const int32_t* 
   });
 }
 
+// ---- small fronts (m <= MS): shared-memory blocked LDL^T on DMMA -----------------
+// The whole front lives in shared memory (column-major, ld MS+2: conflict-free
+// DMMA fragment loads). Pivots go in blocks of 8: warp 0 factors the 8 x 8
+// diagonal block with shuffles, the rows below are solved one thread per row,
+// and the rank-8 trailing update runs on DMMA over the 8 x 8 lower blocks of
+// the trailing matrix (4 real MMAs per complex product). Three barriers per
+// 8 pivots instead of one or two per pivot, and 8x fewer FMA instructions.
+template <int MS, int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
+    KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
+    double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
+    double* minpiv) {
+  constexpr int NTH = 32 * NW, LD = MS + 2, BK = 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // front, S[c*LD + r]
+  double2* W = S + MS * LD;                           // W[k*LD + r] = L[r][kb+k] d_{kb+k}
+  double2* dinv = W + BK * LD;                        // 1/d of the current block
+  __shared__ Kids kids;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+
+  // ---- assembly: pull children into the lower triangle, then add originals
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  __syncthreads();
+  for (int idx = tid; idx < m * m; idx += NTH) {
+    const int c = idx / m, r = idx - c * m;
+    if (r < c) continue;
+    double2 v = make_double2(0.0, 0.0);
+    for (int k = 0; k < kids.n; ++k) {
+      const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+      const int ci = C.cmap[r], cj = C.cmap[c];
+      if (ci >= 0 && cj >= 0) v = cadd(v, C.U[ci + cj * C.q]);
+    }
+    S[c * LD + r] = v;
+  }
+  __syncthreads();
+  const double2 Lm = lam[b];
+  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
+    const int64_t s = T.orig_src[e];
+    const int d = T.orig_dst[e];
+    double2* t = S + (d / m) * LD + (d % m);
+    *t = cadd(*t, make_double2(fma(Lm.x, T.av[s], T.mv[s]), Lm.y * T.av[s]));
+  }
+  __syncthreads();
+
+  double minp = DBL_MAX;
+  for (int kb = 0; kb < p; kb += BK) {
+    const int w = min(BK, p - kb);
+    // (a) diagonal block: lane i < w holds row i of the w x w block
+    if (warp == 0) {
+      double2 a[BK];
+#pragma unroll
+      for (int j = 0; j < BK; ++j)
+        a[j] = (lane < w && j <= lane) ? S[(kb + j) * LD + kb + lane] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        if (k < w) {
+          const double2 dk = shfl2(a[k], k);
+          const double2 di = cinv(dk);
+          const double2 lik = cmul(a[k], di);
+#pragma unroll
+          for (int j = k + 1; j < BK; ++j) {
+            const double2 ajk = shfl2(a[k], j);
+            if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
+          }
+          if (lane > k && lane < w) a[k] = lik;
+          if (lane == 0) {
+            dinv[k] = di;
+            const double ad = sqrt(cabs2(dk));
+            minp = (ad != ad) ? -1.0 : fmin(minp, ad);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BK; ++j)
+        if (lane < w && j <= lane) S[(kb + j) * LD + kb + lane] = a[j];
+    }
+    __syncthreads();
+    // (b) rows below: v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k]; L[r][kb+j] = v_j / d_j
+    const int s0 = kb + w;
+    for (int r = s0 + tid; r < m; r += NTH) {
+      double2 v[BK];
+#pragma unroll
+      for (int j = 0; j < BK; ++j) {
+        if (j < w) {
+          double2 x = S[(kb + j) * LD + r];
+#pragma unroll
+          for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[(kb + k) * LD + kb + j]);
+          v[j] = x;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BK; ++j) {
+        if (j < w) {
+          W[j * LD + r] = v[j];
+          S[(kb + j) * LD + r] = cmul(v[j], dinv[j]);
+        } else {
+          W[j * LD + r] = make_double2(0.0, 0.0);
+        }
+      }
+    }
+    __syncthreads();
+    // (c) trailing update on DMMA: S[r][c] -= sum_k L[r][kb+k] W[c][k], s0 <= c <= r < m
+    const int nb = (m - s0 + 7) / 8;
+    const int g = lane >> 2, t = lane & 3;
+    for (int task = warp; task < nb * (nb + 1) / 2; task += NW) {
+      int bi = 0, rem = task;
+      while (rem > bi) rem -= ++bi;  // task -> (bi, bj = rem), bj <= bi
+      const int r0 = s0 + 8 * bi, c0 = s0 + 8 * rem;
+      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        const int k = ks + t;
+        const int ra = r0 + g, cb = c0 + g;
+        const double2 af = (k < w && ra < m) ? S[(kb + k) * LD + ra] : make_double2(0.0, 0.0);
+        const double2 bf = (cb < m) ? W[k * LD + cb] : make_double2(0.0, 0.0);
+        dmma884(cr[0], cr[1], af.x, bf.x);
+        dmma884(cr[0], cr[1], -af.y, bf.y);
+        dmma884(ci[0], ci[1], af.x, bf.y);
+        dmma884(ci[0], ci[1], af.y, bf.x);
+      }
+      const int rr = r0 + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = c0 + 2 * t + h;
+        if (rr < m && cc < m && rr >= cc) {
+          double2* d = S + cc * LD + rr;
+          *d = make_double2(d->x - cr[h], d->y - ci[h]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- write the panel and the update matrix (lower parts)
+  for (int idx = tid; idx < m * m; idx += NTH) {
+    const int c = idx / m, r = idx - c * m;
+    if (r < c) continue;
+    const double2 v = S[c * LD + r];
+    if (c < p) P[r + c * m] = v;
+    else U[(r - p) + (c - p) * q] = v;
+  }
+  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+}
+
 // ---- small fronts (m <= MS): register-resident right-looking LDL^T ----------
 // The front is assembled in shared memory, then held in registers: thread t
 // owns row i = t % MS at columns j = t / MS + 4c. Pivot k costs one barrier:
@@ -1238,6 +1388,41 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   dim3 grid(nlev, batch);
+  // KH_SMALL_KERNEL=reg selects the register-resident kernels (A/B comparisons)
+  static const bool use_reg = [] {
+    const char* e = std::getenv("KH_SMALL_KERNEL");
+    return e && e[0] == 'r';
+  }();
+  if (!use_reg) {
+    auto dsmem = [](int s) { return ((s + 8) * (s + 2) + 8) * 16; };
+    static bool dattr = false;
+    if (!dattr) {
+      cudaError_t e = cudaFuncSetAttribute(factor_dmma_small_kernel<64, 4>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem(64));
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(factor_dmma_small_kernel<48, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               dsmem(48));
+      if (e != cudaSuccess) return e;
+      dattr = true;
+    }
+    switch (ms) {
+      case 32:
+        factor_dmma_small_kernel<32, 2><<<grid, 64, dsmem(32), stream>>>(
+            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        break;
+      case 48:
+        factor_dmma_small_kernel<48, 2><<<grid, 64, dsmem(48), stream>>>(
+            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        break;
+      case 64:
+        factor_dmma_small_kernel<64, 4><<<grid, 128, dsmem(64), stream>>>(
+            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        break;
+      default:
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   auto smem = [](int s) { return (s * (s + 1) / 2 + 2 * s) * 16; };
   static bool attr = false;
   if (!attr) {
