@@ -81,16 +81,27 @@ int kh_symbolic_fronts(const kh_symbolic* s, int64_t* first, int32_t* npiv, int3
 /* Concatenated update-row lists (permuted positions), sum of nupd entries. */
 int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows);
 void kh_symbolic_free(kh_symbolic* s);
+/* Host: scatter the values of a canonical n x n CSR (sorted, no duplicates)
+ * onto a canonical pattern (pat_*) that contains it (out: one double per
+ * pattern entry, zero where absent). Returns KH_ERR_DIMENSION if the matrix
+ * has an entry outside the pattern. This is the per-shift matrix build
+ * K = Mc + lam*Ac of solvers.py:384 moved ahead of the loop: M and A are
+ * aligned once and the shift is applied on the device. */
+int kh_align_values(int64_t n, const int64_t* pat_indptr, const int64_t* pat_indices, const int64_t* indptr,
+                    const int64_t* indices, const double* vals, double* out);
 
 /* Numeric plan on `device`: uploads the analysis and the value arrays of the
  * two matrices M and A (host, aligned with the analyzed CSR `indptr/indices`,
  * which must be the pattern given to kh_analyze). The plan factors shifted
  * matrices M + lambda A. It allocates factor storage for `factor_slots`
- * shifts and work space for up to `max_batch` shifts per call. */
+ * shifts and work space for up to `max_batch` shifts per call. All device
+ * memory of the plan is carved from one workspace: `workspace` (device, at
+ * least kh_plan_bytes() bytes, caller-owned, e.g. from a caching allocator)
+ * or, if NULL, one cudaMalloc owned by the plan. */
 int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, const int64_t* indices,
                    const double* m_vals, const double* a_vals, int64_t max_batch, int64_t factor_slots,
-                   kh_plan** out);
-/* Bytes the plan would allocate (no allocation). */
+                   void* workspace, int64_t workspace_bytes, kh_plan** out);
+/* Exact workspace size of a plan (no allocation). */
 int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes);
 int kh_plan_set_values(kh_plan* plan, const double* m_vals, const double* a_vals);
 /* Factor M + lambda_s A for s < nshift into slots slot0.. ; `lambda_ri` is a

@@ -77,6 +77,7 @@ struct kh_plan {
   std::vector<BigLevel> big;
   std::vector<KbInfo> kbinfo;
   int32_t* btasks = nullptr;
+  char* owned = nullptr;           // workspace allocated by the plan (null if caller-provided)
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -116,21 +117,8 @@ struct kh_plan {
 namespace {
 
 void plan_release(kh_plan* p) {
-  void* ptrs[] = {p->fronts, p->child_list, p->relind, p->orig_dst, p->level_fronts, p->urows, p->orig_src,
-                  p->perm, p->indptr, p->indices, p->mv, p->av, p->panels, p->upd[0], p->upd[1], p->rupd[0],
-                  p->rupd[1], p->y, p->lam, p->minpiv_work, p->absmax_work, p->minpiv, p->absmax,
-                  p->resid_part, p->tasks, p->cmap, p->btasks};
-  for (void* q : ptrs)
-    if (q) cudaFree(q);
-}
-
-int64_t plan_bytes(const kh::Symbolic& S, int64_t max_batch, int64_t slots) {
-  int64_t b = 0;
-  b += slots * S.panel_total * 16;
-  b += max_batch * (S.upd_size[0] + S.upd_size[1] + S.rupd_size[0] + S.rupd_size[1] + S.n) * 16;
-  b += (int64_t)S.fronts.size() * (sizeof(KhDevFront) + max_batch * 8);
-  b += (int64_t)(S.urows.size() * 12 + S.cmap.size() * 4 + S.orig_src.size() * 12 + S.n * 16 + S.nnz * 24);
-  return b;
+  if (p->owned) cudaFree(p->owned);
+  p->owned = nullptr;
 }
 
 }  // namespace
@@ -262,6 +250,23 @@ int kh_symbolic_fronts(const kh_symbolic* s, int64_t* first, int32_t* npiv, int3
   return KH_OK;
 }
 
+int kh_align_values(int64_t n, const int64_t* pat_indptr, const int64_t* pat_indices, const int64_t* indptr,
+                    const int64_t* indices, const double* vals, double* out) {
+  if (n < 0 || (n > 0 && (!pat_indptr || !indptr))) return fail(KH_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t q = pat_indptr[i];
+    const int64_t qe = pat_indptr[i + 1];
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      const int64_t j = indices[e];
+      while (q < qe && pat_indices[q] < j) out[q++] = 0.0;
+      if (q == qe || pat_indices[q] != j) return fail(KH_ERR_DIMENSION, "matrix has entries outside the analyzed pattern");
+      out[q++] = vals[e];
+    }
+    while (q < qe) out[q++] = 0.0;
+  }
+  return KH_OK;
+}
+
 int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows) {
   if (!s || (!rows && !s->S.urows.empty())) return fail(KH_ERR_INVALID, "null argument");
   std::copy(s->S.urows.begin(), s->S.urows.end(), rows);
@@ -270,38 +275,26 @@ int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows) {
 
 void kh_symbolic_free(kh_symbolic* s) { delete s; }
 
-int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes) {
-  if (!s || !bytes) return fail(KH_ERR_INVALID, "null argument");
-  *bytes = plan_bytes(s->S, max_batch, factor_slots);
-  return KH_OK;
-}
+}  // extern "C"
 
-int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, const int64_t* indices,
-                   const double* m_vals, const double* a_vals, int64_t max_batch, int64_t factor_slots,
-                   kh_plan** out) {
-  if (!s || !out || !indptr || (s->S.nnz && (!indices || !m_vals || !a_vals)))
-    return fail(KH_ERR_INVALID, "null argument");
-  if (max_batch < 1 || factor_slots < max_batch) return fail(KH_ERR_INVALID, "need factor_slots >= max_batch >= 1");
-  const kh::Symbolic& S = s->S;
-  if (indptr[S.n] != S.nnz) return fail(KH_ERR_DIMENSION, "CSR does not match the analyzed pattern");
-  KH_CUDA(cudaSetDevice(device));
-  kh_plan* p = new kh_plan();
-  p->device = device;
-  p->n = S.n;
-  p->nnz = S.nnz;
-  p->max_batch = max_batch;
-  p->slots = factor_slots;
-  p->nf = (int32_t)S.fronts.size();
-  p->depth = S.max_depth;
-  p->panel_total = S.panel_total;
-  for (int k = 0; k < 2; ++k) {
-    p->upd_size[k] = std::max<int64_t>(S.upd_size[k], 1);
-    p->rupd_size[k] = std::max<int64_t>(S.rupd_size[k], 1);
-  }
-  std::vector<KhDevFront> df(p->nf);
-  for (int32_t f = 0; f < p->nf; ++f) {
+namespace {
+
+// Host-side launch schedule derived from the analysis: fronts grouped per
+// level and kernel class, Schur tiles and the large-front block lists.
+struct Sched {
+  std::vector<KhDevFront> df;
+  std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
+  std::vector<kh_plan::BigLevel> big;
+  std::vector<kh_plan::KbInfo> kbinfo;
+  int32_t max_p = 0;
+};
+
+void build_schedule(const kh::Symbolic& S, Sched& X) {
+  const int32_t nf = (int32_t)S.fronts.size();
+  X.df.resize(nf);
+  for (int32_t f = 0; f < nf; ++f) {
     const kh::Front& F = S.fronts[f];
-    KhDevFront& D = df[f];
+    KhDevFront& D = X.df[f];
     D.first = F.first;
     D.p = F.p;
     D.q = F.q;
@@ -316,120 +309,210 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     D.cmap_begin = F.cmap_begin;
     D.depth = F.depth;
     D.pad = 0;
-    p->max_p = std::max(p->max_p, F.p);
+    X.max_p = std::max(X.max_p, F.p);
   }
-  // each level's fronts grouped by kernel class: m <= 32, m <= 64 (register-
-  // resident kernels), larger (tiled DMMA kernel); KH_SMALL_MAX caps the
-  // register-resident classes (0 disables them, for A/B measurements)
+  // KH_SMALL_MAX caps the register/shared-memory small-front classes
+  // (0 disables them, for A/B measurements)
   int small_max = 64;
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
-  std::vector<int32_t> lf;
-  p->level_off.push_back(0);
   auto front_class = [&](int32_t m) {
     for (int c = 0; c < kSmallClasses; ++c)
       if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
     return kSmallClasses;  // large
   };
+  X.level_off.push_back(0);
   for (const auto& lev : S.levels) {
-    const int32_t base = (int32_t)lf.size();
+    const int32_t base = (int32_t)X.lf.size();
     for (int c = 0; c <= kSmallClasses; ++c) {
-      p->cls_off.push_back((int32_t)lf.size() - base);
+      X.cls_off.push_back((int32_t)X.lf.size() - base);
       for (int32_t f : lev)
-        if (front_class(S.fronts[f].m()) == c) lf.push_back(f);
+        if (front_class(S.fronts[f].m()) == c) X.lf.push_back(f);
     }
-    p->cls_off.push_back((int32_t)lf.size() - base);
-    p->level_off.push_back((int32_t)lf.size());
+    X.cls_off.push_back((int32_t)X.lf.size() - base);
+    X.level_off.push_back((int32_t)X.lf.size());
   }
-  // Schur-update tasks: lower 64x64 tiles of U for every large front, per level
-  std::vector<int32_t> tasks;
-  p->task_off.push_back(0);
+  X.task_off.push_back(0);
   for (size_t d = 0; d < S.levels.size(); ++d) {
-    for (int32_t k = p->level_off[d] + p->classes(d)[kSmallClasses]; k < p->level_off[d + 1]; ++k) {
-      const int32_t f = lf[k];
+    const int32_t first_large = X.level_off[d] + X.cls_off[kClsStride * d + kSmallClasses];
+    std::vector<int32_t> large(X.lf.begin() + first_large, X.lf.begin() + X.level_off[d + 1]);
+    // Schur-update tasks: lower 64x64 tiles of U
+    for (int32_t f : large) {
       const int32_t nt = (S.fronts[f].q + 63) / 64;
       for (int32_t jt = 0; jt < nt; ++jt)
-        for (int32_t it = jt; it < nt; ++it) tasks.insert(tasks.end(), {f, it, jt});
+        for (int32_t it = jt; it < nt; ++it) X.tasks.insert(X.tasks.end(), {f, it, jt});
     }
-    p->task_off.push_back((int32_t)(tasks.size() / 3));
-  }
-  std::vector<int32_t> bt;
-  for (size_t d = 0; d < S.levels.size(); ++d) {
-    std::vector<int32_t> large(lf.begin() + p->level_off[d] + p->classes(d)[kSmallClasses],
-                               lf.begin() + p->level_off[d + 1]);
+    X.task_off.push_back((int32_t)(X.tasks.size() / 3));
     kh_plan::BigLevel L{};
-    L.asm_off = (int32_t)bt.size();
+    L.asm_off = (int32_t)X.bt.size();
     int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
-      for (int32_t idx0 = 0; idx0 < F.m() * F.p + F.q * F.q; idx0 += KH_ASM_CHUNK) bt.insert(bt.end(), {f, idx0});
+      for (int32_t idx0 = 0; idx0 < F.m() * F.p + F.q * F.q; idx0 += KH_ASM_CHUNK)
+        X.bt.insert(X.bt.end(), {f, idx0});
       nkb = std::max(nkb, (F.p + 31) / 32);
     }
-    L.asm_n = ((int32_t)bt.size() - L.asm_off) / 2;
-    L.kb_off = (int32_t)p->kbinfo.size();
+    L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 2;
+    L.kb_off = (int32_t)X.kbinfo.size();
     L.nkb = nkb;
     for (int32_t kbi = 0; kbi < nkb; ++kbi) {
       const int32_t kb = 32 * kbi;
       kh_plan::KbInfo K{};
-      K.diag_off = (int32_t)bt.size();
+      K.diag_off = (int32_t)X.bt.size();
       for (int32_t f : large)
-        if (S.fronts[f].p > kb) bt.push_back(f);
-      K.diag_n = (int32_t)bt.size() - K.diag_off;
-      K.lupd_off = (int32_t)bt.size();
+        if (S.fronts[f].p > kb) X.bt.push_back(f);
+      K.diag_n = (int32_t)X.bt.size() - K.diag_off;
+      K.lupd_off = (int32_t)X.bt.size();
       if (kb > 0)
         for (int32_t f : large) {
           const kh::Front& F = S.fronts[f];
           if (F.p <= kb) continue;
-          for (int32_t i0 = (kb / 64) * 64; i0 < F.m(); i0 += 64) bt.insert(bt.end(), {f, i0});
+          for (int32_t i0 = (kb / 64) * 64; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0});
         }
-      K.lupd_n = ((int32_t)bt.size() - K.lupd_off) / 2;
-      K.trsm_off = (int32_t)bt.size();
+      K.lupd_n = ((int32_t)X.bt.size() - K.lupd_off) / 2;
+      K.trsm_off = (int32_t)X.bt.size();
       for (int32_t f : large) {
         const kh::Front& F = S.fronts[f];
         if (F.p <= kb) continue;
         const int32_t start = kb + std::min(32, F.p - kb);
-        for (int32_t i0 = (start / 64) * 64; i0 < F.m(); i0 += 64) bt.insert(bt.end(), {f, i0});
+        for (int32_t i0 = (start / 64) * 64; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0});
       }
-      K.trsm_n = ((int32_t)bt.size() - K.trsm_off) / 2;
-      p->kbinfo.push_back(K);
+      K.trsm_n = ((int32_t)X.bt.size() - K.trsm_off) / 2;
+      X.kbinfo.push_back(K);
     }
-    p->big.push_back(L);
+    X.big.push_back(L);
   }
-  cudaError_t e = cudaSuccess;
-  auto chk = [&](cudaError_t x) {
-    if (e == cudaSuccess) e = x;
-  };
-  chk(upload(&p->fronts, df.data(), df.size()));
-  chk(upload(&p->child_list, S.child_list.data(), S.child_list.size()));
-  chk(upload(&p->relind, S.relind.data(), S.relind.size()));
-  chk(upload(&p->cmap, S.cmap.data(), S.cmap.size()));
-  chk(upload(&p->urows, S.urows.data(), S.urows.size()));
-  chk(upload(&p->orig_src, S.orig_src.data(), S.orig_src.size()));
-  chk(upload(&p->orig_dst, S.orig_dst.data(), S.orig_dst.size()));
-  chk(upload(&p->level_fronts, lf.data(), lf.size()));
-  chk(upload(&p->tasks, tasks.data(), tasks.size()));
-  chk(upload(&p->btasks, bt.data(), bt.size()));
-  chk(upload(&p->perm, S.perm.data(), S.perm.size()));
-  chk(upload(&p->indptr, indptr, (size_t)S.n + 1));
-  chk(upload(&p->indices, indices, (size_t)S.nnz));
-  chk(upload(&p->mv, m_vals, (size_t)S.nnz));
-  chk(upload(&p->av, a_vals, (size_t)S.nnz));
-  auto alloc = [&](void** ptr, int64_t bytes) {
-    if (e == cudaSuccess) e = cudaMalloc(ptr, (size_t)std::max<int64_t>(bytes, 16));
-  };
-  alloc((void**)&p->panels, factor_slots * S.panel_total * 16);
+}
+
+// Sub-allocator over one device workspace (256-byte aligned pieces). With a
+// null base it only measures, so the same code computes the workspace size.
+struct Carver {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  void take(T** out, size_t count) {
+    off = (off + 255) & ~size_t(255);
+    *out = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += std::max<size_t>(count * sizeof(T), 16);
+  }
+};
+
+void carve(kh_plan* p, const kh::Symbolic& S, const Sched& X, Carver& C) {
+  C.take(&p->fronts, X.df.size());
+  C.take(&p->child_list, S.child_list.size());
+  C.take(&p->relind, S.relind.size());
+  C.take(&p->cmap, S.cmap.size());
+  C.take(&p->urows, S.urows.size());
+  C.take(&p->orig_src, S.orig_src.size());
+  C.take(&p->orig_dst, S.orig_dst.size());
+  C.take(&p->level_fronts, X.lf.size());
+  C.take(&p->tasks, X.tasks.size());
+  C.take(&p->btasks, X.bt.size());
+  C.take(&p->perm, (size_t)S.n);
+  C.take(&p->indptr, (size_t)S.n + 1);
+  C.take(&p->indices, (size_t)S.nnz);
+  C.take(&p->mv, (size_t)S.nnz);
+  C.take(&p->av, (size_t)S.nnz);
+  C.take(&p->panels, (size_t)(p->slots * S.panel_total));
   for (int k = 0; k < 2; ++k) {
-    alloc((void**)&p->upd[k], max_batch * p->upd_size[k] * 16);
-    alloc((void**)&p->rupd[k], max_batch * p->rupd_size[k] * 16);
+    C.take(&p->upd[k], (size_t)(p->max_batch * p->upd_size[k]));
+    C.take(&p->rupd[k], (size_t)(p->max_batch * p->rupd_size[k]));
   }
-  alloc((void**)&p->y, max_batch * S.n * 16);
-  alloc((void**)&p->lam, max_batch * 16);
-  alloc((void**)&p->minpiv_work, max_batch * (int64_t)p->nf * 8);
-  alloc((void**)&p->absmax_work, max_batch * (int64_t)kAbsmaxBlocks * 8);
-  alloc((void**)&p->minpiv, factor_slots * 8);
-  alloc((void**)&p->absmax, factor_slots * 8);
-  alloc((void**)&p->resid_part, 2 * (int64_t)kResidualBlocks * 8);
+  C.take(&p->y, (size_t)(p->max_batch * S.n));
+  C.take(&p->lam, (size_t)p->max_batch);
+  C.take(&p->minpiv_work, (size_t)(p->max_batch * (int64_t)X.df.size()));
+  C.take(&p->absmax_work, (size_t)(p->max_batch * kAbsmaxBlocks));
+  C.take(&p->minpiv, (size_t)p->slots);
+  C.take(&p->absmax, (size_t)p->slots);
+  C.take(&p->resid_part, (size_t)(2 * kResidualBlocks));
+}
+
+void plan_sizes(kh_plan* p, const kh::Symbolic& S, int64_t max_batch, int64_t slots) {
+  p->n = S.n;
+  p->nnz = S.nnz;
+  p->max_batch = max_batch;
+  p->slots = slots;
+  p->nf = (int32_t)S.fronts.size();
+  p->depth = S.max_depth;
+  p->panel_total = S.panel_total;
+  for (int k = 0; k < 2; ++k) {
+    p->upd_size[k] = std::max<int64_t>(S.upd_size[k], 1);
+    p->rupd_size[k] = std::max<int64_t>(S.rupd_size[k], 1);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes) {
+  if (!s || !bytes) return fail(KH_ERR_INVALID, "null argument");
+  kh_plan tmp;
+  Sched X;
+  build_schedule(s->S, X);
+  plan_sizes(&tmp, s->S, max_batch, factor_slots);
+  Carver C;
+  carve(&tmp, s->S, X, C);
+  *bytes = (int64_t)C.off;
+  return KH_OK;
+}
+
+int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, const int64_t* indices,
+                   const double* m_vals, const double* a_vals, int64_t max_batch, int64_t factor_slots,
+                   void* workspace, int64_t workspace_bytes, kh_plan** out) {
+  if (!s || !out || !indptr || (s->S.nnz && (!indices || !m_vals || !a_vals)))
+    return fail(KH_ERR_INVALID, "null argument");
+  if (max_batch < 1 || factor_slots < max_batch) return fail(KH_ERR_INVALID, "need factor_slots >= max_batch >= 1");
+  const kh::Symbolic& S = s->S;
+  if (indptr[S.n] != S.nnz) return fail(KH_ERR_DIMENSION, "CSR does not match the analyzed pattern");
+  KH_CUDA(cudaSetDevice(device));
+  kh_plan* p = new kh_plan();
+  p->device = device;
+  plan_sizes(p, S, max_batch, factor_slots);
+  Sched X;
+  build_schedule(S, X);
+  p->max_p = X.max_p;
+  p->level_off = X.level_off;
+  p->cls_off = X.cls_off;
+  p->task_off = X.task_off;
+  p->big = X.big;
+  p->kbinfo = X.kbinfo;
+  Carver measure;
+  carve(p, S, X, measure);
+  cudaError_t e = cudaSuccess;
+  Carver C;
+  if (workspace) {
+    if (workspace_bytes < (int64_t)measure.off) {
+      delete p;
+      return fail(KH_ERR_INVALID, "workspace smaller than kh_plan_bytes()");
+    }
+    C.base = static_cast<char*>(workspace);
+  } else {
+    e = cudaMalloc(reinterpret_cast<void**>(&p->owned), measure.off);
+    C.base = p->owned;
+  }
+  if (e == cudaSuccess) {
+    carve(p, S, X, C);
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+      if (e == cudaSuccess && bytes) e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    up(p->fronts, X.df.data(), X.df.size() * sizeof(KhDevFront));
+    up(p->child_list, S.child_list.data(), S.child_list.size() * 4);
+    up(p->relind, S.relind.data(), S.relind.size() * 4);
+    up(p->cmap, S.cmap.data(), S.cmap.size() * 4);
+    up(p->urows, S.urows.data(), S.urows.size() * 8);
+    up(p->orig_src, S.orig_src.data(), S.orig_src.size() * 8);
+    up(p->orig_dst, S.orig_dst.data(), S.orig_dst.size() * 4);
+    up(p->level_fronts, X.lf.data(), X.lf.size() * 4);
+    up(p->tasks, X.tasks.data(), X.tasks.size() * 4);
+    up(p->btasks, X.bt.data(), X.bt.size() * 4);
+    up(p->perm, S.perm.data(), S.perm.size() * 8);
+    up(p->indptr, indptr, ((size_t)S.n + 1) * 8);
+    up(p->indices, indices, (size_t)S.nnz * 8);
+    up(p->mv, m_vals, (size_t)S.nnz * 8);
+    up(p->av, a_vals, (size_t)S.nnz * 8);
+  }
   if (e != cudaSuccess) {
-    plan_release(p);
+    if (p->owned) cudaFree(p->owned);
     delete p;
     cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? KH_ERR_NOMEM : KH_ERR_CUDA,

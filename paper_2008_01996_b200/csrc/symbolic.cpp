@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <numeric>
+#include <atomic>
+#include <thread>
 
 namespace kh {
 namespace {
@@ -58,44 +60,51 @@ Graph build_graph(int64_t n, const int64_t* indptr, const int64_t* indices) {
   return g;
 }
 
-struct Builder {
+// A dissection subtree in local postorder: piv[f] are the pivots (original
+// ids) of local front f, kids[f] its children (local indices).
+struct Sub {
+  std::vector<std::vector<int64_t>> piv;
+  std::vector<std::vector<int32_t>> kids;
+};
+
+// Shared, thread-safe state: vertex sets handled concurrently are disjoint,
+// so `dist` is only written for a thread's own vertices; `in_set` stamps are
+// globally unique (atomic counter) and read with relaxed atomics.
+struct Shared {
   const Graph& g;
   int32_t leaf;
-  std::vector<int64_t> iperm;
-  int64_t next_pos = 0;
-  std::vector<std::vector<int64_t>> piv;      // per front (original ids)
-  std::vector<std::vector<int32_t>> kids;
-  // scratch
-  std::vector<int32_t> in_set;  // stamp of current set
-  int32_t stamp = 0;
+  std::vector<std::atomic<int32_t>> in_set;
   std::vector<int32_t> dist;
-  std::vector<int64_t> queue;
-
-  Builder(const Graph& gr, int32_t lf)
-      : g(gr), leaf(lf), iperm(gr.n, -1), in_set(gr.n, 0), dist(gr.n, -1), queue(gr.n) {}
-
-  int32_t make_front(std::vector<int64_t> pivots, std::vector<int32_t> children) {
-    for (int64_t v : pivots) iperm[v] = next_pos++;
-    piv.push_back(std::move(pivots));
-    kids.push_back(std::move(children));
-    return (int32_t)piv.size() - 1;
+  std::atomic<int32_t> stamp{0};
+  Shared(const Graph& gr, int32_t lf) : g(gr), leaf(lf), in_set(gr.n), dist(gr.n, -1) {
+    for (auto& x : in_set) x.store(0, std::memory_order_relaxed);
   }
+};
 
-  // BFS restricted to vertices with in_set == s; fills order (queue) and
-  // level starts; returns number of visited vertices.
+struct Builder {
+  Shared& sh;
+  const Graph& g;
+  std::vector<int64_t> queue;  // per-thread BFS queue
+
+  explicit Builder(Shared& s) : sh(s), g(s.g), queue(s.g.n) {}
+
+  int32_t in(int64_t v) const { return sh.in_set[v].load(std::memory_order_relaxed); }
+  void mark(int64_t v, int32_t s) { sh.in_set[v].store(s, std::memory_order_relaxed); }
+
+  // BFS restricted to vertices stamped s; fills queue and level starts.
   int64_t bfs(int64_t root, int32_t s, std::vector<int64_t>& lvl_start) {
     lvl_start.clear();
     int64_t head = 0, tail = 0;
     queue[tail++] = root;
-    dist[root] = 0;
+    sh.dist[root] = 0;
     int32_t cur = -1;
     while (head < tail) {
       int64_t v = queue[head];
-      if (dist[v] != cur) { cur = dist[v]; lvl_start.push_back(head); }
+      if (sh.dist[v] != cur) { cur = sh.dist[v]; lvl_start.push_back(head); }
       ++head;
       for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
         int64_t u = g.adj[e];
-        if (in_set[u] == s && dist[u] < 0) { dist[u] = dist[v] + 1; queue[tail++] = u; }
+        if (in(u) == s && sh.dist[u] < 0) { sh.dist[u] = sh.dist[v] + 1; queue[tail++] = u; }
       }
     }
     lvl_start.push_back(tail);
@@ -103,12 +112,12 @@ struct Builder {
   }
 
   void reset_dist(const std::vector<int64_t>& V) {
-    for (int64_t v : V) dist[v] = -1;
+    for (int64_t v : V) sh.dist[v] = -1;
   }
 
   int64_t deg_in(int64_t v, int32_t s) const {
     int64_t d = 0;
-    for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) d += (in_set[g.adj[e]] == s);
+    for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) d += (in(g.adj[e]) == s);
     return d;
   }
 
@@ -151,7 +160,7 @@ struct Builder {
       bool up = false;
       for (int64_t a = g.xadj[v]; a < g.xadj[v + 1] && !up; ++a) {
         int64_t u = g.adj[a];
-        up = (in_set[u] == s && dist[u] == best + 1);
+        up = (in(u) == s && sh.dist[u] == best + 1);
       }
       if (up) c.sep.push_back(v);
     }
@@ -166,7 +175,7 @@ struct Builder {
     reset_dist(V);
     std::vector<int64_t> ls;
     for (int64_t v : V) {
-      if (in_set[v] != s || dist[v] >= 0) continue;
+      if (in(v) != s || sh.dist[v] >= 0) continue;
       int64_t N = bfs(v, s, ls);
       std::vector<int64_t> part(queue.begin(), queue.begin() + N);
       std::sort(part.begin(), part.end());
@@ -175,18 +184,25 @@ struct Builder {
     return parts;
   }
 
-  int32_t nd(std::vector<int64_t> V) {
-    if ((int64_t)V.size() <= leaf) {
-      std::sort(V.begin(), V.end());
-      return make_front(std::move(V), {});
-    }
-    int32_t s = ++stamp;
-    for (int64_t v : V) in_set[v] = s;
+  static Sub leaf_sub(std::vector<int64_t> V) {
+    std::sort(V.begin(), V.end());
+    Sub out;
+    out.piv.push_back(std::move(V));
+    out.kids.emplace_back();
+    return out;
+  }
+
+  // Dissect V (a connected set). Large independent parts near the top of
+  // the tree are dissected by separate threads (each with its own Builder).
+  Sub nd(std::vector<int64_t> V, int depth) {
+    if ((int64_t)V.size() <= sh.leaf) return leaf_sub(std::move(V));
+    int32_t s = ++sh.stamp;
+    for (int64_t v : V) mark(v, s);
     // pseudo-peripheral pair
     int64_t r = V[0];
     int64_t ecc = -1, a = r, b = r;
     std::vector<int64_t> ls;
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < 4; ++it) {
       reset_dist(V);
       int64_t N = bfs(r, s, ls);
       int64_t e = (int64_t)ls.size() - 2;
@@ -214,20 +230,42 @@ struct Builder {
     } else if (cb.ok) {
       c = &cb;
     }
-    if (c == nullptr || c->sep_size * 2 > (int64_t)V.size()) {
-      std::sort(V.begin(), V.end());
-      return make_front(std::move(V), {});
-    }
+    if (c == nullptr || c->sep_size * 2 > (int64_t)V.size()) return leaf_sub(std::move(V));
     std::vector<int64_t> sep = std::move(c->sep);
-    int32_t s2 = ++stamp;
-    for (int64_t v : V) in_set[v] = s2;
-    for (int64_t v : sep) in_set[v] = 0;
+    int32_t s2 = ++sh.stamp;
+    for (int64_t v : V) mark(v, s2);
+    for (int64_t v : sep) mark(v, 0);
     auto parts = components(V, s2);
+    const size_t nV = V.size();
     std::vector<int64_t>().swap(V);
-    std::vector<int32_t> children;
-    for (auto& part : parts) children.push_back(nd(std::move(part)));
+    std::vector<Sub> subs(parts.size());
+    const bool par = depth < 4 && nV > 8192 && parts.size() > 1;
+    if (par) {
+      std::vector<std::thread> th;
+      for (size_t k = 1; k < parts.size(); ++k)
+        th.emplace_back([this, &subs, &parts, k, depth] {
+          Builder sub(sh);
+          subs[k] = sub.nd(std::move(parts[k]), depth + 1);
+        });
+      subs[0] = nd(std::move(parts[0]), depth + 1);
+      for (auto& t : th) t.join();
+    } else {
+      for (size_t k = 0; k < parts.size(); ++k) subs[k] = nd(std::move(parts[k]), depth + 1);
+    }
+    Sub out;
+    std::vector<int32_t> roots;
+    for (auto& sb : subs) {
+      const int32_t off = (int32_t)out.piv.size();
+      for (auto& kk : sb.kids)
+        for (auto& x : kk) x += off;
+      for (auto& pv : sb.piv) out.piv.push_back(std::move(pv));
+      for (auto& kk : sb.kids) out.kids.push_back(std::move(kk));
+      roots.push_back((int32_t)out.piv.size() - 1);
+    }
     std::sort(sep.begin(), sep.end());
-    return make_front(std::move(sep), std::move(children));
+    out.piv.push_back(std::move(sep));
+    out.kids.push_back(std::move(roots));
+    return out;
   }
 };
 
@@ -246,31 +284,46 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   S.nnz = n ? indptr[n] : 0;
   S.leaf_size = leaf_size;
   Graph g = build_graph(n, indptr, indices);
-  Builder B(g, leaf_size);
-
-  // connected components of the whole graph -> roots
+  Shared sh(g, leaf_size);
+  Builder B(sh);
+  // connected components of the whole graph -> roots; the dissection trees
+  // are concatenated in postorder and positions assigned in that order
+  std::vector<std::vector<int64_t>> piv;
+  std::vector<std::vector<int32_t>> kids;
   {
-    int32_t s = ++B.stamp;
+    int32_t s = ++sh.stamp;
     std::vector<int64_t> all(n);
     std::iota(all.begin(), all.end(), 0);
-    for (int64_t v : all) B.in_set[v] = s;
+    for (int64_t v : all) B.mark(v, s);
     auto comps = B.components(all, s);
-    for (auto& c : comps) B.nd(std::move(c));
+    for (auto& c : comps) {
+      Sub sb = B.nd(std::move(c), 0);
+      const int32_t off = (int32_t)piv.size();
+      for (auto& kk : sb.kids)
+        for (auto& x : kk) x += off;
+      for (auto& pv : sb.piv) piv.push_back(std::move(pv));
+      for (auto& kk : sb.kids) kids.push_back(std::move(kk));
+    }
   }
-  const int32_t nf = (int32_t)B.piv.size();
+  const int32_t nf = (int32_t)piv.size();
+  S.iperm.assign(n, -1);
+  {
+    int64_t pos = 0;
+    for (auto& pv : piv)
+      for (int64_t v : pv) S.iperm[v] = pos++;
+  }
   S.perm.assign(n, -1);
-  S.iperm = B.iperm;
   for (int64_t v = 0; v < n; ++v) S.perm[S.iperm[v]] = v;
 
   S.fronts.resize(nf);
   S.child_ptr.assign(nf + 1, 0);
-  for (int32_t f = 0; f < nf; ++f) S.child_ptr[f + 1] = S.child_ptr[f] + (int32_t)B.kids[f].size();
+  for (int32_t f = 0; f < nf; ++f) S.child_ptr[f + 1] = S.child_ptr[f] + (int32_t)kids[f].size();
   S.child_list.resize(S.child_ptr[nf]);
   for (int32_t f = 0; f < nf; ++f) {
-    std::copy(B.kids[f].begin(), B.kids[f].end(), S.child_list.begin() + S.child_ptr[f]);
+    std::copy(kids[f].begin(), kids[f].end(), S.child_list.begin() + S.child_ptr[f]);
     Front& F = S.fronts[f];
-    F.p = (int32_t)B.piv[f].size();
-    F.first = F.p ? S.iperm[B.piv[f][0]] : 0;
+    F.p = (int32_t)piv[f].size();
+    F.first = F.p ? S.iperm[piv[f][0]] : 0;
     F.parent = -1;
   }
   for (int32_t f = 0; f < nf; ++f)
@@ -283,7 +336,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     Front& F = S.fronts[f];
     const int64_t last = F.first + F.p - 1;
     std::vector<int64_t>& u = U[f];
-    for (int64_t v : B.piv[f])
+    for (int64_t v : piv[f])
       for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
         int64_t r = S.iperm[g.adj[e]];
         if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }

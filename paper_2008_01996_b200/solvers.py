@@ -173,6 +173,24 @@ def _sync():
     torch.cuda.synchronize()
 
 
+def _to_device(a, dev):
+    """Host array -> device tensor (an async DMA when `a` is pinned memory)."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
+    return t.to(dev, non_blocking=t.is_pinned())
+
+
+def _to_host(t):
+    """Device tensor -> numpy array backed by pinned host memory (full-rate DMA;
+    torch caches pinned blocks, so repeated solves do not re-pin)."""
+    import torch
+
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
+
+
 def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=DEFAULT_REFINE_TOL,
              leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, max_batch=None, keep_factors=None):
     """Fast diagonalization on the GPU: independent complex spatial solves.
@@ -215,7 +233,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     t_setup = time.perf_counter() - t0
 
     t0 = time.perf_counter()
-    F = torch.from_numpy(np.ascontiguousarray(np.asarray(system.rhs, dtype=np.float64))).to(dev).view(nt, n)
+    F = _to_device(system.rhs, dev).view(nt, n)
     U = torch.empty((nt, n), dtype=torch.float64, device=dev)
     eng._gemm(n, 2 * eng.n_k, nt, 1.0, F.data_ptr(), n, eng.w_in.data_ptr(), nt, 0.0, eng.G.data_ptr(), n)
     _sync()
@@ -247,7 +265,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
         rel = new
         if stalled:
             break
-    coeffs = U.reshape(-1).cpu().numpy()
+    coeffs = _to_host(U.reshape(-1))
     report.t_refine = time.perf_counter() - t0
     report.refine_steps = steps
     report.residual = rel

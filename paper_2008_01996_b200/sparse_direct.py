@@ -97,19 +97,25 @@ class SymbolicFactorization:
 
         Raises DimensionMismatch if the matrix has an entry outside it.
         """
-        A = sp.coo_matrix(matrix)
+        A = sp.csr_matrix(matrix)
         if A.shape != (self.n, self.n):
             raise DimensionMismatch(f"matrix shape {A.shape} does not match analysis ({self.n})")
-        rows = np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.indptr))
-        keys = rows * self.n + self.indices
-        akeys = A.row.astype(np.int64) * self.n + A.col.astype(np.int64)
-        pos = np.searchsorted(keys, akeys)
-        pos_c = np.minimum(pos, max(len(keys) - 1, 0))
-        if len(akeys) and (len(keys) == 0 or np.any(keys[pos_c] != akeys)):
-            raise DimensionMismatch("matrix has entries outside the analyzed pattern")
-        out = np.zeros(len(keys), dtype=dtype)
-        np.add.at(out, pos, A.data.astype(dtype))
-        return out
+        if not A.has_canonical_format:
+            A = A.copy()
+            A.sum_duplicates()
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int64)
+        parts = [np.real(A.data)] + ([np.imag(A.data)] if np.iscomplexobj(A.data) else [])
+        outs = []
+        for part in parts:
+            v = np.ascontiguousarray(part, dtype=np.float64)
+            o = np.empty(len(self.indices), dtype=np.float64)
+            _native.call("kh_align_values", self.n, _native.ptr(self.indptr), _native.ptr(self.indices),
+                         _native.ptr(ip), _native.ptr(ix), _native.ptr(v), _native.ptr(o))
+            outs.append(o)
+        if np.dtype(dtype).kind == "c":
+            return outs[0] + 1j * (outs[1] if len(outs) > 1 else 0.0)
+        return outs[0]
 
 
 def analyze(pattern, leaf_size=DEFAULT_LEAF_SIZE):
@@ -137,6 +143,8 @@ class _Plan:
     """Owns a kh_plan* (device factor storage + work space)."""
 
     def __init__(self, symbolic, m_vals, a_vals, max_batch, slots, device):
+        import torch
+
         self.raw = ctypes.c_void_p()
         self.symbolic = symbolic
         self.device = device
@@ -144,9 +152,13 @@ class _Plan:
         self.slots = int(slots)
         mv = np.ascontiguousarray(m_vals, dtype=np.float64)
         av = np.ascontiguousarray(a_vals, dtype=np.float64)
+        # one workspace from torch's caching allocator: repeated solves reuse
+        # it without cudaMalloc/cudaFree (which would synchronize the device)
+        nbytes = plan_bytes(symbolic, self.max_batch, self.slots)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", int(device)))
         _native.call("kh_plan_create", symbolic.handle.raw, int(device), _native.ptr(symbolic.indptr),
                      _native.ptr(symbolic.indices), _native.ptr(mv), _native.ptr(av), self.max_batch,
-                     self.slots, ctypes.byref(self.raw))
+                     self.slots, self.workspace.data_ptr(), nbytes, ctypes.byref(self.raw))
 
     def factor(self, slot0, lambdas, stream):
         lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.complex128))
