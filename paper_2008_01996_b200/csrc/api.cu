@@ -78,6 +78,10 @@ struct kh_plan {
   std::vector<KbInfo> kbinfo;
   int32_t* btasks = nullptr;
   char* owned = nullptr;           // workspace allocated by the plan (null if caller-provided)
+  // side stream: the small-front kernels of a level run there, concurrently
+  // with the large-front kernels on the caller's stream (levels are joined)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr;
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -119,6 +123,26 @@ namespace {
 void plan_release(kh_plan* p) {
   if (p->owned) cudaFree(p->owned);
   p->owned = nullptr;
+  if (p->ev_main) cudaEventDestroy(p->ev_main);
+  if (p->ev_side) cudaEventDestroy(p->ev_side);
+  if (p->side) cudaStreamDestroy(p->side);
+  p->ev_main = p->ev_side = nullptr;
+  p->side = nullptr;
+}
+
+// fork: `side` starts after the work queued so far on `st`
+cudaError_t fork_side(kh_plan* p, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(p->ev_main, st);
+  return e == cudaSuccess ? cudaStreamWaitEvent(p->side, p->ev_main, 0) : e;
+}
+
+// join both ways: the next level on either stream sees this level's results
+cudaError_t join_side(kh_plan* p, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(p->ev_side, p->side);
+  if (e == cudaSuccess) e = cudaEventRecord(p->ev_main, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->ev_side, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->side, p->ev_main, 0);
+  return e;
 }
 
 }  // namespace
@@ -490,6 +514,9 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     e = cudaMalloc(reinterpret_cast<void**>(&p->owned), measure.off);
     C.base = p->owned;
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_main, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_side, cudaEventDisableTiming);
   if (e == cudaSuccess) {
     carve(p, S, X, C);
     auto up = [&](void* dst, const void* src, size_t bytes) {
@@ -512,7 +539,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     up(p->av, a_vals, (size_t)S.nnz * 8);
   }
   if (e != cudaSuccess) {
-    if (p->owned) cudaFree(p->owned);
+    plan_release(p);
     delete p;
     cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? KH_ERR_NOMEM : KH_ERR_CUDA,
@@ -540,6 +567,7 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
   KH_CUDA(cudaMemcpyAsync(p->lam, lambda_ri, nshift * 16, cudaMemcpyHostToDevice, st));
   const KhTree T = p->tree();
   double2* panels = p->panels + slot0 * p->panel_total;
+  KH_CUDA(fork_side(p, st));
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
@@ -548,7 +576,7 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
     const int32_t ns = (int32_t)nshift;
     for (int c = 0; c < kSmallClasses; ++c)
       KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                     uch, sch, p->minpiv_work, st));
+                                     uch, sch, p->minpiv_work, p->side));
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uc, sc, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
@@ -560,6 +588,7 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
     }
     KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
                             sc, uch, sch, st));
+    KH_CUDA(join_side(p, st));
   }
   KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));
   KH_CUDA(kh_launch_shift_absmax_nnz(p->mv, p->av, p->nnz, (int32_t)nshift, p->lam, p->absmax_work,
@@ -612,6 +641,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   const double2* panels = p->panels + slot0 * p->panel_total;
   const int32_t ns = (int32_t)nshift;
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
+  KH_CUDA(fork_side(p, st));
   // fronts with m <= 64 (the small classes) use the warp-per-front kernels
   constexpr int L = kSmallClasses;
   for (int32_t d = p->depth; d >= 0; --d) {
@@ -619,14 +649,16 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[L + 1] - co[L], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(join_side(p, st));
   }
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, st));
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[L + 1] - co[L], ns, p->max_p, panels, p->y, st));
+    KH_CUDA(join_side(p, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
   return KH_OK;
