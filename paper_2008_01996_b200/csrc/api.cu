@@ -398,7 +398,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
         const kh::Front& F = S.fronts[f];
         if (F.p <= kb) continue;
         const int32_t start = kb + std::min(32, F.p - kb);
-        for (int32_t i0 = (start / 64) * 64; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0});
+        for (int32_t i0 = start; i0 < F.m(); i0 += KH_TRSM_ROWS) X.bt.insert(X.bt.end(), {f, i0});
       }
       K.trsm_n = ((int32_t)X.bt.size() - K.trsm_off) / 2;
       X.kbinfo.push_back(K);

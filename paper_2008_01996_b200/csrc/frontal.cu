@@ -615,65 +615,71 @@ __global__ void __launch_bounds__(128) big_lupdate_kernel(KhTree T, const int32_
   });
 }
 
-// One warp per (front, shift): factor the w x w diagonal block at kb.
+// One warp per (front, shift): LDL^T of the w x w diagonal block at kb.
+// Lane j holds column j of the block in registers (rows i >= j, static
+// register index i); pivot k publishes its (unscaled) column to a per-warp
+// shared vector, and every lane applies the rank-1 update to its column.
+// No block barriers and no dynamic register indexing.
 constexpr int DIAG_WARPS = 4;
 __global__ void __launch_bounds__(32 * DIAG_WARPS) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
                                                                    int nfr, int kb, double2* panels,
                                                                    double* minpiv) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double2 colbuf[DIAG_WARPS][NB];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int idx = blockIdx.x * DIAG_WARPS + wid;
   if (idx >= nfr) return;
-  double2* S = reinterpret_cast<double2*>(smem_raw) + wid * NB * (NB + 1);  // row-major, ld NB+1
+  double2* cb = colbuf[wid];
   const int32_t f = fronts[idx];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
   const int p = F.p, m = p + F.q, w = min(NB, p - kb);
   double2* B = panels + (int64_t)b * T.panel_total + F.panel_off + kb + (int64_t)kb * m;
-  // load: lane = column j (coalesced along rows i)
-  for (int j = 0; j < w; ++j)
-    if (lane < w) S[lane * (NB + 1) + j] = lane >= j ? B[lane + (int64_t)j * m] : make_double2(0.0, 0.0);
-  __syncwarp();
+  const int j = lane;
+  double2 a[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) a[i] = (j < w && i >= j && i < w) ? B[i + (int64_t)j * m] : make_double2(0.0, 0.0);
   double minp = DBL_MAX;
   for (int k = 0; k < w; ++k) {
-    const double2 dk = S[k * (NB + 1) + k];
-    const double2 di = cinv(dk);
-    if (lane > k && lane < w) {
-      const double2 lik = cmul(S[lane * (NB + 1) + k], di);
-      for (int j = k + 1; j <= lane; ++j)
-        S[lane * (NB + 1) + j] = cfms(S[lane * (NB + 1) + j], lik, S[j * (NB + 1) + k]);
+    if (j == k) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i >= k) cb[i] = a[i];
     }
     __syncwarp();
-    if (lane > k && lane < w) S[lane * (NB + 1) + k] = cmul(S[lane * (NB + 1) + k], di);
+    const double2 dk = cb[k];
+    const double2 di = cinv(dk);
+    if (j > k && j < w) {
+      const double2 fj = cmul(cb[j], di);  // l_jk
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i >= j) a[i] = cfms(a[i], cb[i], fj);
+    }
+    if (j == k) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i > k) a[i] = cmul(a[i], di);
+    }
     const double ad = sqrt(cabs2(dk));
     minp = (ad != ad) ? -1.0 : fmin(minp, ad);
     __syncwarp();
   }
-  // write L (strict lower) and D back
-  for (int j = 0; j < w; ++j)
-    if (lane < w && lane >= j) B[lane + (int64_t)j * m] = S[lane * (NB + 1) + j];
-  // L^-1: lane j computes column j (x_j = 1, x_i = -sum_{k=j}^{i-1} L[i][k] x_k),
-  // keeping x_i in the free upper triangle of its own row of S, then stores
-  // Linv[i][j] (i > j) transposed at block position (j, i)
-  if (lane < w) {
-    double2* x = S + lane * (NB + 1);
-    for (int i = lane + 1; i < w; ++i) {
-      double2 s = make_double2(-S[i * (NB + 1) + lane].x, -S[i * (NB + 1) + lane].y);
-      for (int k = lane + 1; k < i; ++k) s = cfms(s, S[i * (NB + 1) + k], x[k]);
-      x[i] = s;
-    }
-    for (int i = lane + 1; i < w; ++i) B[lane + (int64_t)i * m] = x[i];
-  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+    if (j < w && i >= j && i < w) B[i + (int64_t)j * m] = a[i];
   if (lane == 0) {
     double* mp = minpiv + (int64_t)b * T.nf + f;
     *mp = kb == 0 ? minp : fmin(*mp, minp);
   }
 }
 
-__global__ void __launch_bounds__(128) big_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
-                                                       double2* panels) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+// Rows below the factored diagonal block: one thread per row r solves
+// v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k], L[r][kb+j] = v_j / d_j (the
+// block L and 1/d staged in shared memory, read as broadcasts).
+constexpr int TRSM_ROWS = KH_TRSM_ROWS;
+__global__ void __launch_bounds__(TRSM_ROWS) big_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
+                                                             double2* panels) {
+  __shared__ double2 sL[NB][NB + 1];
+  __shared__ double2 sdi[NB];
   const int32_t f = tasks[2 * blockIdx.x];
   const int i0 = tasks[2 * blockIdx.x + 1];
   const int b = blockIdx.y;
@@ -681,17 +687,28 @@ __global__ void __launch_bounds__(128) big_trsm_kernel(KhTree T, const int32_t* 
   const int p = F.p, m = p + F.q, w = min(NB, p - kb);
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   const double2* Bk = P + kb + (int64_t)kb * m;
-  Acc acc;
-  // acc = sum_{k<j} A[r, kb+k] Linv[j][k]; the unit diagonal term is added below
-  tile_mma_cp<2, MODE_TRSM>(acc, w, P + i0 + (int64_t)kb * m, m, m - i0, Bk, m, w, nullptr, 0, st);
-  tile_epilogue(acc, [&](int i, int j, double2 v) {
-    const int r = i0 + i;
-    if (r < m && r >= kb + w && j < w) {
-      double2* d = P + r + (int64_t)(kb + j) * m;
-      const double2 dj = Bk[j + (int64_t)j * m];
-      *d = cmul(cadd(v, *d), cinv(dj));
-    }
-  });
+  for (int e = threadIdx.x; e < NB * NB; e += TRSM_ROWS) {
+    const int r = e % NB, c = e / NB;
+    sL[r][c] = (r < w && c < r) ? Bk[r + (int64_t)c * m] : make_double2(0.0, 0.0);
+  }
+  if (threadIdx.x < NB) sdi[threadIdx.x] = threadIdx.x < w ? cinv(Bk[threadIdx.x * (int64_t)(m + 1)]) : make_double2(0.0, 0.0);
+  __syncthreads();
+  const int r = i0 + threadIdx.x;
+  if (r < kb + w || r >= m) return;
+  double2* row = P + r + (int64_t)kb * m;
+  double2 v[NB];
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) v[jj] = jj < w ? row[(int64_t)jj * m] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int jj = 1; jj < NB; ++jj) {
+    double2 x = v[jj];
+#pragma unroll
+    for (int k = 0; k < jj; ++k) x = cfms(x, v[k], sL[jj][k]);
+    v[jj] = x;
+  }
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj)
+    if (jj < w) row[(int64_t)jj * m] = cmul(v[jj], sdi[jj]);
 }
 
 // ---- small fronts (m <= MS): shared-memory blocked LDL^T on DMMA -----------------
@@ -1256,11 +1273,7 @@ cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t
 cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t nfr, int kb, int32_t batch,
                                double2* panels, double* minpiv, cudaStream_t stream) {
   if (nfr == 0 || batch == 0) return cudaSuccess;
-  static bool done = false;
-  const int smem = DIAG_WARPS * NB * (NB + 1) * (int)sizeof(double2);
-  cudaError_t e = set_smem_once((const void*)big_diag_kernel, smem, done);
-  if (e != cudaSuccess) return e;
-  big_diag_kernel<<<dim3((nfr + DIAG_WARPS - 1) / DIAG_WARPS, batch), 32 * DIAG_WARPS, smem, stream>>>(
+  big_diag_kernel<<<dim3((nfr + DIAG_WARPS - 1) / DIAG_WARPS, batch), 32 * DIAG_WARPS, 0, stream>>>(
       T, fronts, nfr, kb, panels, minpiv);
   return cudaGetLastError();
 }
@@ -1268,11 +1281,7 @@ cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t n
 cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
                                double2* panels, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  static bool done = false;
-  const int smem = (int)(2 * sizeof(CpStage));
-  cudaError_t e = set_smem_once((const void*)big_trsm_kernel, smem, done);
-  if (e != cudaSuccess) return e;
-  big_trsm_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
+  big_trsm_kernel<<<dim3(ntasks, batch), TRSM_ROWS, 0, stream>>>(T, tasks, kb, panels);
   return cudaGetLastError();
 }
 
