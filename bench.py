@@ -257,7 +257,9 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    launches0 = eng.gpu_launches
+    from paper_2008_01996_b200 import _native
+
+    launches0 = _native.launch_count()
     clocks = ClockSampler(local)
     clocks.start()
     t_start = torch.cuda.Event(enable_timing=True)
@@ -277,7 +279,7 @@ def main():
         tt = torch.tensor([elapsed], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(tt.item())
-    launches = (eng.gpu_launches - launches0) // max(args.steps, 1)
+    launches = (_native.launch_count() - launches0) // max(args.steps, 1)
     ms = elapsed / args.steps * 1e3
     value = dof * args.steps / elapsed
 

@@ -65,6 +65,8 @@ typedef struct {
 } kh_symbolic_stats;
 
 int kh_version(void);
+/* Number of kernels the library has launched so far in this process. */
+int64_t kh_launch_count(void);
 const char* kh_status_string(int status);
 const char* kh_last_error(void);
 

@@ -53,6 +53,7 @@ _P = ctypes.POINTER
 # name -> (restype, argtypes); every symbol include/khb200.h declares
 SIGNATURES = {
     "kh_version": (ctypes.c_int, []),
+    "kh_launch_count": (ctypes.c_int64, []),
     "kh_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "kh_last_error": (ctypes.c_char_p, []),
     "kh_analyze": (ctypes.c_int, [_i64, _vp, _vp, _i32, _P(_vp)]),
@@ -120,6 +121,11 @@ def ptr(t):
     if hasattr(t, "data_ptr"):
         return t.data_ptr()
     return t.ctypes.data
+
+
+def launch_count():
+    """Kernel launches made by libkhb200 so far (for bench.py's gpu_launches)."""
+    return int(load().kh_launch_count())
 
 
 def require_cuda():

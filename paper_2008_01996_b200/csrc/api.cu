@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -15,6 +16,9 @@
 struct kh_symbolic {
   kh::Symbolic S;
 };
+
+static std::atomic<long long> g_launches{0};
+void kh_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -150,6 +154,8 @@ cudaError_t join_side(kh_plan* p, cudaStream_t st) {
 extern "C" {
 
 int kh_version(void) { return 1; }
+
+int64_t kh_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* kh_status_string(int status) {
   switch (status) {

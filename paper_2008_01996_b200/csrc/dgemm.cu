@@ -122,5 +122,6 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
   }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
   dgemm_kernel<<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  kh_note_launch();
   return cudaGetLastError();
 }

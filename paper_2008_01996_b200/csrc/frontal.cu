@@ -36,68 +36,6 @@ struct Acc {
   double i[4][2][2];
 };
 
-// acc(i, j) = sum_k a(i, k) * b(j, k) over k in [0, K), i, j in [0, 64).
-// `la(i, k)` / `lb(j, k)` return the (already masked/scaled) operands.
-// Register-prefetch double buffering: the next chunk's loads are in flight
-// while the current one is multiplied out of shared memory.
-template <class LA, class LB>
-KH_DEV void tile_mma(Acc& acc, int K, LA la, LB lb, double2* sA, double2* sB) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wi = warp & 1, wj = warp >> 1;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) acc.r[a][b][h] = acc.i[a][b][h] = 0.0;
-  const int nch = (K + KC - 1) / KC;
-  double2 ra[4], rb[4];
-  auto fetch = [&](int c) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int idx = tid + r * NT;
-      int i = idx & (TB - 1), k = idx >> 6;
-      int kk = c * KC + k;
-      ra[r] = kk < K ? la(i, kk) : make_double2(0.0, 0.0);
-      rb[r] = kk < K ? lb(i, kk) : make_double2(0.0, 0.0);
-    }
-  };
-  if (nch > 0) fetch(0);
-  for (int c = 0; c < nch; ++c) {
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int idx = tid + r * NT;
-      int i = idx & (TB - 1), k = idx >> 6;
-      sA[k * LDS + i] = ra[r];
-      sB[k * LDS + i] = rb[r];
-    }
-    __syncthreads();
-    if (c + 1 < nch) fetch(c + 1);
-#pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      double2 af[4], bf[2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = sA[(kk + t) * LDS + wi * 32 + mt * 8 + g];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = sB[(kk + t) * LDS + wj * 16 + nt * 8 + g];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        double nai = -af[mt].y;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], af[mt].x, bf[nt].x);
-          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], nai, bf[nt].y);
-          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].x, bf[nt].y);
-          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].y, bf[nt].x);
-        }
-      }
-    }
-  }
-  __syncthreads();
-}
-
 // Visit the accumulator: ep(row, col, value) with row, col in [0, 64).
 template <class EP>
 KH_DEV void tile_epilogue(const Acc& acc, EP ep) {
@@ -175,29 +113,6 @@ KH_DEV ChildRef kid(const KhTree& T, const KhDevFront& F, const double2* upd_chi
   return {upd_child + (int64_t)b * stride_child + C.upd_off, T.cmap + C.cmap_begin, C.q};
 }
 
-// Extend-add of one child's update matrix (lower triangle, q_c x q_c, ld q_c):
-// add(parent_row, parent_col, value). A warp walks a column so the reads of
-// U_c and relind are contiguous; distinct (a, b) map to distinct targets.
-template <int NTH, class AD>
-KH_DEV void extend_add_child(const double2* __restrict__ Uc, int qc, const int32_t* __restrict__ rel, AD add) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = NTH / 32;
-  for (int bb = warp; bb < qc; bb += NW) {
-    const int rb = rel[bb];
-    const double2* colp = Uc + (int64_t)bb * qc;
-    for (int a0 = bb + lane; a0 < qc; a0 += 64) {
-      const int a1 = a0 + 32;
-      const bool ok1 = a1 < qc;
-      const double2 v0 = colp[a0];
-      const int r0 = rel[a0];
-      const double2 v1 = ok1 ? colp[a1] : make_double2(0.0, 0.0);
-      const int r1 = ok1 ? rel[a1] : 0;
-      add(r0, rb, v0);
-      if (ok1) add(r1, rb, v1);
-    }
-  }
-}
-
 // One pipeline stage of the cp.async tile engine: 16 K-columns of A and B
 // (64 rows each, [k][row] with the conflict-free pad) and the 16 pivots d_k.
 struct CpStage {
@@ -210,13 +125,10 @@ struct CpStage {
 // on a 64 x (16 NWJ) tile computed by 2 x NWJ warps (64 NWJ threads).
 //  MODE_SCALED: B(j, k) = B[j + k*ldb], s_k = d_k = D[k*ldd] (the pivots on the
 //               panel diagonal): Schur complements and left-looking updates.
-//  MODE_TRSM:   B(j, k) = B[k + j*ldb] for k < j, else 0, s_k = 1: the strictly
-//               lower unit-triangular inverse stored transposed in the upper
-//               triangle of a factored 32 x 32 diagonal block.
 // Two-stage cp.async ring: the next chunk streams in while DMMA consumes the
 // current one; out-of-range operands are zero-filled by the copy itself. The
 // pivot scaling is applied to the B fragments in registers.
-constexpr int MODE_SCALED = 0, MODE_TRSM = 1;
+constexpr int MODE_SCALED = 0;
 
 template <int NWJ, int MODE>
 KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t lda, int rowsA,
@@ -248,13 +160,8 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
       const int idx = tid + r * NTH;
       const int j = idx % TN, k = idx / TN;
       const int kk = c * KC + k;
-      if (MODE == MODE_SCALED) {
-        const bool ob = kk < K && j < rowsB;
-        cp_async16(&S.b[k * LDS + j], ob ? B + j + (int64_t)kk * ldb : B, ob);
-      } else {
-        const bool ob = kk < K && j < rowsB && kk < j;
-        cp_async16(&S.b[k * LDS + j], ob ? B + kk + (int64_t)j * ldb : B, ob);
-      }
+      const bool ob = kk < K && j < rowsB;
+      cp_async16(&S.b[k * LDS + j], ob ? B + j + (int64_t)kk * ldb : B, ob);
     }
     if (MODE == MODE_SCALED && tid < KC) {
       const int kk = c * KC + tid;
@@ -300,183 +207,14 @@ KH_DEV double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-// One warp factors the w x w (w <= 32) diagonal block at B (column-major, ld
-// m) in registers: lane i holds row i, pivot k is broadcast by shuffles, so
-// the block costs no CTA barriers. Writes L (unit lower) and D back to B, a
-// row-major copy to sd (ld NB+1) and 1/d_k to dinv. Returns min |d_k| on
-// lane 0 (-1 if a pivot is not finite).
-KH_DEV double warp_ldlt_block(double2* B, int64_t m, int w, double2* sd, double2* dinv) {
-  const int lane = threadIdx.x & 31;
-  double2 a[NB];
-#pragma unroll
-  for (int j = 0; j < NB; ++j)
-    a[j] = (lane < w && j <= lane) ? B[lane + (int64_t)j * m] : make_double2(0.0, 0.0);
-  double minp = DBL_MAX;
-#pragma unroll
-  for (int k = 0; k < NB; ++k) {
-    if (k < w) {
-      const double2 dk = shfl2(a[k], k);
-      const double2 di = cinv(dk);
-      const double2 lik = cmul(a[k], di);
-#pragma unroll
-      for (int j = k + 1; j < NB; ++j) {
-        const double2 ajk = shfl2(a[k], j);
-        if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
-      }
-      if (lane > k && lane < w) a[k] = lik;
-      if (lane == 0) {
-        dinv[k] = di;
-        const double ad = sqrt(cabs2(dk));
-        minp = (ad != ad) ? -1.0 : fmin(minp, ad);
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NB; ++j)
-    if (lane < w && j <= lane) {
-      B[lane + (int64_t)j * m] = a[j];
-      sd[lane * (NB + 1) + j] = a[j];
-    }
-  __syncwarp();
-  return minp;
-}
-
-struct FactorSmem {
-  CpStage st[2];
-  double2 d[NB * (NB + 1)];   // diagonal block, [i][j] at i*(NB+1)+j
-  double2 li[NB * (NB + 1)];  // unit-lower inverse
-  double2 dinv[NB];
-};
-
-// Panel kernel for fronts with m > 64 (one CTA per (front, shift)):
-// assembly of P (m x p) and U (q x q), then a left-looking blocked LDL^T of
-// the m x p panel. For pivot block [kb, kb+w): the block column is first
-// updated with all earlier columns in one long-K DMMA product
-//   P[kb:, kb:kb+w] -= L[kb:, :kb] D L[kb:kb+w, :kb]^T,
-// then the w x w diagonal block is factored in shared memory and the rows
-// below are solved against it (TRSM as a GEMM with the unit-lower inverse).
-// The Schur complement U -= L21 D L21^T is left to schur_update_kernel.
-__global__ void __launch_bounds__(NT, 2) factor_panel_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
-                                                             const double2* __restrict__ lam, double2* panels,
-                                                             double2* upd_cur, int64_t upd_stride_cur,
-                                                             const double2* __restrict__ upd_child,
-                                                             int64_t upd_stride_child, double* minpiv) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FactorSmem& S = *reinterpret_cast<FactorSmem*>(smem_raw);
-  const int tid = threadIdx.x;
-  const int32_t f = level_fronts[blockIdx.x];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, q = F.q, m = p + q;
-  const double2 L = lam[b];
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  (void)upd_cur;
-  (void)upd_stride_cur;
-  (void)q;
-
-  // ---- assembly of P (pull children, then add the originals) --------------------
-  // The strict upper triangle of the pivot block is never read, so it is not
-  // written; U is assembled by schur_update_kernel.
-  __shared__ Kids kids;
-  load_kids(T, F, upd_child, upd_stride_child, b, kids);
-  __syncthreads();
-  {
-    // flat walk over the m x p panel, 8 independent entries per thread in flight
-    const int total = m * p;
-    for (int base = tid; base < total; base += 8 * NT) {
-      int rr[8], cc[8];
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * NT;
-        cc[u] = idx / m;
-        rr[u] = idx - cc[u] * m;
-        v[u] = make_double2(0.0, 0.0);
-      }
-      for (int k = 0; k < kids.n; ++k) {
-        const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (base + u * NT < total && rr[u] >= cc[u]) {
-            const int ci = C.cmap[rr[u]], cj = C.cmap[cc[u]];
-            if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (base + u * NT < total && rr[u] >= cc[u]) P[base + u * NT] = v[u];
-    }
-  }
-  __syncthreads();
-  scatter_originals<NT>(T, F, L, [&](int d, double2 v) { P[d] = cadd(P[d], v); });
-  __syncthreads();
-
-  // ---- left-looking pivot blocks ----------------------------------------------
-  double minp = DBL_MAX;
-  Acc acc;
-  for (int kb = 0; kb < p; kb += NB) {
-    const int w = min(NB, p - kb);
-    if (kb > 0) {
-      for (int i0 = kb; i0 < m; i0 += TB) {
-        tile_mma_cp<4, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, S.st);
-        tile_epilogue(acc, [&](int i, int j, double2 v) {
-          const int r = i0 + i;
-          if (r < m && j < w && r >= kb + j) {
-            double2* d = P + r + (int64_t)(kb + j) * m;
-            *d = csub(*d, v);
-          }
-        });
-      }
-      __syncthreads();
-    }
-    if (tid < 32) {
-      const double mp = warp_ldlt_block(P + kb + (int64_t)kb * m, m, w, S.d, S.dinv);
-      if (tid == 0) minp = fmin(minp, mp);  // -1 (non-finite pivot) is sticky
-    }
-    __syncthreads();
-    // explicit inverse of the unit-lower block, row by row
-    for (int idx = tid; idx < NB * NB; idx += NT) {
-      int i = idx / NB, j = idx % NB;
-      S.li[i * (NB + 1) + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    }
-    __syncthreads();
-    for (int i = 1; i < w; ++i) {
-      for (int j = tid; j < i; j += NT) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int k = j; k < i; ++k) s = cfms(s, S.d[i * (NB + 1) + k], S.li[k * (NB + 1) + j]);
-        S.li[i * (NB + 1) + j] = s;
-      }
-      __syncthreads();
-    }
-    // TRSM of the rows below: L[r, kb+j] = (A[r, kb:kb+w] Linv^T)[j] / d_j
-    for (int i0 = kb + w; i0 < m; i0 += TB) {
-      const int rows = m - i0;
-      tile_mma(
-          acc, w,
-          [&](int i, int k) { return i < rows ? P[(i0 + i) + (int64_t)(kb + k) * m] : make_double2(0.0, 0.0); },
-          [&](int j, int k) { return j < w ? S.li[j * (NB + 1) + k] : make_double2(0.0, 0.0); }, S.st[0].a,
-          S.st[0].b);
-      tile_epilogue(acc, [&](int i, int j, double2 v) {
-        if (i < rows && j < w) P[(i0 + i) + (int64_t)(kb + j) * m] = cmul(v, S.dinv[j]);
-      });
-    }
-    __syncthreads();
-  }
-  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
-}
-
 // Schur complement of the large fronts of one level: one CTA per 64 x 64
 // lower tile of U, per shift: U[i0:, j0:] -= L21[i0:, :] D L21[j0:, :]^T
 // (K = p). Tasks are (front, tile row, tile col) triples built on the host.
 __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                              const double2* __restrict__ panels, double2* upd_cur,
-                                                             int64_t upd_stride_cur,
-                                                             const double2* __restrict__ upd_child,
-                                                             int64_t upd_stride_child) {
+                                                             int64_t upd_stride_cur) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
-  __shared__ Kids kids;
   const int32_t f = tasks[3 * blockIdx.x];
   const int i0 = tasks[3 * blockIdx.x + 1] * TB, j0 = tasks[3 * blockIdx.x + 2] * TB;
   const int b = blockIdx.y;
@@ -484,9 +222,6 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   const int p = F.p, q = F.q, m = p + q;
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
-  (void)kids;
-  (void)upd_child;
-  (void)upd_stride_child;
   Acc acc;
   tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
   // U holds the pulled children's contributions (big_assemble): U -= L21 D L21^T
@@ -860,102 +595,6 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
 }
 
-// ---- small fronts (m <= MS): register-resident right-looking LDL^T ----------
-// The front is assembled in shared memory, then held in registers: thread t
-// owns row i = t % MS at columns j = t / MS + 4c. Pivot k costs one barrier:
-// the owners of column k publish it to a double-buffered shared column and
-// every thread applies the rank-1 update to its entries. The trailing
-// q x q block left in registers after p pivots is the update matrix U.
-template <int MS>
-__global__ void __launch_bounds__(MS * 4) factor_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
-                                                              const double2* __restrict__ lam, double2* panels,
-                                                              double2* upd_cur, int64_t upd_stride_cur,
-                                                              const double2* __restrict__ upd_child,
-                                                              int64_t upd_stride_child, double* minpiv) {
-  constexpr int NTH = MS * 4, NC = MS / 4, NPK = MS * (MS + 1) / 2;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* sO = reinterpret_cast<double2*>(smem_raw);  // originals, packed lower triangle
-  double2(*col)[MS] = reinterpret_cast<double2(*)[MS]>(sO + NPK);
-  __shared__ Kids kids;
-  const int tid = threadIdx.x;
-  const int i = tid % MS, jg = tid / MS;
-  const int32_t f = level_fronts[blockIdx.x];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, q = F.q, m = p + q;
-  const double2 L = lam[b];
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
-  auto pk = [](int r, int c) { return c * MS - (c * (c - 1)) / 2 + (r - c); };
-
-  for (int idx = tid; idx < NPK; idx += NTH) sO[idx] = make_double2(0.0, 0.0);
-  load_kids(T, F, upd_child, upd_stride_child, b, kids);
-  __syncthreads();
-  scatter_originals<NTH>(T, F, L, [&](int d, double2 v) { sO[pk(d % m, d / m)] = v; });
-  __syncthreads();
-  // registers <- originals + pulled children contributions
-  double2 a[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int j = jg + 4 * c;
-    a[c] = (i < m && j <= i) ? sO[pk(i, j)] : make_double2(0.0, 0.0);
-  }
-  for (int k = 0; k < kids.n; ++k) {
-    const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-    const int ci = i < m ? C.cmap[i] : -1;
-    if (ci < 0) continue;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int j = jg + 4 * c;
-      if (j <= i) {
-        const int cj = C.cmap[j];
-        if (cj >= 0) a[c] = cadd(a[c], C.U[ci + cj * C.q]);
-      }
-    }
-  }
-
-  // pivot k = 4c + r lives in register slot c of the threads with jg == r;
-  // c is a compile-time index so the front never leaves the register file
-  double minp = DBL_MAX;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-#pragma unroll 1
-    for (int r = 0; r < 4; ++r) {
-      const int k = 4 * c + r;
-      if (k < p) {
-        double2* buf = col[k & 1];
-        if (jg == r) buf[i] = a[c];
-        __syncthreads();
-        const double2 dk = buf[k];
-        const double2 di = cinv(dk);
-        if (i > k && i < m) {
-          const double2 li = cmul(buf[i], di);
-#pragma unroll
-          for (int c2 = c; c2 < NC; ++c2) {
-            if (4 * c2 >= m) break;  // uniform: slots beyond the front order are dead
-            const int j = jg + 4 * c2;
-            if (j > k && j <= i) a[c2] = cfms(a[c2], li, buf[j]);
-          }
-          if (jg == r) a[c] = li;
-        }
-        if (tid == 0) {
-          double ad = sqrt(cabs2(dk));
-          minp = (ad != ad) ? -1.0 : fmin(minp, ad);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int j = jg + 4 * c;
-    if (i < m && j <= i) {
-      if (j < p) P[i + (int64_t)j * m] = a[c];
-      else U[(i - p) + (int64_t)(j - p) * q] = a[c];
-    }
-  }
-  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
-}
-
 // ---- forward solve: y <- L^{-1} b, fronts bottom-up ------------------------
 __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                        const double2* __restrict__ panels, double2* y,
@@ -1038,15 +677,6 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
 // ---- warp-per-front solves for fronts with m <= 64 ------------------------------
 // Lane l owns front rows l and l + 32. No block barriers: pivots are broadcast
 // with shuffles and every column of the panel is read with one coalesced load.
-KH_DEV double2 warp_sum2(double2 v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-  }
-  return v;
-}
-
 __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y, double2* ru_cur,
                                                         int64_t ru_stride_cur, const double2* __restrict__ ru_child,
@@ -1249,6 +879,7 @@ cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_
   if (ntasks == 0 || batch == 0) return cudaSuccess;
   big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_cur, upd_stride_cur,
                                                               upd_child, upd_stride_child);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1267,6 +898,7 @@ cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t
   cudaError_t e = set_smem_once((const void*)big_lupdate_kernel, smem, done);
   if (e != cudaSuccess) return e;
   big_lupdate_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1275,6 +907,7 @@ cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t n
   if (nfr == 0 || batch == 0) return cudaSuccess;
   big_diag_kernel<<<dim3((nfr + DIAG_WARPS - 1) / DIAG_WARPS, batch), 32 * DIAG_WARPS, 0, stream>>>(
       T, fronts, nfr, kb, panels, minpiv);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1282,6 +915,7 @@ cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t nt
                                double2* panels, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
   big_trsm_kernel<<<dim3(ntasks, batch), TRSM_ROWS, 0, stream>>>(T, tasks, kb, panels);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1293,32 +927,10 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
   const int smem = (int)(2 * sizeof(CpStage));
   cudaError_t e = set_smem_once((const void*)schur_update_kernel, smem, done);
   if (e != cudaSuccess) return e;
-  schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
-                                                                 upd_child, upd_stride_child);
-  return cudaGetLastError();
-}
-
-cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, const int32_t* tasks,
-                                   int32_t ntasks, int32_t batch, const double2* lam, double2* panels,
-                                   double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
-                                   int64_t upd_stride_child, double* minpiv, cudaStream_t stream) {
-  if (nlev == 0 || batch == 0) return cudaSuccess;
-  static bool attr = false;
-  const int smem = (int)sizeof(FactorSmem);
-  const int smem_s = (int)(2 * sizeof(CpStage));
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(factor_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  factor_panel_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, lam, panels, upd_cur,
-                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || ntasks == 0) return e;
-  schur_update_kernel<<<dim3(ntasks, batch), NT, smem_s, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
-                                                                   upd_child, upd_stride_child);
+  (void)upd_child;
+  (void)upd_stride_child;
+  schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1328,6 +940,7 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
   if (nlev == 0 || batch == 0) return cudaSuccess;
   fwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y, ru_cur,
                                                                     ru_stride_cur, ru_child, ru_stride_child);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1335,6 +948,7 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
                                 const double2* panels, double2* y, cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   bwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1344,6 +958,7 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
   if (nlev == 0 || batch == 0) return cudaSuccess;
   fwd_level_kernel<<<dim3(nlev, batch), NT, 0, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
                                                          ru_child, ru_stride_child);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1358,6 +973,7 @@ cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, in
     attr = smem;
   }
   bwd_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1366,6 +982,7 @@ cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, 
   if (n == 0 || batch == 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
   gather_rhs_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(n, perm, g_re, g_im, ldg, y);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1374,6 +991,7 @@ cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm,
   if (n == 0 || batch == 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
   scatter_sol_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(n, perm, y, z_re, z_im, ldz);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1381,6 +999,7 @@ cudaError_t kh_launch_shift_absmax_nnz(const double* mv, const double* av, int64
                                        const double2* lam, double* part, int32_t nblk, cudaStream_t stream) {
   if (batch == 0) return cudaSuccess;
   shift_absmax_kernel<<<dim3(nblk, batch), NT, 0, stream>>>(mv, av, nnz, lam, part);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1388,6 +1007,7 @@ cudaError_t kh_launch_rowreduce(const double* in, int64_t len, int32_t rows, int
                                 cudaStream_t stream) {
   if (rows == 0) return cudaSuccess;
   rowreduce_kernel<<<rows, NT, 0, stream>>>(in, len, op, out);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -1397,12 +1017,7 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   dim3 grid(nlev, batch);
-  // KH_SMALL_KERNEL=reg selects the register-resident kernels (A/B comparisons)
-  static const bool use_reg = [] {
-    const char* e = std::getenv("KH_SMALL_KERNEL");
-    return e && e[0] == 'r';
-  }();
-  if (!use_reg) {
+  {
     auto dsmem = [](int s) { return ((s + 8) * (s + 2) + 8) * 16; };
     static bool dattr = false;
     if (!dattr) {
@@ -1418,43 +1033,22 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
       case 32:
         factor_dmma_small_kernel<32, 2><<<grid, 64, dsmem(32), stream>>>(
             T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        kh_note_launch();
         break;
       case 48:
         factor_dmma_small_kernel<48, 2><<<grid, 64, dsmem(48), stream>>>(
             T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        kh_note_launch();
         break;
       case 64:
         factor_dmma_small_kernel<64, 4><<<grid, 128, dsmem(64), stream>>>(
             T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
+        kh_note_launch();
         break;
       default:
         return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
-  }
-  auto smem = [](int s) { return (s * (s + 1) / 2 + 2 * s) * 16; };
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(factor_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem(64));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  switch (ms) {
-    case 32:
-      factor_small_kernel<32><<<grid, 128, smem(32), stream>>>(T, level_fronts, lam, panels, upd_cur,
-                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
-      break;
-    case 48:
-      factor_small_kernel<48><<<grid, 192, smem(48), stream>>>(T, level_fronts, lam, panels, upd_cur,
-                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
-      break;
-    case 64:
-      factor_small_kernel<64><<<grid, 256, smem(64), stream>>>(T, level_fronts, lam, panels, upd_cur,
-                                                               upd_stride_cur, upd_child, upd_stride_child, minpiv);
-      break;
-    default:
-      return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -1,5 +1,6 @@
 // Internal launcher interfaces shared by the .cu translation units.
 #pragma once
+
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -33,13 +34,6 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
                             const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                             cudaStream_t stream);
 
-// Factor every front of one depth level for `batch` shifts.
-// Large fronts (m > 64): panel kernel, then the Schur update over `tasks`
-// ((front, tile row, tile col) triples of the level).
-cudaError_t kh_launch_factor_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, const int32_t* tasks,
-                                   int32_t ntasks, int32_t batch, const double2* lam, double2* panels,
-                                   double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
-                                   int64_t upd_stride_child, double* minpiv, cudaStream_t stream);
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
                                 const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream);
@@ -81,8 +75,11 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream);
-// Register-resident factorization of fronts with m <= ms (ms = 32 or 64).
+// Shared-memory DMMA factorization of fronts with m <= ms (ms = 32, 48 or 64).
 cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                    const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
                                    cudaStream_t stream);
+
+// Counts every kernel launch made by the library (kh_launch_count in the ABI).
+void kh_note_launch();

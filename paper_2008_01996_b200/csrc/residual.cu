@@ -85,11 +85,13 @@ cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y,
   if (n <= 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   daxpy_kernel<<<blocks, 256, 0, stream>>>(n, alpha, x, y);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream) {
   sumsq_kernel<<<nblk, 256, 0, stream>>>(x, n, part);
+  kh_note_launch();
   return cudaGetLastError();
 }
 
@@ -98,5 +100,6 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
                                     int32_t nblk, cudaStream_t stream) {
   pair_residual_kernel<<<nblk, 256, 0, stream>>>(n, nt, indptr, indices, mv, av, Y, ldy, F, ldf, R, ldr, part);
+  kh_note_launch();
   return cudaGetLastError();
 }

@@ -1,0 +1,53 @@
+"""Summarize an ncu launch-list CSV (gpu__time_duration.sum [+ dram bytes])
+into per-kernel totals: python profiles/summarize.py launches.csv [out.md]."""
+
+import collections
+import csv
+import sys
+
+
+def load(path):
+    with open(path) as fh:
+        lines = [l for l in fh if l.startswith('"')]
+    rows = collections.defaultdict(dict)
+    names = {}
+    for r in csv.DictReader(lines):
+        key = int(r["ID"])
+        names[key] = r["Kernel Name"]
+        v = r["Metric Value"].replace(",", "")
+        try:
+            rows[key][r["Metric Name"]] = float(v)
+        except ValueError:
+            pass
+    return names, rows
+
+
+def short(name):
+    return name.split("(")[0].replace("void ", "").replace("<unnamed>::", "")[:48]
+
+
+def main():
+    names, rows = load(sys.argv[1])
+    tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for k, m in rows.items():
+        if any(x in names[k] for x in ("at::", "cutlass", "cublas", "gemv", "splitKreduce")):
+            continue  # torch / cuBLAS work of the input generators and the peak measurement
+        t = tot[short(names[k])]
+        t[0] += 1
+        t[1] += m.get("gpu__time_duration.sum", 0.0)
+        t[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    all_t = sum(v[1] for v in tot.values())
+    out = ["| kernel | launches | time (ms) | share | DRAM bytes (GB) |", "|---|---|---|---|---|"]
+    for name, (n, t, b) in sorted(tot.items(), key=lambda x: -x[1][1]):
+        out.append(f"| `{name}` | {n} | {t / 1e6:.3f} | {t / all_t:.1%} | {b / 1e9:.2f} |")
+    out.append(f"| total | {sum(v[0] for v in tot.values())} | {all_t / 1e6:.3f} | 100% | "
+               f"{sum(v[2] for v in tot.values()) / 1e9:.2f} |")
+    text = "\n".join(out)
+    print(text)
+    if len(sys.argv) > 2:
+        with open(sys.argv[2], "w") as fh:
+            fh.write(text + "\n")
+
+
+if __name__ == "__main__":
+    main()
