@@ -61,3 +61,19 @@ def test_separable_projection_matches_generic():
     a = fem.project_rhs(mx, mt, lambda x, y, t: s(x, y) * g(t), quad_order=6)
     b = fem.project_rhs_separable(mx, mt, s, g, quad_order=6)
     assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
+
+
+def test_c1_inputs_match_reference_fixture():
+    # BASELINE config 1 built by the restated generators equals the inputs the
+    # reference assembled for the golden fixture (same mesh, series, seed)
+    from conftest import load_golden
+    from paper_2008_01996_b200 import problems
+
+    system, _ = problems.build_system("c1")
+    ref, _ = load_golden("c1")
+    assert np.array_equal(system.rhs, ref.rhs)
+    for mine, theirs in ((system.temporal.A, ref.temporal.A), (system.temporal.M, ref.temporal.M)):
+        assert np.max(np.abs(mine - theirs)) <= 1e-13 * np.max(np.abs(theirs))
+    for mine, theirs in ((system.spatial.M_II, ref.spatial.M_II), (system.spatial.A_II, ref.spatial.A_II)):
+        d = sp.csr_matrix(mine) - theirs
+        assert (abs(d).max() if d.nnz else 0.0) <= 1e-14 * abs(theirs).max()
