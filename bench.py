@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--j-max", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the multi-GPU driver even with one rank (testing the N>1 path on one GPU)")
     return ap.parse_args()
 
 
@@ -207,7 +209,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.force_sharded
+    if sharded:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -223,7 +226,7 @@ def main():
     dof = system.dof
     leaf = args.leaf_size or sparse_direct.DEFAULT_LEAF_SIZE
 
-    if world > 1:
+    if sharded:
         from paper_2008_01996_b200.distributed import ShardedFD
 
         runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
@@ -255,7 +258,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         torch.distributed.barrier()
     from paper_2008_01996_b200 import _native
 
@@ -275,7 +278,7 @@ def main():
     torch.cuda.synchronize()
     ck = clocks.stop()
     elapsed = t_start.elapsed_time(t_end) / 1e3
-    if world > 1:
+    if sharded:
         tt = torch.tensor([elapsed], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(tt.item())
@@ -290,8 +293,10 @@ def main():
     peaks = measured_peaks(dev) if rank == 0 else {}
 
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if not sharded and rank == 0 and not args.no_e2e:
         e2e = measure_e2e(system, pencil, args, leaf)
+    elif sharded and not args.no_e2e:
+        e2e = measure_e2e_sharded(system, runner, args, dev)
 
     if rank == 0:
         achieved = fac_flops / fac_s / 1e12 if fac_s > 0 else None
@@ -305,7 +310,7 @@ def main():
                        "shifts_solved": int(modal.n_k), "conjugate_pairs": int(modal.n_pairs),
                        "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
                            stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
-                       "parallelism": f"shift-sharded x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"shift-sharded x{world} + NCCL reduce-scatter" if sharded else "single GPU"},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),
@@ -326,7 +331,7 @@ def main():
                                                f"{cb['sample_shifts']} of {cb['n_t']} SuperLU shift solves "
                                                f"timed and extrapolated; t_total={cb['t_total']:.2f}s")}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
@@ -366,6 +371,39 @@ def measure_e2e(system, pencil, args, leaf):
             "d2h_bytes_per_step": int(8 * n * nt), "steps": len(times),
             "includes": "symbolic analysis, plan upload, factorization, solve, refinement, D2H of u",
             "residual": rep.residual}
+
+
+def measure_e2e_sharded(system, runner, args, dev):
+    """N GPUs: each step copies f from pinned host memory to every rank, runs
+    the sharded solve (NCCL reduce-scatter of the back transform) and reads
+    each rank's rows of u back to pinned host memory; max time over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    n, nt = system.m_x, system.n_t
+    pinned = torch.empty(system.rhs.shape, dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(system.rhs))
+    F = torch.empty((nt, n), dtype=torch.float64, device=dev)
+    out = torch.empty(runner.U.shape, dtype=torch.float64, pin_memory=True)
+
+    def one():
+        F.view(-1).copy_(pinned, non_blocking=True)
+        U, _ = runner.solve(F, refine=args.refine)
+        out.copy_(U)
+        torch.cuda.synchronize()
+
+    one()
+    dist.barrier()
+    steps = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    el = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    return {"value": system.dof / float(el.item()), "unit": UNIT, "h2d_bytes_per_step": int(8 * n * nt),
+            "d2h_bytes_per_step": int(8 * runner.rp * nt), "steps": steps,
+            "includes": "H2D of f on every rank, sharded factor/solve/refinement, NCCL reduce-scatter, "
+                        "D2H of each rank's rows of u"}
 
 
 def run_reference(args, world, rank):
