@@ -196,3 +196,46 @@ class ShardedFD:
         allU = torch.zeros((self.world, self.n_t, self.rp), dtype=self.U.dtype, device=self.U.device)
         dist.all_gather_into_tensor(allU.view(-1), self.U.view(-1), group=self.group)
         return allU.permute(1, 0, 2).reshape(self.n_t, self.world * self.rp)[:, :self.n].contiguous()
+
+
+def solve_fd_sharded(system, pencil=None, refine=3, refine_tol=1e-13, leaf_size=None, group=None):
+    """Multi-GPU counterpart of solvers.solve_fd (reference solvers.py:348-403)
+    for one process per GPU under an initialized torch.distributed group.
+
+    Every rank passes the same `system`; rank r returns its row block of u:
+    (rows, U_rows, report) where `rows` = (r0, r1) are interior spatial rows
+    and U_rows is the host (N_t, r1 - r0) array of u[r0:r1, :] (column-major
+    layout of the reference's coefficient vector restricted to those rows).
+    The report is the same on every rank except the timings.
+    """
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native, solvers
+    from .engine import modal_plan
+
+    _native.require_cuda()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    report = solvers.SolveReport(variant="fd", dof=system.dof, n_t=system.n_t, m_x=system.m_x)
+    t0 = time.perf_counter()
+    if pencil is None:
+        pencil = solvers.build_pencil(system.temporal, "fd")
+    modal = modal_plan(system.temporal, pencil)
+    report.t_decompose = time.perf_counter() - t0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    report.device = torch.cuda.get_device_name(dev)
+    n, nt = system.m_x, system.n_t
+    t0 = time.perf_counter()
+    runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
+                       leaf_size=leaf_size, group=group)
+    F = solvers._to_device(system.rhs, dev).view(nt, n)
+    U, info = runner.solve(F, refine=refine, tol=refine_tol)
+    r0, rows = runner.rows(rank)
+    out = solvers._to_host(U[:, :rows])
+    report.t_spatial = time.perf_counter() - t0
+    report.fd_residual = info["residuals"][0]
+    report.refine_steps = info["refine_steps"]
+    report.residual = info["residual"]
+    return (r0, r0 + rows), out, report

@@ -38,5 +38,14 @@ def test_sharded_fd_world1_nccl(cuda_ok):
         u = run.gather().reshape(-1).cpu().numpy()
         assert rel_diff(u, ref["bs"]) < 1e-10
         assert info["residual"] < 1e-11
+
+        # public multi-GPU entry point: same rows as solve_fd, host output
+        from paper_2008_01996_b200.distributed import solve_fd_sharded
+
+        (r0, r1), U_rows, rep = solve_fd_sharded(system)
+        assert (r0, r1) == (0, system.m_x)
+        assert U_rows.shape == (system.n_t, system.m_x)
+        assert rel_diff(U_rows.reshape(-1), ref["bs"]) < 1e-10
+        assert rep.residual < 1e-11
     finally:
         dist.destroy_process_group()
