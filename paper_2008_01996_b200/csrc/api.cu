@@ -42,8 +42,10 @@ int cuda_fail(cudaError_t e, const char* where) {
 constexpr int32_t kDefaultLeaf = 24;
 // fronts with m <= kClassMax[c] use the register-resident kernels; the rest
 // ("large", class kSmallClasses) the level-synchronous DMMA kernels
-constexpr int kSmallClasses = 3;
-constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64};
+constexpr int kSmallClasses = 5;
+constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, 96, 128};
+// the warp-per-front solve kernels take the classes with m <= 64
+constexpr int kSolveSmallClasses = 3;
 constexpr int kClsStride = kSmallClasses + 2;
 constexpr int32_t kAbsmaxBlocks = 64;
 constexpr int32_t kResidualBlocks = 1184;  // 8 x 148 SMs
@@ -93,6 +95,8 @@ struct kh_plan {
   int32_t *child_list = nullptr, *relind = nullptr, *cmap = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
   int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
   double *mv = nullptr, *av = nullptr;
+  double *om = nullptr, *oa = nullptr;  // values in front-original order (gathered on the device)
+  int64_t n_orig = 0;
   double2* panels = nullptr;
   double2* upd[2] = {nullptr, nullptr};
   double2* rupd[2] = {nullptr, nullptr};
@@ -115,6 +119,8 @@ struct kh_plan {
     T.orig_dst = orig_dst;
     T.mv = mv;
     T.av = av;
+    T.om = om;
+    T.oa = oa;
     T.nf = nf;
     T.n = n;
     T.panel_total = panel_total;
@@ -343,7 +349,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   }
   // KH_SMALL_MAX caps the register/shared-memory small-front classes
   // (0 disables them, for A/B measurements)
-  int small_max = 64;
+  int small_max = 128;
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
   auto front_class = [&](int32_t m) {
     for (int c = 0; c < kSmallClasses; ++c)
@@ -442,6 +448,8 @@ void carve(kh_plan* p, const kh::Symbolic& S, const Sched& X, Carver& C) {
   C.take(&p->indices, (size_t)S.nnz);
   C.take(&p->mv, (size_t)S.nnz);
   C.take(&p->av, (size_t)S.nnz);
+  C.take(&p->om, S.orig_src.size());
+  C.take(&p->oa, S.orig_src.size());
   C.take(&p->panels, (size_t)(p->slots * S.panel_total));
   for (int k = 0; k < 2; ++k) {
     C.take(&p->upd[k], (size_t)(p->max_batch * p->upd_size[k]));
@@ -543,6 +551,9 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     up(p->indices, indices, (size_t)S.nnz * 8);
     up(p->mv, m_vals, (size_t)S.nnz * 8);
     up(p->av, a_vals, (size_t)S.nnz * 8);
+    p->n_orig = (int64_t)S.orig_src.size();
+    if (e == cudaSuccess) e = kh_launch_gather_orig(p->n_orig, p->orig_src, p->mv, p->av, p->om, p->oa, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
     plan_release(p);
@@ -560,6 +571,8 @@ int kh_plan_set_values(kh_plan* p, const double* m_vals, const double* a_vals) {
   KH_CUDA(cudaSetDevice(p->device));
   KH_CUDA(cudaMemcpy(p->mv, m_vals, p->nnz * 8, cudaMemcpyHostToDevice));
   KH_CUDA(cudaMemcpy(p->av, a_vals, p->nnz * 8, cudaMemcpyHostToDevice));
+  KH_CUDA(kh_launch_gather_orig(p->n_orig, p->orig_src, p->mv, p->av, p->om, p->oa, 0));
+  KH_CUDA(cudaDeviceSynchronize());
   return KH_OK;
 }
 
@@ -648,22 +661,23 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   const int32_t ns = (int32_t)nshift;
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
   KH_CUDA(fork_side(p, st));
-  // fronts with m <= 64 (the small classes) use the warp-per-front kernels
-  constexpr int L = kSmallClasses;
+  // fronts with m <= 64 use the warp-per-front kernels, the rest the CTA ones
+  constexpr int L = kSolveSmallClasses;
   for (int32_t d = p->depth; d >= 0; --d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
     KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side));
-    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[L + 1] - co[L], ns, panels, p->y, rc, sc, rch, sch, st));
+    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, panels, p->y, rc, sc, rch, sch,
+                                st));
     KH_CUDA(join_side(p, st));
   }
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
     KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side));
-    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[L + 1] - co[L], ns, p->max_p, panels, p->y, st));
+    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, panels, p->y, st));
     KH_CUDA(join_side(p, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));

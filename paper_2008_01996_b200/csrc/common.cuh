@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #define KH_DEV __device__ __forceinline__
+#define KH_HD __host__ __device__
 
 // ---- complex fp64 -----------------------------------------------------------
 KH_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }

@@ -17,6 +17,7 @@
 // of the remaining pivot columns, and finally one SYRK-like update of U with
 // K = p. All three GEMM-shaped steps run on DMMA (mma.sync m8n8k4 f64) as
 // complex products built from four real MMAs.
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -50,32 +51,6 @@ KH_DEV void tile_epilogue(const Acc& acc, EP ep) {
       for (int h = 0; h < 2; ++h)
         ep(wi * 32 + mt * 8 + g, wj * 16 + nt * 8 + 2 * t + h,
            make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
-}
-
-// Original entries of the front's pivot columns: store(local_offset, value)
-// with value = M_ij + lambda A_ij. Four entries per thread are in flight at
-// once (the index -> value loads are dependent, so batching hides latency).
-template <int NTH, class ST>
-KH_DEV void scatter_originals(const KhTree& T, const KhDevFront& F, double2 L, ST store) {
-  for (int64_t e0 = F.orig_begin + threadIdx.x; e0 < F.orig_end; e0 += 4 * NTH) {
-    int64_t s[4];
-    int d[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e = e0 + (int64_t)u * NTH;
-      s[u] = e < F.orig_end ? T.orig_src[e] : -1;
-      d[u] = e < F.orig_end ? T.orig_dst[e] : 0;
-    }
-    double mv[4], av[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      mv[u] = s[u] >= 0 ? T.mv[s[u]] : 0.0;
-      av[u] = s[u] >= 0 ? T.av[s[u]] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (s[u] >= 0) store(d[u], make_double2(fma(L.x, av[u], mv[u]), L.y * av[u]));
-  }
 }
 
 // ---- pull assembly ------------------------------------------------------------
@@ -323,9 +298,9 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
   }
   const double2 L = lam[b];
   for (int64_t e = lo + tid; e < hi; e += NT) {
-    const int64_t s = T.orig_src[e];
     const int d = T.orig_dst[e];
-    P[d] = cadd(P[d], make_double2(fma(L.x, T.av[s], T.mv[s]), L.y * T.av[s]));
+    const double av = T.oa[e];
+    P[d] = cadd(P[d], make_double2(fma(L.x, av, T.om[e]), L.y * av));
   }
 }
 
@@ -348,63 +323,6 @@ __global__ void __launch_bounds__(128) big_lupdate_kernel(KhTree T, const int32_
       *d = csub(*d, v);
     }
   });
-}
-
-// One warp per (front, shift): LDL^T of the w x w diagonal block at kb.
-// Lane j holds column j of the block in registers (rows i >= j, static
-// register index i); pivot k publishes its (unscaled) column to a per-warp
-// shared vector, and every lane applies the rank-1 update to its column.
-// No block barriers and no dynamic register indexing.
-constexpr int DIAG_WARPS = 4;
-__global__ void __launch_bounds__(32 * DIAG_WARPS) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
-                                                                   int nfr, int kb, double2* panels,
-                                                                   double* minpiv) {
-  __shared__ double2 colbuf[DIAG_WARPS][NB];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int idx = blockIdx.x * DIAG_WARPS + wid;
-  if (idx >= nfr) return;
-  double2* cb = colbuf[wid];
-  const int32_t f = fronts[idx];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
-  double2* B = panels + (int64_t)b * T.panel_total + F.panel_off + kb + (int64_t)kb * m;
-  const int j = lane;
-  double2 a[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) a[i] = (j < w && i >= j && i < w) ? B[i + (int64_t)j * m] : make_double2(0.0, 0.0);
-  double minp = DBL_MAX;
-  for (int k = 0; k < w; ++k) {
-    if (j == k) {
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (i >= k) cb[i] = a[i];
-    }
-    __syncwarp();
-    const double2 dk = cb[k];
-    const double2 di = cinv(dk);
-    if (j > k && j < w) {
-      const double2 fj = cmul(cb[j], di);  // l_jk
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (i >= j) a[i] = cfms(a[i], cb[i], fj);
-    }
-    if (j == k) {
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (i > k) a[i] = cmul(a[i], di);
-    }
-    const double ad = sqrt(cabs2(dk));
-    minp = (ad != ad) ? -1.0 : fmin(minp, ad);
-    __syncwarp();
-  }
-#pragma unroll
-  for (int i = 0; i < NB; ++i)
-    if (j < w && i >= j && i < w) B[i + (int64_t)j * m] = a[i];
-  if (lane == 0) {
-    double* mp = minpiv + (int64_t)b * T.nf + f;
-    *mp = kb == 0 ? minp : fmin(*mp, minp);
-  }
 }
 
 // Rows below the factored diagonal block: one thread per row r solves
@@ -446,65 +364,31 @@ __global__ void __launch_bounds__(TRSM_ROWS) big_trsm_kernel(KhTree T, const int
     if (jj < w) row[(int64_t)jj * m] = cmul(v[jj], sdi[jj]);
 }
 
-// ---- small fronts (m <= MS): shared-memory blocked LDL^T on DMMA -----------------
-// The whole front lives in shared memory (column-major, ld MS+2: conflict-free
-// DMMA fragment loads). Pivots go in blocks of 8: warp 0 factors the 8 x 8
-// diagonal block with shuffles, the rows below are solved one thread per row,
-// and the rank-8 trailing update runs on DMMA over the 8 x 8 lower blocks of
-// the trailing matrix (4 real MMAs per complex product). Three barriers per
-// 8 pivots instead of one or two per pivot, and 8x fewer FMA instructions.
-template <int MS, int NW>
-__global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
-    KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
-    double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
-    double* minpiv) {
-  constexpr int NTH = 32 * NW, LD = MS + 2, BK = 8;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* S = reinterpret_cast<double2*>(smem_raw);  // front, S[c*LD + r]
-  double2* W = S + MS * LD;                           // W[k*LD + r] = L[r][kb+k] d_{kb+k}
-  double2* dinv = W + BK * LD;                        // 1/d of the current block
-  __shared__ Kids kids;
+// Right-looking blocked LDL^T of the m x m lower matrix S over its first p
+// pivots, by 32*NW threads. Entry (r, c), r >= c, lives at S[cb[c] + r]
+// (cb: per-column base offsets in shared memory, so dense and packed
+// block-column layouts share the code). Pivots go in blocks of 8: warp 0
+// factors the 8 x 8 diagonal block with shuffles, the rows below are solved
+// one thread per row, and the rank-8 trailing update of S[s0:, s0:] runs on
+// DMMA over 8 x 8 lower blocks (4 real MMAs per complex product). W (8 rows of
+// ldw) and dinv (8) are shared scratch. Returns the smallest |d| (or -1 for a
+// non-finite pivot) on thread 0.
+template <int NW>
+KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, double2* dinv, int m, int p) {
+  constexpr int NTH = 32 * NW, BK = 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t f = level_fronts[blockIdx.x];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, q = F.q, m = p + q;
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
-
-  // ---- assembly: pull children into the lower triangle, then add originals
-  load_kids(T, F, upd_child, upd_stride_child, b, kids);
-  __syncthreads();
-  for (int idx = tid; idx < m * m; idx += NTH) {
-    const int c = idx / m, r = idx - c * m;
-    if (r < c) continue;
-    double2 v = make_double2(0.0, 0.0);
-    for (int k = 0; k < kids.n; ++k) {
-      const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-      const int ci = C.cmap[r], cj = C.cmap[c];
-      if (ci >= 0 && cj >= 0) v = cadd(v, C.U[ci + cj * C.q]);
-    }
-    S[c * LD + r] = v;
-  }
-  __syncthreads();
-  const double2 Lm = lam[b];
-  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
-    const int64_t s = T.orig_src[e];
-    const int d = T.orig_dst[e];
-    double2* t = S + (d / m) * LD + (d % m);
-    *t = cadd(*t, make_double2(fma(Lm.x, T.av[s], T.mv[s]), Lm.y * T.av[s]));
-  }
-  __syncthreads();
-
   double minp = DBL_MAX;
   for (int kb = 0; kb < p; kb += BK) {
     const int w = min(BK, p - kb);
+    int cbk[BK];
+#pragma unroll
+    for (int j = 0; j < BK; ++j) cbk[j] = cb[min(kb + j, m - 1)];
     // (a) diagonal block: lane i < w holds row i of the w x w block
     if (warp == 0) {
       double2 a[BK];
 #pragma unroll
       for (int j = 0; j < BK; ++j)
-        a[j] = (lane < w && j <= lane) ? S[(kb + j) * LD + kb + lane] : make_double2(0.0, 0.0);
+        a[j] = (lane < w && j <= lane) ? S[cbk[j] + kb + lane] : make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < BK; ++k) {
         if (k < w) {
@@ -526,7 +410,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
       }
 #pragma unroll
       for (int j = 0; j < BK; ++j)
-        if (lane < w && j <= lane) S[(kb + j) * LD + kb + lane] = a[j];
+        if (lane < w && j <= lane) S[cbk[j] + kb + lane] = a[j];
     }
     __syncthreads();
     // (b) rows below: v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k]; L[r][kb+j] = v_j / d_j
@@ -536,19 +420,19 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
 #pragma unroll
       for (int j = 0; j < BK; ++j) {
         if (j < w) {
-          double2 x = S[(kb + j) * LD + r];
+          double2 x = S[cbk[j] + r];
 #pragma unroll
-          for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[(kb + k) * LD + kb + j]);
+          for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[cbk[k] + kb + j]);
           v[j] = x;
         }
       }
 #pragma unroll
       for (int j = 0; j < BK; ++j) {
         if (j < w) {
-          W[j * LD + r] = v[j];
-          S[(kb + j) * LD + r] = cmul(v[j], dinv[j]);
+          W[j * ldw + r] = v[j];
+          S[cbk[j] + r] = cmul(v[j], dinv[j]);
         } else {
-          W[j * LD + r] = make_double2(0.0, 0.0);
+          W[j * ldw + r] = make_double2(0.0, 0.0);
         }
       }
     }
@@ -556,6 +440,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
     // (c) trailing update on DMMA: S[r][c] -= sum_k L[r][kb+k] W[c][k], s0 <= c <= r < m
     const int nb = (m - s0 + 7) / 8;
     const int g = lane >> 2, t = lane & 3;
+    const int ca0 = cb[min(kb + t, m - 1)], ca1 = cb[min(kb + t + 4, m - 1)];
     for (int task = warp; task < nb * (nb + 1) / 2; task += NW) {
       int bi = 0, rem = task;
       while (rem > bi) rem -= ++bi;  // task -> (bi, bj = rem), bj <= bi
@@ -564,9 +449,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
 #pragma unroll
       for (int ks = 0; ks < BK; ks += 4) {
         const int k = ks + t;
-        const int ra = r0 + g, cb = c0 + g;
-        const double2 af = (k < w && ra < m) ? S[(kb + k) * LD + ra] : make_double2(0.0, 0.0);
-        const double2 bf = (cb < m) ? W[k * LD + cb] : make_double2(0.0, 0.0);
+        const int ra = r0 + g, cbv = c0 + g;
+        const double2 af = (k < w && ra < m) ? S[(ks ? ca1 : ca0) + ra] : make_double2(0.0, 0.0);
+        const double2 bf = (cbv < m) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
         dmma884(cr[0], cr[1], af.x, bf.x);
         dmma884(cr[0], cr[1], -af.y, bf.y);
         dmma884(ci[0], ci[1], af.x, bf.y);
@@ -577,20 +462,151 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) factor_dmma_small_kernel(
       for (int h = 0; h < 2; ++h) {
         const int cc = c0 + 2 * t + h;
         if (rr < m && cc < m && rr >= cc) {
-          double2* d = S + cc * LD + rr;
+          double2* d = S + cb[cc] + rr;
           *d = make_double2(d->x - cr[h], d->y - ci[h]);
         }
       }
     }
     __syncthreads();
   }
-  // ---- write the panel and the update matrix (lower parts)
-  for (int idx = tid; idx < m * m; idx += NTH) {
+  return minp;
+}
+
+// LDL^T of the w x w diagonal block at kb of a large front: one 64-thread CTA
+// per (front, shift), the block staged in shared memory and factored by
+// blocked_ldlt (8-pivot blocks, DMMA trailing updates).
+constexpr int DIAG_NW = 2, DIAG_LD = NB + 2;
+__global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
+                                                                int nfr, int kb, double2* panels, double* minpiv) {
+  __shared__ double2 S[NB * DIAG_LD];
+  __shared__ double2 W[8 * DIAG_LD];
+  __shared__ double2 dinv[8];
+  __shared__ int32_t cb[NB];
+  if (threadIdx.x < NB) cb[threadIdx.x] = threadIdx.x * DIAG_LD;
+  const int32_t f = fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
+  double2* B = panels + (int64_t)b * T.panel_total + F.panel_off + kb + (int64_t)kb * m;
+  for (int e = threadIdx.x; e < w * w; e += 32 * DIAG_NW) {
+    const int c = e / w, r = e - c * w;
+    if (r >= c) S[c * DIAG_LD + r] = B[r + (int64_t)c * m];
+  }
+  __syncthreads();
+  const double minp = blocked_ldlt<DIAG_NW>(S, cb, W, DIAG_LD, dinv, w, w);
+  for (int e = threadIdx.x; e < w * w; e += 32 * DIAG_NW) {
+    const int c = e / w, r = e - c * w;
+    if (r >= c) B[r + (int64_t)c * m] = S[c * DIAG_LD + r];
+  }
+  if (threadIdx.x == 0) {
+    double* mp = minpiv + (int64_t)b * T.nf + f;
+    *mp = kb == 0 ? minp : fmin(*mp, minp);
+  }
+}
+
+// ---- fused fronts (m <= MS): assemble + factor + Schur complement in one CTA ----
+// The front's lower triangle lives in shared memory in packed block-column
+// form: the 8-column block b holds rows 8b..m-1 with a leading dimension
+// ld_b = roundup8(m - 8b) + 2 (= 2 mod 8 in 16-byte units: conflict-free DMMA
+// fragment loads), so a 128-row front needs 140 KB instead of 260 KB. The
+// whole LDL^T, including the update matrix U = C - L21 D L21^T, is done by
+// blocked_ldlt; the panel and U are then written once, coalesced.
+KH_HD constexpr int packed_ld(int m, int b) { return ((m - 8 * b + 7) / 8) * 8 + 2; }
+KH_HD constexpr int packed_elems(int m) {
+  int e = 0;
+  for (int b = 0; 8 * b < m; ++b) e += 8 * packed_ld(m, b);
+  return e;
+}
+KH_HD constexpr int front_smem_bytes(int ms) {
+  return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8) + 4 * ms + 4 * 4 * ms;
+}
+
+template <int MS, int NW>
+__global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_front_kernel(
+    KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
+    double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
+    double* minpiv) {
+  constexpr int NTH = 32 * NW, LDW = MS + 2, RK = 4;  // RK: children whose relind maps are staged
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // packed lower triangle
+  double2* W = S + packed_elems(MS);                  // W[k*LDW + r] = L[r][kb+k] d_{kb+k}
+  double2* dinv = W + 8 * LDW;                        // 1/d of the current block
+  int32_t* cb = reinterpret_cast<int32_t*>(dinv + 8);  // column bases
+  int32_t* rel = cb + MS;                              // rel[k*MS + i]
+  const int tid = threadIdx.x;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+
+  // ---- assembly: zero the front, add the originals (values pre-gathered in
+  // front order: one coalesced stream), then push each child's update block
+  // through its relind map (coalesced reads of the child's U, conflict-free
+  // within a child; children in order, so the sums are deterministic)
+  const int ne = packed_elems(m);
+  for (int idx = tid; idx < ne; idx += NTH) S[idx] = make_double2(0.0, 0.0);
+  for (int c = tid; c < m; c += NTH) {
+    const int bc = c >> 3;
+    int off = 0;
+    for (int bb = 0; bb < bc; ++bb) off += 8 * packed_ld(m, bb);
+    cb[c] = off + (c & 7) * packed_ld(m, bc) - 8 * bc;
+  }
+  const int nkids = F.child_end - F.child_begin;
+  for (int idx = tid; idx < RK * MS; idx += NTH) {
+    const int k = idx / MS, i = idx - k * MS;
+    if (k < nkids) {
+      const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+      if (i < C.q) rel[idx] = T.relind[C.rows_begin + i];
+    }
+  }
+  __syncthreads();
+  const double2 Lm = lam[b];
+  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
+    const int d = T.orig_dst[e];
+    const int c = d / m;
+    const double av = T.oa[e];
+    double2* t = S + cb[c] + (d - c * m);
+    *t = cadd(*t, make_double2(fma(Lm.x, av, T.om[e]), Lm.y * av));
+  }
+  for (int k = 0; k < nkids; ++k) {
+    __syncthreads();
+    const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+    const double2* Uc = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
+    const int32_t* rk = k < RK ? rel + k * MS : T.relind + C.rows_begin;
+    const int qk = C.q, qq = qk * qk;
+    for (int base = 0; base < qq; base += 4 * NTH) {
+      double2 v[4];
+      int ci[4], cj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + tid + u * NTH;
+        cj[u] = idx / max(qk, 1);
+        ci[u] = idx - cj[u] * qk;
+        const bool ok = idx < qq && ci[u] >= cj[u];
+        v[u] = ok ? Uc[idx] : make_double2(0.0, 0.0);
+        if (!ok) ci[u] = -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ci[u] >= 0) {
+          double2* t = S + cb[rk[cj[u]]] + rk[ci[u]];
+          *t = cadd(*t, v[u]);
+        }
+    }
+  }
+  __syncthreads();
+
+  const double minp = blocked_ldlt<NW>(S, cb, W, LDW, dinv, m, p);
+  // ---- write the panel and the update matrix (lower parts), coalesced
+  for (int idx = tid; idx < m * p; idx += NTH) {
     const int c = idx / m, r = idx - c * m;
-    if (r < c) continue;
-    const double2 v = S[c * LD + r];
-    if (c < p) P[r + c * m] = v;
-    else U[(r - p) + (c - p) * q] = v;
+    if (r >= c) P[idx] = S[cb[c] + r];
+  }
+  for (int idx = tid; idx < q * q; idx += NTH) {
+    const int c = idx / q, r = idx - c * q;
+    if (r >= c) U[idx] = S[cb[p + c] + p + r];
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
 }
@@ -816,6 +832,15 @@ __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* 
   for (int k = tid; k < p; k += NT) yy[k] = st[k];
 }
 
+__global__ void gather_orig_kernel(int64_t n, const int64_t* __restrict__ src, const double* __restrict__ mv,
+                                   const double* __restrict__ av, double* __restrict__ om, double* __restrict__ oa) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = src[e];
+    om[e] = mv[s];
+    oa[e] = av[s];
+  }
+}
+
 __global__ void gather_rhs_kernel(int64_t n, const int64_t* __restrict__ perm, const double* __restrict__ g_re,
                                   const double* __restrict__ g_im, int64_t ldg, double2* y) {
   const int b = blockIdx.y;
@@ -905,8 +930,7 @@ cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t
 cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t nfr, int kb, int32_t batch,
                                double2* panels, double* minpiv, cudaStream_t stream) {
   if (nfr == 0 || batch == 0) return cudaSuccess;
-  big_diag_kernel<<<dim3((nfr + DIAG_WARPS - 1) / DIAG_WARPS, batch), 32 * DIAG_WARPS, 0, stream>>>(
-      T, fronts, nfr, kb, panels, minpiv);
+  big_diag_kernel<<<dim3(nfr, batch), 32 * DIAG_NW, 0, stream>>>(T, fronts, nfr, kb, panels, minpiv);
   kh_note_launch();
   return cudaGetLastError();
 }
@@ -977,6 +1001,15 @@ cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, in
   return cudaGetLastError();
 }
 
+cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const double* mv, const double* av, double* om,
+                                  double* oa, cudaStream_t stream) {
+  if (n_orig <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n_orig + 255) / 256, 148 * 8);
+  gather_orig_kernel<<<blocks, 256, 0, stream>>>(n_orig, src, mv, av, om, oa);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
                                  const double* g_im, int64_t ldg, double2* y, cudaStream_t stream) {
   if (n == 0 || batch == 0) return cudaSuccess;
@@ -1016,39 +1049,26 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
                                    cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  dim3 grid(nlev, batch);
-  {
-    auto dsmem = [](int s) { return ((s + 8) * (s + 2) + 8) * 16; };
-    static bool dattr = false;
-    if (!dattr) {
-      cudaError_t e = cudaFuncSetAttribute(factor_dmma_small_kernel<64, 4>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem(64));
+  const dim3 grid(nlev, batch);
+  auto run = [&](auto kernel, int ms_, int threads, bool& attr) -> cudaError_t {
+    const int smem = front_smem_bytes(ms_);
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(factor_dmma_small_kernel<48, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               dsmem(48));
-      if (e != cudaSuccess) return e;
-      dattr = true;
+      attr = true;
     }
-    switch (ms) {
-      case 32:
-        factor_dmma_small_kernel<32, 2><<<grid, 64, dsmem(32), stream>>>(
-            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
-        kh_note_launch();
-        break;
-      case 48:
-        factor_dmma_small_kernel<48, 2><<<grid, 64, dsmem(48), stream>>>(
-            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
-        kh_note_launch();
-        break;
-      case 64:
-        factor_dmma_small_kernel<64, 4><<<grid, 128, dsmem(64), stream>>>(
-            T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child, upd_stride_child, minpiv);
-        kh_note_launch();
-        break;
-      default:
-        return cudaErrorInvalidValue;
-    }
+    kernel<<<grid, threads, smem, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child,
+                                            upd_stride_child, minpiv);
+    kh_note_launch();
     return cudaGetLastError();
+  };
+  static bool a32 = false, a48 = false, a64 = false, a96 = false, a128 = false;
+  switch (ms) {
+    case 32: return run(factor_front_kernel<32, 2>, 32, 64, a32);
+    case 48: return run(factor_front_kernel<48, 2>, 48, 64, a48);
+    case 64: return run(factor_front_kernel<64, 4>, 64, 128, a64);
+    case 96: return run(factor_front_kernel<96, 4>, 96, 128, a96);
+    case 128: return run(factor_front_kernel<128, 8>, 128, 256, a128);
+    default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }

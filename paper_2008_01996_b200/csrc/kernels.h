@@ -25,6 +25,8 @@ struct KhTree {  // device pointers shared by every level kernel
   const int32_t* orig_dst;
   const double* mv;  // M values aligned with the analyzed CSR
   const double* av;  // A values aligned with the analyzed CSR
+  const double* om;  // M values in front-original order: om[e] = mv[orig_src[e]]
+  const double* oa;  // A values in front-original order
   int32_t nf;
   int64_t n;
   int64_t panel_total;
@@ -80,6 +82,10 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
                                    cudaStream_t stream);
+
+// om[e] = mv[src[e]], oa[e] = av[src[e]] (values in the order the fronts read them).
+cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const double* mv, const double* av, double* om,
+                                  double* oa, cudaStream_t stream);
 
 // Counts every kernel launch made by the library (kh_launch_count in the ABI).
 void kh_note_launch();
