@@ -29,17 +29,19 @@ def needs_rebuild():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_rebuild():
+def build(force=False, verbose=False, out=OUT, defines=()):
+    """Compile the library; `out`/`defines` build instrumented variants for
+    the probes under profiles/probes (the product uses the default)."""
+    if out == OUT and not defines and not force and not needs_rebuild():
         return OUT
     cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+           *[f"-D{d}" for d in defines], "-o", out + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -21,7 +21,7 @@ KH_DEV double2 cfms(double2 a, double2 b, double2 c) {
 KH_DEV double2 cinv(double2 a) {
   // One IEEE reciprocal instead of two divisions. Smith-style scaling is
   // unnecessary: pivots passing the reference's threshold check are O(1).
-  const double r = 1.0 / (a.x * a.x + a.y * a.y);
+  const double r = __drcp_rn(a.x * a.x + a.y * a.y);  // == 1.0 / x, correctly rounded
   return make_double2(a.x * r, -a.y * r);
 }
 KH_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }

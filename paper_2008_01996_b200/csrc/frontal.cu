@@ -364,94 +364,220 @@ __global__ void __launch_bounds__(TRSM_ROWS) big_trsm_kernel(KhTree T, const int
     if (jj < w) row[(int64_t)jj * m] = cmul(v[jj], sdi[jj]);
 }
 
-// Right-looking blocked LDL^T of the m x m lower matrix S over its first p
-// pivots, by 32*NW threads. Entry (r, c), r >= c, lives at S[cb[c] + r]
-// (cb: per-column base offsets in shared memory, so dense and packed
-// block-column layouts share the code). Pivots go in blocks of 8: warp 0
-// factors the 8 x 8 diagonal block with shuffles, the rows below are solved
-// one thread per row, and the rank-8 trailing update of S[s0:, s0:] runs on
-// DMMA over 8 x 8 lower blocks (4 real MMAs per complex product). W (8 rows of
-// ldw) and dinv (8) are shared scratch. Returns the smallest |d| (or -1 for a
-// non-finite pivot) on thread 0.
-template <int NW>
-KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, double2* dinv, int m, int p) {
+// Lower-triangle tile index -> (bi, bj), bj <= bi, tiles numbered row by row.
+KH_DEV void tri_index(int t, int& bi, int& bj) {
+  int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  if ((i + 1) * (i + 2) / 2 <= t) ++i;
+  if (i * (i + 1) / 2 > t) --i;
+  bi = i;
+  bj = t - i * (i + 1) / 2;
+}
+
+// Blocked LDL^T of the m x m lower matrix S over its first p pivots, by
+// 32*NW threads, leaving the Schur complement C - L21 D L21^T in S[p:, p:].
+// Entry (r, c), r >= c, lives at S[cb[c] + r] (cb: per-column base offsets in
+// shared memory, so dense and packed block-column layouts share the code).
+//  * pivots in blocks of 8: warp 0 factors the 8 x 8 diagonal block with
+//    shuffles; the rows below are solved one thread per row; the rank-8
+//    trailing update runs on DMMA;
+//  * for a large update block (q >= kDeferSyrk) the rank-8 updates cover the
+//    panel columns only and S[p:, p:] is computed once with K = p afterwards
+//    (deferred SYRK: accumulate in registers over all pivots, one read-
+//    modify-write per 8 x 8 tile) instead of p/8 rank-8 passes.
+// W (8 rows of ldw), dinv (8) and dg (p pivots) are shared scratch. Returns the
+// smallest |d| (or -1 for a non-finite pivot) on thread 0.
+constexpr int kDeferSyrk = 48;
+#ifndef KH_LOOKAHEAD_MIN_NW
+#define KH_LOOKAHEAD_MIN_NW 4
+#endif
+// look-ahead pays off when the CTA has warps enough to hide the serial (a) phase
+KH_HD constexpr bool kLookAhead(int nw) { return nw >= KH_LOOKAHEAD_MIN_NW; }
+
+// LDL^T of the w x w diagonal block at column kb by warp 0 (lane i holds row
+// i, pivots broadcast with shuffles): L in the strict lower part, D on the
+// diagonal, 1/d in dinv and d in dg.
+KH_DEV void diag_block_ldlt(double2* S, const int32_t* cb, double2* dinv, double2* dg, int kb, int w, int m,
+                            double& minp) {
+  constexpr int BK = 8;
+  const int lane = threadIdx.x & 31;
+  int cbk[BK];
+#pragma unroll
+  for (int j = 0; j < BK; ++j) cbk[j] = cb[min(kb + j, m - 1)];
+  double2 a[BK];
+#pragma unroll
+  for (int j = 0; j < BK; ++j) a[j] = (lane < w && j <= lane) ? S[cbk[j] + kb + lane] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < BK; ++k) {
+    if (k < w) {
+      const double2 dk = shfl2(a[k], k);
+      const double2 di = cinv(dk);
+      const double2 lik = cmul(a[k], di);
+#pragma unroll
+      for (int j = k + 1; j < BK; ++j) {
+        const double2 ajk = shfl2(a[k], j);
+        if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
+      }
+      if (lane > k && lane < w) a[k] = lik;
+      if (lane == 0) {
+        dinv[k] = di;
+        dg[kb + k] = dk;
+        const double ad = sqrt(cabs2(dk));
+        minp = (ad != ad) ? -1.0 : fmin(minp, ad);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < BK; ++j)
+    if (lane < w && j <= lane) S[cbk[j] + kb + lane] = a[j];
+}
+
+// One 8 x 8 tile (rows r0.., cols c0..) of the rank-8 update
+// S[r][c] -= sum_k L[r][kb+k] W[c][k] (c < cl, c <= r < m) on DMMA, by one warp.
+KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw, int kb, int w, int r0, int c0,
+                       int cl, int m) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int ca = cb[min(kb + t, m - 1)], cb4 = cb[min(kb + t + 4, m - 1)];
+  double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+#pragma unroll
+  for (int ks = 0; ks < 8; ks += 4) {
+    const int k = ks + t;
+    const int ra = r0 + g, cbv = c0 + g;
+    const double2 af = (k < w && ra < m) ? S[(ks ? cb4 : ca) + ra] : make_double2(0.0, 0.0);
+    const double2 bf = (cbv < cl) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
+    dmma884(cr[0], cr[1], af.x, bf.x);
+    dmma884(cr[0], cr[1], -af.y, bf.y);
+    dmma884(ci[0], ci[1], af.x, bf.y);
+    dmma884(ci[0], ci[1], af.y, bf.x);
+  }
+  const int rr = r0 + g;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cc = c0 + 2 * t + h;
+    if (rr < m && cc < cl && rr >= cc) {
+      double2* d = S + cb[cc] + rr;
+      *d = make_double2(d->x - cr[h], d->y - ci[h]);
+    }
+  }
+}
+
+// Blocked LDL^T of the m x m lower matrix S over its first p pivots, by
+// 32*NW threads, leaving the Schur complement C - L21 D L21^T in S[p:, p:].
+// Entry (r, c), r >= c, lives at S[cb[c] + r] (cb: per-column base offsets in
+// shared memory, so dense and packed block-column layouts share the code).
+// Pivots go in blocks of 8:
+//  (a) warp 0 factors the 8 x 8 diagonal block with shuffles;
+//  (b) the rows below are solved one thread per row (W = L D of the block);
+//  (c) rank-8 trailing update on DMMA, 8 x 8 tiles handed out through a
+//      shared counter. Look-ahead: warp 0 first updates the next block's
+//      diagonal tile and factors it (the next (a)) while the other warps work
+//      through the remaining tiles, then joins them; the serial (a) chain is
+//      thus hidden behind the update instead of idling the CTA.
+// For a large update block (q >= kDeferSyrk) the rank-8 updates cover the
+// panel columns only and S[p:, p:] is computed once with K = p at the end
+// (deferred SYRK: one read-modify-write per tile instead of p/8).
+// W (8 rows of ldw), dinv (8), dg (p pivots) and ctr (1 int) are shared
+// scratch. Returns the smallest |d| (or -1 for a non-finite pivot) on thread 0.
+template <int NW, bool LA>
+KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, double2* dinv, double2* dg,
+                           int* ctr, int m, int p) {
   constexpr int NTH = 32 * NW, BK = 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const bool defer = m - p >= kDeferSyrk;
+  const int cl = defer ? p : m;  // columns updated inside the pivot loop
   double minp = DBL_MAX;
+  if (LA) {
+    if (p > 0 && warp == 0) diag_block_ldlt(S, cb, dinv, dg, 0, min(BK, p), m, minp);
+    __syncthreads();
+  }
   for (int kb = 0; kb < p; kb += BK) {
     const int w = min(BK, p - kb);
-    int cbk[BK];
-#pragma unroll
-    for (int j = 0; j < BK; ++j) cbk[j] = cb[min(kb + j, m - 1)];
-    // (a) diagonal block: lane i < w holds row i of the w x w block
-    if (warp == 0) {
-      double2 a[BK];
-#pragma unroll
-      for (int j = 0; j < BK; ++j)
-        a[j] = (lane < w && j <= lane) ? S[cbk[j] + kb + lane] : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int k = 0; k < BK; ++k) {
-        if (k < w) {
-          const double2 dk = shfl2(a[k], k);
-          const double2 di = cinv(dk);
-          const double2 lik = cmul(a[k], di);
-#pragma unroll
-          for (int j = k + 1; j < BK; ++j) {
-            const double2 ajk = shfl2(a[k], j);
-            if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
-          }
-          if (lane > k && lane < w) a[k] = lik;
-          if (lane == 0) {
-            dinv[k] = di;
-            const double ad = sqrt(cabs2(dk));
-            minp = (ad != ad) ? -1.0 : fmin(minp, ad);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < BK; ++j)
-        if (lane < w && j <= lane) S[cbk[j] + kb + lane] = a[j];
+    if (!LA) {
+      if (warp == 0) diag_block_ldlt(S, cb, dinv, dg, kb, w, m, minp);
+      __syncthreads();
     }
-    __syncthreads();
     // (b) rows below: v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k]; L[r][kb+j] = v_j / d_j
     const int s0 = kb + w;
-    for (int r = s0 + tid; r < m; r += NTH) {
-      double2 v[BK];
+    {
+      int cbk[BK];
 #pragma unroll
-      for (int j = 0; j < BK; ++j) {
-        if (j < w) {
-          double2 x = S[cbk[j] + r];
+      for (int j = 0; j < BK; ++j) cbk[j] = cb[min(kb + j, m - 1)];
+      for (int r = s0 + tid; r < m; r += NTH) {
+        double2 v[BK];
 #pragma unroll
-          for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[cbk[k] + kb + j]);
-          v[j] = x;
+        for (int j = 0; j < BK; ++j) {
+          if (j < w) {
+            double2 x = S[cbk[j] + r];
+#pragma unroll
+            for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[cbk[k] + kb + j]);
+            v[j] = x;
+          }
         }
-      }
 #pragma unroll
-      for (int j = 0; j < BK; ++j) {
-        if (j < w) {
-          W[j * ldw + r] = v[j];
-          S[cbk[j] + r] = cmul(v[j], dinv[j]);
-        } else {
-          W[j * ldw + r] = make_double2(0.0, 0.0);
+        for (int j = 0; j < BK; ++j) {
+          if (j < w) {
+            W[j * ldw + r] = v[j];
+            S[cbk[j] + r] = cmul(v[j], dinv[j]);
+          } else {
+            W[j * ldw + r] = make_double2(0.0, 0.0);
+          }
         }
       }
     }
+    if (tid == 0) *ctr = 0;
     __syncthreads();
-    // (c) trailing update on DMMA: S[r][c] -= sum_k L[r][kb+k] W[c][k], s0 <= c <= r < m
-    const int nb = (m - s0 + 7) / 8;
-    const int g = lane >> 2, t = lane & 3;
-    const int ca0 = cb[min(kb + t, m - 1)], ca1 = cb[min(kb + t + 4, m - 1)];
+    // (c) tiles (bi, bj), bj <= bi, of rows s0..m-1 x columns s0..cl-1,
+    //     enumerated column block by column block; tile 0 is the next
+    //     diagonal block
+    if (!LA) {
+      if (s0 < cl) {
+        const int nrb = (m - s0 + 7) / 8, ncb = (cl - s0 + 7) / 8;
+        for (int task = warp;; task += NW) {
+          int bj = 0, rem = task;
+          while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
+          if (bj >= ncb) break;
+          rank8_tile(S, cb, W, ldw, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
+        }
+      }
+    } else if (s0 < cl) {
+      const int nrb = (m - s0 + 7) / 8, ncb = (cl - s0 + 7) / 8;
+      int first = 0;
+      if (warp == 0 && s0 < p) {  // look-ahead
+        rank8_tile(S, cb, W, ldw, kb, w, s0, s0, cl, m);
+        __syncwarp();
+        diag_block_ldlt(S, cb, dinv, dg, s0, min(BK, p - s0), m, minp);
+      }
+      if (s0 < p) first = 1;
+      for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(ctr, 1) + first;
+        task = __shfl_sync(0xffffffffu, task, 0);
+        int bj = 0, rem = task;
+        while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
+        if (bj >= ncb) break;
+        rank8_tile(S, cb, W, ldw, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
+      }
+    }
+    __syncthreads();
+  }
+  // deferred SYRK: S[p:, p:] -= L21 D L21^T, K = p, one RMW per 8 x 8 tile
+  const int q = m - p;
+  if (defer && p > 0) {
+    const int nb = (q + 7) / 8;
     for (int task = warp; task < nb * (nb + 1) / 2; task += NW) {
-      int bi = 0, rem = task;
-      while (rem > bi) rem -= ++bi;  // task -> (bi, bj = rem), bj <= bi
-      const int r0 = s0 + 8 * bi, c0 = s0 + 8 * rem;
+      int bi, bj;
+      tri_index(task, bi, bj);
+      const int r0 = p + 8 * bi, c0 = p + 8 * bj;
+      const int ra = r0 + g, cv = c0 + g;
       double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
-#pragma unroll
-      for (int ks = 0; ks < BK; ks += 4) {
+      for (int ks = 0; ks < p; ks += 4) {
         const int k = ks + t;
-        const int ra = r0 + g, cbv = c0 + g;
-        const double2 af = (k < w && ra < m) ? S[(ks ? ca1 : ca0) + ra] : make_double2(0.0, 0.0);
-        const double2 bf = (cbv < m) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
+        double2 af = make_double2(0.0, 0.0), bf = make_double2(0.0, 0.0);
+        if (k < p) {
+          const int ck = cb[k];
+          if (ra < m) af = S[ck + ra];
+          if (cv < m) bf = cmul(S[ck + cv], dg[k]);
+        }
         dmma884(cr[0], cr[1], af.x, bf.x);
         dmma884(cr[0], cr[1], -af.y, bf.y);
         dmma884(ci[0], ci[1], af.x, bf.y);
@@ -482,6 +608,8 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
   __shared__ double2 W[8 * DIAG_LD];
   __shared__ double2 dinv[8];
   __shared__ int32_t cb[NB];
+  __shared__ double2 dg[NB];
+  __shared__ int ctr;
   if (threadIdx.x < NB) cb[threadIdx.x] = threadIdx.x * DIAG_LD;
   const int32_t f = fronts[blockIdx.x];
   const int b = blockIdx.y;
@@ -493,7 +621,7 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
     if (r >= c) S[c * DIAG_LD + r] = B[r + (int64_t)c * m];
   }
   __syncthreads();
-  const double minp = blocked_ldlt<DIAG_NW>(S, cb, W, DIAG_LD, dinv, w, w);
+  const double minp = blocked_ldlt<DIAG_NW, false>(S, cb, W, DIAG_LD, dinv, dg, &ctr, w, w);
   for (int e = threadIdx.x; e < w * w; e += 32 * DIAG_NW) {
     const int c = e / w, r = e - c * w;
     if (r >= c) B[r + (int64_t)c * m] = S[c * DIAG_LD + r];
@@ -518,8 +646,14 @@ KH_HD constexpr int packed_elems(int m) {
   return e;
 }
 KH_HD constexpr int front_smem_bytes(int ms) {
-  return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8) + 4 * ms + 4 * 4 * ms;
+  return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8 + ms) + 4 * ms + 4 * 4 * ms;
 }
+
+#ifdef KH_PHASE_TIMING
+// debug builds only (profiles/probes/phase_timing.py): clock64 cycles per
+// phase of factor_front_kernel, summed over CTAs, [MS/16][phase]
+__device__ unsigned long long g_phase[9 * 8];
+#endif
 
 template <int MS, int NW>
 __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_front_kernel(
@@ -531,9 +665,24 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
   double2* S = reinterpret_cast<double2*>(smem_raw);  // packed lower triangle
   double2* W = S + packed_elems(MS);                  // W[k*LDW + r] = L[r][kb+k] d_{kb+k}
   double2* dinv = W + 8 * LDW;                        // 1/d of the current block
-  int32_t* cb = reinterpret_cast<int32_t*>(dinv + 8);  // column bases
+  double2* dg = dinv + 8;                              // pivots d_k
+  int32_t* cb = reinterpret_cast<int32_t*>(dg + MS);   // column bases
   int32_t* rel = cb + MS;                              // rel[k*MS + i]
+  __shared__ int ctr;
   const int tid = threadIdx.x;
+#ifdef KH_PHASE_TIMING
+  long long t_0 = clock64();
+  auto phase = [&](int i) {
+    if (tid == 0) {
+      const long long t1 = clock64();
+      atomicAdd(&g_phase[(MS / 16) * 8 + i], (unsigned long long)(t1 - t_0));
+      if (i == 0) atomicAdd(&g_phase[(MS / 16) * 8 + 7], 1ull);
+      t_0 = t1;
+    }
+  };
+#else
+  auto phase = [](int) {};
+#endif
   const int32_t f = level_fronts[blockIdx.x];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
@@ -562,6 +711,7 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
     }
   }
   __syncthreads();
+  phase(0);
   const double2 Lm = lam[b];
   for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
     const int d = T.orig_dst[e];
@@ -597,8 +747,10 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
     }
   }
   __syncthreads();
+  phase(1);
 
-  const double minp = blocked_ldlt<NW>(S, cb, W, LDW, dinv, m, p);
+  const double minp = blocked_ldlt<NW, kLookAhead(NW)>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
+  phase(2);
   // ---- write the panel and the update matrix (lower parts), coalesced
   for (int idx = tid; idx < m * p; idx += NTH) {
     const int c = idx / m, r = idx - c * m;
@@ -609,6 +761,7 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
     if (r >= c) U[idx] = S[cb[p + c] + p + r];
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+  phase(3);
 }
 
 // ---- forward solve: y <- L^{-1} b, fronts bottom-up ------------------------
@@ -1072,3 +1225,11 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
     default: return cudaErrorInvalidValue;
   }
 }
+
+#ifdef KH_PHASE_TIMING
+extern "C" int kh_debug_phase_cycles(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 9 * 8) != cudaSuccess) return 4;
+  static const unsigned long long zero[9 * 8] = {};
+  return cudaMemcpyToSymbol(g_phase, zero, sizeof zero) == cudaSuccess ? 0 : 4;
+}
+#endif
