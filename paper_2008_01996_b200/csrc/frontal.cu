@@ -845,7 +845,11 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
 
 // ---- warp-per-front solves for fronts with m <= 64 ------------------------------
 // Lane l owns front rows l and l + 32. No block barriers: pivots are broadcast
-// with shuffles and every column of the panel is read with one coalesced load.
+// with shuffles. The panel is streamed in chunks of 8 columns loaded into
+// registers before use (the first chunk while the rhs is gathered), so the
+// loads of a chunk are in flight together instead of one round trip per column.
+constexpr int SOLVE_CH = 8;
+
 __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y, double2* ru_cur,
                                                         int64_t ru_stride_cur, const double2* __restrict__ ru_child,
@@ -860,7 +864,18 @@ __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t*
   double2* yy = y + (int64_t)b * T.n + F.first;
   double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
   const int r0 = lane, r1 = lane + 32;
-  double2 x0 = make_double2(0.0, 0.0), x1 = make_double2(0.0, 0.0);
+  const double2 z = make_double2(0.0, 0.0);
+  auto load_chunk = [&](int k0, double2* c0, double2* c1) {
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int k = k0 + u;
+      c0[u] = (k < p && r0 > k && r0 < m) ? P[r0 + (int64_t)k * m] : z;
+      c1[u] = (k < p && r1 > k && r1 < m) ? P[r1 + (int64_t)k * m] : z;
+    }
+  };
+  double2 a0[SOLVE_CH], a1[SOLVE_CH];
+  load_chunk(0, a0, a1);  // first panel chunk streams in during the rhs gather
+  double2 x0 = z, x1 = z;
   for (int c = F.child_begin; c < F.child_end; ++c) {
     const KhDevFront C = T.fronts[T.child_list[c]];
     const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
@@ -872,12 +887,17 @@ __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t*
   }
   if (r0 < p) x0 = cadd(x0, yy[r0]);
   if (r1 < p) x1 = cadd(x1, yy[r1]);
-  for (int k = 0; k < p; ++k) {
-    const double2 l0 = (r0 > k && r0 < m) ? P[r0 + (int64_t)k * m] : make_double2(0.0, 0.0);
-    const double2 l1 = (r1 > k && r1 < m) ? P[r1 + (int64_t)k * m] : make_double2(0.0, 0.0);
-    const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
-    x0 = cfms(x0, l0, yk);
-    x1 = cfms(x1, l1, yk);
+  for (int k0 = 0; k0 < p; k0 += SOLVE_CH) {
+    if (k0 > 0) load_chunk(k0, a0, a1);
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int k = k0 + u;
+      if (k < p) {
+        const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
+        x0 = cfms(x0, a0[u], yk);
+        x1 = cfms(x1, a1[u], yk);
+      }
+    }
   }
   if (r0 < p) yy[r0] = x0;
   else if (r0 < m) ru[r0 - p] = x0;
@@ -897,21 +917,42 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
   double2* yb = y + (int64_t)b * T.n;
   double2* yy = yb + F.first;
   const int64_t* urows = T.urows + F.rows_begin;
-  // solution values of the update rows (already final: ancestors are done)
-  const double2 xu0 = lane < q ? yb[urows[lane]] : make_double2(0.0, 0.0);
-  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : make_double2(0.0, 0.0);
-  // lane k (and k+32) owns pivot k: t_k = y_k / d_k - sum_a L21[a, k] xu[a].
-  // Row form: xu[a] is broadcast and every lane updates its own t_k, so there
-  // is no reduction on the dependency chain; the strided panel reads hit L1
-  // (a front's panel is a few tens of KB and every line is reused).
-  const int k0 = lane, k1 = lane + 32;
-  double2 t0 = k0 < p ? cmul(yy[k0], cinv(P[k0 + (int64_t)k0 * m])) : make_double2(0.0, 0.0);
-  double2 t1 = k1 < p ? cmul(yy[k1], cinv(P[k1 + (int64_t)k1 * m])) : make_double2(0.0, 0.0);
-  for (int a = 0; a < q; ++a) {
-    const double2 xa = shfl2(a < 32 ? xu0 : xu1, a & 31);
-    if (k0 < p) t0 = cfms(t0, P[p + a + (int64_t)k0 * m], xa);
-    if (k1 < p) t1 = cfms(t1, P[p + a + (int64_t)k1 * m], xa);
+  const double2 z = make_double2(0.0, 0.0);
+  // solution values of the update rows (already final: ancestors are done);
+  // lane a holds xu[a] and xu[a + 32]
+  const double2 xu0 = lane < q ? yb[urows[lane]] : z;
+  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : z;
+  // t_k = y_k / d_k - sum_a L21[a, k] xu[a]: lane a reads rows p+a of column k
+  // (coalesced); the column sums are warp reductions, SOLVE_CH columns at a
+  // time so their shuffle trees overlap; lane k & 31 keeps the result
+  double2 t0 = z, t1 = z;
+  for (int k0 = 0; k0 < p; k0 += SOLVE_CH) {
+    double2 s[SOLVE_CH];
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int k = k0 + u;
+      const double2* col = P + p + (int64_t)k * m;
+      const double2 l0 = (k < p && lane < q) ? col[lane] : z;
+      const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
+      s[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < SOLVE_CH; ++u) {
+        s[u].x += __shfl_xor_sync(0xffffffffu, s[u].x, o);
+        s[u].y += __shfl_xor_sync(0xffffffffu, s[u].y, o);
+      }
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int k = k0 + u;
+      if (k < 32 && lane == k) t0 = s[u];
+      if (k >= 32 && lane == k - 32) t1 = s[u];
+    }
   }
+  const int k0 = lane, k1 = lane + 32;
+  if (k0 < p) t0 = csub(cmul(yy[k0], cinv(P[k0 + (int64_t)k0 * m])), t0);
+  if (k1 < p) t1 = csub(cmul(yy[k1], cinv(P[k1 + (int64_t)k1 * m])), t1);
   // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for j < i
   for (int i = p - 1; i > 0; --i) {
     const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
