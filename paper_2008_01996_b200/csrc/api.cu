@@ -383,7 +383,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
-      for (int32_t idx0 = 0; idx0 < F.m() * F.p + F.q * F.q; idx0 += KH_ASM_CHUNK)
+      for (int32_t idx0 = 0; idx0 < F.m() * F.p; idx0 += KH_ASM_CHUNK)
         X.bt.insert(X.bt.end(), {f, idx0});
       nkb = std::max(nkb, (F.p + 31) / 32);
     }
@@ -597,7 +597,7 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
       KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
                                      uch, sch, p->minpiv_work, p->side));
     const kh_plan::BigLevel& B = p->big[d];
-    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uc, sc, uch, sch, st));
+    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
       const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
       const int kb = 32 * kbi;

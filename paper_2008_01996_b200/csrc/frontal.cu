@@ -183,13 +183,19 @@ KH_DEV double2 shfl2(double2 v, int src) {
 }
 
 // Schur complement of the large fronts of one level: one CTA per 64 x 64
-// lower tile of U, per shift: U[i0:, j0:] -= L21[i0:, :] D L21[j0:, :]^T
-// (K = p). Tasks are (front, tile row, tile col) triples built on the host.
+// lower tile of U, per shift: U[i0:, j0:] = C - L21[i0:, :] D L21[j0:, :]^T
+// (K = p), where C is the children's extend-add onto the tile, pulled in the
+// epilogue (the update block is written exactly once: no separate assembly
+// pass over U and no read-modify-write). Tasks are (front, tile row, tile
+// col) triples built on the host.
 __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                              const double2* __restrict__ panels, double2* upd_cur,
-                                                             int64_t upd_stride_cur) {
+                                                             int64_t upd_stride_cur,
+                                                             const double2* __restrict__ upd_child,
+                                                             int64_t upd_stride_child) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+  __shared__ Kids kids;
   const int32_t f = tasks[3 * blockIdx.x];
   const int i0 = tasks[3 * blockIdx.x + 1] * TB, j0 = tasks[3 * blockIdx.x + 2] * TB;
   const int b = blockIdx.y;
@@ -197,16 +203,60 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   const int p = F.p, q = F.q, m = p + q;
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  load_kids(T, F, upd_child, upd_stride_child, b, kids);
   Acc acc;
   tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
-  // U holds the pulled children's contributions (big_assemble): U -= L21 D L21^T
-  tile_epilogue(acc, [&](int i, int j, double2 v) {
-    const int r = i0 + i, c = j0 + j;
-    if (r < q && c < q && r >= c) {
-      double2* d = U + r + (int64_t)c * q;
-      *d = csub(*d, v);
+  __syncthreads();  // kids visible even when p = 0
+  // epilogue: this thread's 16 tile entries (rows wi*32+mt*8+g, cols
+  // wj*16+nt*8+2t+h), in two halves of rows to bound register pressure;
+  // children pulled in order (deterministic sums)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3, wi = warp & 1, wj = warp >> 1;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    double2 cacc[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cacc[a][nt][h] = make_double2(0.0, 0.0);
+    for (int k = 0; k < kids.n; ++k) {
+      const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+      int ri[2], cj[2][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int r = i0 + wi * 32 + (2 * half + a) * 8 + g;
+        ri[a] = r < q ? C.cmap[p + r] : -1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = j0 + wj * 16 + nt * 8 + 2 * t + h;
+          cj[nt][h] = c < q ? C.cmap[p + c] : -1;
+        }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (ri[a] >= 0 && cj[nt][h] >= 0)
+              cacc[a][nt][h] = cadd(cacc[a][nt][h], C.U[ri[a] + (int64_t)cj[nt][h] * C.q]);
     }
-  });
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int mt = 2 * half + a;
+          const int r = i0 + wi * 32 + mt * 8 + g, c = j0 + wj * 16 + nt * 8 + 2 * t + h;
+          if (r < q && c < q && r >= c)
+            U[r + (int64_t)c * q] = csub(cacc[a][nt][h], make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
+        }
+  }
 }
 
 // ---- large fronts, level-synchronous batched kernels ------------------------------
@@ -225,21 +275,19 @@ constexpr int ASM_CHUNK = KH_ASM_CHUNK;
 
 __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                           const double2* __restrict__ lam, double2* panels,
-                                                          double2* upd_cur, int64_t upd_stride_cur,
                                                           const double2* __restrict__ upd_child,
                                                           int64_t upd_stride_child) {
-  // index space of a front: [0, m*p) = panel P (column-major m x p), then
-  // [m*p, m*p + q*q) = update block U (column-major q x q); lower parts only
+  // index space: the panel P (column-major m x p, lower part) in chunks of
+  // ASM_CHUNK entries; the update block is assembled by schur_update_kernel
   __shared__ Kids kids;
   const int tid = threadIdx.x;
   const int32_t f = tasks[2 * blockIdx.x];
   const int idx0 = tasks[2 * blockIdx.x + 1];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
-  const int p = F.p, q = F.q, m = p + q, np = m * p;
-  const int total = min(np + q * q, idx0 + ASM_CHUNK);
+  const int p = F.p, m = p + F.q;
+  const int total = min(m * p, idx0 + ASM_CHUNK);
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
   __syncthreads();
   int rr[ASM_CHUNK / NT], cc[ASM_CHUNK / NT];  // front-local row / column
@@ -247,15 +295,8 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
 #pragma unroll
   for (int u = 0; u < ASM_CHUNK / NT; ++u) {
     const int idx = idx0 + tid + u * NT;
-    if (idx < np) {
-      cc[u] = idx / m;
-      rr[u] = idx - cc[u] * m;
-    } else {
-      const int w = idx - np;
-      cc[u] = w / max(q, 1);
-      rr[u] = p + (w - cc[u] * q);
-      cc[u] += p;
-    }
+    cc[u] = idx / m;
+    rr[u] = idx - cc[u] * m;
     v[u] = make_double2(0.0, 0.0);
   }
   for (int k = 0; k < kids.n; ++k) {
@@ -271,12 +312,8 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
 #pragma unroll
   for (int u = 0; u < ASM_CHUNK / NT; ++u) {
     const int idx = idx0 + tid + u * NT;
-    if (idx < total && rr[u] >= cc[u]) {
-      if (idx < np) P[idx] = v[u];
-      else U[idx - np] = v[u];
-    }
+    if (idx < total && rr[u] >= cc[u]) P[idx] = v[u];
   }
-  if (idx0 >= np) return;  // chunk lies in U: no original entries
   __syncthreads();
   // originals whose (sorted) destinations fall into this chunk
   int64_t lo = F.orig_begin, hi = F.orig_end;
@@ -1093,11 +1130,10 @@ __global__ void rowreduce_kernel(const double* __restrict__ in, int64_t len, int
 }  // namespace
 
 cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
-                                   const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
-                                   const double2* upd_child, int64_t upd_stride_child, cudaStream_t stream) {
+                                   const double2* lam, double2* panels, const double2* upd_child,
+                                   int64_t upd_stride_child, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_cur, upd_stride_cur,
-                                                              upd_child, upd_stride_child);
+  big_assemble_kernel<<<dim3(ntasks, batch), NT, 0, stream>>>(T, tasks, lam, panels, upd_child, upd_stride_child);
   kh_note_launch();
   return cudaGetLastError();
 }
@@ -1145,9 +1181,8 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
   const int smem = (int)(2 * sizeof(CpStage));
   cudaError_t e = set_smem_once((const void*)schur_update_kernel, smem, done);
   if (e != cudaSuccess) return e;
-  (void)upd_child;
-  (void)upd_stride_child;
-  schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur);
+  schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
+                                                                 upd_child, upd_stride_child);
   kh_note_launch();
   return cudaGetLastError();
 }
