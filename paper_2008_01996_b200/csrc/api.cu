@@ -319,6 +319,7 @@ namespace {
 // level and kernel class, Schur tiles and the large-front block lists.
 struct Sched {
   std::vector<KhDevFront> df;
+  std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
   std::vector<kh_plan::KbInfo> kbinfo;
@@ -356,6 +357,17 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
       if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
     return kSmallClasses;  // large
   };
+  // originals of fused fronts address the packed block-column layout directly
+  X.orig_dst = S.orig_dst;
+  for (int32_t f = 0; f < nf; ++f) {
+    const kh::Front& F = S.fronts[f];
+    const int32_t m = F.m();
+    if (front_class(m) >= kSmallClasses) continue;
+    for (int64_t e = F.orig_begin; e < F.orig_end; ++e) {
+      const int32_t d = X.orig_dst[e], c = d / m, r = d - c * m;
+      X.orig_dst[e] = kh_packed_col_base(m, c) + r;
+    }
+  }
   X.level_off.push_back(0);
   for (const auto& lev : S.levels) {
     const int32_t base = (int32_t)X.lf.size();
@@ -542,7 +554,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     up(p->cmap, S.cmap.data(), S.cmap.size() * 4);
     up(p->urows, S.urows.data(), S.urows.size() * 8);
     up(p->orig_src, S.orig_src.data(), S.orig_src.size() * 8);
-    up(p->orig_dst, S.orig_dst.data(), S.orig_dst.size() * 4);
+    up(p->orig_dst, X.orig_dst.data(), X.orig_dst.size() * 4);
     up(p->level_fronts, X.lf.data(), X.lf.size() * 4);
     up(p->tasks, X.tasks.data(), X.tasks.size() * 4);
     up(p->btasks, X.bt.data(), X.bt.size() * 4);

@@ -670,21 +670,19 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
 }
 
 // ---- fused fronts (m <= MS): assemble + factor + Schur complement in one CTA ----
-// The front's lower triangle lives in shared memory in packed block-column
-// form: the 8-column block b holds rows 8b..m-1 with a leading dimension
-// ld_b = roundup8(m - 8b) + 2 (= 2 mod 8 in 16-byte units: conflict-free DMMA
-// fragment loads), so a 128-row front needs 140 KB instead of 260 KB. The
+// The front's lower triangle lives in shared memory in the packed block-column
+// layout of kernels.h (a 128-row front needs 140 KB instead of 260 KB). The
 // whole LDL^T, including the update matrix U = C - L21 D L21^T, is done by
 // blocked_ldlt; the panel and U are then written once, coalesced.
-KH_HD constexpr int packed_ld(int m, int b) { return ((m - 8 * b + 7) / 8) * 8 + 2; }
-KH_HD constexpr int packed_elems(int m) {
-  int e = 0;
-  for (int b = 0; 8 * b < m; ++b) e += 8 * packed_ld(m, b);
-  return e;
-}
+KH_HD constexpr int packed_elems(int m) { return kh_packed_elems(m); }
 KH_HD constexpr int front_smem_bytes(int ms) {
   return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8 + ms) + 4 * ms + 4 * 4 * ms;
 }
+
+struct KidInfo {
+  int64_t upd_off, rows_begin;
+  int32_t q, pad;
+};
 
 #ifdef KH_PHASE_TIMING
 // debug builds only (profiles/probes/phase_timing.py): clock64 cycles per
@@ -720,67 +718,80 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
 #else
   auto phase = [](int) {};
 #endif
+  const int lane = tid & 31, warp = tid >> 5;
   const int32_t f = level_fronts[blockIdx.x];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
   const int p = F.p, q = F.q, m = p + q;
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  const int nkids = F.child_end - F.child_begin;
+  __shared__ KidInfo kinfo[RK];
 
   // ---- assembly: zero the front, add the originals (values pre-gathered in
-  // front order: one coalesced stream), then push each child's update block
-  // through its relind map (coalesced reads of the child's U, conflict-free
-  // within a child; children in order, so the sums are deterministic)
+  // front order, destinations pre-packed on the host: one coalesced stream),
+  // then push each child's update block through its relind map (coalesced
+  // column reads of the child's U, conflict-free within a child; children in
+  // order, so the sums are deterministic)
+  if (tid < RK && tid < nkids) {
+    const KhDevFront C = T.fronts[T.child_list[F.child_begin + tid]];
+    kinfo[tid] = {C.upd_off, C.rows_begin, C.q, 0};
+  }
   const int ne = packed_elems(m);
   for (int idx = tid; idx < ne; idx += NTH) S[idx] = make_double2(0.0, 0.0);
-  for (int c = tid; c < m; c += NTH) {
-    const int bc = c >> 3;
-    int off = 0;
-    for (int bb = 0; bb < bc; ++bb) off += 8 * packed_ld(m, bb);
-    cb[c] = off + (c & 7) * packed_ld(m, bc) - 8 * bc;
-  }
-  const int nkids = F.child_end - F.child_begin;
-  for (int idx = tid; idx < RK * MS; idx += NTH) {
-    const int k = idx / MS, i = idx - k * MS;
-    if (k < nkids) {
-      const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
-      if (i < C.q) rel[idx] = T.relind[C.rows_begin + i];
-    }
-  }
+  for (int c = tid; c < m; c += NTH) cb[c] = kh_packed_col_base(m, c);
   __syncthreads();
   phase(0);
-  const double2 Lm = lam[b];
-  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
-    const int d = T.orig_dst[e];
-    const int c = d / m;
-    const double av = T.oa[e];
-    double2* t = S + cb[c] + (d - c * m);
-    *t = cadd(*t, make_double2(fma(Lm.x, av, T.om[e]), Lm.y * av));
+  for (int idx = tid; idx < RK * MS; idx += NTH) {
+    const int k = idx / MS, i = idx - k * MS;
+    if (k < nkids && i < kinfo[k].q) rel[idx] = T.relind[kinfo[k].rows_begin + i];
   }
+  {
+    const double2 Lm = lam[b];
+    for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
+      const int d = T.orig_dst[e];
+      const double av = T.oa[e];
+      S[d] = cadd(S[d], make_double2(fma(Lm.x, av, T.om[e]), Lm.y * av));
+    }
+  }
+  constexpr int R = (MS + 31) / 32;  // row passes per column
   for (int k = 0; k < nkids; ++k) {
     __syncthreads();
-    const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
-    const double2* Uc = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
-    const int32_t* rk = k < RK ? rel + k * MS : T.relind + C.rows_begin;
-    const int qk = C.q, qq = qk * qk;
-    for (int base = 0; base < qq; base += 4 * NTH) {
-      double2 v[4];
-      int ci[4], cj[4];
+    int64_t upd_off, rows_begin;
+    int qk;
+    if (k < RK) {
+      upd_off = kinfo[k].upd_off;
+      rows_begin = kinfo[k].rows_begin;
+      qk = kinfo[k].q;
+    } else {
+      const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+      upd_off = C.upd_off;
+      rows_begin = C.rows_begin;
+      qk = C.q;
+    }
+    const double2* Uc = upd_child + (int64_t)b * upd_stride_child + upd_off;
+    const int32_t* rk = k < RK ? rel + k * MS : T.relind + rows_begin;
+    // warp w takes columns w, w + NW, ... two at a time; lanes walk the rows
+    for (int cj0 = warp; cj0 < qk; cj0 += 2 * NW) {
+      double2 v[2][R];
+      int dst[2][R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + tid + u * NTH;
-        cj[u] = idx / max(qk, 1);
-        ci[u] = idx - cj[u] * qk;
-        const bool ok = idx < qq && ci[u] >= cj[u];
-        v[u] = ok ? Uc[idx] : make_double2(0.0, 0.0);
-        if (!ok) ci[u] = -1;
+      for (int h = 0; h < 2; ++h) {
+        const int cj = cj0 + h * NW;
+        const int base = cj < qk ? cb[rk[cj]] : 0;
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const int ci = cj + lane + 32 * u;
+          const bool ok = cj < qk && ci < qk;
+          v[h][u] = ok ? Uc[ci + (int64_t)cj * qk] : make_double2(0.0, 0.0);
+          dst[h][u] = ok ? base + rk[ci] : -1;
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (ci[u] >= 0) {
-          double2* t = S + cb[rk[cj[u]]] + rk[ci[u]];
-          *t = cadd(*t, v[u]);
-        }
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+          if (dst[h][u] >= 0) S[dst[h][u]] = cadd(S[dst[h][u]], v[h][u]);
     }
   }
   __syncthreads();
@@ -788,14 +799,15 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
 
   const double minp = blocked_ldlt<NW, kLookAhead(NW)>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
   phase(2);
-  // ---- write the panel and the update matrix (lower parts), coalesced
-  for (int idx = tid; idx < m * p; idx += NTH) {
-    const int c = idx / m, r = idx - c * m;
-    if (r >= c) P[idx] = S[cb[c] + r];
+  // ---- write the panel and the update matrix (lower parts), coalesced:
+  // warp per column, lanes down the rows
+  for (int c = warp; c < p; c += NW) {
+    const int base = cb[c];
+    for (int r = c + lane; r < m; r += 32) P[r + (int64_t)c * m] = S[base + r];
   }
-  for (int idx = tid; idx < q * q; idx += NTH) {
-    const int c = idx / q, r = idx - c * q;
-    if (r >= c) U[idx] = S[cb[p + c] + p + r];
+  for (int c = warp; c < q; c += NW) {
+    const int base = cb[p + c] + p;
+    for (int r = c + lane; r < q; r += 32) U[r + (int64_t)c * q] = S[base + r];
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
   phase(3);

@@ -15,6 +15,22 @@ struct KhDevFront {
   int32_t depth, pad;
 };
 
+// Packed block-column layout of a fused front (m <= 128) in shared memory:
+// the 8-column block b stores rows 8b..m-1 with leading dimension
+// roundup8(m - 8b) + 2 (2 mod 8 in 16-byte units: conflict-free DMMA
+// fragment loads). Entry (r, c), r >= c, sits at kh_packed_col_base(m, c) + r.
+__host__ __device__ constexpr int kh_packed_ld(int m, int b) { return ((m - 8 * b + 7) / 8) * 8 + 2; }
+__host__ __device__ constexpr int kh_packed_elems(int m) {
+  int e = 0;
+  for (int b = 0; 8 * b < m; ++b) e += 8 * kh_packed_ld(m, b);
+  return e;
+}
+__host__ __device__ constexpr int kh_packed_col_base(int m, int c) {
+  int off = 0;
+  for (int b = 0; b < (c >> 3); ++b) off += 8 * kh_packed_ld(m, b);
+  return off + (c & 7) * kh_packed_ld(m, c >> 3) - 8 * (c >> 3);
+}
+
 struct KhTree {  // device pointers shared by every level kernel
   const KhDevFront* fronts;
   const int32_t* child_list;
@@ -22,7 +38,7 @@ struct KhTree {  // device pointers shared by every level kernel
   const int32_t* cmap;
   const int64_t* urows;
   const int64_t* orig_src;
-  const int32_t* orig_dst;
+  const int32_t* orig_dst;  // panel offset (r + c*m); packed offset for fused fronts
   const double* mv;  // M values aligned with the analyzed CSR
   const double* av;  // A values aligned with the analyzed CSR
   const double* om;  // M values in front-original order: om[e] = mv[orig_src[e]]
