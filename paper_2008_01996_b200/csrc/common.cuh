@@ -29,8 +29,9 @@ KH_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 // ---- DMMA ---------------------------------------------------------------------
 // D(8x8) = A(8x4, row) * B(4x8, col) + C. Lane (g = lane>>2, t = lane&3):
 // a = A[g][t], b = B[t][g], c/d = C[g][2t], C[g][2t+1].
+// (not volatile: the compiler may interleave independent MMAs and loads)
 KH_DEV void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));

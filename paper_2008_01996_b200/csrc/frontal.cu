@@ -423,6 +423,12 @@ KH_DEV void tri_index(int t, int& bi, int& bj) {
 //    modify-write per 8 x 8 tile) instead of p/8 rank-8 passes.
 // W (8 rows of ldw), dinv (8) and dg (p pivots) are shared scratch. Returns the
 // smallest |d| (or -1 for a non-finite pivot) on thread 0.
+#ifdef KH_PHASE_TIMING
+// debug builds only (profiles/probes/phase_timing.py): clock64 cycles per
+// phase of factor_front_kernel, summed over CTAs, [MS/16][phase]
+__device__ unsigned long long g_phase[9 * 8];
+#endif
+
 constexpr int kDeferSyrk = 48;
 #ifndef KH_LOOKAHEAD_MIN_NW
 #define KH_LOOKAHEAD_MIN_NW 4
@@ -443,24 +449,27 @@ KH_DEV void diag_block_ldlt(double2* S, const int32_t* cb, double2* dinv, double
   double2 a[BK];
 #pragma unroll
   for (int j = 0; j < BK; ++j) a[j] = (lane < w && j <= lane) ? S[cbk[j] + kb + lane] : make_double2(0.0, 0.0);
+  // branch-free over k (w is uniform; inactive pivots use d = 1 and write
+  // nothing), so the broadcasts of column k are issued together, ahead of
+  // the reciprocal on the dependency chain
 #pragma unroll
   for (int k = 0; k < BK; ++k) {
-    if (k < w) {
-      const double2 dk = shfl2(a[k], k);
-      const double2 di = cinv(dk);
-      const double2 lik = cmul(a[k], di);
+    const bool act = k < w;
+    double2 col[BK];
 #pragma unroll
-      for (int j = k + 1; j < BK; ++j) {
-        const double2 ajk = shfl2(a[k], j);
-        if (lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, ajk);
-      }
-      if (lane > k && lane < w) a[k] = lik;
-      if (lane == 0) {
-        dinv[k] = di;
-        dg[kb + k] = dk;
-        const double ad = sqrt(cabs2(dk));
-        minp = (ad != ad) ? -1.0 : fmin(minp, ad);
-      }
+    for (int j = k; j < BK; ++j) col[j] = shfl2(a[k], j);
+    const double2 dk = act ? col[k] : make_double2(1.0, 0.0);
+    const double2 di = cinv(dk);
+    const double2 lik = cmul(a[k], di);
+#pragma unroll
+    for (int j = k + 1; j < BK; ++j)
+      if (act && lane > k && j <= lane && lane < w) a[j] = cfms(a[j], lik, col[j]);
+    if (act && lane > k && lane < w) a[k] = lik;
+    if (act && lane == 0) {
+      dinv[k] = di;
+      dg[kb + k] = dk;
+      const double ad = sqrt(cabs2(dk));
+      minp = (ad != ad) ? -1.0 : fmin(minp, ad);
     }
   }
 #pragma unroll
@@ -474,25 +483,31 @@ KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw,
                        int cl, int m) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int ca = cb[min(kb + t, m - 1)], cb4 = cb[min(kb + t + 4, m - 1)];
-  double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+  const int ra = r0 + g, cbv = c0 + g;
+  double2 af[2], bf[2];
 #pragma unroll
-  for (int ks = 0; ks < 8; ks += 4) {
-    const int k = ks + t;
-    const int ra = r0 + g, cbv = c0 + g;
-    const double2 af = (k < w && ra < m) ? S[(ks ? cb4 : ca) + ra] : make_double2(0.0, 0.0);
-    const double2 bf = (cbv < cl) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
-    dmma884(cr[0], cr[1], af.x, bf.x);
-    dmma884(cr[0], cr[1], -af.y, bf.y);
-    dmma884(ci[0], ci[1], af.x, bf.y);
-    dmma884(ci[0], ci[1], af.y, bf.x);
+  for (int s = 0; s < 2; ++s) {
+    const int k = 4 * s + t;
+    af[s] = (k < w && ra < m) ? S[(s ? cb4 : ca) + ra] : make_double2(0.0, 0.0);
+    bf[s] = (cbv < cl) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
   }
-  const int rr = r0 + g;
+  // four independent accumulators (re*re, -im*im, re*im, im*re): MMA chains
+  // of depth 2 instead of 4
+  double rr[2] = {0.0, 0.0}, ii[2] = {0.0, 0.0}, ri[2] = {0.0, 0.0}, ir[2] = {0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    dmma884(rr[0], rr[1], af[s].x, bf[s].x);
+    dmma884(ii[0], ii[1], -af[s].y, bf[s].y);
+    dmma884(ri[0], ri[1], af[s].x, bf[s].y);
+    dmma884(ir[0], ir[1], af[s].y, bf[s].x);
+  }
+  const int row = r0 + g;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int cc = c0 + 2 * t + h;
-    if (rr < m && cc < cl && rr >= cc) {
-      double2* d = S + cb[cc] + rr;
-      *d = make_double2(d->x - cr[h], d->y - ci[h]);
+    if (row < m && cc < cl && row >= cc) {
+      double2* d = S + cb[cc] + row;
+      *d = make_double2(d->x - (rr[h] + ii[h]), d->y - (ri[h] + ir[h]));
     }
   }
 }
@@ -514,11 +529,23 @@ KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw,
 // (deferred SYRK: one read-modify-write per tile instead of p/8).
 // W (8 rows of ldw), dinv (8), dg (p pivots) and ctr (1 int) are shared
 // scratch. Returns the smallest |d| (or -1 for a non-finite pivot) on thread 0.
-template <int NW, bool LA>
+template <int NW, bool LA, int TSLOT = 0>
 KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, double2* dinv, double2* dg,
                            int* ctr, int m, int p) {
   constexpr int NTH = 32 * NW, BK = 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef KH_PHASE_TIMING
+  long long ts0 = clock64();
+  auto sub = [&](int i) {  // sub-phases 4 (a), 5 (b), 6 (c + SYRK) of the fused kernel
+    if (TSLOT > 0 && tid == 0) {
+      const long long t1 = clock64();
+      atomicAdd(&g_phase[TSLOT * 8 + i], (unsigned long long)(t1 - ts0));
+      ts0 = t1;
+    }
+  };
+#else
+  auto sub = [](int) {};
+#endif
   const int g = lane >> 2, t = lane & 3;
   const bool defer = m - p >= kDeferSyrk;
   const int cl = defer ? p : m;  // columns updated inside the pivot loop
@@ -532,6 +559,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
     if (!LA) {
       if (warp == 0) diag_block_ldlt(S, cb, dinv, dg, kb, w, m, minp);
       __syncthreads();
+      sub(4);
     }
     // (b) rows below: v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k]; L[r][kb+j] = v_j / d_j
     const int s0 = kb + w;
@@ -563,6 +591,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
     }
     if (tid == 0) *ctr = 0;
     __syncthreads();
+    sub(5);
     // (c) tiles (bi, bj), bj <= bi, of rows s0..m-1 x columns s0..cl-1,
     //     enumerated column block by column block; tile 0 is the next
     //     diagonal block
@@ -596,6 +625,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
       }
     }
     __syncthreads();
+    sub(6);
   }
   // deferred SYRK: S[p:, p:] -= L21 D L21^T, K = p, one RMW per 8 x 8 tile
   const int q = m - p;
@@ -631,6 +661,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
       }
     }
     __syncthreads();
+    sub(6);
   }
   return minp;
 }
@@ -679,19 +710,21 @@ KH_HD constexpr int front_smem_bytes(int ms) {
   return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8 + ms) + 4 * ms + 4 * 4 * ms;
 }
 
+#ifndef KH_F32_MINB
+#define KH_F32_MINB 8
+#endif
+// resident CTAs per SM the register allocation must allow
+KH_HD constexpr int front_min_blocks(int ms, int nw) {
+  return ms <= 32 ? KH_F32_MINB : ((16 / nw) > 1 ? 16 / nw : 1);
+}
+
 struct KidInfo {
   int64_t upd_off, rows_begin;
   int32_t q, pad;
 };
 
-#ifdef KH_PHASE_TIMING
-// debug builds only (profiles/probes/phase_timing.py): clock64 cycles per
-// phase of factor_front_kernel, summed over CTAs, [MS/16][phase]
-__device__ unsigned long long g_phase[9 * 8];
-#endif
-
 template <int MS, int NW>
-__global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_front_kernel(
+__global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_front_kernel(
     KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
     double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
     double* minpiv) {
@@ -742,6 +775,12 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
   for (int c = tid; c < m; c += NTH) cb[c] = kh_packed_col_base(m, c);
   __syncthreads();
   phase(0);
+  // warm L2 with the children's update blocks (read after the originals)
+  for (int k = 0; k < nkids && k < RK; ++k) {
+    const char* base = reinterpret_cast<const char*>(upd_child + (int64_t)b * upd_stride_child + kinfo[k].upd_off);
+    const int lines = (kinfo[k].q * kinfo[k].q * 16 + 127) >> 7;
+    for (int l = tid; l < lines; l += NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
+  }
   for (int idx = tid; idx < RK * MS; idx += NTH) {
     const int k = idx / MS, i = idx - k * MS;
     if (k < nkids && i < kinfo[k].q) rel[idx] = T.relind[kinfo[k].rows_begin + i];
@@ -797,7 +836,7 @@ __global__ void __launch_bounds__(32 * NW, (16 / NW) > 1 ? 16 / NW : 1) factor_f
   __syncthreads();
   phase(1);
 
-  const double minp = blocked_ldlt<NW, kLookAhead(NW)>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
+  const double minp = blocked_ldlt<NW, kLookAhead(NW), MS / 16>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
   phase(2);
   // ---- write the panel and the update matrix (lower parts), coalesced:
   // warp per column, lanes down the rows

@@ -19,6 +19,8 @@ VARIANTS = {
     "default": [],
     "nola": ["KH_LOOKAHEAD_MIN_NW=99"],
     "allla": ["KH_LOOKAHEAD_MIN_NW=1"],
+    "f32b10": ["KH_F32_MINB=10"],
+    "f32b12": ["KH_F32_MINB=12"],
 }
 
 
@@ -63,13 +65,13 @@ def run(v):
             fn(buf.ctypes.data)  # discard warm-up counts
     fn(buf.ctypes.data)
     print(f"variant {v}: factor ms/step {np.mean(times[1:]):.2f}")
-    names = ["staging", "assembly", "ldlt", "write"]
+    names = ["staging", "assembly", "ldlt", "write", "(a)", "(b)", "(c)"]
     for ms in (2, 3, 4, 6, 8):
         row = buf[ms * 8: ms * 8 + 8].astype(float)
         n = row[7]
         if n == 0:
             continue
-        parts = " ".join(f"{nm}={row[i] / n:8.0f}" for i, nm in enumerate(names))
+        parts = " ".join(f"{nm}={row[i] / n:6.0f}" for i, nm in enumerate(names))
         print(f"  MS={ms * 16:3d} CTAs={int(n):7d} cycles/CTA: {parts} total={row[:4].sum() / n:8.0f}")
 
 
