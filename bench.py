@@ -315,7 +315,8 @@ def main():
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),
             "clocks": ck,
-            "roofline": {"kernel": "factor_level_kernel (batched complex LDL^T, all levels)",
+            "roofline": {"kernel": "batched multifrontal complex LDL^T: all launches of one factorization "
+                                   "(factor_front_kernel, big_*, schur_update_kernel)",
                          "bound": "tensor", "achieved": achieved, "peak": peaks.get("fp64_tflops"),
                          "unit": "TFLOP/s", "frac": (achieved / peaks["fp64_tflops"]) if achieved else None,
                          "peak_source": peaks.get("fp64_source"),
@@ -337,11 +338,14 @@ def main():
 
 
 def load_traffic(cfg):
+    """DRAM bytes per step of the factorization launches, from the committed
+    ncu launch list (profiles/traffic.json, written by profiles/summarize.py)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(cfg)
-    except (OSError, ValueError):
+            ent = json.load(fh).get(cfg)
+        return None if ent is None else ent["factor_dram_bytes_per_step"]
+    except (OSError, ValueError, KeyError):
         return None
 
 

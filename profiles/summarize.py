@@ -1,5 +1,7 @@
 """Summarize an ncu launch-list CSV (gpu__time_duration.sum [+ dram bytes])
-into per-kernel totals: python profiles/summarize.py launches.csv [out.md]."""
+into per-kernel totals: python profiles/summarize.py launches.csv [out.md]
+[--traffic traffic.json CONFIG STEPS] (the last form records the DRAM bytes
+of the factorization launches per step for bench.py's roofline.traffic)."""
 
 import collections
 import csv
@@ -20,6 +22,9 @@ def load(path):
         except ValueError:
             pass
     return names, rows
+
+
+FACTOR_PREFIXES = ("factor_front_kernel", "big_", "schur_update_kernel", "shift_absmax", "rowreduce")
 
 
 def short(name):
@@ -47,6 +52,23 @@ def main():
     if len(sys.argv) > 2:
         with open(sys.argv[2], "w") as fh:
             fh.write(text + "\n")
+    if "--traffic" in sys.argv:
+        import json
+
+        i = sys.argv.index("--traffic")
+        path, cfg, steps = sys.argv[i + 1], sys.argv[i + 2], int(sys.argv[i + 3])
+        fac = [v for k, v in tot.items() if k.startswith(FACTOR_PREFIXES)]
+        data = {}
+        try:
+            with open(path) as fh:
+                data = json.load(fh)
+        except (OSError, ValueError):
+            pass
+        data[cfg] = {"factor_dram_bytes_per_step": sum(v[2] for v in fac) / steps,
+                     "factor_kernel_ms_per_step": sum(v[1] for v in fac) / steps / 1e6,
+                     "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (serialised launches)"}
+        with open(path, "w") as fh:
+            json.dump(data, fh, indent=1)
 
 
 if __name__ == "__main__":
