@@ -182,6 +182,33 @@ KH_DEV double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
+KH_DEV double2 shfl_xor2(double2 v, int o) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+// Warp transpose-reduction of 8 values per lane: returns, on lane l, the sum
+// over all 32 lanes of v[u] with u = 4*bit4(l) + 2*bit3(l) + bit2(l).
+KH_DEV double2 warp_sum8(double2 (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double2 send = b4 ? v[j] : v[j + 4], keep = b4 ? v[j + 4] : v[j];
+    v[j] = cadd(keep, shfl_xor2(send, 16));
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double2 send = b3 ? v[j] : v[j + 2], keep = b3 ? v[j + 2] : v[j];
+    v[j] = cadd(keep, shfl_xor2(send, 8));
+  }
+  {
+    const double2 send = b2 ? v[0] : v[1], keep = b2 ? v[1] : v[0];
+    v[0] = cadd(keep, shfl_xor2(send, 4));
+  }
+  v[0] = cadd(v[0], shfl_xor2(v[0], 2));
+  v[0] = cadd(v[0], shfl_xor2(v[0], 1));
+  return v[0];
+}
+
 // Schur complement of the large fronts of one level: one CTA per 64 x 64
 // lower tile of U, per shift: U[i0:, j0:] = C - L21[i0:, :] D L21[j0:, :]^T
 // (K = p), where C is the children's extend-add onto the tile, pulled in the
@@ -1024,18 +1051,20 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
       const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
       s[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
     }
+    // transpose-reduce the 8 column sums over the warp (9 exchanges instead
+    // of 40): afterwards lane l holds the full sum of column u(l) =
+    // 4*bit4(l) + 2*bit3(l) + bit2(l)
+    const double2 v = warp_sum8(s, lane);
+    // the owner lane of column k0 + u fetches it from a lane holding u
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < SOLVE_CH; ++u) {
-        s[u].x += __shfl_xor_sync(0xffffffffu, s[u].x, o);
-        s[u].y += __shfl_xor_sync(0xffffffffu, s[u].y, o);
+    for (int h = 0; h < 2; ++h) {
+      const int kk = lane + 32 * h, u = kk - k0;
+      const int src = ((u >> 2) & 1) << 4 | ((u >> 1) & 1) << 3 | (u & 1) << 2;
+      const double2 got = shfl2(v, src & 31);
+      if (u >= 0 && u < SOLVE_CH && kk < p) {
+        if (h == 0) t0 = got;
+        else t1 = got;
       }
-#pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
-      const int k = k0 + u;
-      if (k < 32 && lane == k) t0 = s[u];
-      if (k >= 32 && lane == k - 32) t1 = s[u];
     }
   }
   const int k0 = lane, k1 = lane + 32;
