@@ -64,7 +64,7 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 struct kh_plan {
   int device = 0;
   int64_t n = 0, nnz = 0, max_batch = 0, slots = 0;
-  int32_t nf = 0, max_p = 0;
+  int32_t nf = 0, max_p = 0, max_m = 0;
   std::vector<int32_t> level_off;  // levels d -> [level_off[d], level_off[d+1]) in level_fronts
   // kClsStride per level: starts of the front classes (m <= 32, 48, 64, large)
   // relative to level_off[d], plus the end
@@ -323,7 +323,7 @@ struct Sched {
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
   std::vector<kh_plan::KbInfo> kbinfo;
-  int32_t max_p = 0;
+  int32_t max_p = 0, max_m = 0;
 };
 
 void build_schedule(const kh::Symbolic& S, Sched& X) {
@@ -347,6 +347,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     D.depth = F.depth;
     D.pad = 0;
     X.max_p = std::max(X.max_p, F.p);
+    X.max_m = std::max(X.max_m, F.m());
   }
   // KH_SMALL_MAX caps the register/shared-memory small-front classes
   // (0 disables them, for A/B measurements)
@@ -521,6 +522,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   Sched X;
   build_schedule(S, X);
   p->max_p = X.max_p;
+  p->max_m = X.max_m;
   p->level_off = X.level_off;
   p->cls_off = X.cls_off;
   p->task_off = X.task_off;
@@ -681,15 +683,16 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
     KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side));
-    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, panels, p->y, rc, sc, rch, sch,
-                                st));
+    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
+                                rch, sch, st));
     KH_CUDA(join_side(p, st));
   }
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
     KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side));
-    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, panels, p->y, st));
+    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
+                                p->y, st));
     KH_CUDA(join_side(p, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));

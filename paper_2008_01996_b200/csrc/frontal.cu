@@ -880,6 +880,9 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
 }
 
 // ---- forward solve: y <- L^{-1} b, fronts bottom-up ------------------------
+// Large fronts of a wide level (many CTAs per SM): one CTA per (front,
+// shift), blocks of 32 pivots solved by one warp in shared memory, rows below
+// updated one thread per row.
 __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                        const double2* __restrict__ panels, double2* y,
                                                        double2* ru_cur, int64_t ru_stride_cur,
@@ -955,6 +958,127 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
       else ru[r - p] = csub(ru[r - p], s);
     }
     __syncthreads();
+  }
+}
+
+// Large fronts of a narrow level (top of the tree: fewer CTAs than SMs x 8),
+// one CTA per (front, shift). The front's rhs segment x[0:m) is
+// kept in shared memory. Per 32-column block: warp 0 loads the block's rows
+// into registers (coalesced per column) and solves it with shuffles (no
+// barriers on the chain), while warps 1..7 already load their rows' 32 panel
+// entries below the block; after one barrier they finish the GEMV update
+// x[r] -= L[r, blk] x[blk] from registers. Rows beyond 224 below the block
+// take extra passes by all warps.
+constexpr int FWD_W = 32;
+// levels with at most this many (front, shift) CTAs use the narrow-level solves
+constexpr int64_t kNarrowLevelCtas = 1024;
+__global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                          const double2* __restrict__ panels, double2* y,
+                                                          double2* ru_cur, int64_t ru_stride_cur,
+                                                          const double2* __restrict__ ru_child,
+                                                          int64_t ru_stride_child) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* xs = reinterpret_cast<double2*>(smem_raw);  // m entries
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  const double2 z = make_double2(0.0, 0.0);
+  // gather: pivots' rhs plus the children's rhs updates (pull, fixed child order)
+  __shared__ const double2* kru[MAXC];
+  __shared__ const int32_t* kcm[MAXC];
+  const int nk = F.child_end - F.child_begin;
+  if (tid < MAXC && tid < nk) {
+    const KhDevFront C = T.fronts[T.child_list[F.child_begin + tid]];
+    kru[tid] = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+    kcm[tid] = T.cmap + C.cmap_begin;
+  }
+  __syncthreads();
+  for (int r = tid; r < m; r += NT) {
+    double2 v = r < p ? yy[r] : z;
+    for (int k = 0; k < nk; ++k) {
+      const double2* rc;
+      const int32_t* cm;
+      if (k < MAXC) {
+        rc = kru[k];
+        cm = kcm[k];
+      } else {
+        const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+        rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+        cm = T.cmap + C.cmap_begin;
+      }
+      const int ci = cm[r];
+      if (ci >= 0) v = cadd(v, rc[ci]);
+    }
+    xs[r] = v;
+  }
+  __syncthreads();
+  for (int kb = 0; kb < p; kb += FWD_W) {
+    const int w = min(FWD_W, p - kb), r0 = kb + w;
+    constexpr int H = FWD_W / 2;  // register arrays hold half a block (2 CTAs per SM)
+    double2 l[H];
+    if (warp == 0) {
+      // lane i: row kb+i of the block, L[kb+i][kb+k] for k < i; two halves
+      const int i = lane;
+      double2 xi = i < w ? xs[kb + i] : z;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const int kk = hh * H + k;
+          l[k] = (kk < i && i < w) ? P[(kb + i) + (int64_t)(kb + kk) * m] : z;
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const double2 xk = shfl2(xi, hh * H + k);
+          xi = cfms(xi, l[k], xk);  // l[k] = 0 unless kk < i < w
+        }
+      }
+      if (i < w) xs[kb + i] = xi;
+    } else {
+      const int r = r0 + tid - 32;
+#pragma unroll
+      for (int k = 0; k < H; ++k) l[k] = (r < m && k < w) ? P[r + (int64_t)(kb + k) * m] : z;
+    }
+    __syncthreads();
+    if (warp > 0) {
+      const int r = r0 + tid - 32;
+      if (r < m) {
+        double2 s0 = z, s1 = z;
+#pragma unroll
+        for (int k = 0; k < H; k += 2) {
+          s0 = cadd(s0, cmul(l[k], xs[kb + k]));
+          s1 = cadd(s1, cmul(l[k + 1], xs[kb + k + 1]));
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k) l[k] = (H + k < w) ? P[r + (int64_t)(kb + H + k) * m] : z;
+#pragma unroll
+        for (int k = 0; k < H; k += 2) {
+          s0 = cadd(s0, cmul(l[k], xs[kb + H + k]));
+          s1 = cadd(s1, cmul(l[k + 1], xs[kb + H + k + 1]));
+        }
+        xs[r] = csub(xs[r], cadd(s0, s1));
+      }
+    }
+    for (int r = r0 + (NT - 32) + tid; r < m; r += NT) {  // rows beyond the first pass
+      double2 s0 = z, s1 = z;
+#pragma unroll 8
+      for (int k = 0; k < w; ++k) {
+        const double2 lv = P[r + (int64_t)(kb + k) * m];
+        if (k & 1) s1 = cadd(s1, cmul(lv, xs[kb + k]));
+        else s0 = cadd(s0, cmul(lv, xs[kb + k]));
+      }
+      xs[r] = csub(xs[r], cadd(s0, s1));
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < m; r += NT) {
+    if (r < p) yy[r] = xs[r];
+    else ru[r - p] = xs[r];
   }
 }
 
@@ -1078,6 +1202,89 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
   }
   if (k0 < p) yy[k0] = t0;
   if (k1 < p) yy[k1] = t1;
+}
+
+// Backward solve of the large fronts of a narrow level (top of the tree):
+// one CTA per (front, shift), t and x[urows] in shared memory.
+//  1. t_k = y_k / d_k - sum_a L21[a, k] x[urows[a]]: warps over chunks of 8
+//     columns, lanes down the rows (coalesced), warp_sum8 reductions;
+//  2. blocks of 32 pivots from the last: warp 0 stages the block (coalesced)
+//     in shared memory and solves L_blk^T x = t with shuffles while warps 1..7
+//     load their first chunk of L[blk, 0:kb] (independent of x); after one
+//     barrier, t[0:kb] -= L[blk, 0:kb]^T x[blk] by warp reductions.
+__global__ void __launch_bounds__(NT, 2) bwd_top_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                        const double2* __restrict__ panels, double2* y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ts = reinterpret_cast<double2*>(smem_raw);  // p entries, then xu: q entries
+  __shared__ double2 blk[FWD_W][FWD_W + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t f = level_fronts[blockIdx.x];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  double2* xu = ts + p;
+  const int64_t* urows = T.urows + F.rows_begin;
+  const double2 z = make_double2(0.0, 0.0);
+  for (int a = tid; a < q; a += NT) xu[a] = yb[urows[a]];
+  __syncthreads();
+  // 1. t = D^-1 y - L21^T xu
+  for (int k0 = 8 * warp; k0 < p; k0 += 8 * (NT / 32)) {
+    double2 sacc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sacc[u] = z;
+    for (int a = lane; a < q; a += 32) {
+      const double2 xa = xu[a];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < p) sacc[u] = cadd(sacc[u], cmul(P[p + a + (int64_t)(k0 + u) * m], xa));
+    }
+    const double2 v = warp_sum8(sacc, lane);
+    const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    const int k = k0 + u;
+    if ((lane & 3) == 0 && k < p) ts[k] = csub(cmul(yy[k], cinv(P[k + (int64_t)k * m])), v);
+  }
+  __syncthreads();
+  // 2. L11^T x = t, blocks of 32 from the last
+  const int nblk = (p + FWD_W - 1) / FWD_W;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * FWD_W, w = min(FWD_W, p - kb);
+    const int nch = kb / 8;  // chunks of 8 columns left of the block
+    double2 l[8];
+    if (warp == 0) {
+      for (int c = 0; c < w; ++c) blk[lane][c] = lane < w ? P[(kb + lane) + (int64_t)(kb + c) * m] : z;
+      __syncwarp();
+      double2 t = lane < w ? ts[kb + lane] : z;
+      for (int i = w - 1; i > 0; --i) {
+        const double2 xi = shfl2(t, i);
+        if (lane < i) t = cfms(t, blk[i][lane], xi);
+      }
+      if (lane < w) ts[kb + lane] = t;
+    } else if (warp < nch) {  // chunk c = warp: prefetch L[kb+lane, 8c : 8c+8]
+#pragma unroll
+      for (int u = 0; u < 8; ++u) l[u] = lane < w ? P[(kb + lane) + (int64_t)(8 * warp + u) * m] : z;
+    }
+    __syncthreads();
+    if (nch > 0) {
+      const double2 xl = lane < w ? ts[kb + lane] : z;
+      for (int c = warp; c < nch; c += NT / 32) {
+        if (c != warp || warp == 0) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) l[u] = lane < w ? P[(kb + lane) + (int64_t)(8 * c + u) * m] : z;
+        }
+        double2 sacc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sacc[u] = cmul(l[u], xl);
+        const double2 v = warp_sum8(sacc, lane);
+        const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0) ts[8 * c + u] = csub(ts[8 * c + u], v);
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < p; k += NT) yy[k] = ts[k];
 }
 
 // ---- backward solve: x <- L^{-T} D^{-1} y, fronts top-down -------------------
@@ -1286,26 +1493,45 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
 }
 
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
-                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream) {
+                                int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
+                                int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
+                                cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  fwd_level_kernel<<<dim3(nlev, batch), NT, 0, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
-                                                         ru_child, ru_stride_child);
+  if ((int64_t)nlev * batch > kNarrowLevelCtas) {
+    fwd_level_kernel<<<dim3(nlev, batch), NT, 0, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
+                                                           ru_child, ru_stride_child);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
+  const size_t smem = sizeof(double2) * (size_t)max_m;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  fwd_top_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
+                                                          ru_child, ru_stride_child);
   kh_note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                int32_t max_p, const double2* panels, double2* y, cudaStream_t stream) {
+                                int32_t max_p, int32_t max_m, const double2* panels, double2* y,
+                                cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  size_t smem = sizeof(double2) * (size_t)max_p;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(bwd_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtas;
+  const size_t smem = sizeof(double2) * (size_t)(narrow ? max_m : max_p);
+  static size_t attr = 0, attr_top = 0;
+  size_t& a = narrow ? attr_top : attr;
+  if (smem > 48 * 1024 && smem > a) {
+    cudaError_t e = cudaFuncSetAttribute(narrow ? (const void*)bwd_top_kernel : (const void*)bwd_level_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    a = smem;
   }
-  bwd_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
+  if (narrow) bwd_top_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
+  else bwd_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
   kh_note_launch();
   return cudaGetLastError();
 }

@@ -53,8 +53,9 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
                             cudaStream_t stream);
 
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
-                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream);
+                                int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
+                                int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
+                                cudaStream_t stream);
 // Level-synchronous kernels for the large fronts (see frontal.cu). Tasks are
 // (front, index) int32 pairs; schur tasks are (front, tile row, tile col).
 constexpr int KH_ASM_CHUNK = 1024;
@@ -78,7 +79,8 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, cudaStream_t stream);
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                int32_t max_p, const double2* panels, double2* y, cudaStream_t stream);
+                                int32_t max_p, int32_t max_m, const double2* panels, double2* y,
+                                cudaStream_t stream);
 cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
                                  const double* g_im, int64_t ldg, double2* y, cudaStream_t stream);
 cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm, const double2* y,
