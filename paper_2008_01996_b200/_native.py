@@ -11,6 +11,10 @@ import os
 from .errors import DeviceError, DimensionMismatch, SingularMatrix, UsageError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkhb200.so")
+# instrumented / experimental builds of the same sources (profiles/probes) can be
+# loaded instead for measurements; the product path uses the in-tree library
+if os.environ.get("KHB200_LIB"):
+    LIB_PATH = os.environ["KHB200_LIB"]
 
 KH_OK = 0
 KH_ERR_DIMENSION = 1

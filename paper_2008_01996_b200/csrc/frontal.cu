@@ -970,8 +970,9 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
 // x[r] -= L[r, blk] x[blk] from registers. Rows beyond 224 below the block
 // take extra passes by all warps.
 constexpr int FWD_W = 32;
-// levels with at most this many (front, shift) CTAs use the narrow-level solves
-constexpr int64_t kNarrowLevelCtas = 1024;
+// levels with at most this many (front, shift) CTAs use the narrow-level
+// solves (crossover measured at c3: profiles/r1_solve_levels.md)
+constexpr int64_t kNarrowLevelCtas = 1024, kNarrowLevelCtasBwd = 2048;
 __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                           const double2* __restrict__ panels, double2* y,
                                                           double2* ru_cur, int64_t ru_stride_cur,
@@ -1235,6 +1236,7 @@ __global__ void __launch_bounds__(NT, 2) bwd_top_kernel(KhTree T, const int32_t*
     double2 sacc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) sacc[u] = z;
+#pragma unroll 2
     for (int a = lane; a < q; a += 32) {
       const double2 xa = xu[a];
 #pragma unroll
@@ -1253,9 +1255,10 @@ __global__ void __launch_bounds__(NT, 2) bwd_top_kernel(KhTree T, const int32_t*
     const int kb = bi * FWD_W, w = min(FWD_W, p - kb);
     const int nch = kb / 8;  // chunks of 8 columns left of the block
     double2 l[8];
+    // stage the block with all warps (warp c&7 loads columns c = warp, warp+8, ..)
+    for (int c = warp; c < w; c += NT / 32) blk[lane][c] = lane < w ? P[(kb + lane) + (int64_t)(kb + c) * m] : z;
+    __syncthreads();
     if (warp == 0) {
-      for (int c = 0; c < w; ++c) blk[lane][c] = lane < w ? P[(kb + lane) + (int64_t)(kb + c) * m] : z;
-      __syncwarp();
       double2 t = lane < w ? ts[kb + lane] : z;
       for (int i = w - 1; i > 0; --i) {
         const double2 xi = shfl2(t, i);
@@ -1520,7 +1523,7 @@ cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, in
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
                                 cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtas;
+  const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtasBwd;
   const size_t smem = sizeof(double2) * (size_t)(narrow ? max_m : max_p);
   static size_t attr = 0, attr_top = 0;
   size_t& a = narrow ? attr_top : attr;
