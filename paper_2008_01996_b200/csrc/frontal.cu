@@ -6,17 +6,21 @@
 // (solvers.py:383-393 -> sparse_direct.py:155-209). All shifts share one
 // symbolic analysis (symbolic.cpp) and are processed level by level of the
 // dissection tree, deepest level first; every launch covers all fronts of a
-// level for all shifts of a batch, so the grid is (#fronts x #shifts).
+// level (of one size class) for all shifts of a batch: grid (#fronts, #shifts).
 //
 // Per front (m = p + q rows, p pivots):
 //   panel P (m x p, column-major, ld m) in the retained factor storage,
 //   update U (q x q, lower) in a depth-parity buffer consumed by the parent.
-// Factorization: assemble (originals + extend-add of children), then 32-wide
-// pivot blocks: LDL^T of the diagonal block in shared memory, TRSM of the rows
-// below as a GEMM with the explicit unit-triangular inverse, trailing update
-// of the remaining pivot columns, and finally one SYRK-like update of U with
-// K = p. All three GEMM-shaped steps run on DMMA (mma.sync m8n8k4 f64) as
-// complex products built from four real MMAs.
+// Fronts with m <= 128 (factor_front_kernel): the whole front is assembled in
+//   shared memory (packed block-column layout, push extend-add of the
+//   children), factored by blocked_ldlt (8-pivot blocks, DMMA trailing
+//   updates) and written out once.
+// Larger fronts (level-synchronous kernels): big_assemble (panel), then per
+//   32-pivot block big_lupdate / big_diag / big_trsm, then
+//   schur_update_kernel, which pulls the children's contributions into its
+//   64 x 64 tiles of U in the epilogue.
+// Every GEMM-shaped step runs on DMMA (mma.sync m8n8k4 f64) with complex
+// products built from four real MMAs.
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
