@@ -510,8 +510,11 @@ KH_DEV void diag_block_ldlt(double2* S, const int32_t* cb, double2* dinv, double
 
 // One 8 x 8 tile (rows r0.., cols c0..) of the rank-8 update
 // S[r][c] -= sum_k L[r][kb+k] W[c][k] (c < cl, c <= r < m) on DMMA, by one warp.
-KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw, int kb, int w, int r0, int c0,
-                       int cl, int m) {
+// HW = false: no W buffer; the scaled operand L[c][kb+k] d_{kb+k} is formed
+// from the stored L and the pivots dg (saves 8 x MS x 16 B of shared memory).
+template <bool HW = true>
+KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw, const double2* dg, int kb, int w,
+                       int r0, int c0, int cl, int m) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int ca = cb[min(kb + t, m - 1)], cb4 = cb[min(kb + t + 4, m - 1)];
   const int ra = r0 + g, cbv = c0 + g;
@@ -520,7 +523,8 @@ KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw,
   for (int s = 0; s < 2; ++s) {
     const int k = 4 * s + t;
     af[s] = (k < w && ra < m) ? S[(s ? cb4 : ca) + ra] : make_double2(0.0, 0.0);
-    bf[s] = (cbv < cl) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
+    if (HW) bf[s] = (cbv < cl) ? W[k * ldw + cbv] : make_double2(0.0, 0.0);
+    else bf[s] = (cbv < cl && k < w) ? cmul(S[(s ? cb4 : ca) + cbv], dg[kb + k]) : make_double2(0.0, 0.0);
   }
   // four independent accumulators (re*re, -im*im, re*im, im*re): MMA chains
   // of depth 2 instead of 4
@@ -560,7 +564,7 @@ KH_DEV void rank8_tile(double2* S, const int32_t* cb, const double2* W, int ldw,
 // (deferred SYRK: one read-modify-write per tile instead of p/8).
 // W (8 rows of ldw), dinv (8), dg (p pivots) and ctr (1 int) are shared
 // scratch. Returns the smallest |d| (or -1 for a non-finite pivot) on thread 0.
-template <int NW, bool LA, int TSLOT = 0>
+template <int NW, bool LA, int TSLOT = 0, bool HW = true>
 KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, double2* dinv, double2* dg,
                            int* ctr, int m, int p) {
   constexpr int NTH = 32 * NW, BK = 8;
@@ -612,9 +616,9 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
 #pragma unroll
         for (int j = 0; j < BK; ++j) {
           if (j < w) {
-            W[j * ldw + r] = v[j];
+            if (HW) W[j * ldw + r] = v[j];
             S[cbk[j] + r] = cmul(v[j], dinv[j]);
-          } else {
+          } else if (HW) {
             W[j * ldw + r] = make_double2(0.0, 0.0);
           }
         }
@@ -633,14 +637,14 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
           int bj = 0, rem = task;
           while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
           if (bj >= ncb) break;
-          rank8_tile(S, cb, W, ldw, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
+          rank8_tile<HW>(S, cb, W, ldw, dg, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
         }
       }
     } else if (s0 < cl) {
       const int nrb = (m - s0 + 7) / 8, ncb = (cl - s0 + 7) / 8;
       int first = 0;
       if (warp == 0 && s0 < p) {  // look-ahead
-        rank8_tile(S, cb, W, ldw, kb, w, s0, s0, cl, m);
+        rank8_tile<HW>(S, cb, W, ldw, dg, kb, w, s0, s0, cl, m);
         __syncwarp();
         diag_block_ldlt(S, cb, dinv, dg, s0, min(BK, p - s0), m, minp);
       }
@@ -652,7 +656,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
         int bj = 0, rem = task;
         while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
         if (bj >= ncb) break;
-        rank8_tile(S, cb, W, ldw, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
+        rank8_tile<HW>(S, cb, W, ldw, dg, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
       }
     }
     __syncthreads();
@@ -737,8 +741,10 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
 // whole LDL^T, including the update matrix U = C - L21 D L21^T, is done by
 // blocked_ldlt; the panel and U are then written once, coalesced.
 KH_HD constexpr int packed_elems(int m) { return kh_packed_elems(m); }
+// classes whose residency is bounded by shared memory drop the W buffer
+KH_HD constexpr bool front_has_w(int ms) { return ms != 48; }
 KH_HD constexpr int front_smem_bytes(int ms) {
-  return 16 * (packed_elems(ms) + 8 * (ms + 2) + 8 + ms) + 4 * ms + 4 * 4 * ms;
+  return 16 * (packed_elems(ms) + (front_has_w(ms) ? 8 * (ms + 2) : 0) + 8 + ms) + 4 * ms + 4 * 4 * ms;
 }
 
 #ifndef KH_F32_MINB
@@ -763,7 +769,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* S = reinterpret_cast<double2*>(smem_raw);  // packed lower triangle
   double2* W = S + packed_elems(MS);                  // W[k*LDW + r] = L[r][kb+k] d_{kb+k}
-  double2* dinv = W + 8 * LDW;                        // 1/d of the current block
+  double2* dinv = W + (front_has_w(MS) ? 8 * LDW : 0);  // 1/d of the current block
   double2* dg = dinv + 8;                              // pivots d_k
   int32_t* cb = reinterpret_cast<int32_t*>(dg + MS);   // column bases
   int32_t* rel = cb + MS;                              // rel[k*MS + i]
@@ -867,7 +873,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   __syncthreads();
   phase(1);
 
-  const double minp = blocked_ldlt<NW, kLookAhead(NW), MS / 16>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
+  const double minp = blocked_ldlt<NW, kLookAhead(NW), MS / 16, front_has_w(MS)>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
   phase(2);
   // ---- write the panel and the update matrix (lower parts), coalesced:
   // warp per column, lanes down the rows
