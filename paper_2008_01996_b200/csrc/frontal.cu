@@ -605,14 +605,13 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
       for (int r = s0 + tid; r < m; r += NTH) {
         double2 v[BK];
 #pragma unroll
-        for (int j = 0; j < BK; ++j) {
-          if (j < w) {
-            double2 x = S[cbk[j] + r];
+        for (int j = 0; j < BK; ++j) v[j] = j < w ? S[cbk[j] + r] : make_double2(0.0, 0.0);
+        // column-oriented (same subtraction order as the row form, depth BK)
 #pragma unroll
-            for (int k = 0; k < j; ++k) x = cfms(x, v[k], S[cbk[k] + kb + j]);
-            v[j] = x;
-          }
-        }
+        for (int j = 0; j < BK - 1; ++j)
+#pragma unroll
+          for (int i = j + 1; i < BK; ++i)
+            if (i < w) v[i] = cfms(v[i], v[j], S[cbk[j] + kb + i]);
 #pragma unroll
         for (int j = 0; j < BK; ++j) {
           if (j < w) {
