@@ -10,6 +10,9 @@
 // rows; the elimination order is the postorder of the dissection tree, which
 // is what the reference's etree postorder achieves for its MMD ordering
 // (sparse_direct.py:71-109, :144-145).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "symbolic.h"
 
 #include <algorithm>
@@ -84,9 +87,9 @@ struct Shared {
 struct Builder {
   Shared& sh;
   const Graph& g;
-  std::vector<int64_t> queue;  // per-thread BFS queue
+  std::vector<int64_t> queue;  // per-thread BFS queue, sized to the largest set it handles
 
-  explicit Builder(Shared& s) : sh(s), g(s.g), queue(s.g.n) {}
+  explicit Builder(Shared& s) : sh(s), g(s.g) {}
 
   int32_t in(int64_t v) const { return sh.in_set[v].load(std::memory_order_relaxed); }
   void mark(int64_t v, int32_t s) { sh.in_set[v].store(s, std::memory_order_relaxed); }
@@ -196,6 +199,7 @@ struct Builder {
   // the tree are dissected by separate threads (each with its own Builder).
   Sub nd(std::vector<int64_t> V, int depth) {
     if ((int64_t)V.size() <= sh.leaf) return leaf_sub(std::move(V));
+    if (queue.size() < V.size()) queue.resize(V.size());
     int32_t s = ++sh.stamp;
     for (int64_t v : V) mark(v, s);
     // pseudo-peripheral pair
@@ -239,7 +243,8 @@ struct Builder {
     const size_t nV = V.size();
     std::vector<int64_t>().swap(V);
     std::vector<Sub> subs(parts.size());
-    const bool par = depth < 4 && nV > 8192 && parts.size() > 1;
+    const bool par = depth < 6 && nV > 4096 && parts.size() > 1;
+
     if (par) {
       std::vector<std::thread> th;
       for (size_t k = 1; k < parts.size(); ++k)
@@ -273,6 +278,16 @@ struct Builder {
 
 std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
                     int32_t leaf_size, Symbolic& S) {
+  // KH_ANALYZE_TIMING=1 prints the phase times to stderr (tuning aid)
+  const bool timing = std::getenv("KH_ANALYZE_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "kh_analyze %-10s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   if (n < 0) return "negative dimension";
   if (leaf_size < 1) leaf_size = 1;
   for (int64_t i = 0; i < n; ++i)
@@ -284,6 +299,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   S.nnz = n ? indptr[n] : 0;
   S.leaf_size = leaf_size;
   Graph g = build_graph(n, indptr, indices);
+  lap("graph");
   Shared sh(g, leaf_size);
   Builder B(sh);
   // connected components of the whole graph -> roots; the dissection trees
@@ -295,6 +311,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     std::vector<int64_t> all(n);
     std::iota(all.begin(), all.end(), 0);
     for (int64_t v : all) B.mark(v, s);
+    B.queue.resize(n);
     auto comps = B.components(all, s);
     for (auto& c : comps) {
       Sub sb = B.nd(std::move(c), 0);
@@ -305,6 +322,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       for (auto& kk : sb.kids) kids.push_back(std::move(kk));
     }
   }
+  lap("dissection");
   const int32_t nf = (int32_t)piv.size();
   S.iperm.assign(n, -1);
   {
@@ -347,6 +365,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     std::sort(u.begin(), u.end());
     F.q = (int32_t)u.size();
   }
+  lap("updrows");
   // depth (parents have larger index than children)
   for (int32_t f = nf - 1; f >= 0; --f) {
     Front& F = S.fronts[f];
@@ -398,6 +417,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       S.relind[F.relind_begin + a] = loc;
     }
   }
+  lap("relind");
   // pull maps: for child c of P, cmap[c][r] = a with relind_c[a] = r (r < m_P), else -1
   {
     int64_t tot = 0;
@@ -426,6 +446,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     S.rupd_size[d & 1] = std::max(S.rupd_size[d & 1], ru);
   }
 
+  lap("cmap");
   // original entries: CSR entry (r, c) with iperm[r] >= iperm[c] lands in the
   // front owning pivot iperm[c] at local (row(iperm[r]), iperm[c]-first)
   std::vector<int32_t> front_of(n, -1);
@@ -462,18 +483,36 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       S.orig_dst[pos[f]] = (int32_t)dst;
       ++pos[f];
     }
-  for (int32_t f = 0; f < nf; ++f) {
-    S.fronts[f].orig_begin = cnt[f];
-    S.fronts[f].orig_end = cnt[f + 1];
-    // deterministic, write-coalescing order inside the front
+  // deterministic, write-coalescing order inside each front (fronts are
+  // independent: sorted by a few threads over contiguous front ranges)
+  auto sort_fronts = [&](int32_t f0, int32_t f1) {
     std::vector<std::pair<int32_t, int64_t>> tmp;
-    for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) tmp.emplace_back(S.orig_dst[k], S.orig_src[k]);
-    std::sort(tmp.begin(), tmp.end());
-    for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) {
-      S.orig_dst[k] = tmp[k - cnt[f]].first;
-      S.orig_src[k] = tmp[k - cnt[f]].second;
+    for (int32_t f = f0; f < f1; ++f) {
+      S.fronts[f].orig_begin = cnt[f];
+      S.fronts[f].orig_end = cnt[f + 1];
+      tmp.clear();
+      for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) tmp.emplace_back(S.orig_dst[k], S.orig_src[k]);
+      std::sort(tmp.begin(), tmp.end());
+      for (int64_t k = cnt[f]; k < cnt[f + 1]; ++k) {
+        S.orig_dst[k] = tmp[k - cnt[f]].first;
+        S.orig_src[k] = tmp[k - cnt[f]].second;
+      }
+    }
+  };
+  {
+    const int nth = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (nf < 256 || nth == 1) {
+      sort_fronts(0, nf);
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < nth; ++t) {
+        const int32_t f0 = (int32_t)((int64_t)nf * t / nth), f1 = (int32_t)((int64_t)nf * (t + 1) / nth);
+        th.emplace_back(sort_fronts, f0, f1);
+      }
+      for (auto& x : th) x.join();
     }
   }
+  lap("originals");
   return "";
 }
 

@@ -55,8 +55,8 @@ class _Handle:
     def __init__(self, raw):
         self.raw = raw
 
-    def __del__(self):
-        if self.raw and _native._lib is not None:
+    def __del__(self, _native=_native):  # module globals may be gone at interpreter exit
+        if self.raw and _native is not None and _native._lib is not None:
             _native._lib.kh_symbolic_free(self.raw)
             self.raw = None
 
@@ -176,8 +176,8 @@ class _Plan:
         _native.call("kh_plan_residual", self.raw, int(nt), Y, int(ldy), F, int(ldf), R, int(ldr), norms2,
                      stream)
 
-    def __del__(self):
-        if getattr(self, "raw", None) and self.raw.value and _native._lib is not None:
+    def __del__(self, _native=_native):
+        if getattr(self, "raw", None) and self.raw.value and _native is not None and _native._lib is not None:
             _native._lib.kh_plan_free(self.raw)
             self.raw = ctypes.c_void_p()
 
