@@ -84,10 +84,11 @@ struct kh_plan {
   std::vector<KbInfo> kbinfo;
   int32_t* btasks = nullptr;
   char* owned = nullptr;           // workspace allocated by the plan (null if caller-provided)
-  // side stream: the small-front kernels of a level run there, concurrently
-  // with the large-front kernels on the caller's stream (levels are joined)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+  // side streams: the fused-front kernels of a level run there (one stream
+  // per size class, so the classes overlap each other's tails), concurrently
+  // with the large-front kernels on the caller's stream; levels are joined
+  cudaStream_t side[kSmallClasses] = {};
+  cudaEvent_t ev_main = nullptr, ev_side[kSmallClasses] = {};
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -134,24 +135,29 @@ void plan_release(kh_plan* p) {
   if (p->owned) cudaFree(p->owned);
   p->owned = nullptr;
   if (p->ev_main) cudaEventDestroy(p->ev_main);
-  if (p->ev_side) cudaEventDestroy(p->ev_side);
-  if (p->side) cudaStreamDestroy(p->side);
-  p->ev_main = p->ev_side = nullptr;
-  p->side = nullptr;
+  p->ev_main = nullptr;
+  for (int c = 0; c < kSmallClasses; ++c) {
+    if (p->ev_side[c]) cudaEventDestroy(p->ev_side[c]);
+    if (p->side[c]) cudaStreamDestroy(p->side[c]);
+    p->ev_side[c] = nullptr;
+    p->side[c] = nullptr;
+  }
 }
 
-// fork: `side` starts after the work queued so far on `st`
+// fork: the side streams start after the work queued so far on `st`
 cudaError_t fork_side(kh_plan* p, cudaStream_t st) {
   cudaError_t e = cudaEventRecord(p->ev_main, st);
-  return e == cudaSuccess ? cudaStreamWaitEvent(p->side, p->ev_main, 0) : e;
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(p->side[c], p->ev_main, 0);
+  return e;
 }
 
-// join both ways: the next level on either stream sees this level's results
+// join every way: the next level on any stream sees this level's results
 cudaError_t join_side(kh_plan* p, cudaStream_t st) {
-  cudaError_t e = cudaEventRecord(p->ev_side, p->side);
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaEventRecord(p->ev_side[c], p->side[c]);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(st, p->ev_side[c], 0);
   if (e == cudaSuccess) e = cudaEventRecord(p->ev_main, st);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->ev_side, 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->side, p->ev_main, 0);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(p->side[c], p->ev_main, 0);
   return e;
 }
 
@@ -542,9 +548,11 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     e = cudaMalloc(reinterpret_cast<void**>(&p->owned), measure.off);
     C.base = p->owned;
   }
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  for (int c = 0; c < kSmallClasses; ++c) {
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side[c], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_side[c], cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_main, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_side, cudaEventDisableTiming);
   if (e == cudaSuccess) {
     carve(p, S, X, C);
     auto up = [&](void* dst, const void* src, size_t bytes) {
@@ -609,7 +617,7 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
     const int32_t ns = (int32_t)nshift;
     for (int c = 0; c < kSmallClasses; ++c)
       KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                     uch, sch, p->minpiv_work, p->side));
+                                     uch, sch, p->minpiv_work, p->side[c]));
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
@@ -682,7 +690,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side));
+    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side[0]));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
                                 rch, sch, st));
     KH_CUDA(join_side(p, st));
@@ -690,7 +698,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side));
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side[0]));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
                                 p->y, st));
     KH_CUDA(join_side(p, st));
