@@ -469,9 +469,9 @@ KH_HD constexpr bool kLookAhead(int nw) { return nw >= KH_LOOKAHEAD_MIN_NW; }
 
 // LDL^T of the w x w diagonal block at column kb by warp 0 (lane i holds row
 // i, pivots broadcast with shuffles): L in the strict lower part, D on the
-// diagonal, 1/d in dinv and d in dg.
+// diagonal, 1/d in dinv and d in dg; minp tracks min |d|^2 (or -1).
 KH_DEV void diag_block_ldlt(double2* S, const int32_t* cb, double2* dinv, double2* dg, int kb, int w, int m,
-                            double& minp) {
+                            double& minp) {  // minp: running min |d|^2
   constexpr int BK = 8;
   const int lane = threadIdx.x & 31;
   int cbk[BK];
@@ -499,10 +499,17 @@ KH_DEV void diag_block_ldlt(double2* S, const int32_t* cb, double2* dinv, double
     if (act && lane == 0) {
       dinv[k] = di;
       dg[kb + k] = dk;
-      const double ad = sqrt(cabs2(dk));
-      minp = (ad != ad) ? -1.0 : fmin(minp, ad);
     }
   }
+  // pivot magnitudes off the dependency chain: min |d|^2 (-1 if non-finite);
+  // blocked_ldlt takes the square root once
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < BK; ++k)
+      if (k < w) {
+        const double a2 = cabs2(dg[kb + k]);
+        minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
+      }
 #pragma unroll
   for (int j = 0; j < BK; ++j)
     if (lane < w && j <= lane) S[cbk[j] + kb + lane] = a[j];
@@ -697,7 +704,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
     __syncthreads();
     sub(6);
   }
-  return minp;
+  return minp < 0.0 ? -1.0 : sqrt(minp);  // min |d|
 }
 
 // LDL^T of the w x w diagonal block at kb of a large front: one 64-thread CTA
