@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--refine", type=int, default=3)
+    ap.add_argument("--refine", type=int, default=5)
     ap.add_argument("--leaf-size", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--j-max", type=int, default=None)
@@ -243,6 +243,7 @@ def main():
 
     def step(record=False):
         eng.factored = False
+        eng.event_log = fac_events if record else None  # refactoring when the factors are not kept
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

@@ -165,7 +165,7 @@ class ShardedFD:
         self.Y.copy_(self.Yall.permute(1, 0, 2).reshape(2 * self.n_t, self.world * self.rp)[:, :self.n])
         return self.ops.residual_full(self.Y, self._F)
 
-    def solve(self, F, refine=3, tol=1e-13, factor_events=None):
+    def solve(self, F, refine=5, tol=1e-13, factor_events=None):
         """Returns (U_shard, info): U_shard is (N_t, rp) = column-major rows
         [rank*rp, rank*rp + rows) of u."""
         self._F = F
@@ -198,7 +198,7 @@ class ShardedFD:
         return allU.permute(1, 0, 2).reshape(self.n_t, self.world * self.rp)[:, :self.n].contiguous()
 
 
-def solve_fd_sharded(system, pencil=None, refine=3, refine_tol=1e-13, leaf_size=None, group=None):
+def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=None, group=None):
     """Multi-GPU counterpart of solvers.solve_fd (reference solvers.py:348-403)
     for one process per GPU under an initialized torch.distributed group.
 

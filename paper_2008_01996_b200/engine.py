@@ -139,7 +139,7 @@ class FDEngine:
     """Device-resident FD solver for one (M_x, A_x, temporal pencil) triple."""
 
     def __init__(self, M_x, A_x, modal, device=None, keep_factors=None, max_batch=None,
-                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.7, symbolic=None):
+                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None):
         import torch
 
         _native.require_cuda()
@@ -166,7 +166,14 @@ class FDEngine:
         nk = max(self.n_k, 1)
         batch = min(nk, max_batch or nk)
         if keep_factors is None:
-            keep_factors = sparse_direct.plan_bytes(self.sym, batch, nk) <= budget
+            # keep every shift's factors if they fit with a working batch of
+            # at least 16 shifts in flight (update buffers scale with it)
+            b = batch
+            while b > 16 and sparse_direct.plan_bytes(self.sym, b, nk) > budget:
+                b = (b + 1) // 2
+            keep_factors = sparse_direct.plan_bytes(self.sym, b, nk) <= budget
+            if keep_factors:
+                batch = b
         if keep_factors:
             slots = nk
         else:
@@ -191,6 +198,10 @@ class FDEngine:
         self.norms = torch.zeros(4, dtype=f64, device=dev)
         self.lam = np.ascontiguousarray(modal.lam)
         self.gpu_launches = 0
+        # optional list of (start, end) CUDA events around every factorization
+        # launch sequence (bench.py's roofline; also covers refactoring when
+        # the factors are not kept)
+        self.event_log = None
 
     # ---- primitives -----------------------------------------------------------
     def _stream(self):
@@ -225,6 +236,8 @@ class FDEngine:
 
     def _spatial(self):
         """Z[:, k] = (M_x + lambda_k A_x)^-1 G[:, k] for all modes."""
+        import torch
+
         st = self._stream()
         n, nk = self.n, self.n_k
         g, z = self.G.data_ptr(), self.Z.data_ptr()
@@ -234,7 +247,13 @@ class FDEngine:
             if self.keep_factors:
                 slot = s0
             else:
+                if self.event_log is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
                 self.plan.factor(0, self.lam[s0:s1], st)
+                if self.event_log is not None:
+                    e1.record()
+                    self.event_log.append((e0, e1))
                 self.plan.pivot_check(0, s1 - s0, st)
                 self.gpu_launches += depth + 3
                 slot = 0
@@ -260,7 +279,7 @@ class FDEngine:
         self.gpu_launches += 2
         return self.norms[:2]
 
-    def solve(self, F, U=None, refine=3, tol=1e-13):
+    def solve(self, F, U=None, refine=5, tol=1e-13):
         """Full FD solve of K u = f on the device with iterative refinement.
 
         Returns (U, info); U is a device tensor (N_t, n) = column-major n x N_t.

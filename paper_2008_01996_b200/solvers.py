@@ -35,7 +35,7 @@ from .dense import (ComplexSchurForm, EigenSvdForm, RealSchurForm, cholesky_lowe
 from .errors import DefectivePencil, DimensionMismatch, ImaginaryResidueTooLarge
 
 FD_IMAG_TOL = 1e-6       # solvers.py:400
-DEFAULT_REFINE = 3
+DEFAULT_REFINE = 5  # c3 stops after 1 step (1e-13 reached), c4 needs 4
 DEFAULT_REFINE_TOL = 1e-13
 
 
