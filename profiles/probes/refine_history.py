@@ -16,3 +16,15 @@ print("keep_factors", eng.keep_factors, "batch", eng.batch)
 F = torch.from_numpy(np.ascontiguousarray(system.rhs)).to(dev).view(system.n_t, system.m_x)
 U, inf = eng.solve(F, refine=refine, tol=1e-15)
 print("residuals", ["%.3e" % r for r in inf["residuals"]])
+if len(sys.argv) > 3 and sys.argv[3] == "host":
+    # the same solution's residual evaluated on the host (numpy/scipy, other rounding)
+    import time
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "..", "oracle"))
+    u = U.reshape(-1).cpu().numpy()
+    t0 = time.time()
+    n, nt = system.m_x, system.n_t
+    Um = u.reshape(n, nt, order="F")
+    KU = system.spatial.M_II @ (Um @ system.temporal.A.T) + system.spatial.A_II @ (Um @ system.temporal.M.T)
+    r = np.linalg.norm(system.rhs.reshape(n, nt, order="F") - KU) / np.linalg.norm(system.rhs)
+    print("host residual (numpy/scipy) %.3e  (%.1f s)" % (r, time.time() - t0))
+    print("gpu residual of the same u %.3e" % solvers.residual(system, u))
