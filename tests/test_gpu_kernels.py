@@ -143,19 +143,27 @@ def test_rhs_dimension_check(cuda_ok):
         num.solve(np.ones(5))
 
 
-@pytest.mark.parametrize("mesh", [("square", 40), ("lshape", 4), ("square", 128)])
-def test_batched_shifts_match_superlu(cuda_ok, mesh):
-    """Many complex shifts M + lam_k A in one batched factorization vs SuperLU."""
+@pytest.mark.parametrize("mesh,small_max,leaf", [
+    (("square", 40), None, None), (("lshape", 4), None, None), (("square", 128), None, None),
+    # every front through the level-synchronous large-front kernels
+    (("square", 64), "0", None), (("lshape", 4), "0", None),
+    # fused classes capped at m <= 64 / leaves large enough for the 96 and 128 classes
+    (("square", 64), "64", None), (("square", 96), None, 80), (("square", 64), None, 8)])
+def test_batched_shifts_match_superlu(cuda_ok, monkeypatch, mesh, small_max, leaf):
+    """Many complex shifts M + lam_k A in one batched factorization vs SuperLU,
+    through every front-class code path (KH_SMALL_MAX caps the fused classes)."""
     import torch
 
     from paper_2008_01996_b200 import fem, problems
 
+    if small_max is not None:
+        monkeypatch.setenv("KH_SMALL_MAX", small_max)
     ops = fem.assemble_p1(problems.spatial_mesh(*mesh))
     M, A = ops.M_II.tocsr(), ops.A_II.tocsr()
     n = M.shape[0]
     rng = np.random.default_rng(3)
     lam = rng.uniform(0.01, 3.0, 9) + 1j * rng.uniform(-40.0, 40.0, 9)
-    sym = sd.analyze((M + A).tocsr())
+    sym = sd.analyze((M + A).tocsr(), **({} if leaf is None else {"leaf_size": leaf}))
     plan = sd._Plan(sym, sym.align_values(M), sym.align_values(A), 4, 9, torch.cuda.current_device())
     st = _native.stream_handle()
     for s0 in range(0, 9, 4):
@@ -175,3 +183,31 @@ def test_batched_shifts_match_superlu(cuda_ok, mesh):
         ref = spla.spsolve(K, B[:, k])
         assert np.linalg.norm(X[:, k] - ref) / np.linalg.norm(ref) < 1e-11, k
         assert np.linalg.norm(K @ X[:, k] - B[:, k]) / np.linalg.norm(B[:, k]) < 1e-12
+
+
+def test_many_shifts_wide_level_kernels(cuda_ok):
+    """160 shifts in one batch: the large-front levels exceed the narrow-level
+    CTA threshold, so the wide-level solve kernels run (the 9-shift cases above
+    use the narrow ones)."""
+    import torch
+
+    from paper_2008_01996_b200 import fem, problems
+
+    ops = fem.assemble_p1(problems.spatial_mesh("square", 96))
+    M, A = ops.M_II.tocsr(), ops.A_II.tocsr()
+    n, ns = M.shape[0], 160
+    rng = np.random.default_rng(8)
+    lam = rng.uniform(0.01, 3.0, ns) + 1j * rng.uniform(-40.0, 40.0, ns)
+    sym = sd.analyze((M + A).tocsr())
+    plan = sd._Plan(sym, sym.align_values(M), sym.align_values(A), ns, ns, torch.cuda.current_device())
+    st = _native.stream_handle()
+    plan.factor(0, lam, st)
+    plan.pivot_check(0, ns, st)
+    B = rng.standard_normal((n, ns)) + 1j * rng.standard_normal((n, ns))
+    bre, bim = _dev(B.real.T), _dev(B.imag.T)
+    xre, xim = torch.empty_like(bre), torch.empty_like(bim)
+    plan.solve(0, ns, bre.data_ptr(), bim.data_ptr(), n, xre.data_ptr(), xim.data_ptr(), n, st)
+    X = xre.cpu().numpy().T + 1j * xim.cpu().numpy().T
+    for k in (0, 57, 159):
+        K = (M + lam[k] * A).astype(complex).tocsc()
+        assert np.linalg.norm(K @ X[:, k] - B[:, k]) / np.linalg.norm(B[:, k]) < 1e-12, k
