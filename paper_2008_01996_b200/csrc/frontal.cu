@@ -112,7 +112,9 @@ constexpr int MODE_SCALED = 0;
 template <int NWJ, int MODE>
 KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t lda, int rowsA,
                         const double2* __restrict__ B, int64_t ldb, int rowsB, const double2* __restrict__ D,
-                        int64_t ldd, CpStage* st) {
+                        int64_t ldd, CpStage* st, bool idle = false) {
+  // idle: this warp's 32 x 16 sub-tile is not needed (above the diagonal or
+  // past the last row/column); it still stages operands and joins barriers
   constexpr int NTH = 64 * NWJ, TN = 16 * NWJ;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -156,7 +158,7 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
     __syncthreads();
     const CpStage& S = st[c & 1];
 #pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
+    for (int kk = 0; kk < (idle ? 0 : KC); kk += 4) {
       double2 af[4], bf[2];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) af[mt] = S.a[(kk + t) * LDS + wi * 32 + mt * 8 + g];
@@ -236,7 +238,11 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
   Acc acc;
-  tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st);
+  // warps whose 32 x 16 sub-tile lies strictly above the diagonal (diagonal
+  // tiles) or beyond row/column q skip their MMAs
+  const int wrp = threadIdx.x >> 5, r0w = i0 + (wrp & 1) * 32, c0w = j0 + (wrp >> 1) * 16;
+  const bool idle = c0w > r0w + 31 || r0w >= q || c0w >= q;
+  tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st, idle);
   __syncthreads();  // kids visible even when p = 0
   // epilogue: this thread's 16 tile entries (rows wi*32+mt*8+g, cols
   // wj*16+nt*8+2t+h), in two halves of rows to bound register pressure;
