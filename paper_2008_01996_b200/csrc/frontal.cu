@@ -389,7 +389,10 @@ __global__ void __launch_bounds__(128) big_lupdate_kernel(KhTree T, const int32_
   const int p = F.p, m = p + F.q, w = min(NB, p - kb);
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   Acc acc;
-  tile_mma_cp<2, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, st);
+  // warps whose 32 rows all lie above the block (r < kb) or past m skip their MMAs
+  const int r0w = i0 + ((threadIdx.x >> 5) & 1) * 32;
+  const bool idle = r0w + 31 < kb || r0w >= m;
+  tile_mma_cp<2, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, st, idle);
   tile_epilogue(acc, [&](int i, int j, double2 v) {
     const int r = i0 + i, c = kb + j;
     if (r < m && j < w && r >= c) {
