@@ -13,6 +13,12 @@
 
 namespace {
 
+// Work item = (256 consecutive rows, RES_TCH consecutive time columns): each
+// thread keeps its row's CSR entries in registers (read once, not once per
+// time column) and sweeps the time columns; consecutive threads touch
+// consecutive rows, so the Y / F / R accesses are coalesced. Items are handed
+// out by a fixed grid-stride loop, so the partial sums are deterministic.
+constexpr int RES_TCH = 16, RES_ROWNZ = 8;
 __global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t nt, const int64_t* __restrict__ indptr,
                                                             const int64_t* __restrict__ indices,
                                                             const double* __restrict__ mv,
@@ -21,24 +27,44 @@ __global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t n
                                                             const double* __restrict__ F, int64_t ldf, double* R,
                                                             int64_t ldr, double* part) {
   __shared__ double red[2][8];
-  const int64_t total = n * nt;
+  const int64_t nrb = (n + 255) / 256, ntc = (nt + RES_TCH - 1) / RES_TCH;
   double rr = 0.0, ff = 0.0;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = idx / n, i = idx - t * n;
-    const double* y1 = Y + t * ldy;
-    const double* y2 = Y + (t + nt) * ldy;
-    double s = 0.0;
-    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
-      const int64_t j = indices[e];
-      s = fma(mv[e], y1[j], s);
-      s = fma(av[e], y2[j], s);
+  for (int64_t item = blockIdx.x; item < nrb * ntc; item += gridDim.x) {
+    const int64_t rb = item % nrb, tc = item / nrb;
+    const int64_t i = rb * 256 + threadIdx.x;
+    if (i >= n) continue;
+    const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+    const int nz = (int)(e1 - e0);
+    int64_t col[RES_ROWNZ];
+    double mm[RES_ROWNZ], aa[RES_ROWNZ];
+#pragma unroll
+    for (int k = 0; k < RES_ROWNZ; ++k) {
+      const bool ok = k < nz;
+      col[k] = ok ? indices[e0 + k] : i;
+      mm[k] = ok ? mv[e0 + k] : 0.0;
+      aa[k] = ok ? av[e0 + k] : 0.0;
     }
-    const double f = F[i + t * ldf];
-    const double r = f - s;
-    if (R) R[i + t * ldr] = r;
-    rr = fma(r, r, rr);
-    ff = fma(f, f, ff);
+    const int64_t t1 = min(nt, (tc + 1) * RES_TCH);
+    for (int64_t t = tc * RES_TCH; t < t1; ++t) {
+      const double* y1 = Y + t * ldy;
+      const double* y2 = Y + (t + nt) * ldy;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < RES_ROWNZ; ++k) {
+        s = fma(mm[k], y1[col[k]], s);
+        s = fma(aa[k], y2[col[k]], s);
+      }
+      for (int64_t e = e0 + RES_ROWNZ; e < e1; ++e) {  // rows longer than RES_ROWNZ
+        const int64_t j = indices[e];
+        s = fma(mv[e], y1[j], s);
+        s = fma(av[e], y2[j], s);
+      }
+      const double f = F[i + t * ldf];
+      const double r = f - s;
+      if (R) R[i + t * ldr] = r;
+      rr = fma(r, r, rr);
+      ff = fma(f, f, ff);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     rr += __shfl_xor_sync(0xffffffffu, rr, o);
