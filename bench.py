@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--j-max", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--collective", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 back-transform reduce-scatter: fused GEMM + peer-memory scatter, or NCCL")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-GPU driver even with one rank (testing the N>1 path on one GPU)")
     return ap.parse_args()
@@ -230,7 +232,7 @@ def main():
         from paper_2008_01996_b200.distributed import ShardedFD
 
         runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
-                           leaf_size=leaf)
+                           leaf_size=leaf, collective=args.collective)
         eng = runner.engine
     else:
         runner = None
@@ -311,7 +313,9 @@ def main():
                        "shifts_solved": int(modal.n_k), "conjugate_pairs": int(modal.n_pairs),
                        "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
                            stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
-                       "parallelism": f"shift-sharded x{world} + NCCL reduce-scatter" if sharded else "single GPU"},
+                       "parallelism": (f"shift-sharded x{world}, back transform + reduce-scatter: "
+                                       + ("fused GEMM->peer-memory scatter" if args.collective == "p2p"
+                                          else "GEMM + NCCL reduce_scatter")) if sharded else "single GPU"},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),
@@ -407,13 +411,14 @@ def measure_e2e_sharded(system, pencil, args, leaf):
     pinned = torch.empty(system.rhs.shape, dtype=torch.float64, pin_memory=True)
     pinned.copy_(torch.from_numpy(system.rhs))
     system = dataclasses.replace(system, rhs=pinned.numpy())
-    solve_fd_sharded(system, pencil=None, refine=args.refine, leaf_size=leaf)  # warm-up
+    solve_fd_sharded(system, pencil=None, refine=args.refine, leaf_size=leaf, collective=args.collective)
     torch.cuda.synchronize()
     dist.barrier()
     steps = max(1, args.e2e_steps)
     t0 = time.perf_counter()
     for _ in range(steps):
-        (r0, r1), _, rep = solve_fd_sharded(system, pencil=None, refine=args.refine, leaf_size=leaf)
+        (r0, r1), _, rep = solve_fd_sharded(system, pencil=None, refine=args.refine, leaf_size=leaf,
+                                            collective=args.collective)
     el = torch.tensor([(time.perf_counter() - t0) / steps], device=torch.device("cuda", torch.cuda.current_device()))
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     nnz = system.spatial.M_II.nnz

@@ -14,6 +14,9 @@
  *   kh_dgemm .................. modal transforms (zgemm)                solvers.py:368-372, :397-400
  *   kh_plan_residual .......... residual / kron_apply_right             solvers.py:428-440, dense.py:264-286
  *   kh_sumsq .................. norms of _discard_imaginary              solvers.py:406-413
+ *   kh_dgemm_rowscatter ....... multi-GPU back transform fused with the scatter of its
+ *   kh_sum_parts                reduce-scatter (solvers.py:397-400 per rank)
+ *   kh_ipc_handle/open/close .. peer-memory mapping of the receive slots (one process per GPU)
  *
  * Conventions: plain pointers and 64-bit sizes, column-major matrices,
  * caller-owned buffers. Pointers documented "device" must be CUDA device
@@ -138,6 +141,22 @@ int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int
 int kh_daxpy(int64_t n, double alpha, const double* x, double* y, void* stream);
 /* out (device, 1 double) = sum_i x_i^2 over n device doubles. */
 int kh_sumsq(const double* x, int64_t n, double* out, void* stream);
+/* Multi-GPU back transform (one process per GPU). C = A B (m x n, K = k,
+ * device arrays, column-major), with row r written to part c = r / rows_per_part
+ * at dst[c] + (r - c rows_per_part) + j ld_dst, where `dst` is a DEVICE array of
+ * `parts` pointers, typically peer-mapped receive slots of the other ranks
+ * (kh_ipc_open): each finished tile goes straight over NVLink to the rank that
+ * owns its rows, fusing the GEMM with the scatter of a reduce-scatter. */
+int kh_dgemm_rowscatter(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* const* dst, int32_t parts, int64_t rows_per_part, int64_t ld_dst, void* stream);
+/* out[e] = sum_{c < parts} slots[c part_elems + e] in slot order (deterministic
+ * reduction of the received partial sums; device arrays). */
+int kh_sum_parts(int32_t parts, const double* slots, int64_t part_elems, double* out, void* stream);
+/* CUDA IPC: `handle` is 64 opaque bytes (host). kh_ipc_open maps another
+ * process's device allocation into this process (peer access enabled). */
+int kh_ipc_handle(const void* dev_ptr, void* handle);
+int kh_ipc_open(const void* handle, void** dev_ptr);
+int kh_ipc_close(void* dev_ptr);
 int kh_set_device(int device);
 int kh_stream_sync(void* stream);
 

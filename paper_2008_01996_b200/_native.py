@@ -80,6 +80,11 @@ SIGNATURES = {
     "kh_daxpy": (ctypes.c_int, [_i64, _dbl, _vp, _vp, _vp]),
     "kh_csr_pair_residual": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                                             _vp, _vp]),
+    "kh_dgemm_rowscatter": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _i64, _i64, _vp]),
+    "kh_sum_parts": (ctypes.c_int, [_i32, _vp, _i64, _vp, _vp]),
+    "kh_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "kh_ipc_open": (ctypes.c_int, [_vp, _P(_vp)]),
+    "kh_ipc_close": (ctypes.c_int, [_vp]),
     "kh_set_device": (ctypes.c_int, [ctypes.c_int]),
     "kh_stream_sync": (ctypes.c_int, [_vp]),
 }

@@ -736,4 +736,45 @@ int kh_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int
   return KH_OK;
 }
 
+int kh_dgemm_rowscatter(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* const* dst, int32_t parts, int64_t rows_per_part, int64_t ld_dst, void* stream) {
+  if (m < 0 || n < 0 || k < 0 || parts < 1 || rows_per_part < 1) return fail(KH_ERR_DIMENSION, "bad scatter shape");
+  if ((int64_t)parts * rows_per_part < m) return fail(KH_ERR_DIMENSION, "parts do not cover the rows");
+  if ((m > 0 && lda < m) || (k > 0 && ldb < k) || ld_dst < rows_per_part)
+    return fail(KH_ERR_DIMENSION, "GEMM leading dimension too small");
+  if (m && n && (!dst || (k && (!A || !B)))) return fail(KH_ERR_INVALID, "null GEMM operand");
+  KH_CUDA(kh_launch_dgemm_rowscatter(m, n, k, A, lda, B, ldb, dst, rows_per_part, ld_dst,
+                                     static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
+int kh_sum_parts(int32_t parts, const double* slots, int64_t part_elems, double* out, void* stream) {
+  if (parts < 1 || part_elems < 0) return fail(KH_ERR_DIMENSION, "bad part count");
+  if (part_elems && (!slots || !out)) return fail(KH_ERR_INVALID, "null argument");
+  KH_CUDA(kh_launch_sum_parts(parts, slots, part_elems, out, static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
+int kh_ipc_handle(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(KH_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  KH_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &h, sizeof h);
+  return KH_OK;
+}
+
+int kh_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(KH_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  KH_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return KH_OK;
+}
+
+int kh_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(KH_ERR_INVALID, "null argument");
+  KH_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return KH_OK;
+}
+
 }  // extern "C"

@@ -18,10 +18,16 @@ constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
 constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
 constexpr size_t SMEM_BYTES = sizeof(double) * NST * (A_STAGE + B_STAGE);
 
+// SCATTER: row r of the result goes to part c = r / rp at dst[c] (row r - c rp,
+// leading dimension ldd): the back transform's partial sums are written
+// straight into each destination rank's receive slot over NVLink peer memory,
+// tile by tile as the tiles finish (fused GEMM + scatter of the reduce-scatter).
+template <bool SCATTER>
 __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
                                                     const double* __restrict__ A, int64_t lda,
                                                     const double* __restrict__ B, int64_t ldb,
-                                                    double beta, double* __restrict__ C, int64_t ldc) {
+                                                    double beta, double* __restrict__ C, int64_t ldc,
+                                                    double* const* __restrict__ dst, int64_t rp, int64_t ldd) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + NST * A_STAGE;
@@ -99,11 +105,48 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_
       for (int h = 0; h < 2; ++h) {
         int64_t col = n0 + wn * 32 + nt * 8 + 2 * t + h;
         if (col >= N) continue;
-        double* c = C + row + col * ldc;
         double v = alpha * acc[mt][nt][h];
-        if (beta != 0.0) v = fma(beta, *c, v);
-        *c = v;
+        if (SCATTER) {
+          const int64_t part = row / rp;
+          dst[part][(row - part * rp) + col * ldd] = v;
+        } else {
+          double* c = C + row + col * ldc;
+          if (beta != 0.0) v = fma(beta, *c, v);
+          *c = v;
+        }
       }
+  }
+}
+
+}  // namespace
+
+namespace {
+
+template <bool SCATTER>
+cudaError_t launch(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double beta, double* C, int64_t ldc, double* const* dst, int64_t rp, int64_t ldd,
+                   cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  dgemm_kernel<SCATTER><<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, dst, rp,
+                                                           ldd);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+// out[e] = sum_{c < g} parts[c * len + e], in slot order (deterministic)
+__global__ void sum_parts_kernel(int32_t g, const double* __restrict__ parts, int64_t len, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = parts[e];
+    for (int32_t c = 1; c < g; ++c) s += parts[c * len + e];
+    out[e] = s;
   }
 }
 
@@ -112,16 +155,19 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_
 cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                             const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                             cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-  dgemm_kernel<<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  return launch<false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nullptr, 1, 0, stream);
+}
+
+cudaError_t kh_launch_dgemm_rowscatter(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                                       const double* B, int64_t ldb, double* const* dst, int64_t rp, int64_t ldd,
+                                       cudaStream_t stream) {
+  return launch<true>(M, N, K, 1.0, A, lda, B, ldb, 0.0, nullptr, 0, dst, rp, ldd, stream);
+}
+
+cudaError_t kh_launch_sum_parts(int32_t g, const double* parts, int64_t len, double* out, cudaStream_t stream) {
+  if (len <= 0) return cudaSuccess;
+  const int blocks = (int)((len + 255) / 256 < 148 * 8 ? (len + 255) / 256 : 148 * 8);
+  sum_parts_kernel<<<blocks, 256, 0, stream>>>(g, parts, len, out);
   kh_note_launch();
   return cudaGetLastError();
 }

@@ -52,6 +52,13 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
                             const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                             cudaStream_t stream);
 
+// C = A B with row r written to dst[r / rp] (row r % rp, ld ldd): fused GEMM +
+// scatter into peer receive slots; and the ordered sum of g slots.
+cudaError_t kh_launch_dgemm_rowscatter(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                                       const double* B, int64_t ldb, double* const* dst, int64_t rp, int64_t ldd,
+                                       cudaStream_t stream);
+cudaError_t kh_launch_sum_parts(int32_t g, const double* parts, int64_t len, double* out, cudaStream_t stream);
+
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
                                 int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,

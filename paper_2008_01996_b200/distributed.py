@@ -20,6 +20,16 @@ rank, so the refinement loop takes the same branch everywhere.
 The device work is behind `ops` (default: the FDEngine kernels); the
 collectives are plain torch.distributed calls, so the same driver runs on
 NCCL/GPU and, in tests, on gloo/CPU with an emulated `ops`.
+
+Steps 3-4 have two implementations (`collective=`):
+  "nccl": per destination chunk a local GEMM into P_r[c], then
+          `reduce_scatter_tensor` (the baseline);
+  "p2p":  ONE GEMM kernel (`kh_dgemm_rowscatter`) writes each finished tile of
+          P_r[c] straight into rank c's receive slot r through CUDA-IPC peer
+          mappings over NVLink, so the transfer overlaps the math tile by tile;
+          after a barrier each rank sums its g slots in rank order
+          (`kh_sum_parts`: deterministic, identical to the NCCL result up to
+          the summation order).
 """
 
 import math
@@ -79,6 +89,16 @@ class EngineOps:
         e._gemm(rows, e.n_t, nk2, 1.0, e.Z.data_ptr() + 8 * r0, e.n, e.w_out.data_ptr(), nk2, 0.0,
                 dst.data_ptr(), ldd)
 
+    def out_scatter(self, dst_table, parts, rp):
+        """Z W_out_local with row block c written to dst_table[c] (fused scatter)."""
+        from . import _native
+
+        e = self.e
+        nk2 = 2 * e.n_k
+        _native.call("kh_dgemm_rowscatter", e.n, e.n_t, nk2, e.Z.data_ptr(), e.n, e.w_out.data_ptr(), max(nk2, 1),
+                     dst_table.data_ptr(), parts, rp, rp, e._stream())
+        e.gpu_launches += 1
+
     def y_shard(self, U_shard, rows, ld, dst):
         """dst (rows x 2N_t, ld) = U_shard [A_t^T | M_t^T]."""
         e = self.e
@@ -98,13 +118,59 @@ class EngineOps:
         _native.call("kh_daxpy", y.numel(), 1.0, x.data_ptr(), y.data_ptr(), self.e._stream())
 
 
+class PeerSlots:
+    """Receive slots for the fused GEMM + reduce-scatter over peer memory.
+
+    recv[s] (column-major rp x N_t) receives the partial back transform that
+    rank s computed for this rank's rows. Every rank maps the other ranks'
+    receive buffers with CUDA IPC and keeps a device table dst[c] = (rank c's
+    recv) + slot `rank`, the target of kh_dgemm_rowscatter.
+    """
+
+    def __init__(self, world, rank, nt, rp, device, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _native
+
+        self.world, self.rank, self.group = world, rank, group
+        self.slot = nt * rp
+        self.recv = torch.zeros((world, nt, rp), dtype=torch.float64, device=device)
+        handle = ctypes.create_string_buffer(64)
+        _native.call("kh_ipc_handle", self.recv.data_ptr(), handle)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.mapped = []
+        bases = []
+        for c in range(world):
+            if c == rank:
+                bases.append(self.recv.data_ptr())
+            else:
+                ptr = ctypes.c_void_p()
+                _native.call("kh_ipc_open", ctypes.create_string_buffer(handles[c], 64), ctypes.byref(ptr))
+                self.mapped.append(ptr.value)
+                bases.append(ptr.value)
+        self.dst = torch.tensor([b + 8 * rank * self.slot for b in bases], dtype=torch.int64, device=device)
+
+    def close(self):
+        from . import _native
+
+        for ptr in self.mapped:
+            _native.call("kh_ipc_close", ptr)
+        self.mapped = []
+
+
 class ShardedFD:
     """FD over `world` ranks of torch.distributed (row-sharded result)."""
 
     def __init__(self, M_x, A_x, modal, rank, world, device=None, leaf_size=None, ops=None, group=None,
-                 engine_kwargs=None):
+                 engine_kwargs=None, collective="nccl"):
         import torch
 
+        if collective not in ("nccl", "p2p"):
+            raise ValueError(f"unknown collective {collective!r}")
         self.rank, self.world, self.group = rank, world, group
         self.k0, self.k1 = shard_range(modal.n_k, world, rank)
         self.local = restrict_modal(modal, self.k0, self.k1)
@@ -136,6 +202,8 @@ class ShardedFD:
         self.Yall = torch.zeros((g, 2 * nt, rp), dtype=f64, device=dev)
         self.Y = torch.zeros((2 * nt, self.n), dtype=f64, device=dev)  # col-major n x 2N_t
         self.gpu_launches = 0
+        self.collective = collective
+        self.peers = PeerSlots(world, rank, nt, rp, dev, group) if collective == "p2p" else None
 
     def rows(self, c):
         r0 = c * self.rp
@@ -146,6 +214,9 @@ class ShardedFD:
         import torch.distributed as dist
 
         self.ops.apply_local(F)
+        if self.peers is not None:
+            self._apply_p2p(out)
+            return
         for c in range(self.world):
             r0, rows = self.rows(c)
             if rows < self.rp:
@@ -153,6 +224,22 @@ class ShardedFD:
             if rows:
                 self.ops.out_chunk(r0, rows, self.P[c], self.rp)
         dist.reduce_scatter_tensor(out.view(-1), self.P.view(-1), group=self.group)
+
+    def _apply_p2p(self, out):
+        """Fused back transform + reduce-scatter over peer memory."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _native
+
+        pe = self.peers
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # every rank has consumed its slots of the previous exchange
+        self.ops.out_scatter(pe.dst, self.world, self.rp)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # all tiles destined to this rank have landed
+        _native.call("kh_sum_parts", self.world, pe.recv.data_ptr(), pe.slot, out.data_ptr(),
+                     _native.stream_handle())
 
     def _residual(self):
         import torch.distributed as dist
@@ -198,7 +285,8 @@ class ShardedFD:
         return allU.permute(1, 0, 2).reshape(self.n_t, self.world * self.rp)[:, :self.n].contiguous()
 
 
-def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=None, group=None):
+def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=None, group=None,
+                     collective="p2p"):
     """Multi-GPU counterpart of solvers.solve_fd (reference solvers.py:348-403)
     for one process per GPU under an initialized torch.distributed group.
 
@@ -229,7 +317,7 @@ def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=
     n, nt = system.m_x, system.n_t
     t0 = time.perf_counter()
     runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
-                       leaf_size=leaf_size, group=group)
+                       leaf_size=leaf_size, group=group, collective=collective)
     F = solvers._to_device(system.rhs, dev).view(nt, n)
     U, info = runner.solve(F, refine=refine, tol=refine_tol)
     r0, rows = runner.rows(rank)

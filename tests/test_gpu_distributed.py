@@ -19,7 +19,8 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_sharded_fd_world1_nccl(cuda_ok):
+@pytest.mark.parametrize("collective", ["nccl", "p2p"])
+def test_sharded_fd_world1_nccl(cuda_ok, collective):
     import torch
     import torch.distributed as dist
 
@@ -29,10 +30,12 @@ def test_sharded_fd_world1_nccl(cuda_ok):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    run = None
     try:
         system, ref = load_golden("c1")
         modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
-        run = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, 0, 1, device=torch.device("cuda", 0))
+        run = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, 0, 1, device=torch.device("cuda", 0),
+                        collective=collective)
         F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
         _, info = run.solve(F)
         u = run.gather().reshape(-1).cpu().numpy()
@@ -42,10 +45,39 @@ def test_sharded_fd_world1_nccl(cuda_ok):
         # public multi-GPU entry point: same rows as solve_fd, host output
         from paper_2008_01996_b200.distributed import solve_fd_sharded
 
-        (r0, r1), U_rows, rep = solve_fd_sharded(system)
+        (r0, r1), U_rows, rep = solve_fd_sharded(system, collective=collective)
         assert (r0, r1) == (0, system.m_x)
         assert U_rows.shape == (system.n_t, system.m_x)
         assert rel_diff(U_rows.reshape(-1), ref["bs"]) < 1e-10
         assert rep.residual < 1e-11
     finally:
+        if run is not None and run.peers is not None:
+            run.peers.close()
         dist.destroy_process_group()
+
+
+def test_rowscatter_gemm_and_slot_sum(cuda_ok):
+    """kh_dgemm_rowscatter writes row block c of A B to dst[c]; kh_sum_parts adds
+    g slots in order (the two halves of the fused reduce-scatter, on one GPU)."""
+    import torch
+
+    from paper_2008_01996_b200 import _native
+
+    rng = np.random.default_rng(2)
+    m, n, k, g = 1000, 48, 37, 3
+    rp = -(-m // g)
+    A = torch.from_numpy(rng.standard_normal((k, m))).cuda()   # column-major m x k
+    B = torch.from_numpy(rng.standard_normal((n, k))).cuda()   # column-major k x n
+    recv = torch.zeros((g, n, rp), dtype=torch.float64, device="cuda")
+    dst = torch.tensor([recv[c].data_ptr() for c in range(g)], dtype=torch.int64, device="cuda")
+    _native.call("kh_dgemm_rowscatter", m, n, k, A.data_ptr(), m, B.data_ptr(), k, dst.data_ptr(), g, rp, rp,
+                 _native.stream_handle())
+    C = (A.T @ B.T).cpu().numpy()                               # m x n
+    got = recv.cpu().numpy()
+    for c in range(g):
+        rows = C[c * rp:(c + 1) * rp]
+        assert np.allclose(got[c].T[:len(rows)], rows, rtol=1e-13, atol=1e-12)
+    out = torch.empty((n, rp), dtype=torch.float64, device="cuda")
+    _native.call("kh_sum_parts", g, recv.data_ptr(), n * rp, out.data_ptr(), _native.stream_handle())
+    want = got[0] + got[1] + got[2]
+    assert np.array_equal(out.cpu().numpy(), want)
