@@ -309,9 +309,11 @@ def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=
     report = solvers.SolveReport(variant="fd", dof=system.dof, n_t=system.n_t, m_x=system.m_x)
     t0 = time.perf_counter()
     if pencil is None:
-        pencil = solvers.build_pencil(system.temporal, "fd")
+        pencil = solvers.build_pencil(system.temporal, "fd", eig="reduced")
     modal = modal_plan(system.temporal, pencil)
     report.t_decompose = time.perf_counter() - t0
+    report.min_re_lambda = pencil.min_re_lambda
+    report.spectral = pencil.spectral_stats
     dev = torch.device("cuda", torch.cuda.current_device())
     report.device = torch.cuda.get_device_name(dev)
     n, nt = system.m_x, system.n_t

@@ -25,7 +25,7 @@ import scipy.linalg as sla
 import scipy.sparse as sp
 
 from . import _native, sparse_direct
-from .dense import spd_solve
+from .dense import real_basis, spd_solve
 from .errors import DefectivePencil, DimensionMismatch
 
 
@@ -89,20 +89,19 @@ def modal_plan(temporal, pencil):
     if any(abs(form.D[j].imag) > 0.0 for j in singles):
         # only reachable for complex pencils that dggev never produces for real (M_t, A_t)
         raise DefectivePencil("unpaired complex eigenvalue in a real pencil")
-    # real basis: pair j -> columns (Re x_j, Im x_j); real eigenvalue -> x_j
-    cols, where = [], {}
-    for j in reps:
-        where[j] = len(cols)
-        cols += [X[:, j].real, X[:, j].imag]
-    for j in singles:
-        where[j] = len(cols)
-        cols.append(X[:, j].real)
-    Xr = np.column_stack(cols)
-    Ur, sr, Vrh = sla.svd(Xr)
+    # real basis in eigenvalue order: pair j -> columns (Re x_j, Im x_j);
+    # real eigenvalue -> x_j; Y = X_r diag(s) has the singular values of X
+    Xr, s = real_basis(X, form.D)
+    where = {j: j for j in list(reps) + list(singles)}
+    if getattr(form, "real_svd", None) is not None:
+        Ur, sr, Vrh, s = form.real_svd
+    else:
+        Ur, sr, Vrh = sla.svd(Xr * s[None, :])
     if sr[-1] <= 0.0:
         raise DefectivePencil("eigenvector matrix is numerically singular")
-    # W_r = A_t^-1 X_r^-T = A_t^-1 U_r S_r^-1 V_r^T (damped through the SVD)
-    Wr = spd_solve(pencil.chol_A, Ur / sr[None, :]) @ Vrh
+    # W_r = A_t^-1 X_r^-T = A_t^-1 Y^-T diag(s) = A_t^-1 U S^-1 V^T diag(s)
+    # (damped through the SVD like the reference's X^-1)
+    Wr = (spd_solve(pencil.chol_A, Ur / sr[None, :]) @ Vrh) * s[None, :]
     nk = len(reps) + len(singles)
     w_in = np.zeros((n_t, 2 * nk))
     w_out = np.zeros((2 * nk, n_t))

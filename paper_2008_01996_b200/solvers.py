@@ -23,7 +23,7 @@ refinement).
 
 import time
 from concurrent.futures import ThreadPoolExecutor
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
@@ -31,7 +31,8 @@ import scipy.sparse as sp
 
 from . import sparse_direct
 from .dense import (ComplexSchurForm, EigenSvdForm, RealSchurForm, cholesky_lower, complex_schur,
-                    eig_pencil, real_schur, spd_solve, svd_of_eigenvectors)
+                    eig_pencil, eig_pencil_reduced, pencil_residual, real_schur, spd_solve,
+                    svd_of_eigenvectors, svd_of_eigenvectors_real)
 from .errors import DefectivePencil, DimensionMismatch, ImaginaryResidueTooLarge
 
 FD_IMAG_TOL = 1e-6       # solvers.py:400
@@ -73,6 +74,25 @@ class PencilFactorization:
     variant: str
     chol_A: np.ndarray
     form: object
+    # the temporal operators, kept by the "reduced" eigensolver so that the
+    # reference's spectral statistics can be produced on demand
+    temporal: object = field(default=None, repr=False, compare=False)
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def spectral_stats(self):
+        """(sigma_min, sigma_max) of X_t in the reference's convention (dggev
+        vectors; solvers.py:146-163). A "qz" pencil has them in its SVD; for a
+        "reduced" pencil they depend on the phase dggev assigns each complex
+        vector (see build_pencil), so they are computed by the QZ route on the
+        first request and cached: a diagnostic, not an input of the solve."""
+        form = self.form
+        if getattr(form, "real_svd", None) is None or self.temporal is None:
+            return float(form.sigma[-1]), float(form.sigma[0])
+        if "qz" not in self._cache:
+            vals, vecs = eig_pencil(self.temporal.M, self.temporal.A)
+            sig = np.linalg.svd(vecs, compute_uv=False)
+            self._cache["qz"] = (float(sig[-1]), float(sig[0]))
+        return self._cache["qz"]
 
     @property
     def eigenvalues(self):
@@ -116,9 +136,6 @@ class SolveReport:
     t_transform_out: float = 0.0
     residual: float = 0.0
     min_re_lambda: float = 0.0
-    sigma_min: float = 0.0
-    sigma_max: float = 0.0
-    kappa2: float = 0.0
     threads: int = 1
     analyze_calls: int = 0
     fallback: Optional[str] = None
@@ -128,6 +145,29 @@ class SolveReport:
     imag_residue: float = 0.0
     fd_residual: float = 0.0
     device: str = ""
+    # host-side milestones of solve_fd in seconds since its start (pencil,
+    # analyze, host_joined, plan, factored): where the end-to-end time goes
+    phases: dict = field(default_factory=dict)
+    # (sigma_min, sigma_max) of X_t, or a callable producing them on first use
+    spectral: object = field(default=(0.0, 0.0), repr=False)
+
+    def _spectral(self):
+        if callable(self.spectral):
+            self.spectral = tuple(self.spectral())
+        return self.spectral
+
+    @property
+    def sigma_min(self):
+        return self._spectral()[0]
+
+    @property
+    def sigma_max(self):
+        return self._spectral()[1]
+
+    @property
+    def kappa2(self):
+        lo, hi = self._spectral()
+        return hi / lo if lo > 0.0 else 0.0
 
     @property
     def t_total(self):
@@ -147,8 +187,22 @@ class SolveReport:
                 "t_transform_out,residual,minReLambda,kappa2,threads")
 
 
-def build_pencil(temporal, variant):
-    """Decompose the temporal pencil on the host (solvers.py:166-206)."""
+def build_pencil(temporal, variant, eig="qz"):
+    """Decompose the temporal pencil on the host (solvers.py:166-206).
+
+    ``eig`` picks the "fd" eigensolver: "qz" (default) is the reference's
+    dggev + complex SVD; "reduced" reduces the pencil with the Cholesky factor
+    of A_t, runs dgeev on L^-1 M_t L^-T and takes the SVD of X in its real
+    basis: 3-6x less host time at N_t=256, ~15x at N_t=1024. Both give the
+    same eigenvalues to rounding and the same vector conventions (pairs
+    adjacent, +Im first, exact conjugates, max |Re|+|Im| = 1 per column), so
+    the FD solution is the same; sigma and kappa_2 of X differ by a few
+    percent, because that scaling depends on the phase LAPACK happens to give
+    each complex vector, which the two algorithms choose differently
+    (tests/test_pencil.py). `solve_fd` uses "reduced" when it builds the
+    pencil itself; its report still carries the reference's statistics
+    (`PencilFactorization.spectral_stats`, computed when first read).
+    """
     L = cholesky_lower(temporal.A)
     P = spd_solve(L, temporal.M)
     if variant == "bs-real":
@@ -156,14 +210,23 @@ def build_pencil(temporal, variant):
     elif variant == "bs-complex":
         form = complex_schur(P)
     elif variant == "fd":
-        vals, vecs = eig_pencil(temporal.M, temporal.A)
         scale = max(np.linalg.norm(P, "fro"), 1.0)
-        if np.linalg.norm(P @ vecs - vecs * vals[None, :], "fro") > 1e-8 * scale:
-            raise DefectivePencil("eigenvector residual above tolerance")
-        form = svd_of_eigenvectors(vecs, vals)
+        if eig == "reduced":
+            vals, vecs = eig_pencil_reduced(temporal.M, temporal.A, L)
+            if pencil_residual(P, vecs, vals) > 1e-8 * scale:
+                raise DefectivePencil("eigenvector residual above tolerance")
+            form = svd_of_eigenvectors_real(vecs, vals)
+        elif eig == "qz":
+            vals, vecs = eig_pencil(temporal.M, temporal.A)
+            if np.linalg.norm(P @ vecs - vecs * vals[None, :], "fro") > 1e-8 * scale:
+                raise DefectivePencil("eigenvector residual above tolerance")
+            form = svd_of_eigenvectors(vecs, vals)
+        else:
+            raise ValueError(f"unknown eigensolver: {eig!r}")
     else:
         raise ValueError(f"unknown pencil variant: {variant!r}")
-    pencil = PencilFactorization(variant=variant, chol_A=L, form=form)
+    pencil = PencilFactorization(variant=variant, chol_A=L, form=form,
+                                 temporal=temporal if variant == "fd" and eig == "reduced" else None)
     if pencil.min_re_lambda <= 0.0:
         raise DefectivePencil("pencil eigenvalue with nonpositive real part")
     return pencil
@@ -227,30 +290,47 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     t0 = time.perf_counter()
     analyze_before = sparse_direct.analyze_call_count()
     pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
+    phases = report.phases
+
+    def _analyze():
+        a0 = time.perf_counter()
+        out = sparse_direct.analyze(pattern, leaf_size)
+        phases["analyze"] = time.perf_counter() - a0
+        return out
+
+    # a pinned rhs goes up asynchronously right away (the copy engine works
+    # while the host computes the pencil); a pageable one after the pencil
+    rhs_t = torch.from_numpy(np.ascontiguousarray(np.asarray(system.rhs, dtype=np.float64)))
+    F = rhs_t.to(dev, non_blocking=True).view(nt, n) if rhs_t.is_pinned() else None
     with ThreadPoolExecutor(max_workers=1) as pool:
-        fut = pool.submit(sparse_direct.analyze, pattern, leaf_size)
-        if pencil is None:
-            pencil = build_pencil(system.temporal, "fd")
-        form = pencil.form
-        if not (isinstance(form, EigenSvdForm) or all(hasattr(form, a) for a in ("X", "D", "U", "sigma", "Vh"))):
-            raise DimensionMismatch("solve_fd needs an eigen-SVD pencil")
-        # few BLAS threads: the N_t x N_t SVD gains nothing from more, and the
-        # dissection threads of the analysis need the cores
-        with _blas_threads(2):
+        fut = pool.submit(_analyze)
+        # few BLAS threads: dgeev / the SVD of an N_t <= 512 matrix gain
+        # nothing from more, and the dissection threads of the analysis
+        # need the cores
+        with _blas_threads(1 if nt <= 512 else 4):
+            if pencil is None:
+                pencil = build_pencil(system.temporal, "fd", eig="reduced")
+            phases["pencil"] = time.perf_counter() - t0
+            form = pencil.form
+            if not (isinstance(form, EigenSvdForm)
+                    or all(hasattr(form, a) for a in ("X", "D", "U", "sigma", "Vh"))):
+                raise DimensionMismatch("solve_fd needs an eigen-SVD pencil")
             modal = modal_plan(system.temporal, pencil)
         report.t_decompose = time.perf_counter() - t0
-        F = _to_device(system.rhs, dev).view(nt, n)
+        if F is None:
+            F = rhs_t.to(dev).view(nt, n)
         symbolic = fut.result()
+        phases["host_joined"] = time.perf_counter() - t0
     report.min_re_lambda = pencil.min_re_lambda
-    report.sigma_min = float(form.sigma[-1])
-    report.sigma_max = float(form.sigma[0])
-    report.kappa2 = float(form.sigma[0] / form.sigma[-1])
+    report.spectral = pencil.spectral_stats
 
     # spatial setup: numeric plan + factorization of every shift
     eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev, leaf_size=leaf_size,
                    max_batch=max_batch, keep_factors=keep_factors, symbolic=symbolic)
+    phases["plan"] = time.perf_counter() - t0
     eng.factor()
     _sync()
+    phases["factored"] = time.perf_counter() - t0
     report.analyze_calls = sparse_direct.analyze_call_count() - analyze_before
     t_setup = time.perf_counter() - t0 - report.t_decompose
 
