@@ -11,8 +11,10 @@ partition + right-hand side built here:
 Seeded load vectors use numpy default_rng(0).standard_normal(N_t*M_x) in
 reference order (reference idiom, tests/test_solvers.py:97-98). j_max is the
 reference default 2e6 (temporal.py:40) unless overridden (tests use less).
-Config 5 (P2 in space and time) has no reference discretization and is not
-built here (out of scope for round 1).
+* c5: unit square 128x128 with P2 in space (M_x=65,025), P2 in time on 512
+  cells graded toward t=0 (t_i = (i/512)^2, 1024 temporal dofs), rhs ~ N(0,1)
+  seed 0. The reference has no P2 discretization: `p2.py` builds it and pins
+  it to the reference's P1 assembly through the exact P1-in-P2 embedding.
 """
 
 import numpy as np
@@ -25,6 +27,7 @@ CONFIGS = {
     "c2": dict(mesh=("lshape", 5), n_t=128, rhs="sin_sin_t2"),
     "c3": dict(mesh=("square", 256), n_t=256, rhs="seeded"),
     "c4": dict(mesh=("square", 512), n_t=1024, rhs="sin_sin2_sint"),
+    "c5": dict(mesh=("square", 128), n_t=512, rhs="seeded", degree=2, grading=2.0),
 }
 
 
@@ -37,17 +40,34 @@ def spatial_mesh(kind, size):
 
 
 def build_system(name=None, *, mesh=None, n_t=None, rhs="seeded", j_max=temporal.DEFAULT_J_MAX,
-                 temporal_device=None, seed=0, nodes=None):
-    """Returns (SpaceTimeSystem, info dict)."""
+                 temporal_device=None, seed=0, nodes=None, degree=1, grading=1.0):
+    """Returns (SpaceTimeSystem, info dict).
+
+    ``n_t`` is the number of temporal cells; with ``degree=2`` (P2 in space
+    and time, `p2.py`) the system has 2 n_t temporal dofs. ``grading`` g
+    places the nodes at t_i = (i / n_t)^g unless ``nodes`` is given.
+    """
     if name is not None:
         cfg = CONFIGS[name]
         mesh, n_t, rhs = cfg["mesh"], cfg["n_t"], cfg["rhs"]
+        degree, grading = cfg.get("degree", 1), cfg.get("grading", 1.0)
     mesh_x = spatial_mesh(*mesh)
-    ops = fem.assemble_p1(mesh_x)
     if nodes is None:
-        nodes = np.linspace(0.0, 1.0, n_t + 1)
+        nodes = (np.arange(n_t + 1) / n_t) ** grading if grading != 1.0 else np.linspace(0.0, 1.0, n_t + 1)
     mesh_t = temporal.TemporalMesh(nodes)
-    temp = temporal.assemble_temporal_operators(mesh_t, j_max=j_max, device=temporal_device)
+    if degree == 1:
+        ops = fem.assemble_p1(mesh_x)
+        temp = temporal.assemble_temporal_operators(mesh_t, j_max=j_max, device=temporal_device)
+    elif degree == 2:
+        from . import p2
+
+        if rhs != "seeded":
+            raise ValueError("P2 systems take a seeded load vector")
+        ops = p2.assemble_p2(mesh_x)
+        temp = p2.assemble_temporal_operators_p2(mesh_t, j_max=j_max, device=temporal_device)
+    else:
+        raise ValueError(f"degree must be 1 or 2, got {degree}")
+    n_t = temp.A.shape[0]
     m_x = ops.n_interior
     if rhs == "seeded":
         f = np.random.default_rng(seed).standard_normal(n_t * m_x)
@@ -67,5 +87,5 @@ def build_system(name=None, *, mesh=None, n_t=None, rhs="seeded", j_max=temporal
         raise ValueError(f"unknown rhs kind {rhs!r}")
     system = SpaceTimeSystem(temporal=temp, spatial=ops, rhs=np.ascontiguousarray(f))
     info = {"m_x": m_x, "n_t": n_t, "dof": m_x * n_t, "mesh": f"{mesh[0]}-{mesh[1]}", "rhs": rhs,
-            "j_max": j_max}
+            "j_max": j_max, "degree": degree, "grading": grading}
     return system, info
