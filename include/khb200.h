@@ -17,6 +17,8 @@
  *   kh_dgemm_rowscatter ....... multi-GPU back transform fused with the scatter of its
  *   kh_sum_parts                reduce-scatter (solvers.py:397-400 per rank)
  *   kh_ipc_handle/open/close .. peer-memory mapping of the receive slots (one process per GPU)
+ *   kh_ht_assemble ............ temporal H_T matrices A_t, M_t, C_t     temporal.py:98-151, :300-329
+ *   kh_ht_workspace_bytes       (P1 hats as the reference; P2 Lagrange basis for config c5)
  *
  * Conventions: plain pointers and 64-bit sizes, column-major matrices,
  * caller-owned buffers. Pointers documented "device" must be CUDA device
@@ -157,6 +159,16 @@ int kh_sum_parts(int32_t parts, const double* slots, int64_t part_elems, double*
 int kh_ipc_handle(const void* dev_ptr, void* handle);
 int kh_ipc_open(const void* handle, void** dev_ptr);
 int kh_ipc_close(void* dev_ptr);
+/* Temporal H_T matrices (reference temporal.py:300-329) of the P1 (degree 1)
+ * or P2 (degree 2) basis on the partition `nodes` (device, n_cells + 1
+ * doubles, nodes[0] = 0, T = nodes[n_cells]), truncated at j_max. Outputs
+ * (device, column-major, overwritten): A and M (nr x nr), C (nr x n_cells),
+ * nr = degree * n_cells; A is the full product (the caller mirrors its lower
+ * triangle like the reference's dsyrk). `workspace`: device, at least
+ * kh_ht_workspace_bytes(). */
+int kh_ht_workspace_bytes(int32_t degree, int64_t n_cells, int64_t* bytes);
+int kh_ht_assemble(int32_t degree, int64_t n_cells, const double* nodes, int64_t j_max, double* A, double* M,
+                   double* C, void* workspace, int64_t workspace_bytes, void* stream);
 int kh_set_device(int device);
 int kh_stream_sync(void* stream);
 

@@ -85,6 +85,8 @@ SIGNATURES = {
     "kh_ipc_handle": (ctypes.c_int, [_vp, _vp]),
     "kh_ipc_open": (ctypes.c_int, [_vp, _P(_vp)]),
     "kh_ipc_close": (ctypes.c_int, [_vp]),
+    "kh_ht_workspace_bytes": (ctypes.c_int, [_i32, _i64, _P(_i64)]),
+    "kh_ht_assemble": (ctypes.c_int, [_i32, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "kh_set_device": (ctypes.c_int, [ctypes.c_int]),
     "kh_stream_sync": (ctypes.c_int, [_vp]),
 }

@@ -755,6 +755,32 @@ int kh_sum_parts(int32_t parts, const double* slots, int64_t part_elems, double*
   return KH_OK;
 }
 
+int kh_ht_workspace_bytes(int32_t degree, int64_t n_cells, int64_t* bytes) {
+  if ((degree != 1 && degree != 2) || n_cells < 1 || degree * n_cells > (1 << 20))
+    return fail(KH_ERR_DIMENSION, "H_T assembly: degree must be 1 or 2 and n_cells >= 1");
+  if (!bytes) return fail(KH_ERR_INVALID, "null argument");
+  const int nr = (int)(degree * n_cells);
+  *bytes = (int64_t)sizeof(double) * kh_ht::workspace_doubles(nr, (int)n_cells, kh_ht::chunk(nr));
+  return KH_OK;
+}
+
+int kh_ht_assemble(int32_t degree, int64_t n_cells, const double* nodes, int64_t j_max, double* A, double* M,
+                   double* C, void* workspace, int64_t workspace_bytes, void* stream) {
+  int64_t need = 0;
+  int st = kh_ht_workspace_bytes(degree, n_cells, &need);
+  if (st != KH_OK) return st;
+  if (j_max < 0) return fail(KH_ERR_DIMENSION, "j_max must be >= 0");
+  if (!nodes || !A || !M || !C || !workspace) return fail(KH_ERR_INVALID, "null argument");
+  if (workspace_bytes < need) return fail(KH_ERR_DIMENSION, "H_T workspace too small");
+  double T = 0.0;
+  KH_CUDA(cudaMemcpy(&T, nodes + n_cells, sizeof(double), cudaMemcpyDeviceToHost));
+  if (!(T > 0.0)) return fail(KH_ERR_INVALID, "nodes must end at T > 0");
+  const int nr = (int)(degree * n_cells);
+  KH_CUDA(kh_ht::assemble(degree, (int)n_cells, nodes, T, j_max, kh_ht::chunk(nr), A, M, C,
+                          static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
 int kh_ipc_handle(const void* dev_ptr, void* handle) {
   if (!dev_ptr || !handle) return fail(KH_ERR_INVALID, "null argument");
   cudaIpcMemHandle_t h;

@@ -27,8 +27,13 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_
                                                     const double* __restrict__ A, int64_t lda,
                                                     const double* __restrict__ B, int64_t ldb,
                                                     double beta, double* __restrict__ C, int64_t ldc,
-                                                    double* const* __restrict__ dst, int64_t rp, int64_t ldd) {
+                                                    double* const* __restrict__ dst, int64_t rp, int64_t ldd,
+                                                    int64_t sA, int64_t sB, int64_t sC) {
   extern __shared__ __align__(16) double smem[];
+  // batched (strided) GEMMs: blockIdx.z selects the problem
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  if (!SCATTER) C += blockIdx.z * sC;
   double* As = smem;
   double* Bs = smem + NST * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -125,8 +130,8 @@ namespace {
 template <bool SCATTER>
 cudaError_t launch(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double beta, double* C, int64_t ldc, double* const* dst, int64_t rp, int64_t ldd,
-                   cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
+                   cudaStream_t stream, int32_t batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
+  if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -134,9 +139,9 @@ cudaError_t launch(int64_t M, int64_t N, int64_t K, double alpha, const double* 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
   dgemm_kernel<SCATTER><<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, dst, rp,
-                                                           ldd);
+                                                           ldd, sA, sB, sC);
   kh_note_launch();
   return cudaGetLastError();
 }
@@ -156,6 +161,12 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
                             const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                             cudaStream_t stream) {
   return launch<false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nullptr, 1, 0, stream);
+}
+
+cudaError_t kh_launch_dgemm_batched(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                                    int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C,
+                                    int64_t ldc, int64_t sC, int32_t batch, cudaStream_t stream) {
+  return launch<false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, nullptr, 1, 0, stream, batch, sA, sB, sC);
 }
 
 cudaError_t kh_launch_dgemm_rowscatter(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,

@@ -54,6 +54,9 @@ cudaError_t kh_launch_dgemm(int64_t M, int64_t N, int64_t K, double alpha, const
 
 // C = A B with row r written to dst[r / rp] (row r % rp, ld ldd): fused GEMM +
 // scatter into peer receive slots; and the ordered sum of g slots.
+cudaError_t kh_launch_dgemm_batched(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                                    int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C,
+                                    int64_t ldc, int64_t sC, int32_t batch, cudaStream_t stream);
 cudaError_t kh_launch_dgemm_rowscatter(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                                        const double* B, int64_t ldb, double* const* dst, int64_t rp, int64_t ldd,
                                        cudaStream_t stream);
@@ -114,3 +117,12 @@ cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const doub
 
 // Counts every kernel launch made by the library (kh_launch_count in the ABI).
 void kh_note_launch();
+
+// Temporal H_T assembly (temporal.cu).
+namespace kh_ht {
+int splits(int nr);
+int chunk(int nr);
+int64_t workspace_doubles(int nr, int n_cells, int jc);
+cudaError_t assemble(int degree, int n_cells, const double* d_nodes, double T, int64_t j_max, int jc, double* A,
+                     double* M, double* C, double* ws, cudaStream_t st);
+}  // namespace kh_ht

@@ -40,7 +40,7 @@ import scipy.sparse as sp
 
 from .errors import DegenerateElement
 from .fem import SpatialOperators, triangle_rule
-from .temporal import _CHUNK, DEFAULT_J_MAX, TemporalOperators
+from .temporal import _CHUNK, DEFAULT_J_MAX, TemporalOperators, _is_cuda, assemble_native
 
 # ---------------------------------------------------------------------------
 # space
@@ -189,9 +189,13 @@ def _p2_coeffs(xp, nd, theta, T, sign):
 
 def assemble_temporal_operators_p2(mesh, j_max=DEFAULT_J_MAX, device=None):
     """A_t, M_t (2N x 2N) and C_t (2N x N) of the P2 temporal space, same
-    truncated series and chunk order as the P1 assembly (temporal.py)."""
+    truncated series and chunk order as the P1 assembly (temporal.py); on a
+    CUDA device through the hand-written kernels (csrc/temporal.cu)."""
     if j_max < 0:
         raise ValueError("j_max must be >= 0")
+    if _is_cuda(device):
+        A, M, C = assemble_native(mesh.nodes, 2, j_max, device)
+        return TemporalOperators(A=A, M=M, C=C, j_max=int(j_max))
     nodes = np.asarray(mesh.nodes, dtype=float)
     T = float(nodes[-1])
     n = len(nodes) - 1

@@ -16,6 +16,7 @@ host route costs minutes. Either way this runs once
 per problem, outside the timed solve.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -83,9 +84,48 @@ def _slope_bracket(xp, vals, h):
     return out
 
 
+def _is_cuda(device):
+    return device is not None and str(device).startswith("cuda")
+
+
+def assemble_native(nodes, degree, j_max, device):
+    """A, M, C from the hand-written CUDA assembly (csrc/temporal.cu,
+    kh_ht_assemble) on a CUDA `device`; returned as host arrays with A's lower
+    triangle mirrored like the reference's dsyrk (temporal.py:325-328)."""
+    import torch
+
+    from . import _native
+
+    _native.load()
+    dev = torch.device(device)
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    n_cells = len(nodes) - 1
+    nr = degree * n_cells
+    need = ctypes.c_int64()
+    _native.call("kh_ht_workspace_bytes", int(degree), int(n_cells), ctypes.byref(need))
+    with torch.cuda.device(dev):
+        d_nodes = torch.from_numpy(nodes).to(dev)
+        A = torch.empty((nr, nr), dtype=torch.float64, device=dev)      # column-major storage
+        M = torch.empty_like(A)
+        C = torch.empty((n_cells, nr), dtype=torch.float64, device=dev)
+        ws = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
+        _native.call("kh_ht_assemble", int(degree), int(n_cells), d_nodes.data_ptr(), int(j_max), A.data_ptr(),
+                     M.data_ptr(), C.data_ptr(), ws.data_ptr(), int(need.value), _native.stream_handle())
+        A, M, C = (x.T.cpu().numpy() for x in (A, M, C))
+    low = np.tril(A)
+    return np.ascontiguousarray(low + np.tril(low, -1).T), np.ascontiguousarray(M), np.ascontiguousarray(C)
+
+
 def assemble_temporal_operators(mesh, j_max=DEFAULT_J_MAX, device=None):
+    """P1 temporal H_T matrices. ``device`` None: numpy/BLAS on the host (the
+    reference's route); a CUDA device: the hand-written kernels of
+    csrc/temporal.cu; another torch device (e.g. "cpu"): the same series in
+    torch ops (kept to cross-check the chunk arithmetic)."""
     if j_max < 0:
         raise ValueError("j_max must be >= 0")
+    if _is_cuda(device):
+        A, M, C = assemble_native(mesh.nodes, 1, j_max, device)
+        return TemporalOperators(A=A, M=M, C=C, j_max=int(j_max))
     nodes = np.asarray(mesh.nodes, dtype=float)
     T = float(nodes[-1])
     n = len(nodes) - 1
