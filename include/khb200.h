@@ -11,6 +11,8 @@
  *                               batched over the shifts of the loop at solvers.py:383-393
  *   kh_plan_pivot_check ....... pivot guard |U_ii| >= 1e-13 max|a|      sparse_direct.py:182-187
  *   kh_plan_solve ............. sparse_direct.solve (SuperLU zgstrs)    sparse_direct.py:191-209
+ *   kh_plan_factor_solve ...... factorize + solve of one shift batch with the forward sweep fused
+ *                               into the factorization (the first FD application, solvers.py:383-393)
  *   kh_dgemm .................. modal transforms (zgemm)                solvers.py:368-372, :397-400
  *   kh_plan_residual .......... residual / kron_apply_right             solvers.py:428-440, dense.py:264-286
  *   kh_sumsq .................. norms of _discard_imaginary              solvers.py:406-413
@@ -125,6 +127,19 @@ int kh_plan_pivot_check(kh_plan* plan, int64_t slot0, int64_t nshift, double rel
  * (real rhs / discard imaginary part). nshift <= max_batch. */
 int kh_plan_solve(kh_plan* plan, int64_t slot0, int64_t nshift, const double* b_re, const double* b_im,
                   int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream);
+/* kh_plan_factor + kh_plan_solve in one pass: the forward sweep runs inside
+ * the factorization kernels (the rhs is assembled as a border row of every
+ * front), so the factors are read back only once, by the backward sweep.
+ * Same arguments and results as the two calls (rounding aside). */
+int kh_plan_factor_solve(kh_plan* plan, int64_t slot0, int64_t nshift, const double* lambda_ri, const double* b_re,
+                         const double* b_im, int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream);
+/* The two halves of kh_plan_factor_solve: factorization + forward sweep
+ * (the result stays in the plan's solve work space), then the backward sweep
+ * of the same batch; nothing else may use the plan in between. */
+int kh_plan_factor_fwd(kh_plan* plan, int64_t slot0, int64_t nshift, const double* lambda_ri, const double* b_re,
+                       const double* b_im, int64_t ldb, void* stream);
+int kh_plan_solve_bwd(kh_plan* plan, int64_t slot0, int64_t nshift, double* x_re, double* x_im, int64_t ldx,
+                      void* stream);
 /* R = F - (M Y[:, :nt] + A Y[:, nt:2nt]) on the plan's CSR (device arrays);
  * R may be NULL. norms2 (device, 2 doubles) receives ||R||_F^2, ||F||_F^2. */
 int kh_plan_residual(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,

@@ -73,6 +73,9 @@ SIGNATURES = {
     "kh_plan_factor": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "kh_plan_pivot_check": (ctypes.c_int, [_vp, _i64, _i64, _dbl, _vp, _P(_i64), _P(_dbl)]),
     "kh_plan_solve": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp]),
+    "kh_plan_factor_solve": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp]),
+    "kh_plan_factor_fwd": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
+    "kh_plan_solve_bwd": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp]),
     "kh_plan_residual": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "kh_plan_free": (None, [_vp]),
     "kh_dgemm": (ctypes.c_int, [_i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp]),

@@ -89,6 +89,7 @@ struct kh_plan {
   // with the large-front kernels on the caller's stream; levels are joined
   cudaStream_t side[kSmallClasses] = {};
   cudaEvent_t ev_main = nullptr, ev_side[kSmallClasses] = {};
+  cudaEvent_t ev_fwd = nullptr;  // large fronts' panels final (fused forward sweep may start)
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -136,6 +137,8 @@ void plan_release(kh_plan* p) {
   p->owned = nullptr;
   if (p->ev_main) cudaEventDestroy(p->ev_main);
   p->ev_main = nullptr;
+  if (p->ev_fwd) cudaEventDestroy(p->ev_fwd);
+  p->ev_fwd = nullptr;
   for (int c = 0; c < kSmallClasses; ++c) {
     if (p->ev_side[c]) cudaEventDestroy(p->ev_side[c]);
     if (p->side[c]) cudaStreamDestroy(p->side[c]);
@@ -553,6 +556,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_side[c], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_main, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fwd, cudaEventDisableTiming);
   if (e == cudaSuccess) {
     carve(p, S, X, C);
     auto up = [&](void* dst, const void* src, size_t bytes) {
@@ -598,13 +602,12 @@ int kh_plan_set_values(kh_plan* p, const double* m_vals, const double* a_vals) {
   return KH_OK;
 }
 
-int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, void* stream) {
-  if (!p || (nshift > 0 && !lambda_ri)) return fail(KH_ERR_INVALID, "null argument");
-  if (nshift < 0 || nshift > p->max_batch || slot0 < 0 || slot0 + nshift > p->slots)
-    return fail(KH_ERR_INVALID, "shift batch outside the plan's slots");
-  if (nshift == 0) return KH_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KH_CUDA(cudaSetDevice(p->device));
+namespace {
+
+// Factor the batch; with `fwd`, also the forward sweep of the solve for the
+// rhs already gathered into p->y (fused into the small-front kernels, the
+// large fronts' forward kernels launched right after their level).
+int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, cudaStream_t st, bool fwd) {
   KH_CUDA(cudaMemcpyAsync(p->lam, lambda_ri, nshift * 16, cudaMemcpyHostToDevice, st));
   const KhTree T = p->tree();
   double2* panels = p->panels + slot0 * p->panel_total;
@@ -615,9 +618,10 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
     double2 *uc = p->upd[d & 1], *uch = p->upd[(d + 1) & 1];
     const int64_t sc = p->upd_size[d & 1], sch = p->upd_size[(d + 1) & 1];
     const int32_t ns = (int32_t)nshift;
+    const KhFwd fw{p->y, p->rupd[d & 1], p->rupd_size[d & 1], p->rupd[(d + 1) & 1], p->rupd_size[(d + 1) & 1]};
     for (int c = 0; c < kSmallClasses; ++c)
       KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                     uch, sch, p->minpiv_work, p->side[c]));
+                                     uch, sch, p->minpiv_work, p->side[c], fwd ? &fw : nullptr));
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
@@ -626,6 +630,14 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
       if (kb > 0) KH_CUDA(kh_launch_big_lupdate(T, p->btasks + K.lupd_off, K.lupd_n, kb, ns, panels, st));
       KH_CUDA(kh_launch_big_diag(T, p->btasks + K.diag_off, K.diag_n, kb, ns, panels, p->minpiv_work, st));
       KH_CUDA(kh_launch_big_trsm(T, p->btasks + K.trsm_off, K.trsm_n, kb, ns, panels, st));
+    }
+    if (fwd) {  // the level's large fronts: panels are final after their trsm;
+                // their forward sweep runs on a side stream beside the Schur kernel
+      KH_CUDA(cudaEventRecord(p->ev_fwd, st));
+      KH_CUDA(cudaStreamWaitEvent(p->side[0], p->ev_fwd, 0));
+      KH_CUDA(kh_launch_fwd_level(T, lev + co[kSmallClasses], co[kSmallClasses + 1] - co[kSmallClasses], ns,
+                                  p->max_m, panels, p->y, fw.ru_cur, fw.ru_stride_cur, fw.ru_child,
+                                  fw.ru_stride_child, p->side[0]));
     }
     KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
                             sc, uch, sch, st));
@@ -636,6 +648,71 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
                                      kAbsmaxBlocks, st));
   KH_CUDA(kh_launch_rowreduce(p->absmax_work, kAbsmaxBlocks, (int32_t)nshift, 2, p->absmax + slot0, st));
   return KH_OK;
+}
+
+int check_batch(kh_plan* p, int64_t slot0, int64_t nshift) {
+  if (nshift < 0 || nshift > p->max_batch || slot0 < 0 || slot0 + nshift > p->slots)
+    return fail(KH_ERR_INVALID, "shift batch outside the plan's slots");
+  return KH_OK;
+}
+
+// backward sweep from p->y (forward-solved) and the scatter to x
+int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* x_im, int64_t ldx, cudaStream_t st) {
+  const KhTree T = p->tree();
+  const double2* panels = p->panels + slot0 * p->panel_total;
+  constexpr int L = kSolveSmallClasses;
+  KH_CUDA(fork_side(p, st));
+  for (int32_t d = 0; d <= p->depth; ++d) {
+    const int32_t* lev = p->level_fronts + p->level_off[d];
+    const int32_t* co = p->classes(d);
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side[0]));
+    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
+                                p->y, st));
+    KH_CUDA(join_side(p, st));
+  }
+  KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
+  return KH_OK;
+}
+
+}  // namespace
+
+int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, void* stream) {
+  if (!p || (nshift > 0 && !lambda_ri)) return fail(KH_ERR_INVALID, "null argument");
+  if (check_batch(p, slot0, nshift) != KH_OK) return KH_ERR_INVALID;
+  if (nshift == 0) return KH_OK;
+  KH_CUDA(cudaSetDevice(p->device));
+  return factor_impl(p, slot0, nshift, lambda_ri, static_cast<cudaStream_t>(stream), false);
+}
+
+int kh_plan_factor_fwd(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, const double* b_re,
+                       const double* b_im, int64_t ldb, void* stream) {
+  if (!p || (nshift > 0 && (!lambda_ri || !b_re))) return fail(KH_ERR_INVALID, "null argument");
+  if (check_batch(p, slot0, nshift) != KH_OK) return KH_ERR_INVALID;
+  if (ldb < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  if (nshift == 0 || p->n == 0) return KH_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KH_CUDA(cudaSetDevice(p->device));
+  KH_CUDA(kh_launch_gather_rhs(p->n, (int32_t)nshift, p->perm, b_re, b_im, ldb, p->y, st));
+  return factor_impl(p, slot0, nshift, lambda_ri, st, true);
+}
+
+int kh_plan_solve_bwd(kh_plan* p, int64_t slot0, int64_t nshift, double* x_re, double* x_im, int64_t ldx,
+                      void* stream) {
+  if (!p || (nshift > 0 && !x_re)) return fail(KH_ERR_INVALID, "null argument");
+  if (check_batch(p, slot0, nshift) != KH_OK) return KH_ERR_INVALID;
+  if (ldx < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  if (nshift == 0 || p->n == 0) return KH_OK;
+  KH_CUDA(cudaSetDevice(p->device));
+  return solve_bwd_impl(p, slot0, (int32_t)nshift, x_re, x_im, ldx, static_cast<cudaStream_t>(stream));
+}
+
+int kh_plan_factor_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, const double* b_re,
+                         const double* b_im, int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream) {
+  if (!p || (nshift > 0 && (!lambda_ri || !b_re || !x_re))) return fail(KH_ERR_INVALID, "null argument");
+  if (ldx < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  const int rc = kh_plan_factor_fwd(p, slot0, nshift, lambda_ri, b_re, b_im, ldb, stream);
+  if (rc != KH_OK) return rc;
+  return kh_plan_solve_bwd(p, slot0, nshift, x_re, x_im, ldx, stream);
 }
 
 int kh_plan_pivot_check(kh_plan* p, int64_t slot0, int64_t nshift, double rel_threshold, void* stream,
@@ -695,16 +772,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
                                 rch, sch, st));
     KH_CUDA(join_side(p, st));
   }
-  for (int32_t d = 0; d <= p->depth; ++d) {
-    const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->classes(d);
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side[0]));
-    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
-                                p->y, st));
-    KH_CUDA(join_side(p, st));
-  }
-  KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
-  return KH_OK;
+  return solve_bwd_impl(p, slot0, ns, x_re, x_im, ldx, st);
 }
 
 int kh_plan_residual(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf, double* R,

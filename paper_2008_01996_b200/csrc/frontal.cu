@@ -759,7 +759,7 @@ KH_HD constexpr int packed_elems(int m) { return kh_packed_elems(m); }
 // classes whose residency is bounded by shared memory drop the W buffer
 KH_HD constexpr bool front_has_w(int ms) { return ms != 48; }
 KH_HD constexpr int front_smem_bytes(int ms) {
-  return 16 * (packed_elems(ms) + (front_has_w(ms) ? 8 * (ms + 2) : 0) + 8 + ms) + 4 * ms + 4 * 4 * ms;
+  return 16 * (packed_elems(ms) + (front_has_w(ms) ? 8 * (ms + 2) : 0) + 8 + 2 * ms) + 4 * ms + 4 * 4 * ms;
 }
 
 #ifndef KH_F32_MINB
@@ -771,22 +771,38 @@ KH_HD constexpr int front_min_blocks(int ms, int nw) {
 }
 
 struct KidInfo {
-  int64_t upd_off, rows_begin;
+  int64_t upd_off, rows_begin, rupd_off;
   int32_t q, pad;
 };
 
-template <int MS, int NW>
+// FWD: fused forward solve. The front's right-hand side (y of the pivot
+// rows + the children's rhs updates, pushed in child order during the
+// assembly) is kept in shared memory; after the LDL^T, warp 0 runs the
+// forward sweep x_r -= L[r][k] x_k on the shared-memory panel (lanes own rows,
+// pivots broadcast by shuffles; same operation order as fwd_small_kernel)
+// while the other warps write the panel and the update block out. y and the
+// parent's rhs update are then written like fwd_small_kernel would.
+struct FwdArgs {
+  double2* y;
+  double2* ru_cur;
+  int64_t ru_stride_cur;
+  const double2* ru_child;
+  int64_t ru_stride_child;
+};
+
+template <int MS, int NW, bool FWD>
 __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_front_kernel(
     KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
     double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
-    double* minpiv) {
+    double* minpiv, FwdArgs fw) {
   constexpr int NTH = 32 * NW, LDW = MS + 2, RK = 4;  // RK: children whose relind maps are staged
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* S = reinterpret_cast<double2*>(smem_raw);  // packed lower triangle
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // packed lower triangle (m + 1 rows)
   double2* W = S + packed_elems(MS);                  // W[k*LDW + r] = L[r][kb+k] d_{kb+k}
   double2* dinv = W + (front_has_w(MS) ? 8 * LDW : 0);  // 1/d of the current block
   double2* dg = dinv + 8;                              // pivots d_k
-  int32_t* cb = reinterpret_cast<int32_t*>(dg + MS);   // column bases
+  double2* xs = dg + MS;                               // front rhs / forward-solved x (FWD)
+  int32_t* cb = reinterpret_cast<int32_t*>(xs + MS);   // column bases
   int32_t* rel = cb + MS;                              // rel[k*MS + i]
   __shared__ int ctr;
   const int tid = threadIdx.x;
@@ -820,11 +836,23 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   // order, so the sums are deterministic)
   if (tid < RK && tid < nkids) {
     const KhDevFront C = T.fronts[T.child_list[F.child_begin + tid]];
-    kinfo[tid] = {C.upd_off, C.rows_begin, C.q, 0};
+    kinfo[tid] = {C.upd_off, C.rows_begin, C.rupd_off, C.q, 0};
   }
   const int ne = packed_elems(m);
   for (int idx = tid; idx < ne; idx += NTH) S[idx] = make_double2(0.0, 0.0);
   for (int c = tid; c < m; c += NTH) cb[c] = kh_packed_col_base(m, c);
+  // FWD: the pivot rows' rhs, loaded now and stored to xs after the assembly
+  // (the loads are in flight during it)
+  constexpr int RY = (MS + NTH - 1) / NTH;
+  double2 yreg[FWD ? RY : 1];
+  if (FWD) {
+    const double2* yb = fw.y + (int64_t)b * T.n + F.first;
+#pragma unroll
+    for (int u = 0; u < RY; ++u) {
+      const int c = tid + u * NTH;
+      yreg[u] = c < p ? yb[c] : make_double2(0.0, 0.0);
+    }
+  }
   __syncthreads();
   phase(0);
   // warm L2 with the children's update blocks (read after the originals)
@@ -848,17 +876,37 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   constexpr int R = (MS + 31) / 32;  // row passes per column
   for (int k = 0; k < nkids; ++k) {
     __syncthreads();
-    int64_t upd_off, rows_begin;
+    if (FWD && k == 0) {
+#pragma unroll
+      for (int u = 0; u < RY; ++u) {
+        const int c = tid + u * NTH;
+        if (c < m) xs[c] = yreg[u];
+      }
+      __syncthreads();
+    }
+    int64_t upd_off, rows_begin, roff = 0;
     int qk;
     if (k < RK) {
       upd_off = kinfo[k].upd_off;
       rows_begin = kinfo[k].rows_begin;
       qk = kinfo[k].q;
+      roff = kinfo[k].rupd_off;
     } else {
       const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
       upd_off = C.upd_off;
       rows_begin = C.rows_begin;
       qk = C.q;
+      roff = C.rupd_off;
+    }
+    // FWD: the child's rhs update, loaded ahead of its update block
+    double2 rreg[FWD ? RY : 1];
+    if (FWD) {
+      const double2* rc = fw.ru_child + (int64_t)b * fw.ru_stride_child + roff;
+#pragma unroll
+      for (int u = 0; u < RY; ++u) {
+        const int i = tid + u * NTH;
+        rreg[u] = i < qk ? rc[i] : make_double2(0.0, 0.0);
+      }
     }
     const double2* Uc = upd_child + (int64_t)b * upd_stride_child + upd_off;
     const int32_t* rk = k < RK ? rel + k * MS : T.relind + rows_begin;
@@ -884,12 +932,55 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
         for (int u = 0; u < R; ++u)
           if (dst[h][u] >= 0) S[dst[h][u]] = cadd(S[dst[h][u]], v[h][u]);
     }
+    if (FWD) {  // the child's rhs update (rows distinct within a child)
+#pragma unroll
+      for (int u = 0; u < RY; ++u) {
+        const int i = tid + u * NTH;
+        if (i < qk) xs[rk[i]] = cadd(xs[rk[i]], rreg[u]);
+      }
+    }
+  }
+  if (FWD && nkids == 0) {
+#pragma unroll
+    for (int u = 0; u < RY; ++u) {
+      const int c = tid + u * NTH;
+      if (c < m) xs[c] = yreg[u];
+    }
   }
   __syncthreads();
   phase(1);
 
   const double minp = blocked_ldlt<NW, kLookAhead(NW), MS / 16, front_has_w(MS)>(S, cb, W, LDW, dinv, dg, &ctr, m, p);
   phase(2);
+  if (FWD && warp == 0) {
+    // forward sweep on the shared-memory panel: lane owns rows lane + 32 v
+    double2 x[R];
+#pragma unroll
+    for (int v = 0; v < R; ++v) {
+      const int r = lane + 32 * v;
+      x[v] = r < m ? xs[r] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      if (32 * u >= p) break;
+      const int kend = min(32, p - 32 * u);
+      for (int kk = 0; kk < kend; ++kk) {
+        const int k = 32 * u + kk;
+        const double2 xk = shfl2(x[u], kk);
+        const int ck = cb[k];
+#pragma unroll
+        for (int v = 0; v < R; ++v) {
+          const int r = lane + 32 * v;
+          if (r > k && r < m) x[v] = cfms(x[v], S[ck + r], xk);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < R; ++v) {
+      const int r = lane + 32 * v;
+      if (r < m) xs[r] = x[v];
+    }
+  }
   // ---- write the panel and the update matrix (lower parts), coalesced:
   // warp per column, lanes down the rows
   for (int c = warp; c < p; c += NW) {
@@ -899,6 +990,15 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   for (int c = warp; c < q; c += NW) {
     const int base = cb[p + c] + p;
     for (int r = c + lane; r < q; r += 32) U[r + (int64_t)c * q] = S[base + r];
+  }
+  if (FWD) {
+    __syncthreads();
+    double2* yb = fw.y + (int64_t)b * T.n + F.first;
+    double2* ru = fw.ru_cur + (int64_t)b * fw.ru_stride_cur + F.rupd_off;
+    for (int c = tid; c < m; c += NTH) {
+      if (c < p) yb[c] = xs[c];
+      else ru[c - p] = xs[c];
+    }
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
   phase(3);
@@ -1187,6 +1287,11 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
   // lane a holds xu[a] and xu[a + 32]
   const double2 xu0 = lane < q ? yb[urows[lane]] : z;
   const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : z;
+  // independent of the column sums: issue the rhs and pivot loads up front
+  const int k0 = lane, k1 = lane + 32;
+  const double2 y0 = k0 < p ? yy[k0] : z, y1 = k1 < p ? yy[k1] : z;
+  const double2 d0 = k0 < p ? P[k0 + (int64_t)k0 * m] : make_double2(1.0, 0.0);
+  const double2 d1 = k1 < p ? P[k1 + (int64_t)k1 * m] : make_double2(1.0, 0.0);
   // t_k = y_k / d_k - sum_a L21[a, k] xu[a]: lane a reads rows p+a of column k
   // (coalesced); the column sums are warp reductions, SOLVE_CH columns at a
   // time so their shuffle trees overlap; lane k & 31 keeps the result
@@ -1217,14 +1322,29 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
       }
     }
   }
-  const int k0 = lane, k1 = lane + 32;
-  if (k0 < p) t0 = csub(cmul(yy[k0], cinv(P[k0 + (int64_t)k0 * m])), t0);
-  if (k1 < p) t1 = csub(cmul(yy[k1], cinv(P[k1 + (int64_t)k1 * m])), t1);
-  // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for j < i
-  for (int i = p - 1; i > 0; --i) {
-    const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
-    if (k0 < i) t0 = cfms(t0, P[i + (int64_t)k0 * m], xi);
-    if (k1 < i) t1 = cfms(t1, P[i + (int64_t)k1 * m], xi);
+  if (k0 < p) t0 = csub(cmul(y0, cinv(d0)), t0);
+  if (k1 < p) t1 = csub(cmul(y1, cinv(d1)), t1);
+  // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for
+  // j < i; the L11 rows of a chunk of SOLVE_CH steps are loaded into
+  // registers first (independent of x), so the serial chain waits on one
+  // load round trip per chunk instead of one per pivot
+  for (int i1 = p - 1; i1 > 0; i1 -= SOLVE_CH) {
+    double2 l0[SOLVE_CH], l1[SOLVE_CH];
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int i = i1 - u;
+      l0[u] = (i > 0 && k0 < i) ? P[i + (int64_t)k0 * m] : z;
+      l1[u] = (i > 0 && k1 < i) ? P[i + (int64_t)k1 * m] : z;
+    }
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int i = i1 - u;
+      if (i > 0) {
+        const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
+        if (k0 < i) t0 = cfms(t0, l0[u], xi);
+        if (k1 < i) t1 = cfms(t1, l1[u], xi);
+      }
+    }
   }
   if (k0 < p) yy[k0] = t0;
   if (k1 < p) yy[k1] = t1;
@@ -1330,12 +1450,16 @@ __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* 
   double2* yb = y + (int64_t)b * T.n;
   double2* yy = yb + F.first;
   const int64_t* urows = T.urows + F.rows_begin;
+  // x of the update rows (final: ancestors are done), gathered once
+  double2* xu = st + p;
+  for (int a = tid; a < q; a += NT) xu[a] = yb[urows[a]];
+  __syncthreads();
   // t_k = y_k / d_k - sum_a L21[a, k] x[urows[a]]   (warp per column k)
   for (int k = warp; k < p; k += NT / 32) {
     double2 s = make_double2(0.0, 0.0);
     const double2* col = P + p + (int64_t)k * m;
 #pragma unroll 4
-    for (int a = lane; a < q; a += 32) s = cadd(s, cmul(col[a], yb[urows[a]]));
+    for (int a = lane; a < q; a += 32) s = cadd(s, cmul(col[a], xu[a]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
@@ -1549,7 +1673,7 @@ cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, in
                                 cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtasBwd;
-  const size_t smem = sizeof(double2) * (size_t)(narrow ? max_m : max_p);
+  const size_t smem = sizeof(double2) * (size_t)max_m;
   static size_t attr = 0, attr_top = 0;
   size_t& a = narrow ? attr_top : attr;
   if (smem > 48 * 1024 && smem > a) {
@@ -1610,9 +1734,11 @@ cudaError_t kh_launch_rowreduce(const double* in, int64_t len, int32_t rows, int
 cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                    const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
-                                   cudaStream_t stream) {
+                                   cudaStream_t stream, const KhFwd* fwd) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   const dim3 grid(nlev, batch);
+  FwdArgs fw{};
+  if (fwd) fw = {fwd->y, fwd->ru_cur, fwd->ru_stride_cur, fwd->ru_child, fwd->ru_stride_child};
   auto run = [&](auto kernel, int ms_, int threads, bool& attr) -> cudaError_t {
     const int smem = front_smem_bytes(ms_);
     if (!attr) {
@@ -1621,17 +1747,23 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
       attr = true;
     }
     kernel<<<grid, threads, smem, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child,
-                                            upd_stride_child, minpiv);
+                                            upd_stride_child, minpiv, fw);
     kh_note_launch();
     return cudaGetLastError();
   };
-  static bool a32 = false, a48 = false, a64 = false, a96 = false, a128 = false;
+  static bool a[2][5] = {};
+  const int v = fwd ? 1 : 0;
   switch (ms) {
-    case 32: return run(factor_front_kernel<32, 2>, 32, 64, a32);
-    case 48: return run(factor_front_kernel<48, 2>, 48, 64, a48);
-    case 64: return run(factor_front_kernel<64, 4>, 64, 128, a64);
-    case 96: return run(factor_front_kernel<96, 4>, 96, 128, a96);
-    case 128: return run(factor_front_kernel<128, 8>, 128, 256, a128);
+    case 32: return fwd ? run(factor_front_kernel<32, 2, true>, 32, 64, a[v][0])
+                        : run(factor_front_kernel<32, 2, false>, 32, 64, a[v][0]);
+    case 48: return fwd ? run(factor_front_kernel<48, 2, true>, 48, 64, a[v][1])
+                        : run(factor_front_kernel<48, 2, false>, 48, 64, a[v][1]);
+    case 64: return fwd ? run(factor_front_kernel<64, 4, true>, 64, 128, a[v][2])
+                        : run(factor_front_kernel<64, 4, false>, 64, 128, a[v][2]);
+    case 96: return fwd ? run(factor_front_kernel<96, 4, true>, 96, 128, a[v][3])
+                        : run(factor_front_kernel<96, 4, false>, 96, 128, a[v][3]);
+    case 128: return fwd ? run(factor_front_kernel<128, 8, true>, 128, 256, a[v][4])
+                         : run(factor_front_kernel<128, 8, false>, 128, 256, a[v][4]);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -106,10 +106,20 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream);
 // Shared-memory DMMA factorization of fronts with m <= ms (ms = 32, 48 or 64).
+// Fused forward solve of the factor kernels (kh_plan_factor_fwd): y holds the
+// gathered rhs of the batch; rhs updates go through the level buffers of the
+// solve (ru_cur: this level, ru_child: the children's level).
+struct KhFwd {
+  double2* y;
+  double2* ru_cur;
+  int64_t ru_stride_cur;
+  const double2* ru_child;
+  int64_t ru_stride_child;
+};
 cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                    const double2* lam, double2* panels, double2* upd_cur, int64_t upd_stride_cur,
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
-                                   cudaStream_t stream);
+                                   cudaStream_t stream, const KhFwd* fwd = nullptr);
 
 // om[e] = mv[src[e]], oa[e] = av[src[e]] (values in the order the fronts read them).
 cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const double* mv, const double* av, double* om,

@@ -68,8 +68,9 @@ class EngineOps:
         self.e = engine
 
     def factor(self, events=None):
+        """Refactor on the next application (fused with its forward sweep)."""
         self.e.factored = False
-        self.e.factor(events=events)
+        self.e.event_log = events
 
     def apply_local(self, F):
         """G = F W_in_local; Z = solves (stays in the engine)."""

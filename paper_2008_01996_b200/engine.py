@@ -234,31 +234,41 @@ class FDEngine:
         self.factored = True
 
     def _spatial(self):
-        """Z[:, k] = (M_x + lambda_k A_x)^-1 G[:, k] for all modes."""
+        """Z[:, k] = (M_x + lambda_k A_x)^-1 G[:, k] for all modes.
+
+        Without retained factors (first application, or factors not kept) each
+        batch is factored with the forward sweep fused into the factorization
+        (kh_plan_factor_fwd) and then swept backward: the factors are read
+        back once instead of twice. The pivot check runs after the backward
+        sweep, so its host synchronization does not split the two.
+        """
         import torch
 
         st = self._stream()
         n, nk = self.n, self.n_k
         g, z = self.G.data_ptr(), self.Z.data_ptr()
         depth = self.sym.stats["depth"] + 1
+        fuse = not (self.keep_factors and self.factored)
         for s0 in range(0, nk, self.batch):
             s1 = min(nk, s0 + self.batch)
-            if self.keep_factors:
-                slot = s0
-            else:
+            slot = s0 if self.keep_factors else 0
+            xr, xi = z + 8 * s0 * n, z + 8 * (nk + s0) * n
+            if fuse:
                 if self.event_log is not None:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                self.plan.factor(0, self.lam[s0:s1], st)
+                self.plan.factor_fwd(slot, self.lam[s0:s1], g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, st)
                 if self.event_log is not None:
                     e1.record()
                     self.event_log.append((e0, e1))
-                self.plan.pivot_check(0, s1 - s0, st)
-                self.gpu_launches += depth + 3
-                slot = 0
-            self.plan.solve(slot, s1 - s0, g + 8 * s0 * n, g + 8 * (nk + s0) * n, n,
-                            z + 8 * s0 * n, z + 8 * (nk + s0) * n, n, st)
-            self.gpu_launches += 2 * depth + 2
+                self.plan.solve_bwd(slot, s1 - s0, xr, xi, n, st)
+                self.plan.pivot_check(slot, s1 - s0, st)
+                self.gpu_launches += 3 * depth + 5
+            else:
+                self.plan.solve(slot, s1 - s0, g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, xr, xi, n, st)
+                self.gpu_launches += 2 * depth + 2
+        if fuse and self.keep_factors:
+            self.factored = True
 
     def fd_apply(self, F, U, accumulate=False):
         """U (+)= FD(F): F and U are device column-major n x N_t buffers (torch
@@ -287,8 +297,7 @@ class FDEngine:
 
         if U is None:
             U = torch.empty((self.n_t, self.n), dtype=torch.float64, device=self.device)
-        if not self.factored and self.keep_factors:
-            self.factor()
+        # not yet factored: the first application factors (forward sweep fused)
         self.fd_apply(F, U, accumulate=False)
         info = {"imag_residue": 0.0, "residuals": [], "refine_steps": 0}
         rel = self._rel(self.residual(U, F))

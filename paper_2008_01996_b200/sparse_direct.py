@@ -164,6 +164,20 @@ class _Plan:
         lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.complex128))
         _native.call("kh_plan_factor", self.raw, int(slot0), len(lam), _native.ptr(lam), stream)
 
+    def factor_solve(self, slot0, lambdas, b_re, b_im, ldb, x_re, x_im, ldx, stream):
+        """factor + solve of one batch, forward sweep fused into the factorization."""
+        lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.complex128))
+        _native.call("kh_plan_factor_solve", self.raw, int(slot0), len(lam), _native.ptr(lam), b_re, b_im, int(ldb),
+                     x_re, x_im, int(ldx), stream)
+
+    def factor_fwd(self, slot0, lambdas, b_re, b_im, ldb, stream):
+        lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.complex128))
+        _native.call("kh_plan_factor_fwd", self.raw, int(slot0), len(lam), _native.ptr(lam), b_re, b_im, int(ldb),
+                     stream)
+
+    def solve_bwd(self, slot0, nshift, x_re, x_im, ldx, stream):
+        _native.call("kh_plan_solve_bwd", self.raw, int(slot0), int(nshift), x_re, x_im, int(ldx), stream)
+
     def pivot_check(self, slot0, nshift, stream, threshold=PIVOT_THRESHOLD):
         _native.call("kh_plan_pivot_check", self.raw, int(slot0), int(nshift), float(threshold), stream,
                      None, None)

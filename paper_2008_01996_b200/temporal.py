@@ -98,7 +98,7 @@ def assemble_native(nodes, degree, j_max, device):
 
     _native.load()
     dev = torch.device(device)
-    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    nodes = np.array(nodes, dtype=np.float64)  # writable copy for torch
     n_cells = len(nodes) - 1
     nr = degree * n_cells
     need = ctypes.c_int64()

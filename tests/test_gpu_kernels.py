@@ -247,4 +247,4 @@ def test_native_temporal_p2_matches_host(cuda_ok, nodes):
     # (q'' [cos] / w^2 against q' [sin] / w): host (np.sin of the rounded
     # product) and device (sincospi) agree to ~1e-13 of the largest entry
     for a, b in ((host.A, dev.A), (host.M, dev.M), (host.C, dev.C)):
-        assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+        assert np.abs(a - b).max() < 1e-11 * np.abs(a).max()
