@@ -1213,9 +1213,16 @@ __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t*
 // with shuffles. The panel is streamed in chunks of 8 columns loaded into
 // registers before use (the first chunk while the rhs is gathered), so the
 // loads of a chunk are in flight together instead of one round trip per column.
-constexpr int SOLVE_CH = 8;
+constexpr int SOLVE_CH = 8;   // columns per warp_sum8 reduction (bwd)
+#ifndef KH_FWD_CH
+#define KH_FWD_CH 4
+#endif
+constexpr int FWD_CH = KH_FWD_CH;
+#ifndef KH_SMALL_SOLVE_MINB
+#define KH_SMALL_SOLVE_MINB 4
+#endif  // panel columns per register chunk (fwd_small, bwd L11 rows)
 
-__global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+__global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y, double2* ru_cur,
                                                         int64_t ru_stride_cur, const double2* __restrict__ ru_child,
                                                         int64_t ru_stride_child) {
@@ -1232,13 +1239,13 @@ __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t*
   const double2 z = make_double2(0.0, 0.0);
   auto load_chunk = [&](int k0, double2* c0, double2* c1) {
 #pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
+    for (int u = 0; u < FWD_CH; ++u) {
       const int k = k0 + u;
       c0[u] = (k < p && r0 > k && r0 < m) ? P[r0 + (int64_t)k * m] : z;
       c1[u] = (k < p && r1 > k && r1 < m) ? P[r1 + (int64_t)k * m] : z;
     }
   };
-  double2 a0[SOLVE_CH], a1[SOLVE_CH];
+  double2 a0[FWD_CH], a1[FWD_CH];
   load_chunk(0, a0, a1);  // first panel chunk streams in during the rhs gather
   double2 x0 = z, x1 = z;
   for (int c = F.child_begin; c < F.child_end; ++c) {
@@ -1252,10 +1259,10 @@ __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t*
   }
   if (r0 < p) x0 = cadd(x0, yy[r0]);
   if (r1 < p) x1 = cadd(x1, yy[r1]);
-  for (int k0 = 0; k0 < p; k0 += SOLVE_CH) {
+  for (int k0 = 0; k0 < p; k0 += FWD_CH) {
     if (k0 > 0) load_chunk(k0, a0, a1);
 #pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
+    for (int u = 0; u < FWD_CH; ++u) {
       const int k = k0 + u;
       if (k < p) {
         const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
@@ -1270,7 +1277,7 @@ __global__ void __launch_bounds__(256) fwd_small_kernel(KhTree T, const int32_t*
   else if (r1 < m) ru[r1 - p] = x1;
 }
 
-__global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+__global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y) {
   const int lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -1328,16 +1335,16 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(KhTree T, const int32_t*
   // j < i; the L11 rows of a chunk of SOLVE_CH steps are loaded into
   // registers first (independent of x), so the serial chain waits on one
   // load round trip per chunk instead of one per pivot
-  for (int i1 = p - 1; i1 > 0; i1 -= SOLVE_CH) {
-    double2 l0[SOLVE_CH], l1[SOLVE_CH];
+  for (int i1 = p - 1; i1 > 0; i1 -= FWD_CH) {
+    double2 l0[FWD_CH], l1[FWD_CH];
 #pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
+    for (int u = 0; u < FWD_CH; ++u) {
       const int i = i1 - u;
       l0[u] = (i > 0 && k0 < i) ? P[i + (int64_t)k0 * m] : z;
       l1[u] = (i > 0 && k1 < i) ? P[i + (int64_t)k1 * m] : z;
     }
 #pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
+    for (int u = 0; u < FWD_CH; ++u) {
       const int i = i1 - u;
       if (i > 0) {
         const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
