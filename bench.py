@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--j-max", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--collective", choices=["p2p", "nccl"], default="p2p",
+    ap.add_argument("--collective", choices=["p2p", "nccl", "alltoall"], default="p2p",
                     help="N>1 back-transform reduce-scatter: fused GEMM + peer-memory scatter, or NCCL")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-GPU driver even with one rank (testing the N>1 path on one GPU)")
@@ -296,6 +296,13 @@ def main():
     fac_flops = stats["flops"] * n_shift_local
     peaks = measured_peaks(dev) if rank == 0 else {}
 
+    # the e2e runs build their own plans: release this one's device memory
+    # first (at c4 its retained factors take 136 GB of the 180)
+    eng = runner = U = F = None
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
     e2e = None
     if not sharded and rank == 0 and not args.no_e2e:
         e2e = measure_e2e(system, pencil, args, leaf)
@@ -315,8 +322,10 @@ def main():
                        "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
                            stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
                        "parallelism": (f"shift-sharded x{world}, back transform + reduce-scatter: "
-                                       + ("fused GEMM->peer-memory scatter" if args.collective == "p2p"
-                                          else "GEMM + NCCL reduce_scatter")) if sharded else "single GPU"},
+                                       + {"p2p": "fused GEMM->peer-memory scatter",
+                                          "nccl": "GEMM + NCCL reduce_scatter",
+                                          "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[args.collective])
+                       if sharded else "single GPU"},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),

@@ -405,11 +405,20 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
-      for (int32_t idx0 = 0; idx0 < F.m() * F.p; idx0 += KH_ASM_CHUNK)
-        X.bt.insert(X.bt.end(), {f, idx0});
+      // (front, chunk start, originals range of the chunk): the originals of
+      // a front are sorted by destination, so each chunk's range is found
+      // here once instead of by a binary search in every CTA
+      int64_t e = F.orig_begin;
+      for (int32_t idx0 = 0; idx0 < F.m() * F.p; idx0 += KH_ASM_CHUNK) {
+        const int32_t end = std::min(F.m() * F.p, idx0 + KH_ASM_CHUNK);
+        while (e < F.orig_end && S.orig_dst[e] < idx0) ++e;
+        const int64_t lo = e;
+        while (e < F.orig_end && S.orig_dst[e] < end) ++e;
+        X.bt.insert(X.bt.end(), {f, idx0, (int32_t)lo, (int32_t)e});
+      }
       nkb = std::max(nkb, (F.p + 31) / 32);
     }
-    L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 2;
+    L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 4;
     L.kb_off = (int32_t)X.kbinfo.size();
     L.nkb = nkb;
     for (int32_t kbi = 0; kbi < nkb; ++kbi) {
@@ -524,6 +533,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   if (max_batch < 1 || factor_slots < max_batch) return fail(KH_ERR_INVALID, "need factor_slots >= max_batch >= 1");
   const kh::Symbolic& S = s->S;
   if (indptr[S.n] != S.nnz) return fail(KH_ERR_DIMENSION, "CSR does not match the analyzed pattern");
+  if (S.orig_dst.size() >= (size_t)INT32_MAX)  // assembly tasks carry int32 originals ranges
+    return fail(KH_ERR_DIMENSION, "too many original entries for one plan (>= 2^31)");
   KH_CUDA(cudaSetDevice(device));
   kh_plan* p = new kh_plan();
   p->device = device;

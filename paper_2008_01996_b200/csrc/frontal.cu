@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3, wi = warp & 1, wj = warp >> 1;
   Acc acc;
   // warps whose 32 x 16 sub-tile lies strictly above the diagonal (diagonal
   // tiles) or beyond row/column q skip their MMAs
@@ -247,8 +249,6 @@ __global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int
   // epilogue: this thread's 16 tile entries (rows wi*32+mt*8+g, cols
   // wj*16+nt*8+2t+h), in two halves of rows to bound register pressure;
   // children pulled in order (deterministic sums)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3, wi = warp & 1, wj = warp >> 1;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     double2 cacc[2][2][2];
@@ -318,8 +318,9 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
   // ASM_CHUNK entries; the update block is assembled by schur_update_kernel
   __shared__ Kids kids;
   const int tid = threadIdx.x;
-  const int32_t f = tasks[2 * blockIdx.x];
-  const int idx0 = tasks[2 * blockIdx.x + 1];
+  const int32_t f = tasks[4 * blockIdx.x];
+  const int idx0 = tasks[4 * blockIdx.x + 1];
+  const int64_t olo = tasks[4 * blockIdx.x + 2], ohi = tasks[4 * blockIdx.x + 3];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
   const int p = F.p, m = p + F.q;
@@ -352,26 +353,9 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
     if (idx < total && rr[u] >= cc[u]) P[idx] = v[u];
   }
   __syncthreads();
-  // originals whose (sorted) destinations fall into this chunk
-  int64_t lo = F.orig_begin, hi = F.orig_end;
-  {
-    int64_t a = lo, z = hi;
-    while (a < z) {
-      const int64_t mid = (a + z) >> 1;
-      if (T.orig_dst[mid] < idx0) a = mid + 1;
-      else z = mid;
-    }
-    lo = a;
-    z = hi;
-    while (a < z) {
-      const int64_t mid = (a + z) >> 1;
-      if (T.orig_dst[mid] < total) a = mid + 1;
-      else z = mid;
-    }
-    hi = a;
-  }
+  // originals whose (sorted) destinations fall into this chunk (range from the host)
   const double2 L = lam[b];
-  for (int64_t e = lo + tid; e < hi; e += NT) {
+  for (int64_t e = olo + tid; e < ohi; e += NT) {
     const int d = T.orig_dst[e];
     const double av = T.oa[e];
     P[d] = cadd(P[d], make_double2(fma(L.x, av, T.om[e]), L.y * av));

@@ -100,6 +100,22 @@ class EngineOps:
                      dst_table.data_ptr(), parts, rp, rp, e._stream())
         e.gpu_launches += 1
 
+    def z_rows(self, send, row_blocks):
+        """send[c, :2 nk_local, :rows_c] = Z_local[rows of block c, :]^T (the
+        all-to-all's outgoing blocks: this rank's modes for rank c's rows)."""
+        e = self.e
+        Zt = e.Z.view(2 * e.n_k, e.n)
+        for c, (r0, rows) in enumerate(row_blocks):
+            if rows and e.n_k:
+                send[c, :2 * e.n_k, :rows].copy_(Zt[:, r0:r0 + rows])
+
+    def gemm_rows(self, recv, wperm, out):
+        """out (rp x N_t, col-major) = [received modes] (rp x K) W_perm (K x N_t)."""
+        e = self.e
+        K = recv.shape[0] * recv.shape[1]
+        rp = recv.shape[2]
+        e._gemm(rp, e.n_t, K, 1.0, recv.data_ptr(), rp, wperm.data_ptr(), K, 0.0, out.data_ptr(), rp)
+
     def y_shard(self, U_shard, rows, ld, dst):
         """dst (rows x 2N_t, ld) = U_shard [A_t^T | M_t^T]."""
         e = self.e
@@ -170,7 +186,7 @@ class ShardedFD:
                  engine_kwargs=None, collective="nccl"):
         import torch
 
-        if collective not in ("nccl", "p2p"):
+        if collective not in ("nccl", "p2p", "alltoall"):
             raise ValueError(f"unknown collective {collective!r}")
         self.rank, self.world, self.group = rank, world, group
         self.k0, self.k1 = shard_range(modal.n_k, world, rank)
@@ -205,6 +221,19 @@ class ShardedFD:
         self.gpu_launches = 0
         self.collective = collective
         self.peers = PeerSlots(world, rank, nt, rp, dev, group) if collective == "p2p" else None
+        if collective == "alltoall":
+            # all-to-all of Z by spatial rows, then one local GEMM per rank:
+            # sends 2 N_k n / g values per rank instead of n N_t
+            blocks = [shard_range(modal.n_k, world, c) for c in range(world)]
+            self.kmax = max(1, max(b - a for a, b in blocks))
+            K = world * 2 * self.kmax
+            wperm = np.zeros((K, nt))
+            for c, (a, b) in enumerate(blocks):
+                wperm[c * 2 * self.kmax:c * 2 * self.kmax + 2 * (b - a)] = restrict_modal(modal, a, b).w_out
+            self.send = torch.zeros((world, 2 * self.kmax, rp), dtype=f64, device=dev)
+            self.recv = torch.zeros_like(self.send)
+            self.wperm = (torch.from_numpy(np.ascontiguousarray(wperm.T)).to(dev) if dev.type == "cuda"
+                          else torch.from_numpy(wperm))
 
     def rows(self, c):
         r0 = c * self.rp
@@ -217,6 +246,11 @@ class ShardedFD:
         self.ops.apply_local(F)
         if self.peers is not None:
             self._apply_p2p(out)
+            return
+        if self.collective == "alltoall":
+            self.ops.z_rows(self.send, [self.rows(c) for c in range(self.world)])
+            dist.all_to_all_single(self.recv.view(-1), self.send.view(-1), group=self.group)
+            self.ops.gemm_rows(self.recv, self.wperm, out)
             return
         for c in range(self.world):
             r0, rows = self.rows(c)

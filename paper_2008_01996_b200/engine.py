@@ -18,6 +18,7 @@ reference; needed because FD's accuracy is limited by kappa_2(X_t), see
 DESIGN.md). All kernels are in libkhb200.so; torch only allocates memory.
 """
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -138,7 +139,7 @@ class FDEngine:
     """Device-resident FD solver for one (M_x, A_x, temporal pencil) triple."""
 
     def __init__(self, M_x, A_x, modal, device=None, keep_factors=None, max_batch=None,
-                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None):
+                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None, pipes=1):
         import torch
 
         _native.require_cuda()
@@ -157,31 +158,51 @@ class FDEngine:
         mv = self.sym.align_values(M)
         av = self.sym.align_values(A)
 
+        # shift pipelines: the shifts are split into `pipes` contiguous ranges,
+        # each with its own plan (factor storage, work space, side streams) and
+        # stream, so that one range's narrow top-of-tree launches could overlap
+        # the other's wide ones (KH_PIPES overrides). Measured at c3: 1 pipe
+        # 43.96, 2 pipes 44.22, 4 pipes 46.76 ms/step -- the top-level kernels
+        # already fill the GPU -- so the default is a single plan.
+        nk = max(self.n_k, 1)
+        npipe = max(1, min(nk, int(os.environ.get("KH_PIPES", pipes))))
+        bounds = [round(i * self.n_k / npipe) for i in range(npipe + 1)]
+        sizes = [max(bounds[i + 1] - bounds[i], 1) for i in range(npipe)]
+
+        def total_bytes(b, keep):
+            return sum(sparse_direct.plan_bytes(self.sym, min(b, sz), sz if keep else min(b, sz)) for sz in sizes)
+
         # memory plan: keep every shift's factors when they fit
         with torch.cuda.device(self.device):
             free, _ = torch.cuda.mem_get_info()
+            # blocks torch has cached but not handed out are free for us too
+            free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
         work = 8 * self.n * (2 * self.n_k * 2 + 2 * self.n_t * 3) + 8 * self.n_t * 8 * self.n_t
         budget = mem_fraction * free - work
-        nk = max(self.n_k, 1)
-        batch = min(nk, max_batch or nk)
+        batch = min(max(sizes), max_batch or nk)
         if keep_factors is None:
             # keep every shift's factors if they fit with a working batch of
             # at least 16 shifts in flight (update buffers scale with it)
             b = batch
-            while b > 16 and sparse_direct.plan_bytes(self.sym, b, nk) > budget:
+            floor = max(1, 16 // npipe)
+            while b > floor and total_bytes(b, True) > budget:
                 b = (b + 1) // 2
-            keep_factors = sparse_direct.plan_bytes(self.sym, b, nk) <= budget
+            keep_factors = total_bytes(b, True) <= budget
             if keep_factors:
                 batch = b
-        if keep_factors:
-            slots = nk
-        else:
-            while batch > 1 and sparse_direct.plan_bytes(self.sym, batch, batch) > budget:
+        if not keep_factors:
+            while batch > 1 and total_bytes(batch, False) > budget:
                 batch = (batch + 1) // 2
-            slots = batch
         self.keep_factors = bool(keep_factors)
         self.batch = int(batch)
-        self.plan = sparse_direct._Plan(self.sym, mv, av, self.batch, slots, self.device.index)
+        self.pipes = []
+        for i in range(npipe):
+            k0, k1 = bounds[i], bounds[i + 1]
+            b = min(self.batch, max(k1 - k0, 1))
+            plan = sparse_direct._Plan(self.sym, mv, av, b, (k1 - k0 if self.keep_factors else b) or 1,
+                                       self.device.index)
+            self.pipes.append((plan, k0, k1, b, torch.cuda.Stream(device=self.device)))
+        self.plan = self.pipes[0][0]   # residual kernels (CSR of M, A) and single-pipe callers
         self.factored = False
 
         dev = self.device
@@ -210,6 +231,27 @@ class FDEngine:
         _native.call("kh_dgemm", m, n, k, float(alpha), A, lda, B, ldb, float(beta), C, ldc, self._stream())
         self.gpu_launches += 1
 
+    def _run_pipes(self, body, join=True):
+        """Run body(plan, k0, k1, batch, stream) for every pipe, each on its own
+        stream forked from the current one; join=True joins them back."""
+        import torch
+
+        main = torch.cuda.current_stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for plan, k0, k1, b, st in self.pipes:
+            st.wait_event(fork)
+            body(plan, k0, k1, b, st)
+        if join:
+            self._join_pipes()
+
+    def _join_pipes(self):
+        import torch
+
+        main = torch.cuda.current_stream(self.device)
+        for *_, st in self.pipes:
+            main.wait_stream(st)
+
     def factor(self, events=None):
         """Factor M_x + lambda_k A_x for every retained shift (no-op otherwise).
 
@@ -219,18 +261,23 @@ class FDEngine:
             return
         import torch
 
-        st = self._stream()
         if events is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-        for s0 in range(0, self.n_k, self.batch):
-            s1 = min(self.n_k, s0 + self.batch)
-            self.plan.factor(s0, self.lam[s0:s1], st)
-            self.gpu_launches += self.sym.stats["depth"] + 4
+
+        def body(plan, k0, k1, b, ts):
+            st = _native.stream_handle(ts)
+            for s0 in range(k0, k1, b):
+                s1 = min(k1, s0 + b)
+                plan.factor(s0 - k0, self.lam[s0:s1], st)
+                self.gpu_launches += self.sym.stats["depth"] + 4
+
+        self._run_pipes(body)
         if events is not None:
             e1.record()
             events.append((e0, e1))
-        self.plan.pivot_check(0, self.n_k, st)
+        for plan, k0, k1, b, st in self.pipes:
+            plan.pivot_check(0, k1 - k0, self._stream())
         self.factored = True
 
     def _spatial(self):
@@ -239,34 +286,55 @@ class FDEngine:
         Without retained factors (first application, or factors not kept) each
         batch is factored with the forward sweep fused into the factorization
         (kh_plan_factor_fwd) and then swept backward: the factors are read
-        back once instead of twice. The pivot check runs after the backward
-        sweep, so its host synchronization does not split the two.
+        back once instead of twice. The shift pipelines run concurrently; the
+        pivot checks (host synchronizations) come after everything is queued.
         """
         import torch
 
-        st = self._stream()
         n, nk = self.n, self.n_k
         g, z = self.G.data_ptr(), self.Z.data_ptr()
         depth = self.sym.stats["depth"] + 1
         fuse = not (self.keep_factors and self.factored)
-        for s0 in range(0, nk, self.batch):
-            s1 = min(nk, s0 + self.batch)
-            slot = s0 if self.keep_factors else 0
-            xr, xi = z + 8 * s0 * n, z + 8 * (nk + s0) * n
-            if fuse:
-                if self.event_log is not None:
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record()
-                self.plan.factor_fwd(slot, self.lam[s0:s1], g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, st)
-                if self.event_log is not None:
-                    e1.record()
-                    self.event_log.append((e0, e1))
-                self.plan.solve_bwd(slot, s1 - s0, xr, xi, n, st)
-                self.plan.pivot_check(slot, s1 - s0, st)
-                self.gpu_launches += 3 * depth + 5
-            else:
-                self.plan.solve(slot, s1 - s0, g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, xr, xi, n, st)
-                self.gpu_launches += 2 * depth + 2
+        log = self.event_log if fuse else None
+        main = torch.cuda.current_stream(self.device)
+        if log is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+        fac_done = []
+        checks = []
+
+        def body(plan, k0, k1, b, ts):
+            st = _native.stream_handle(ts)
+            for s0 in range(k0, k1, b):
+                s1 = min(k1, s0 + b)
+                slot = s0 - k0 if self.keep_factors else 0
+                xr, xi = z + 8 * s0 * n, z + 8 * (nk + s0) * n
+                if fuse:
+                    plan.factor_fwd(slot, self.lam[s0:s1], g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, st)
+                    if log is not None:
+                        ev = torch.cuda.Event()
+                        ev.record(ts)
+                        fac_done.append(ev)
+                    plan.solve_bwd(slot, s1 - s0, xr, xi, n, st)
+                    self.gpu_launches += 3 * depth + 5
+                    if self.keep_factors:
+                        checks.append((plan, slot, s1 - s0))
+                    else:  # the slots are reused by the next batch: check now
+                        plan.pivot_check(slot, s1 - s0, st)
+                else:
+                    plan.solve(slot, s1 - s0, g + 8 * s0 * n, g + 8 * (nk + s0) * n, n, xr, xi, n, st)
+                    self.gpu_launches += 2 * depth + 2
+
+        self._run_pipes(body, join=False)
+        if log is not None:
+            # end of the factorization: the last pipe's factor launches
+            for ev in fac_done:
+                main.wait_event(ev)
+            e1.record(main)
+            log.append((e0, e1))
+        self._join_pipes()
+        for plan, slot, cnt in checks:
+            plan.pivot_check(slot, cnt, self._stream())
         if fuse and self.keep_factors:
             self.factored = True
 

@@ -31,8 +31,23 @@ def short(name):
     return name.split("(")[0].replace("void ", "").replace("<unnamed>::", "")[:48]
 
 
+SETUP_PREFIXES = ("ht_coeff_kernel", "ht_accumulate_kernel")
+
+
+def drop_setup(names, rows):
+    """Keep only the launches after the input generators' temporal assembly
+    (kh_ht_assemble: ht_* kernels and their GEMMs) -- the solver's steps."""
+    ids = sorted(rows)
+    last = max((k for k in ids if names[k].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+                .startswith(SETUP_PREFIXES)), default=None)
+    if last is None:
+        return rows
+    return {k: v for k, v in rows.items() if k > last}
+
+
 def main():
     names, rows = load(sys.argv[1])
+    rows = drop_setup(names, rows)
     tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for k, m in rows.items():
         if any(x in names[k] for x in ("at::", "cutlass", "cublas", "gemv", "splitKreduce")):

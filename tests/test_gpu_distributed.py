@@ -19,7 +19,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("collective", ["nccl", "p2p"])
+@pytest.mark.parametrize("collective", ["nccl", "p2p", "alltoall"])
 def test_sharded_fd_world1_nccl(cuda_ok, collective):
     import torch
     import torch.distributed as dist

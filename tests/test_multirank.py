@@ -37,6 +37,15 @@ class _CpuOps:
     def out_chunk(self, r0, rows, dst, ldd):
         dst[:, :rows] = torch.from_numpy((self.Z[r0:r0 + rows] @ self.modal.w_out).T)
 
+    def z_rows(self, send, row_blocks):
+        for c, (r0, rows) in enumerate(row_blocks):
+            if rows:
+                send[c, :self.Z.shape[1], :rows] = torch.from_numpy(np.ascontiguousarray(self.Z[r0:r0 + rows].T))
+
+    def gemm_rows(self, recv, wperm, out):
+        Zcat = recv.numpy().reshape(-1, recv.shape[2]).T       # rp x K
+        out[:] = torch.from_numpy(np.ascontiguousarray((Zcat @ wperm.numpy()).T))
+
     def y_shard(self, U, rows, ld, dst):
         dst[:, :rows] = torch.from_numpy((U[:, :rows].numpy().T @ self.modal.kron_b).T)
 
@@ -51,7 +60,7 @@ class _CpuOps:
         y.add_(x)
 
 
-def _worker(rank, world, port, name, out_dir):
+def _worker(rank, world, port, name, out_dir, collective="nccl"):
     import torch.distributed as dist
 
     from conftest import load_golden
@@ -65,7 +74,7 @@ def _worker(rank, world, port, name, out_dir):
     modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
     k0, k1 = shard_range(modal.n_k, world, rank)
     ops = _CpuOps(system.spatial.M_II, system.spatial.A_II, restrict_modal(modal, k0, k1))
-    run = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, ops=ops)
+    run = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, ops=ops, collective=collective)
     F = torch.from_numpy(np.ascontiguousarray(system.rhs)).view(system.n_t, system.m_x)
     _, info = run.solve(F, refine=3, tol=1e-13)
     U = run.gather()
@@ -80,12 +89,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name", ["lshape0", "c1"])
-def test_two_ranks_match_reference(tmp_path, name):
+@pytest.mark.parametrize("name,collective", [("lshape0", "nccl"), ("c1", "nccl"), ("c1", "alltoall"),
+                                             ("odd", "alltoall")])
+def test_two_ranks_match_reference(tmp_path, name, collective):
+    """reduce-scatter of the partial back transforms ("nccl" path) or
+    all-to-all of Z by rows + local GEMM ("alltoall")."""
     from conftest import load_golden, rel_diff
 
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), collective), nprocs=world, join=True)
     u0, u1 = np.load(tmp_path / "u0.npy"), np.load(tmp_path / "u1.npy")
     assert np.array_equal(u0, u1)  # every rank gathers the same solution
     r0, r1 = np.load(tmp_path / "r0.npy"), np.load(tmp_path / "r1.npy")
