@@ -242,10 +242,12 @@ def main():
     stats = eng.sym.stats
 
     fac_events = []
+    phase_timers = {}
 
     def step(record=False):
         eng.factored = False
         eng.event_log = fac_events if record else None  # refactoring when the factors are not kept
+        eng.timers = phase_timers if record else None
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -296,6 +298,41 @@ def main():
     fac_flops = stats["flops"] * n_shift_local
     peaks = measured_peaks(dev) if rank == 0 else {}
 
+    # per-phase rooflines from the CUDA events around each phase (engine.timers)
+    kernels = {}
+    if not sharded:
+        def ms_of(name):
+            return sum(a.elapsed_time(b) for a, b in phase_timers.get(name, [])) / max(args.steps, 1)
+
+        calls = {k: len(v) / max(args.steps, 1) for k, v in phase_timers.items()}
+        st_ = eng.sym.stats
+        nk_ = eng.n_k
+        hbm = peaks.get("hbm_gbs")
+        fp64 = peaks.get("fp64_tflops")
+        gemm_flops = calls.get("gemm", 0) * 2.0 * n * nt * 2 * nk_ + calls.get("gemm_kron", 0) * 2.0 * n * 2 * nt * nt
+        gemm_ms = ms_of("gemm") + ms_of("gemm_kron")
+        if gemm_ms > 0:
+            a_ = gemm_flops / (gemm_ms / 1e3) / 1e12
+            kernels["transform_gemms"] = {"bound": "tensor", "achieved": a_, "peak": fp64, "unit": "TFLOP/s",
+                                          "frac": a_ / fp64 if fp64 else None, "ms_per_step": gemm_ms,
+                                          "work": "modal transforms F W_in, Z W_out and the residual's "
+                                                  "U [A_t^T | M_t^T]: 2 m n k flops per call (dgemm_kernel)"}
+        if ms_of("solve") > 0:
+            b_ = calls["solve"] * 2 * st_["panel_entries"] * 16.0 * nk_   # forward + backward read every factor
+            a_ = b_ / (ms_of("solve") / 1e3) / 1e9
+            kernels["refinement_solves"] = {"bound": "hbm", "achieved": a_, "peak": hbm, "unit": "GB/s",
+                                            "frac": a_ / hbm if hbm else None, "ms_per_step": ms_of("solve"),
+                                            "work": "forward + backward sweeps over the retained factors "
+                                                    "(16 B per complex factor entry, each read once per sweep)"}
+        if ms_of("residual") > 0:
+            b_ = calls["residual"] * (8.0 * n * nt * 4 + 24.0 * st_["nnz"])
+            a_ = b_ / (ms_of("residual") / 1e3) / 1e9
+            kernels["residual_spmm"] = {"bound": "hbm", "achieved": a_, "peak": hbm, "unit": "GB/s",
+                                        "frac": a_ / hbm if hbm else None, "ms_per_step": ms_of("residual"),
+                                        "work": "R = F - (M_x Y1 + A_x Y2): Y (2 N_t), F, R columns + CSR once"}
+        if ms_of("factor_solve") > 0:
+            kernels["factor_plus_solve_ms_per_step"] = ms_of("factor_solve")
+
     # the e2e runs build their own plans: release this one's device memory
     # first (at c4 its retained factors take 136 GB of the 180)
     eng = runner = U = F = None
@@ -340,6 +377,7 @@ def main():
                          "ms_per_step": fac_s * 1e3, "share_of_step": fac_s * 1e3 / ms,
                          "traffic": traffic},
             "e2e": e2e,
+            "kernels": kernels,
         }
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_fd_sample(system, shift_sample_size(args.config))

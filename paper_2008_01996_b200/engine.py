@@ -222,10 +222,26 @@ class FDEngine:
         # launch sequence (bench.py's roofline; also covers refactoring when
         # the factors are not kept)
         self.event_log = None
+        # optional per-phase CUDA-event timers (bench.py's per-kernel rooflines)
+        self.timers = None
 
     # ---- primitives -----------------------------------------------------------
     def _stream(self):
         return _native.stream_handle()
+
+    def _timed(self, name, fn, *args):
+        """fn(*args), bracketed by CUDA events on the current stream when
+        self.timers (dict name -> [(start, end, info)]) is set (bench.py)."""
+        if self.timers is None:
+            return fn(*args)
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn(*args)
+        e1.record()
+        self.timers.setdefault(name, []).append((e0, e1))
+        return out
 
     def _gemm(self, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc):
         _native.call("kh_dgemm", m, n, k, float(alpha), A, lda, B, ldb, float(beta), C, ldc, self._stream())
@@ -342,17 +358,20 @@ class FDEngine:
         """U (+)= FD(F): F and U are device column-major n x N_t buffers (torch
         tensors of shape (N_t, n))."""
         n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
-        self._gemm(n, nk2, nt, 1.0, F.data_ptr(), n, self.w_in.data_ptr(), nt, 0.0, self.G.data_ptr(), n)
-        self._spatial()
-        self._gemm(n, nt, nk2, 1.0, self.Z.data_ptr(), n, self.w_out.data_ptr(), nk2,
-                   1.0 if accumulate else 0.0, U.data_ptr(), n)
+        self._timed("gemm", self._gemm, n, nk2, nt, 1.0, F.data_ptr(), n, self.w_in.data_ptr(), nt, 0.0,
+                    self.G.data_ptr(), n)
+        fused = not (self.keep_factors and self.factored)
+        self._timed("factor_solve" if fused else "solve", self._spatial)
+        self._timed("gemm", self._gemm, n, nt, nk2, 1.0, self.Z.data_ptr(), n, self.w_out.data_ptr(), nk2,
+                    1.0 if accumulate else 0.0, U.data_ptr(), n)
 
     def residual(self, U, F, keep_r=True):
         """Device: R = F - K U; returns (||R||^2, ||F||^2) as a device tensor slice."""
         n, nt = self.n, self.n_t
-        self._gemm(n, 2 * nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt, 0.0, self.Y.data_ptr(), n)
-        self.plan.residual(nt, self.Y.data_ptr(), n, F.data_ptr(), n, self.R.data_ptr() if keep_r else None, n,
-                           self.norms.data_ptr(), self._stream())
+        self._timed("gemm_kron", self._gemm, n, 2 * nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt, 0.0,
+                    self.Y.data_ptr(), n)
+        self._timed("residual", self.plan.residual, nt, self.Y.data_ptr(), n, F.data_ptr(), n,
+                    self.R.data_ptr() if keep_r else None, n, self.norms.data_ptr(), self._stream())
         self.gpu_launches += 2
         return self.norms[:2]
 
