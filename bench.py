@@ -335,6 +335,7 @@ def main():
 
     # the e2e runs build their own plans: release this one's device memory
     # first (at c4 its retained factors take 136 GB of the 180)
+    coll = runner.collective if runner is not None else args.collective
     eng = runner = U = F = None
     import gc
 
@@ -361,7 +362,7 @@ def main():
                        "parallelism": (f"shift-sharded x{world}, back transform + reduce-scatter: "
                                        + {"p2p": "fused GEMM->peer-memory scatter",
                                           "nccl": "GEMM + NCCL reduce_scatter",
-                                          "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[args.collective])
+                                          "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[coll])
                        if sharded else "single GPU"},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
             "fd_residual": infos[-1]["residuals"][0],
@@ -405,7 +406,7 @@ def load_traffic(cfg):
 
 def measure_e2e(system, pencil, args, leaf):
     """Public API with host buffers, the reference's t_total convention:
-    solve_fd(system) per step (temporal pencil dggev + SVD on the host,
+    solve_fd(system) per step (temporal pencil dgeev + SVD on the host,
     overlapped with the spatial analysis; plan; factor; solve; refinement;
     D2H of u). `pencil_reused` is the same call with a prebuilt pencil."""
     import torch
@@ -437,7 +438,7 @@ def measure_e2e(system, pencil, args, leaf):
     h2d = 8 * n * nt + 8 * nt * (2 * nt) * 3 + 8 * (n + 1) + 8 * 3 * 2 * nnz
     return {"value": system.dof / t_full, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(8 * n * nt), "steps": max(1, args.e2e_steps),
-            "includes": "solve_fd(system): host pencil (dggev, SVD), symbolic analysis, plan upload, H2D of f, "
+            "includes": "solve_fd(system): host pencil (Cholesky-reduced dgeev + real SVD), symbolic analysis, plan upload, H2D of f, "
                         "factorization, solve, refinement, D2H of u",
             "pencil_reused": {"value": system.dof / t_reuse, "unit": UNIT,
                               "includes": "solve_fd(system, pencil) with the pencil built once outside"},

@@ -169,9 +169,11 @@ int kh_dgemm_rowscatter(int64_t m, int64_t n, int64_t k, const double* A, int64_
 /* out[e] = sum_{c < parts} slots[c part_elems + e] in slot order (deterministic
  * reduction of the received partial sums; device arrays). */
 int kh_sum_parts(int32_t parts, const double* slots, int64_t part_elems, double* out, void* stream);
-/* CUDA IPC: `handle` is 64 opaque bytes (host). kh_ipc_open maps another
- * process's device allocation into this process (peer access enabled). */
-int kh_ipc_handle(const void* dev_ptr, void* handle);
+/* CUDA IPC: `handle` is 64 opaque bytes (host) naming the allocation that
+ * contains dev_ptr; `offset` receives dev_ptr's byte offset inside it.
+ * kh_ipc_open maps another process's allocation into this process (peer
+ * access enabled) and returns its base: add the sender's offset. */
+int kh_ipc_handle(const void* dev_ptr, void* handle, int64_t* offset);
 int kh_ipc_open(const void* handle, void** dev_ptr);
 int kh_ipc_close(void* dev_ptr);
 /* Temporal H_T matrices (reference temporal.py:300-329) of the P1 (degree 1)

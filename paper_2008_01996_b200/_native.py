@@ -85,7 +85,7 @@ SIGNATURES = {
                                             _vp, _vp]),
     "kh_dgemm_rowscatter": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _i64, _i64, _vp]),
     "kh_sum_parts": (ctypes.c_int, [_i32, _vp, _i64, _vp, _vp]),
-    "kh_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "kh_ipc_handle": (ctypes.c_int, [_vp, _vp, _P(_i64)]),
     "kh_ipc_open": (ctypes.c_int, [_vp, _P(_vp)]),
     "kh_ipc_close": (ctypes.c_int, [_vp]),
     "kh_ht_workspace_bytes": (ctypes.c_int, [_i32, _i64, _P(_i64)]),

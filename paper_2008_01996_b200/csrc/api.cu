@@ -860,11 +860,23 @@ int kh_ht_assemble(int32_t degree, int64_t n_cells, const double* nodes, int64_t
   return KH_OK;
 }
 
-int kh_ipc_handle(const void* dev_ptr, void* handle) {
-  if (!dev_ptr || !handle) return fail(KH_ERR_INVALID, "null argument");
+int kh_ipc_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(KH_ERR_INVALID, "null argument");
+  // the handle names the whole allocation and opens at its base: report
+  // where dev_ptr sits inside it (caching allocators sub-allocate)
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  KH_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(KH_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+    return fail(KH_ERR_CUDA, "cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
-  KH_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  KH_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
   std::memcpy(handle, &h, sizeof h);
+  *offset = (int64_t)(reinterpret_cast<unsigned long long>(dev_ptr) - base);
   return KH_OK;
 }
 

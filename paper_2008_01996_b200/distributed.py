@@ -155,20 +155,42 @@ class PeerSlots:
         self.world, self.rank, self.group = world, rank, group
         self.slot = nt * rp
         self.recv = torch.zeros((world, nt, rp), dtype=torch.float64, device=device)
-        handle = ctypes.create_string_buffer(64)
-        _native.call("kh_ipc_handle", self.recv.data_ptr(), handle)
-        handles = [None] * world
-        dist.all_gather_object(handles, handle.raw, group=group)
         self.mapped = []
+        # every step is local and its outcome is exchanged before anyone acts
+        # on it, so a failing rank cannot leave the others blocked in a
+        # collective; `ok` tells the caller whether to fall back to NCCL
+        mine = None
+        try:
+            handle = ctypes.create_string_buffer(64)
+            offset = ctypes.c_int64()
+            _native.call("kh_ipc_handle", self.recv.data_ptr(), handle, ctypes.byref(offset))
+            mine = (handle.raw, int(offset.value))
+        except Exception as exc:  # noqa: BLE001 -- reported through the flag
+            self.error = f"kh_ipc_handle: {exc}"
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        opened = all(h is not None for h in handles)
         bases = []
-        for c in range(world):
-            if c == rank:
-                bases.append(self.recv.data_ptr())
-            else:
-                ptr = ctypes.c_void_p()
-                _native.call("kh_ipc_open", ctypes.create_string_buffer(handles[c], 64), ctypes.byref(ptr))
-                self.mapped.append(ptr.value)
-                bases.append(ptr.value)
+        if opened:
+            try:
+                for c in range(world):
+                    if c == rank:
+                        bases.append(self.recv.data_ptr())
+                    else:
+                        ptr = ctypes.c_void_p()
+                        raw, off = handles[c]
+                        _native.call("kh_ipc_open", ctypes.create_string_buffer(raw, 64), ctypes.byref(ptr))
+                        self.mapped.append(ptr.value)
+                        bases.append(ptr.value + off)   # the peer's recv inside its allocation
+            except Exception as exc:  # noqa: BLE001
+                self.error = f"kh_ipc_open: {exc}"
+                opened = False
+        flags = [None] * world
+        dist.all_gather_object(flags, opened, group=group)
+        self.ok = all(flags)
+        if not self.ok:
+            self.close()
+            return
         self.dst = torch.tensor([b + 8 * rank * self.slot for b in bases], dtype=torch.int64, device=device)
 
     def close(self):
@@ -221,6 +243,14 @@ class ShardedFD:
         self.gpu_launches = 0
         self.collective = collective
         self.peers = PeerSlots(world, rank, nt, rp, dev, group) if collective == "p2p" else None
+        if self.peers is not None and not self.peers.ok:
+            # peer mapping failed on some rank: every rank takes the NCCL path
+            import warnings
+
+            warnings.warn("peer-memory slots unavailable (%s); using NCCL reduce-scatter"
+                          % getattr(self.peers, "error", "another rank failed"))
+            self.peers = None
+            self.collective = collective = "nccl"
         if collective == "alltoall":
             # all-to-all of Z by spatial rows, then one local GEMM per rank:
             # sends 2 N_k n / g values per rank instead of n N_t
@@ -339,23 +369,42 @@ def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=
     from . import _native, solvers
     from .engine import modal_plan
 
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+    import scipy.sparse as sp
+
+    from . import sparse_direct
+
     _native.require_cuda()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     report = solvers.SolveReport(variant="fd", dof=system.dof, n_t=system.n_t, m_x=system.m_x)
-    t0 = time.perf_counter()
-    if pencil is None:
-        pencil = solvers.build_pencil(system.temporal, "fd", eig="reduced")
-    modal = modal_plan(system.temporal, pencil)
-    report.t_decompose = time.perf_counter() - t0
-    report.min_re_lambda = pencil.min_re_lambda
-    report.spectral = pencil.spectral_stats
     dev = torch.device("cuda", torch.cuda.current_device())
     report.device = torch.cuda.get_device_name(dev)
     n, nt = system.m_x, system.n_t
+    leaf = leaf_size or sparse_direct.DEFAULT_LEAF_SIZE
+    t0 = time.perf_counter()
+    # as in solvers.solve_fd: pinned rhs up at once, the symbolic analysis on
+    # a worker thread beside the host pencil (few BLAS threads)
+    rhs_t = torch.from_numpy(np.ascontiguousarray(np.asarray(system.rhs, dtype=np.float64)))
+    F = rhs_t.to(dev, non_blocking=True).view(nt, n) if rhs_t.is_pinned() else None
+    pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
+    with ThreadPoolExecutor(max_workers=1) as pool:
+        fut = pool.submit(sparse_direct.analyze, pattern, leaf)
+        with solvers._blas_threads(1 if nt <= 512 else 4):
+            if pencil is None:
+                pencil = solvers.build_pencil(system.temporal, "fd", eig="reduced")
+            modal = modal_plan(system.temporal, pencil)
+        report.t_decompose = time.perf_counter() - t0
+        if F is None:
+            F = rhs_t.to(dev).view(nt, n)
+        symbolic = fut.result()
+    report.min_re_lambda = pencil.min_re_lambda
+    report.spectral = pencil.spectral_stats
     t0 = time.perf_counter()
     runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
-                       leaf_size=leaf_size, group=group, collective=collective)
-    F = solvers._to_device(system.rhs, dev).view(nt, n)
+                       leaf_size=leaf, group=group, collective=collective,
+                       engine_kwargs={"symbolic": symbolic})
     U, info = runner.solve(F, refine=refine, tol=refine_tol)
     r0, rows = runner.rows(rank)
     out = solvers._to_host(U[:, :rows])

@@ -81,3 +81,25 @@ def test_rowscatter_gemm_and_slot_sum(cuda_ok):
     _native.call("kh_sum_parts", g, recv.data_ptr(), n * rp, out.data_ptr(), _native.stream_handle())
     want = got[0] + got[1] + got[2]
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.gpu
+def test_ipc_handle_reports_offset_inside_allocation(cuda_ok):
+    """kh_ipc_handle names the whole allocation; the reported offset locates
+    the pointer inside it (tensors from a caching allocator are sub-blocks)."""
+    import ctypes
+
+    import torch
+
+    from paper_2008_01996_b200 import _native
+
+    x = torch.zeros(1 << 20, dtype=torch.float64, device="cuda")
+    offs = []
+    for t in (x, x[1000:], x[4096:]):
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        _native.call("kh_ipc_handle", t.data_ptr(), h, ctypes.byref(off))
+        offs.append(off.value)
+    assert offs[1] - offs[0] == 8 * 1000
+    assert offs[2] - offs[0] == 8 * 4096
+    assert offs[0] >= 0
