@@ -1202,6 +1202,10 @@ constexpr int SOLVE_CH = 8;   // columns per warp_sum8 reduction (bwd)
 #define KH_FWD_CH 4
 #endif
 constexpr int FWD_CH = KH_FWD_CH;
+#ifndef KH_BWD_L11
+#define KH_BWD_L11 16
+#endif
+constexpr int BWD_L11 = KH_BWD_L11;  // bwd_small stages L11 in shared memory for p <= this
 #ifndef KH_SMALL_SOLVE_MINB
 #define KH_SMALL_SOLVE_MINB 4
 #endif  // panel columns per register chunk (fwd_small, bwd L11 rows)
@@ -1274,6 +1278,18 @@ __global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) bwd_small_kernel(KhT
   double2* yy = yb + F.first;
   const int64_t* urows = T.urows + F.rows_begin;
   const double2 z = make_double2(0.0, 0.0);
+  // the L11 block (p <= BWD_L11) streams into shared memory with cp.async
+  // right away, so the serial L11^T chain at the end reads it on-chip
+  __shared__ __align__(16) double2 l11s[8][BWD_L11 * (BWD_L11 + 1)];
+  double2* Ls = l11s[threadIdx.x >> 5];
+  const bool stage = p <= BWD_L11;
+  if (stage) {
+    for (int e = lane; e < p * p; e += 32) {
+      const int k = e / p, i = e - k * p;
+      cp_async16(Ls + k * (BWD_L11 + 1) + i, P + i + (int64_t)k * m, true);
+    }
+    cp_async_commit();
+  }
   // solution values of the update rows (already final: ancestors are done);
   // lane a holds xu[a] and xu[a + 32]
   const double2 xu0 = lane < q ? yb[urows[lane]] : z;
@@ -1315,6 +1331,17 @@ __global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) bwd_small_kernel(KhT
   }
   if (k0 < p) t0 = csub(cmul(y0, cinv(d0)), t0);
   if (k1 < p) t1 = csub(cmul(y1, cinv(d1)), t1);
+  if (stage) {
+    // L11^T x = t from shared memory (p <= BWD_L11: lane k owns column k)
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int i = p - 1; i > 0; --i) {
+      const double2 xi = shfl2(t0, i);
+      if (k0 < i) t0 = cfms(t0, Ls[k0 * (BWD_L11 + 1) + i], xi);
+    }
+    if (k0 < p) yy[k0] = t0;
+    return;
+  }
   // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for
   // j < i; the L11 rows of a chunk of SOLVE_CH steps are loaded into
   // registers first (independent of x), so the serial chain waits on one

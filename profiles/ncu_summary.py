@@ -41,8 +41,9 @@ def main():
     for label, key in KEYS:
         if key in col:
             print(f"  {label:28s} {vals[col[key]]} {units[col[key]]}")
-    stalls = {h.split("smsp__average_warp_latency_issue_stalled_")[1].split(".")[0]: vals[i]
-              for h, i in col.items() if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio")}
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+    stalls = {h[len(pre):-len(suf)]: vals[i] for h, i in col.items() if h.startswith(pre) and h.endswith(suf)}
+    stalls.pop("selected", None)
     try:
         tot = sum(float(v) for v in stalls.values())
         top = sorted(((float(v), k) for k, v in stalls.items()), reverse=True)[:8]
@@ -53,6 +54,8 @@ def main():
         src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass"))))
     except subprocess.CalledProcessError:
         return
+    if src and src[0] and src[0][0] == "Kernel Name":
+        src = src[1:]
     h = src[0]
     ci = {x: i for i, x in enumerate(h)}
     sk = "Warp Stall Sampling (All Samples)"
