@@ -8,6 +8,8 @@ inputs are built the way the reference builds them:
 * `project_rhs`          -> fem.py:267-297 (cell averages, graded panels on cell 0)
 * `assemble_global_rhs`  -> fem.py:312-346
 * `dirichlet_lift`       -> fem.py:300-309
+* `error_norms`          -> fem.py:358-418 (collapsed rules beyond degree 6: fem.py:67-81)
+* GPU versions of `project_rhs` / `error_norms`: quadrature_gpu.py
 
 These run once per problem, outside every timed region.
 """
@@ -66,15 +68,40 @@ _RULES = {
 }
 
 
+def _collapsed_rule(order):
+    """Collapsed (Duffy) tensor rule exact to total degree `order`
+    (reference fem.py:67-81): x = u (1 - v), y = v, Gauss-Legendre in u and
+    Gauss-Jacobi(1, 0) in v (the Jacobian 1 - v is the Jacobi weight), both
+    mapped to [0, 1]; weights sum to 1/2."""
+    from scipy.special import roots_jacobi
+
+    n = (order + 2) // 2
+    u, wu = np.polynomial.legendre.leggauss(n)
+    u, wu = 0.5 * (u + 1.0), 0.5 * wu
+    xj, wj = roots_jacobi(n, 1.0, 0.0)
+    v, wv = 0.5 * (xj + 1.0), 0.25 * wj
+    uu, vv = np.meshgrid(u, v, indexing="ij")
+    return np.column_stack([(uu * (1.0 - vv)).ravel(), vv.ravel()]), np.outer(wu, wv).ravel()
+
+
 def triangle_rule(order):
-    """Smallest catalogued rule of degree >= order; weights sum to 1/2."""
+    """Smallest catalogued rule of degree >= order, else the collapsed rule
+    (reference fem.py:84-104); weights sum to 1/2."""
     if order < 1:
         raise ValueError("quadrature order must be >= 1")
     for deg in sorted(_RULES):
         if deg >= order:
             pts, wts = _RULES[deg]
             return np.array(pts, dtype=float), 0.5 * np.array(wts, dtype=float)
-    raise ValueError("quadrature order above 6 is not needed by the benchmarks")
+    return _collapsed_rule(order)
+
+
+def error_quadrature(quad_order=None):
+    """(triangle rule, time rule) of the error norms (reference
+    fem.py:349-355): degree 12 / 8 Gauss points by default."""
+    if quad_order is None:
+        return triangle_rule(12), gauss_rule_01(8)
+    return triangle_rule(quad_order), gauss_rule_01((quad_order + 2) // 2)
 
 
 def gauss_rule_01(n):
@@ -183,6 +210,44 @@ def project_rhs_separable(mesh_x, mesh_t, space_fn, time_fn, quad_order=6):
         q, w = _time_panels(ell, tq, tw)
         g[ell] = float(np.sum(w * time_fn(nodes[ell] + h * q)))
     return 2.0 * np.outer(s, g)
+
+
+def error_norms(coeffs, mesh_x, mesh_t, u, grad, dt, quad_order=None):
+    """Space-time L2 and H1-seminorm errors of the P1 x P1 function with
+    nodal coefficients `coeffs` (n_vertices x N_t, boundary values included,
+    zero at t = 0) against exact callables u, grad = (u_x, u_y), dt = u_t
+    (reference fem.py:358-418, same quadrature and summation structure).
+    Host restatement; `quadrature_gpu.error_norms_gpu` is the device path."""
+    if coeffs.shape != (mesh_x.n_vertices, mesh_t.n_cells):
+        raise DimensionMismatch(f"coeffs shape {coeffs.shape} does not match "
+                                f"{(mesh_x.n_vertices, mesh_t.n_cells)}")
+    (pts, wts), (tq, tw) = error_quadrature(quad_order)
+    area, grads = _geometry(mesh_x)
+    tris = mesh_x.triangles
+    x1, x2 = _space_points(mesh_x, pts)
+    lam = np.column_stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]])
+    w_sp = 2.0 * area[:, None] * wts[None, :]
+    full = np.hstack([np.zeros((mesh_x.n_vertices, 1)), coeffs])
+    nodes = np.asarray(mesh_t.nodes)
+    acc_l2 = acc_h1 = 0.0
+    for ell in range(mesh_t.n_cells):
+        h = nodes[ell + 1] - nodes[ell]
+        c_lo, c_hi = full[:, ell][tris], full[:, ell + 1][tris]
+        c_dt = (c_hi - c_lo) / h
+        for q, wq in zip(*_time_panels(ell, tq, tw)):
+            t = nodes[ell] + h * q
+            c = (1.0 - q) * c_lo + q * c_hi
+            uh = np.einsum("ti,qi->tq", c, lam)
+            duh = np.einsum("ti,qi->tq", c_dt, lam)
+            gh = np.einsum("ti,tid->td", c, grads)
+            wt = wq * h
+            e = u(x1, x2, t) - uh
+            acc_l2 += wt * np.sum(w_sp * e * e)
+            ed = dt(x1, x2, t) - duh
+            g1, g2 = grad(x1, x2, t)
+            e1, e2 = g1 - gh[:, None, 0], g2 - gh[:, None, 1]
+            acc_h1 += wt * np.sum(w_sp * (ed * ed + e1 * e1 + e2 * e2))
+    return math.sqrt(acc_l2), math.sqrt(acc_h1)
 
 
 def dirichlet_lift(mesh_x, mesh_t, g):
