@@ -109,7 +109,7 @@ def _tables(mesh_x, mesh_t, pts, wts, tq, tw, device):
     if len(wts) > 64:
         raise DimensionMismatch("at most 64 spatial quadrature points")
     dev = torch.device(device)
-    t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)
+    t = lambda a, dt=torch.float64: torch.as_tensor(np.array(a), dtype=dt).to(dev)
     q0, w0 = _time_panels(0, tq, tw)
     q1, w1 = _time_panels(1, tq, tw)
     tabs = dict(verts=t(mesh_x.vertices), tris=t(mesh_x.triangles, torch.int64), nodes=t(mesh_t.nodes),
