@@ -347,25 +347,6 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   for (int32_t f = 0; f < nf; ++f)
     for (int32_t k = S.child_ptr[f]; k < S.child_ptr[f + 1]; ++k) S.fronts[S.child_list[k]].parent = f;
 
-  // update-row structure, bottom-up (fronts are already in postorder)
-  std::vector<int64_t> mark(n, -1);
-  std::vector<std::vector<int64_t>> U(nf);
-  for (int32_t f = 0; f < nf; ++f) {
-    Front& F = S.fronts[f];
-    const int64_t last = F.first + F.p - 1;
-    std::vector<int64_t>& u = U[f];
-    for (int64_t v : piv[f])
-      for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
-        int64_t r = S.iperm[g.adj[e]];
-        if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
-      }
-    for (int32_t k = S.child_ptr[f]; k < S.child_ptr[f + 1]; ++k)
-      for (int64_t r : U[S.child_list[k]])
-        if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
-    std::sort(u.begin(), u.end());
-    F.q = (int32_t)u.size();
-  }
-  lap("updrows");
   // depth (parents have larger index than children)
   for (int32_t f = nf - 1; f >= 0; --f) {
     Front& F = S.fronts[f];
@@ -374,6 +355,46 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   }
   S.levels.assign(S.max_depth + 1, {});
   for (int32_t f = 0; f < nf; ++f) S.levels[S.fronts[f].depth].push_back(f);
+
+  // update-row structure, bottom-up level by level: the fronts of a level
+  // only read their children's rows, so a level's fronts are split over a
+  // few threads (each with its own marker array); results do not depend on
+  // the split
+  const int nth = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  std::vector<std::vector<int32_t>> marks(nth);
+  std::vector<std::vector<int64_t>> U(nf);
+  auto upd_rows = [&](const std::vector<int32_t>& lev, size_t i0, size_t i1, std::vector<int32_t>& mark) {
+    if (mark.empty()) mark.assign(n, -1);
+    for (size_t i = i0; i < i1; ++i) {
+      const int32_t f = lev[i];
+      Front& F = S.fronts[f];
+      const int64_t last = F.first + F.p - 1;
+      std::vector<int64_t>& u = U[f];
+      for (int64_t v : piv[f])
+        for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
+          int64_t r = S.iperm[g.adj[e]];
+          if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
+        }
+      for (int32_t k = S.child_ptr[f]; k < S.child_ptr[f + 1]; ++k)
+        for (int64_t r : U[S.child_list[k]])
+          if (r > last && mark[r] != f) { mark[r] = f; u.push_back(r); }
+      std::sort(u.begin(), u.end());
+      F.q = (int32_t)u.size();
+    }
+  };
+  for (int32_t d = S.max_depth; d >= 0; --d) {
+    const std::vector<int32_t>& lev = S.levels[d];
+    if (lev.size() < 64 || nth == 1) {
+      upd_rows(lev, 0, lev.size(), marks[0]);
+      continue;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back(upd_rows, std::cref(lev), lev.size() * t / nth, lev.size() * (t + 1) / nth,
+                      std::ref(marks[t]));
+    for (auto& x : th) x.join();
+  }
+  lap("updrows");
 
   // rows, relind, storage offsets, stats
   int64_t rows_total = 0;
@@ -452,37 +473,71 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   std::vector<int32_t> front_of(n, -1);
   for (int32_t f = 0; f < nf; ++f)
     for (int64_t k = 0; k < S.fronts[f].p; ++k) front_of[S.fronts[f].first + k] = f;
+  // two passes over row ranges, one range per thread: count per (thread,
+  // front), then fill at offsets that put thread t's entries of a front
+  // after those of threads < t -- the same order as one serial pass
   std::vector<int64_t> cnt(nf + 1, 0);
-  for (int64_t r = 0; r < n; ++r)
-    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
-      int64_t i = S.iperm[r], j = S.iperm[indices[e]];
-      if (i >= j) ++cnt[front_of[j] + 1];
-    }
-  for (int32_t f = 0; f < nf; ++f) cnt[f + 1] += cnt[f];
+  std::vector<std::vector<int64_t>> tcnt(nth, std::vector<int64_t>(nf, 0));
+  auto row_lo = [&](int t) { return (int64_t)n * t / nth; };
+  {
+    auto count = [&](int t) {
+      std::vector<int64_t>& c = tcnt[t];
+      for (int64_t r = row_lo(t); r < row_lo(t + 1); ++r)
+        for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+          int64_t i = S.iperm[r], j = S.iperm[indices[e]];
+          if (i >= j) ++c[front_of[j]];
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(count, t);
+    count(0);
+    for (auto& x : th) x.join();
+  }
+  for (int32_t f = 0; f < nf; ++f) {
+    int64_t tot = 0;
+    for (int t = 0; t < nth; ++t) tot += tcnt[t][f];
+    cnt[f + 1] = cnt[f] + tot;
+  }
   S.orig_src.resize(cnt[nf]);
   S.orig_dst.resize(cnt[nf]);
-  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-  for (int64_t r = 0; r < n; ++r)
-    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
-      int64_t i = S.iperm[r], j = S.iperm[indices[e]];
-      if (i < j) continue;
-      int32_t f = front_of[j];
-      const Front& F = S.fronts[f];
-      int32_t ri;
-      if (i < F.first + F.p) {
-        ri = (int32_t)(i - F.first);
-      } else {
-        const int64_t* prow = S.urows.data() + F.rows_begin;
-        const int64_t* it = std::lower_bound(prow, prow + F.q, i);
-        if (it == prow + F.q || *it != i) return "internal: entry outside front rows";
-        ri = F.p + (int32_t)(it - prow);
+  std::vector<std::string> errs(nth);
+  {
+    auto fill = [&](int t) {
+      std::vector<int64_t> pos(nf);
+      for (int32_t f = 0; f < nf; ++f) {
+        int64_t o = cnt[f];
+        for (int u = 0; u < t; ++u) o += tcnt[u][f];
+        pos[f] = o;
       }
-      int64_t dst = (int64_t)ri + (j - F.first) * (int64_t)F.m();
-      if (dst > INT32_MAX) return "front too large for 32-bit local offsets";
-      S.orig_src[pos[f]] = e;
-      S.orig_dst[pos[f]] = (int32_t)dst;
-      ++pos[f];
-    }
+      for (int64_t r = row_lo(t); r < row_lo(t + 1); ++r)
+        for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+          int64_t i = S.iperm[r], j = S.iperm[indices[e]];
+          if (i < j) continue;
+          int32_t f = front_of[j];
+          const Front& F = S.fronts[f];
+          int32_t ri;
+          if (i < F.first + F.p) {
+            ri = (int32_t)(i - F.first);
+          } else {
+            const int64_t* prow = S.urows.data() + F.rows_begin;
+            const int64_t* it = std::lower_bound(prow, prow + F.q, i);
+            if (it == prow + F.q || *it != i) { errs[t] = "internal: entry outside front rows"; return; }
+            ri = F.p + (int32_t)(it - prow);
+          }
+          int64_t dst = (int64_t)ri + (j - F.first) * (int64_t)F.m();
+          if (dst > INT32_MAX) { errs[t] = "front too large for 32-bit local offsets"; return; }
+          S.orig_src[pos[f]] = e;
+          S.orig_dst[pos[f]] = (int32_t)dst;
+          ++pos[f];
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(fill, t);
+    fill(0);
+    for (auto& x : th) x.join();
+  }
+  for (auto& e : errs)
+    if (!e.empty()) return e;
   // deterministic, write-coalescing order inside each front (fronts are
   // independent: sorted by a few threads over contiguous front ranges)
   auto sort_fronts = [&](int32_t f0, int32_t f1) {
@@ -500,7 +555,6 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     }
   };
   {
-    const int nth = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
     if (nf < 256 || nth == 1) {
       sort_fronts(0, nf);
     } else {
