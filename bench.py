@@ -298,6 +298,14 @@ def main():
     fac_flops = stats["flops"] * n_shift_local
     peaks = measured_peaks(dev) if rank == 0 else {}
 
+    # per-level roofline of the factorization ("report the
+    # fraction against whichever bound is binding, per tree level"): one more
+    # factorization outside the timed region with CUDA events at the level
+    # boundaries; algorithmic flops and bytes per level from the fronts
+    levels = None
+    if not sharded and len(eng.pipes) == 1 and eng.keep_factors:
+        levels = factor_levels(eng, peaks)
+
     # per-phase rooflines from the CUDA events around each phase (engine.timers)
     kernels = {}
     if not sharded:
@@ -376,7 +384,7 @@ def main():
                          "peak_source": peaks.get("fp64_source"),
                          "flops_per_shift": stats["flops"], "shifts": int(n_shift_local),
                          "ms_per_step": fac_s * 1e3, "share_of_step": fac_s * 1e3 / ms,
-                         "traffic": traffic},
+                         "traffic": traffic, "levels": levels},
             "e2e": e2e,
             "kernels": kernels,
         }
@@ -402,6 +410,47 @@ def load_traffic(cfg):
         return None if ent is None else ent["factor_dram_bytes_per_step"]
     except (OSError, ValueError, KeyError):
         return None
+
+
+def factor_levels(eng, peaks):
+    """Per tree level: fronts, ms, algorithmic TF/s and GB/s and their
+    fractions of the FP64 / HBM peaks, for one factorization of all shifts
+    (forward sweep fused, as in the step). Bytes: each front's panel (m p)
+    and update block (q(q+1)/2) written once and its children's update
+    blocks read once, 16 B per complex entry."""
+    import torch
+
+    plan = eng.pipes[0][0]
+    first, p, q, par, dep, _ = eng.sym.fronts()
+    m = (p + q).astype(np.float64)
+    flops = np.zeros(len(p))
+    for f in range(len(p)):
+        r = m[f] - np.arange(p[f]) - 1.0
+        flops[f] = float(np.sum(8.0 * r * (r + 1.0) / 2.0 + 8.0 * r))
+    upd = q.astype(np.float64) * (q + 1) / 2.0
+    child_upd = np.zeros(len(p))
+    for f in range(len(p)):
+        if par[f] >= 0:
+            child_upd[par[f]] += upd[f]
+    nbytes = 16.0 * (m * p + upd + child_upd)
+    plan.set_level_timing(True)
+    eng.factored = False
+    eng.event_log = eng.timers = None
+    eng._spatial()
+    torch.cuda.synchronize()
+    ms = plan.level_times()
+    plan.set_level_timing(False)
+    nk = eng.n_k
+    out = []
+    for d in range(len(ms)):
+        sel = dep == d
+        fl, by = flops[sel].sum() * nk, nbytes[sel].sum() * nk
+        t = ms[d] / 1e3
+        tf, gb = (fl / t / 1e12, by / t / 1e9) if t > 0 else (0.0, 0.0)
+        out.append({"depth": d, "fronts": int(sel.sum()), "max_m": int(m[sel].max()), "ms": float(ms[d]),
+                    "tflops": tf, "frac_fp64": tf / peaks["fp64_tflops"] if peaks.get("fp64_tflops") else None,
+                    "gbs": gb, "frac_hbm": gb / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None})
+    return out
 
 
 def measure_e2e(system, pencil, args, leaf):

@@ -140,6 +140,13 @@ int kh_plan_factor_fwd(kh_plan* plan, int64_t slot0, int64_t nshift, const doubl
                        const double* b_im, int64_t ldb, void* stream);
 int kh_plan_solve_bwd(kh_plan* plan, int64_t slot0, int64_t nshift, double* x_re, double* x_im, int64_t ldx,
                       void* stream);
+/* Per-level timing of the factorization (measurement aid for the per-level
+ * roofline): with timing on, the next factorizations record CUDA events at
+ * every level boundary on the caller's stream; kh_plan_level_times waits for
+ * the last one and returns the milliseconds of each level of the most recent
+ * factorization, indexed by tree depth (0 = root), n_levels = depth + 1. */
+int kh_plan_set_level_timing(kh_plan* plan, int32_t on);
+int kh_plan_level_times(kh_plan* plan, float* ms, int32_t n_levels);
 /* R = F - (M Y[:, :nt] + A Y[:, nt:2nt]) on the plan's CSR (device arrays);
  * R may be NULL. norms2 (device, 2 doubles) receives ||R||_F^2, ||F||_F^2. */
 int kh_plan_residual(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,

@@ -90,6 +90,10 @@ struct kh_plan {
   cudaStream_t side[kSmallClasses] = {};
   cudaEvent_t ev_main = nullptr, ev_side[kSmallClasses] = {};
   cudaEvent_t ev_fwd = nullptr;  // large fronts' panels final (fused forward sweep may start)
+  // optional per-level timing of the factorization (kh_plan_set_level_timing):
+  // lvl_ev[i] recorded on the caller's stream before level depth - i and at the end
+  bool level_timing = false;
+  std::vector<cudaEvent_t> lvl_ev;
   int32_t depth = 0;
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
@@ -139,6 +143,8 @@ void plan_release(kh_plan* p) {
   p->ev_main = nullptr;
   if (p->ev_fwd) cudaEventDestroy(p->ev_fwd);
   p->ev_fwd = nullptr;
+  for (cudaEvent_t e : p->lvl_ev) cudaEventDestroy(e);
+  p->lvl_ev.clear();
   for (int c = 0; c < kSmallClasses; ++c) {
     if (p->ev_side[c]) cudaEventDestroy(p->ev_side[c]);
     if (p->side[c]) cudaStreamDestroy(p->side[c]);
@@ -623,7 +629,15 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
   const KhTree T = p->tree();
   double2* panels = p->panels + slot0 * p->panel_total;
   KH_CUDA(fork_side(p, st));
+  if (p->level_timing && p->lvl_ev.size() < (size_t)p->depth + 2) {
+    for (size_t i = p->lvl_ev.size(); i < (size_t)p->depth + 2; ++i) {
+      cudaEvent_t e;
+      KH_CUDA(cudaEventCreate(&e));
+      p->lvl_ev.push_back(e);
+    }
+  }
   for (int32_t d = p->depth; d >= 0; --d) {
+    if (p->level_timing) KH_CUDA(cudaEventRecord(p->lvl_ev[p->depth - d], st));
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
     double2 *uc = p->upd[d & 1], *uch = p->upd[(d + 1) & 1];
@@ -654,6 +668,7 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
                             sc, uch, sch, st));
     KH_CUDA(join_side(p, st));
   }
+  if (p->level_timing) KH_CUDA(cudaEventRecord(p->lvl_ev[p->depth + 1], st));
   KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));
   KH_CUDA(kh_launch_shift_absmax_nnz(p->mv, p->av, p->nnz, (int32_t)nshift, p->lam, p->absmax_work,
                                      kAbsmaxBlocks, st));
@@ -724,6 +739,27 @@ int kh_plan_factor_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double
   const int rc = kh_plan_factor_fwd(p, slot0, nshift, lambda_ri, b_re, b_im, ldb, stream);
   if (rc != KH_OK) return rc;
   return kh_plan_solve_bwd(p, slot0, nshift, x_re, x_im, ldx, stream);
+}
+
+int kh_plan_set_level_timing(kh_plan* p, int32_t on) {
+  if (!p) return fail(KH_ERR_INVALID, "null argument");
+  p->level_timing = on != 0;
+  return KH_OK;
+}
+
+int kh_plan_level_times(kh_plan* p, float* ms, int32_t n_levels) {
+  if (!p || !ms) return fail(KH_ERR_INVALID, "null argument");
+  if (n_levels != p->depth + 1) return fail(KH_ERR_DIMENSION, "n_levels must be the tree depth + 1");
+  if (!p->level_timing || p->lvl_ev.size() < (size_t)p->depth + 2)
+    return fail(KH_ERR_INVALID, "level timing was not enabled for the last factorization");
+  KH_CUDA(cudaSetDevice(p->device));
+  KH_CUDA(cudaEventSynchronize(p->lvl_ev[p->depth + 1]));
+  for (int32_t i = 0; i <= p->depth; ++i) {
+    float t = 0.f;
+    KH_CUDA(cudaEventElapsedTime(&t, p->lvl_ev[i], p->lvl_ev[i + 1]));
+    ms[p->depth - i] = t;  // index by depth (0 = root)
+  }
+  return KH_OK;
 }
 
 int kh_plan_pivot_check(kh_plan* p, int64_t slot0, int64_t nshift, double rel_threshold, void* stream,

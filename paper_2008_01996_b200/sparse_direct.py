@@ -170,6 +170,17 @@ class _Plan:
         _native.call("kh_plan_factor_solve", self.raw, int(slot0), len(lam), _native.ptr(lam), b_re, b_im, int(ldb),
                      x_re, x_im, int(ldx), stream)
 
+    def set_level_timing(self, on):
+        _native.call("kh_plan_set_level_timing", self.raw, int(bool(on)))
+
+    def level_times(self):
+        """Milliseconds per tree level (index = depth, 0 = root) of the most
+        recent factorization (after set_level_timing(True))."""
+        nl = int(self.symbolic.stats["depth"]) + 1
+        out = np.zeros(nl, dtype=np.float32)
+        _native.call("kh_plan_level_times", self.raw, out.ctypes.data, nl)
+        return out.astype(np.float64)
+
     def factor_fwd(self, slot0, lambdas, b_re, b_im, ldb, stream):
         lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.complex128))
         _native.call("kh_plan_factor_fwd", self.raw, int(slot0), len(lam), _native.ptr(lam), b_re, b_im, int(ldb),
