@@ -454,6 +454,9 @@ __device__ unsigned long long g_phase[9 * 8];
 #endif
 
 constexpr int kDeferSyrk = 48;
+#ifndef KH_BULK_WRITE
+#define KH_BULK_WRITE 1
+#endif
 #ifndef KH_LOOKAHEAD_MIN_NW
 #define KH_LOOKAHEAD_MIN_NW 4
 #endif
@@ -965,8 +968,39 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
       if (r < m) xs[r] = x[v];
     }
   }
-  // ---- write the panel and the update matrix (lower parts), coalesced:
-  // warp per column, lanes down the rows
+  // ---- write the panel and the update matrix (lower parts)
+#if KH_BULK_WRITE
+  // every column's lower part is contiguous both in the packed shared layout
+  // and in global memory: one bulk async copy (TMA, async proxy) per column,
+  // issued by the last warp's lanes, so the CTA does not spend issue slots
+  // and registers on the stores (it only waits for the shared-memory reads)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const bool issuer = warp == NW - 1;
+  if (issuer) {
+    for (int c = lane; c < m; c += 32) {
+      const double2* src;
+      double2* dst;
+      int rows;
+      if (c < p) {
+        src = S + cb[c] + c;
+        dst = P + c + (int64_t)c * m;
+        rows = m - c;
+      } else {
+        const int cc = c - p;
+        src = S + cb[c] + c;
+        dst = U + cc + (int64_t)cc * q;
+        rows = q - cc;
+      }
+      const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(src));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(saddr),
+                   "r"(rows * 16)
+                   : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+#else
+  // coalesced: warp per column, lanes down the rows
   for (int c = warp; c < p; c += NW) {
     const int base = cb[c];
     for (int r = c + lane; r < m; r += 32) P[r + (int64_t)c * m] = S[base + r];
@@ -975,6 +1009,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
     const int base = cb[p + c] + p;
     for (int r = c + lane; r < q; r += 32) U[r + (int64_t)c * q] = S[base + r];
   }
+#endif
   if (FWD) {
     __syncthreads();
     double2* yb = fw.y + (int64_t)b * T.n + F.first;
@@ -985,6 +1020,10 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
     }
   }
   if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+#if KH_BULK_WRITE
+  // shared memory must outlive the bulk copies' reads of it
+  if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
   phase(3);
 }
 
