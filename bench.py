@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--j-max", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-levels", action="store_true",
+                    help="skip the extra per-level-timed factorization (launch-list captures)")
     ap.add_argument("--collective", choices=["p2p", "nccl", "alltoall"], default="p2p",
                     help="N>1 back-transform reduce-scatter: fused GEMM + peer-memory scatter, or NCCL")
     ap.add_argument("--force-sharded", action="store_true",
@@ -303,7 +305,7 @@ def main():
     # factorization outside the timed region with CUDA events at the level
     # boundaries; algorithmic flops and bytes per level from the fronts
     levels = None
-    if not sharded and len(eng.pipes) == 1 and eng.keep_factors:
+    if not sharded and len(eng.pipes) == 1 and eng.keep_factors and not args.no_levels:
         levels = factor_levels(eng, peaks)
 
     # per-phase rooflines from the CUDA events around each phase (engine.timers)
