@@ -453,12 +453,15 @@ KH_DEV void tri_index(int t, int& bi, int& bj) {
 __device__ unsigned long long g_phase[9 * 8];
 #endif
 
-constexpr int kDeferSyrk = 48;
+#ifndef KH_DEFER_SYRK
+#define KH_DEFER_SYRK 48
+#endif
+constexpr int kDeferSyrk = KH_DEFER_SYRK;
 #ifndef KH_BULK_WRITE
 #define KH_BULK_WRITE 1
 #endif
 #ifndef KH_LOOKAHEAD_MIN_NW
-#define KH_LOOKAHEAD_MIN_NW 4
+#define KH_LOOKAHEAD_MIN_NW 16
 #endif
 // look-ahead pays off when the CTA has warps enough to hide the serial (a) phase
 KH_HD constexpr bool kLookAhead(int nw) { return nw >= KH_LOOKAHEAD_MIN_NW; }
@@ -1130,7 +1133,13 @@ __global__ void __launch_bounds__(NT) fwd_level_kernel(KhTree T, const int32_t* 
 constexpr int FWD_W = 32;
 // levels with at most this many (front, shift) CTAs use the narrow-level
 // solves (crossover measured at c3: profiles/r1_solve_levels.md)
-constexpr int64_t kNarrowLevelCtas = 1024, kNarrowLevelCtasBwd = 2048;
+#ifndef KH_NARROW_FWD
+#define KH_NARROW_FWD 1024
+#endif
+#ifndef KH_NARROW_BWD
+#define KH_NARROW_BWD 2048
+#endif
+constexpr int64_t kNarrowLevelCtas = KH_NARROW_FWD, kNarrowLevelCtasBwd = KH_NARROW_BWD;
 __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                           const double2* __restrict__ panels, double2* y,
                                                           double2* ru_cur, int64_t ru_stride_cur,

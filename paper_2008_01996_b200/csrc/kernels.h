@@ -68,8 +68,14 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
                                 cudaStream_t stream);
 // Level-synchronous kernels for the large fronts (see frontal.cu). Tasks are
 // (front, index) int32 pairs; schur tasks are (front, tile row, tile col).
-constexpr int KH_ASM_CHUNK = 1024;
-constexpr int KH_TRSM_ROWS = 128;  // rows per TRSM task
+#ifndef KH_ASM_CHUNK_DEF
+#define KH_ASM_CHUNK_DEF 512
+#endif
+constexpr int KH_ASM_CHUNK = KH_ASM_CHUNK_DEF;
+#ifndef KH_TRSM_ROWS_DEF
+#define KH_TRSM_ROWS_DEF 128
+#endif
+constexpr int KH_TRSM_ROWS = KH_TRSM_ROWS_DEF;  // rows per TRSM task
 cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
                                    const double2* lam, double2* panels, const double2* upd_child,
                                    int64_t upd_stride_child, cudaStream_t stream);
