@@ -45,7 +45,10 @@ constexpr int32_t kDefaultLeaf = 24;
 constexpr int kSmallClasses = 5;
 constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, 96, 128};
 // the warp-per-front solve kernels take the classes with m <= 64
-constexpr int kSolveSmallClasses = kSmallClasses - 2;  // classes with m <= 64: warp-per-front solves
+#ifndef KH_SOLVE_SMALL_CLASSES
+#define KH_SOLVE_SMALL_CLASSES 3
+#endif
+constexpr int kSolveSmallClasses = KH_SOLVE_SMALL_CLASSES;  // classes m <= 64: warp-per-front solves
 constexpr int kClsStride = kSmallClasses + 2;
 constexpr int32_t kAbsmaxBlocks = 64;
 constexpr int32_t kResidualBlocks = 1184;  // 8 x 148 SMs

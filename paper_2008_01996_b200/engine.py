@@ -311,6 +311,10 @@ class FDEngine:
         g, z = self.G.data_ptr(), self.Z.data_ptr()
         depth = self.sym.stats["depth"] + 1
         fuse = not (self.keep_factors and self.factored)
+        if fuse and self.keep_factors and os.environ.get("KH_FUSED_FWD", "1") == "0":
+            # A/B switch: separate factorization, then the standalone sweeps
+            self.factor(events=self.event_log)
+            fuse = False
         log = self.event_log if fuse else None
         main = torch.cuda.current_stream(self.device)
         if log is not None:
