@@ -346,6 +346,7 @@ def main():
     # the e2e runs build their own plans: release this one's device memory
     # first (at c4 its retained factors take 136 GB of the 180)
     coll = runner.collective if runner is not None else args.collective
+    fused_fwd = bool(getattr(eng, "fuse_forward", False))
     eng = runner = U = F = None
     import gc
 
@@ -379,8 +380,9 @@ def main():
             "gpu_launches": int(launches),
             "clocks": ck,
             "roofline": {"kernel": "batched multifrontal complex LDL^T: all launches of one factorization "
-                                   "(factor_front_kernel, big_*, schur_update_kernel; the first solve's "
-                                   "forward sweep runs fused inside, its flops are not counted)",
+                                   "(factor_front_kernel, big_*, schur_update_kernel"
+                                   + ("; the first solve's forward sweep runs fused inside, its flops are "
+                                      "not counted)" if fused_fwd else ")"),
                          "bound": "tensor", "achieved": achieved, "peak": peaks.get("fp64_tflops"),
                          "unit": "TFLOP/s", "frac": (achieved / peaks["fp64_tflops"]) if achieved else None,
                          "peak_source": peaks.get("fp64_source"),

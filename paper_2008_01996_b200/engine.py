@@ -139,7 +139,8 @@ class FDEngine:
     """Device-resident FD solver for one (M_x, A_x, temporal pencil) triple."""
 
     def __init__(self, M_x, A_x, modal, device=None, keep_factors=None, max_batch=None,
-                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None, pipes=1):
+                 leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None, pipes=1,
+                 fuse_forward=None):
         import torch
 
         _native.require_cuda()
@@ -204,6 +205,16 @@ class FDEngine:
             self.pipes.append((plan, k0, k1, b, torch.cuda.Stream(device=self.device)))
         self.plan = self.pipes[0][0]   # residual kernels (CSR of M, A) and single-pipe callers
         self.factored = False
+        # first application with retained factors: factor with the forward
+        # sweep fused (kh_plan_factor_fwd) or factor, then sweep. Measured
+        # equal at c3 (42.02 ms/step either way: the in-kernel sweep costs
+        # what the standalone pass does), so the default keeps the two
+        # apart and the factorization's roofline clean; without retained
+        # factors every application is fused (no extra pass over factors
+        # that are discarded anyway). KH_FUSED_FWD=1 flips the default.
+        if fuse_forward is None:
+            fuse_forward = os.environ.get("KH_FUSED_FWD", "0") == "1"
+        self.fuse_forward = bool(fuse_forward)
 
         dev = self.device
         f64 = torch.float64
@@ -311,8 +322,8 @@ class FDEngine:
         g, z = self.G.data_ptr(), self.Z.data_ptr()
         depth = self.sym.stats["depth"] + 1
         fuse = not (self.keep_factors and self.factored)
-        if fuse and self.keep_factors and os.environ.get("KH_FUSED_FWD", "1") == "0":
-            # A/B switch: separate factorization, then the standalone sweeps
+        if fuse and self.keep_factors and not self.fuse_forward:
+            # separate factorization, then the standalone sweeps
             self.factor(events=self.event_log)
             fuse = False
         log = self.event_log if fuse else None

@@ -140,3 +140,25 @@ def test_bs_complex_matches_reference(cuda_ok, name):
     assert rel_diff(sol.coefficients, ref["bs"]) < 1e-11
     assert rep.residual < 1e-12
     assert rep.analyze_calls == 1
+
+
+@pytest.mark.parametrize("name", ["c1", "lshape0"])
+def test_fused_forward_sweep_agrees(cuda_ok, name):
+    """The first application with the forward sweep fused into the
+    factorization (kh_plan_factor_fwd) and the separate factor + sweeps give
+    the same solution (different rounding order only)."""
+    import torch
+
+    from paper_2008_01996_b200.engine import FDEngine, modal_plan
+
+    system, ref = load_golden(name)
+    modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
+    F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
+    out = []
+    for fuse in (True, False):
+        eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, fuse_forward=fuse)
+        U, info = eng.solve(F)   # refined: the plain FD amplifies rounding by kappa_2(X_t)
+        out.append(U.cpu().numpy().ravel())
+        assert eng.factored and info["residual"] < 1e-12
+    assert rel_diff(out[0], out[1]) < 1e-12
+    assert rel_diff(out[1], ref["bs"]) < 1e-10
