@@ -43,7 +43,10 @@ constexpr int32_t kDefaultLeaf = 24;
 // fronts with m <= kClassMax[c] use the register-resident kernels; the rest
 // ("large", class kSmallClasses) the level-synchronous DMMA kernels
 constexpr int kSmallClasses = 5;
-constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, 96, 128};
+#ifndef KH_CLASS4
+#define KH_CLASS4 96
+#endif
+constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, KH_CLASS4, 128};
 // the warp-per-front solve kernels take the classes with m <= 64
 #ifndef KH_SOLVE_SMALL_CLASSES
 #define KH_SOLVE_SMALL_CLASSES 3

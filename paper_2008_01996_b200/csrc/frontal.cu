@@ -752,7 +752,11 @@ KH_HD constexpr int front_smem_bytes(int ms) {
   return 16 * (packed_elems(ms) + (front_has_w(ms) ? 8 * (ms + 2) : 0) + 8 + 2 * ms) + 4 * ms + 4 * 4 * ms;
 }
 
-// warps per CTA of the fused classes m <= 64, 96, 128
+// the fourth fused class (m <= KH_CLASS4, between 64 and 128)
+#ifndef KH_CLASS4
+#define KH_CLASS4 96
+#endif
+// warps per CTA of the fused classes m <= 64, KH_CLASS4, 128
 #ifndef KH_NW64
 #define KH_NW64 4
 #endif
@@ -1836,8 +1840,8 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                         : run(factor_front_kernel<48, 2, false>, 48, 64, a[v][1]);
     case 64: return fwd ? run(factor_front_kernel<64, KH_NW64, true>, 64, 32 * KH_NW64, a[v][2])
                         : run(factor_front_kernel<64, KH_NW64, false>, 64, 32 * KH_NW64, a[v][2]);
-    case 96: return fwd ? run(factor_front_kernel<96, KH_NW96, true>, 96, 32 * KH_NW96, a[v][3])
-                        : run(factor_front_kernel<96, KH_NW96, false>, 96, 32 * KH_NW96, a[v][3]);
+    case KH_CLASS4: return fwd ? run(factor_front_kernel<KH_CLASS4, KH_NW96, true>, KH_CLASS4, 32 * KH_NW96, a[v][3])
+                        : run(factor_front_kernel<KH_CLASS4, KH_NW96, false>, KH_CLASS4, 32 * KH_NW96, a[v][3]);
     case 128: return fwd ? run(factor_front_kernel<128, KH_NW128, true>, 128, 32 * KH_NW128, a[v][4])
                          : run(factor_front_kernel<128, KH_NW128, false>, 128, 32 * KH_NW128, a[v][4]);
     default: return cudaErrorInvalidValue;
