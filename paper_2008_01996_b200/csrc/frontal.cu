@@ -709,7 +709,10 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
 // LDL^T of the w x w diagonal block at kb of a large front: one 64-thread CTA
 // per (front, shift), the block staged in shared memory and factored by
 // blocked_ldlt (8-pivot blocks, DMMA trailing updates).
-constexpr int DIAG_NW = 2, DIAG_LD = NB + 2;
+#ifndef KH_DIAG_NW
+#define KH_DIAG_NW 2
+#endif
+constexpr int DIAG_NW = KH_DIAG_NW, DIAG_LD = NB + 2;
 __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
                                                                 int nfr, int kb, double2* panels, double* minpiv) {
   __shared__ double2 S[NB * DIAG_LD];
@@ -757,6 +760,12 @@ KH_HD constexpr int front_smem_bytes(int ms) {
 #define KH_CLASS4 96
 #endif
 // warps per CTA of the fused classes m <= 64, KH_CLASS4, 128
+#ifndef KH_NW32
+#define KH_NW32 2
+#endif
+#ifndef KH_NW48
+#define KH_NW48 2
+#endif
 #ifndef KH_NW64
 #define KH_NW64 4
 #endif
@@ -767,7 +776,7 @@ KH_HD constexpr int front_smem_bytes(int ms) {
 #define KH_NW128 16
 #endif
 #ifndef KH_F32_MINB
-#define KH_F32_MINB 8
+#define KH_F32_MINB 10
 #endif
 // resident CTAs per SM the register allocation must allow
 KH_HD constexpr int front_min_blocks(int ms, int nw) {
@@ -1834,10 +1843,10 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
   static bool a[2][5] = {};
   const int v = fwd ? 1 : 0;
   switch (ms) {
-    case 32: return fwd ? run(factor_front_kernel<32, 2, true>, 32, 64, a[v][0])
-                        : run(factor_front_kernel<32, 2, false>, 32, 64, a[v][0]);
-    case 48: return fwd ? run(factor_front_kernel<48, 2, true>, 48, 64, a[v][1])
-                        : run(factor_front_kernel<48, 2, false>, 48, 64, a[v][1]);
+    case 32: return fwd ? run(factor_front_kernel<32, KH_NW32, true>, 32, 32 * KH_NW32, a[v][0])
+                        : run(factor_front_kernel<32, KH_NW32, false>, 32, 32 * KH_NW32, a[v][0]);
+    case 48: return fwd ? run(factor_front_kernel<48, KH_NW48, true>, 48, 32 * KH_NW48, a[v][1])
+                        : run(factor_front_kernel<48, KH_NW48, false>, 48, 32 * KH_NW48, a[v][1]);
     case 64: return fwd ? run(factor_front_kernel<64, KH_NW64, true>, 64, 32 * KH_NW64, a[v][2])
                         : run(factor_front_kernel<64, KH_NW64, false>, 64, 32 * KH_NW64, a[v][2]);
     case KH_CLASS4: return fwd ? run(factor_front_kernel<KH_CLASS4, KH_NW96, true>, KH_CLASS4, 32 * KH_NW96, a[v][3])
