@@ -140,7 +140,7 @@ class FDEngine:
 
     def __init__(self, M_x, A_x, modal, device=None, keep_factors=None, max_batch=None,
                  leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, mem_fraction=0.85, symbolic=None, pipes=1,
-                 fuse_forward=None):
+                 fuse_forward=None, aligned=None):
         import torch
 
         _native.require_cuda()
@@ -156,8 +156,8 @@ class FDEngine:
         self.n_t = modal.n_t
         self.n_k = modal.n_k
         self.sym = symbolic if symbolic is not None else sparse_direct.analyze((M + A).tocsr(), leaf_size)
-        mv = self.sym.align_values(M)
-        av = self.sym.align_values(A)
+        # values of M and A on the analyzed pattern (`aligned` = precomputed pair)
+        mv, av = aligned if aligned is not None else (self.sym.align_values(M), self.sym.align_values(A))
 
         # shift pipelines: the shifts are split into `pipes` contiguous ranges,
         # each with its own plan (factor storage, work space, side streams) and
@@ -170,8 +170,14 @@ class FDEngine:
         bounds = [round(i * self.n_k / npipe) for i in range(npipe + 1)]
         sizes = [max(bounds[i + 1] - bounds[i], 1) for i in range(npipe)]
 
+        sized = {}
+
         def total_bytes(b, keep):
-            return sum(sparse_direct.plan_bytes(self.sym, min(b, sz), sz if keep else min(b, sz)) for sz in sizes)
+            # each plan_bytes builds the launch schedule on the host: memoise
+            if (b, keep) not in sized:
+                sized[(b, keep)] = sum(sparse_direct.plan_bytes(self.sym, min(b, sz), sz if keep else min(b, sz))
+                                       for sz in sizes)
+            return sized[(b, keep)]
 
         # memory plan: keep every shift's factors when they fit
         with torch.cuda.device(self.device):
