@@ -87,6 +87,10 @@ int kh_symbolic_perm(const kh_symbolic* s, int64_t* perm);
 /* Per-front arrays (host, n_fronts each; any may be NULL). */
 int kh_symbolic_fronts(const kh_symbolic* s, int64_t* first, int32_t* npiv, int32_t* nupd, int32_t* parent,
                        int32_t* depth);
+/* The analyzed CSR (host, n + 1 and stats.nnz entries): the input pattern
+ * symmetrized (A | A^T) with the full diagonal, rows sorted, no duplicates.
+ * Value arrays for kh_plan_create are aligned to it (kh_align_values). */
+int kh_symbolic_pattern(const kh_symbolic* s, int64_t* indptr, int64_t* indices);
 /* Concatenated update-row lists (permuted positions), sum of nupd entries. */
 int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows);
 void kh_symbolic_free(kh_symbolic* s);

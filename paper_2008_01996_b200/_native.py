@@ -65,6 +65,7 @@ SIGNATURES = {
     "kh_symbolic_perm": (ctypes.c_int, [_vp, _vp]),
     "kh_symbolic_fronts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "kh_symbolic_rows": (ctypes.c_int, [_vp, _vp]),
+    "kh_symbolic_pattern": (ctypes.c_int, [_vp, _vp, _vp]),
     "kh_align_values": (ctypes.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kh_symbolic_free": (None, [_vp]),
     "kh_plan_create": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _P(_vp)]),

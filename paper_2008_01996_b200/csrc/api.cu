@@ -324,6 +324,13 @@ int kh_align_values(int64_t n, const int64_t* pat_indptr, const int64_t* pat_ind
   return KH_OK;
 }
 
+int kh_symbolic_pattern(const kh_symbolic* s, int64_t* indptr, int64_t* indices) {
+  if (!s || !indptr || (s->S.nnz && !indices)) return fail(KH_ERR_INVALID, "null argument");
+  std::memcpy(indptr, s->S.pat_ptr.data(), sizeof(int64_t) * s->S.pat_ptr.size());
+  if (s->S.nnz) std::memcpy(indices, s->S.pat_idx.data(), sizeof(int64_t) * s->S.nnz);
+  return KH_OK;
+}
+
 int kh_symbolic_rows(const kh_symbolic* s, int64_t* rows) {
   if (!s || (!rows && !s->S.urows.empty())) return fail(KH_ERR_INVALID, "null argument");
   std::copy(s->S.urows.begin(), s->S.urows.end(), rows);

@@ -31,6 +31,9 @@ struct Front {
 struct Symbolic {
   int64_t n = 0;
   int64_t nnz = 0;                 // entries of the analyzed CSR (values arrays are aligned to it)
+  // the analyzed CSR: the input pattern made symmetric (A | A^T), with the
+  // full diagonal, rows sorted, no duplicates
+  std::vector<int64_t> pat_ptr, pat_idx;
   std::vector<int64_t> perm;       // perm[k] = original index eliminated k-th
   std::vector<int64_t> iperm;      // iperm[orig] = k
   std::vector<Front> fronts;       // postorder (children before parents)

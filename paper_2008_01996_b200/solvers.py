@@ -289,11 +289,11 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     # the two host phases and the H2D copy overlap instead of adding up.
     t0 = time.perf_counter()
     analyze_before = sparse_direct.analyze_call_count()
-    pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
     phases = report.phases
 
     def _analyze():
         a0 = time.perf_counter()
+        pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
         out = sparse_direct.analyze(pattern, leaf_size)
         phases["analyze"] = time.perf_counter() - a0
         return out

@@ -121,16 +121,25 @@ class SymbolicFactorization:
 def analyze(pattern, leaf_size=DEFAULT_LEAF_SIZE):
     """Symbolic analysis of a sparsity pattern (symmetrized by union first)."""
     global _analyze_calls
-    indptr, indices = symmetrized_pattern(pattern)
-    n = len(indptr) - 1
+    # the native analysis symmetrizes the pattern itself (A | A^T, diagonal
+    # added, duplicates merged) and returns that canonical CSR
+    A = sp.csr_matrix(pattern)
+    if A.shape[0] != A.shape[1]:
+        raise DimensionMismatch("pattern must be square")
+    n = A.shape[0]
+    in_ptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    in_idx = np.ascontiguousarray(A.indices, dtype=np.int64)
     lib = _native.load()
     raw = ctypes.c_void_p()
-    _native.check(lib.kh_analyze(n, _native.ptr(indptr), _native.ptr(indices), int(leaf_size),
+    _native.check(lib.kh_analyze(n, _native.ptr(in_ptr), _native.ptr(in_idx), int(leaf_size),
                                  ctypes.byref(raw)))
     handle = _Handle(raw.value)
     st = _native.SymbolicStats()
     _native.check(lib.kh_symbolic_stats_get(handle.raw, ctypes.byref(st)))
     stats = {name: getattr(st, name) for name, _ in st._fields_}
+    indptr = np.zeros(n + 1, np.int64)
+    indices = np.zeros(int(st.nnz), np.int64)
+    _native.check(lib.kh_symbolic_pattern(handle.raw, _native.ptr(indptr), _native.ptr(indices)))
     perm = np.zeros(n, np.int64)
     if n:
         _native.check(lib.kh_symbolic_perm(handle.raw, _native.ptr(perm)))

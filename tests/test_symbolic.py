@@ -125,3 +125,22 @@ def test_analysis_is_deterministic():
     a, b = sd.analyze(K), sd.analyze(K)
     assert np.array_equal(a.perm, b.perm)
     assert a.stats == b.stats
+
+
+def test_native_pattern_is_the_symmetrized_union():
+    """kh_symbolic_pattern returns A | A^T with the full diagonal, sorted and
+    without duplicates -- the same CSR as the host symmetrization."""
+    import scipy.sparse as sp
+
+    from paper_2008_01996_b200 import sparse_direct as sd
+
+    rng = np.random.default_rng(3)
+    n = 300
+    A = sp.random(n, n, density=0.02, random_state=rng, format="csr")
+    A = (A + sp.eye(n, format="csr") * 0).tocsr()
+    dup = sp.csr_matrix((np.ones(5), ([0, 0, 1, 7, 7], [3, 3, 2, 9, 9])), shape=(n, n))
+    P = (A + dup).tocsr()
+    s = sd.analyze(P, 8)
+    ip, ix = sd.symmetrized_pattern(P + sp.eye(n, format="csr"))
+    assert np.array_equal(s.indptr, ip) and np.array_equal(s.indices, ix)
+    assert s.stats["nnz"] == len(ix)
