@@ -21,6 +21,7 @@ reference. The report keeps every reference field and adds `t_refine`,
 refinement).
 """
 
+import os
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -307,7 +308,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
         # few BLAS threads: dgeev / the SVD of an N_t <= 512 matrix gain
         # nothing from more, and the dissection threads of the analysis
         # need the cores
-        with _blas_threads(1 if nt <= 512 else 4):
+        with _blas_threads(int(os.environ.get("KH_PENCIL_THREADS", 1 if nt <= 512 else 4))):
             if pencil is None:
                 pencil = build_pencil(system.temporal, "fd", eig="reduced")
             phases["pencil"] = time.perf_counter() - t0
