@@ -13,7 +13,13 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, NST = 3;
+#ifndef KH_GEMM_BK
+#define KH_GEMM_BK 16
+#endif
+#ifndef KH_GEMM_NST
+#define KH_GEMM_NST 3
+#endif
+constexpr int BM = 128, BN = 64, BK = KH_GEMM_BK, NST = KH_GEMM_NST;
 constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
 constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
 constexpr size_t SMEM_BYTES = sizeof(double) * NST * (A_STAGE + B_STAGE);
