@@ -18,7 +18,10 @@ namespace {
 // time column) and sweeps the time columns; consecutive threads touch
 // consecutive rows, so the Y / F / R accesses are coalesced. Items are handed
 // out by a fixed grid-stride loop, so the partial sums are deterministic.
-constexpr int RES_TCH = 16, RES_ROWNZ = 8;
+#ifndef KH_RES_TCH
+#define KH_RES_TCH 16
+#endif
+constexpr int RES_TCH = KH_RES_TCH, RES_ROWNZ = 8;
 __global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t nt, const int64_t* __restrict__ indptr,
                                                             const int64_t* __restrict__ indices,
                                                             const double* __restrict__ mv,
