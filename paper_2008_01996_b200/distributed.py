@@ -36,7 +36,7 @@ import math
 
 import numpy as np
 
-from .engine import ModalPlan
+from .engine import REFINE_MIN_GAIN, ModalPlan
 
 
 def shard_range(n_items, world, rank):
@@ -332,7 +332,7 @@ class ShardedFD:
             steps += 1
             R, new = self._residual()
             info["residuals"].append(new)
-            stalled = not new < rel
+            stalled = not new < REFINE_MIN_GAIN * rel  # stagnation: classic IR stop rule
             rel = new
             if stalled:
                 break

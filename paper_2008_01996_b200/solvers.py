@@ -277,7 +277,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     import torch
 
     from . import _native
-    from .engine import FDEngine, modal_plan
+    from .engine import REFINE_MIN_GAIN, FDEngine, modal_plan
 
     _native.require_cuda()
     report = SolveReport(variant="fd", dof=system.dof, n_t=system.n_t, m_x=system.m_x, threads=threads)
@@ -363,7 +363,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
         eng.fd_apply(eng.R, U, accumulate=True)
         steps += 1
         new = eng._rel(eng.residual(U, F))
-        stalled = not new < rel
+        stalled = not new < REFINE_MIN_GAIN * rel  # stagnation: classic IR stop rule
         rel = new
         if stalled:
             break
