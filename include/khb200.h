@@ -167,6 +167,10 @@ int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int
                          const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2, void* stream);
 /* y += alpha x over n device doubles (refinement update of a row shard). */
 int kh_daxpy(int64_t n, double alpha, const double* x, double* y, void* stream);
+/* out (device, 1 double) = sum_i x_i y_i (fixed-order partial sums:
+ * deterministic); x *= alpha. Device arrays of n doubles (Krylov refinement). */
+int kh_dot(const double* x, const double* y, int64_t n, double* out, void* stream);
+int kh_dscal(int64_t n, double alpha, double* x, void* stream);
 /* out (device, 1 double) = sum_i x_i^2 over n device doubles. */
 int kh_sumsq(const double* x, int64_t n, double* out, void* stream);
 /* Multi-GPU back transform (one process per GPU). C = A B (m x n, K = k,

@@ -84,6 +84,8 @@ SIGNATURES = {
     "kh_dgemm": (ctypes.c_int, [_i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp]),
     "kh_sumsq": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
     "kh_daxpy": (ctypes.c_int, [_i64, _dbl, _vp, _vp, _vp]),
+    "kh_dot": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "kh_dscal": (ctypes.c_int, [_i64, _dbl, _vp, _vp]),
     "kh_csr_pair_residual": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                                             _vp, _vp]),
     "kh_dgemm_rowscatter": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _i64, _i64, _vp]),

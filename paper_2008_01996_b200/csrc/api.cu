@@ -246,6 +246,22 @@ extern "C" int kh_sumsq(const double* x, int64_t n, double* out, void* stream) {
   return KH_OK;
 }
 
+extern "C" int kh_dot(const double* x, const double* y, int64_t n, double* out, void* stream) {
+  if (!out || (n > 0 && (!x || !y))) return fail(KH_ERR_INVALID, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  KH_CUDA(scratch(&part));
+  KH_CUDA(kh_launch_dot(x, y, n, part, kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 1, 0, out, st));
+  return KH_OK;
+}
+
+extern "C" int kh_dscal(int64_t n, double alpha, double* x, void* stream) {
+  if (n > 0 && !x) return fail(KH_ERR_INVALID, "null argument");
+  KH_CUDA(kh_launch_dscal(n, alpha, x, static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
 int kh_set_device(int device) {
   KH_CUDA(cudaSetDevice(device));
   return KH_OK;

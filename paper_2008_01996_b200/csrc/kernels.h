@@ -111,6 +111,9 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream);
+cudaError_t kh_launch_dot(const double* x, const double* y, int64_t n, double* part, int32_t nblk,
+                          cudaStream_t stream);
+cudaError_t kh_launch_dscal(int64_t n, double alpha, double* x, cudaStream_t stream);
 // Shared-memory DMMA factorization of fronts with m <= ms (ms = 32, 48 or 64).
 // Fused forward solve of the factor kernels (kh_plan_factor_fwd): y holds the
 // gathered rhs of the batch; rhs updates go through the level buffers of the

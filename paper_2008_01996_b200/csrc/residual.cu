@@ -102,6 +102,26 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x
   }
 }
 
+__global__ void __launch_bounds__(256) dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                  int64_t n, double* part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(x[i], y[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) dscal_kernel(int64_t n, double alpha, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= alpha;
+}
+
 __global__ void __launch_bounds__(256) daxpy_kernel(int64_t n, double alpha, const double* __restrict__ x,
                                                     double* __restrict__ y) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -114,6 +134,21 @@ cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y,
   if (n <= 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   daxpy_kernel<<<blocks, 256, 0, stream>>>(n, alpha, x, y);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_dot(const double* x, const double* y, int64_t n, double* part, int32_t nblk,
+                          cudaStream_t stream) {
+  dot_kernel<<<nblk, 256, 0, stream>>>(x, y, n, part);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_dscal(int64_t n, double alpha, double* x, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  dscal_kernel<<<blocks, 256, 0, stream>>>(n, alpha, x);
   kh_note_launch();
   return cudaGetLastError();
 }

@@ -228,6 +228,9 @@ class FDEngine:
         if fuse_forward is None:
             fuse_forward = os.environ.get("KH_FUSED_FWD", "0") == "1"
         self.fuse_forward = bool(fuse_forward)
+        # refinement: "richardson" (u += FD(f - K u)) or "gmres" (FD as the
+        # right preconditioner of a short GMRES cycle); KH_REFINE overrides
+        self.refine_method = os.environ.get("KH_REFINE", "richardson")
 
         dev = self.device
         f64 = torch.float64
@@ -415,9 +418,15 @@ class FDEngine:
         # not yet factored: the first application factors (forward sweep fused)
         self.fd_apply(F, U, accumulate=False)
         info = {"imag_residue": 0.0, "residuals": [], "refine_steps": 0}
-        rel = self._rel(self.residual(U, F))
+        norms = self.residual(U, F).tolist()
+        rel = float(np.sqrt(norms[0]) / np.sqrt(norms[1])) if norms[1] > 0 else float(np.sqrt(norms[0]))
         info["residuals"].append(rel)
         steps = 0
+        if rel > tol and refine > 0 and self.refine_method == "gmres":
+            out = self._gmres(F, U, rel, float(np.sqrt(norms[1])), refine, tol, info)
+            if out is not None:
+                info["refine_steps"], info["residual"] = out
+                return U, info
         while rel > tol and steps < refine:
             self.fd_apply(self.R, U, accumulate=True)
             steps += 1
@@ -430,6 +439,69 @@ class FDEngine:
         info["refine_steps"] = steps
         info["residual"] = rel
         return U, info
+
+    def _dot(self, x, y):
+        _native.call("kh_dot", x.data_ptr(), y.data_ptr(), x.numel(), self._dots.data_ptr(), self._stream())
+        return float(self._dots.item())
+
+    def _gmres(self, F, U, rel0, fnorm, m, tol, info):
+        """Refinement by FD-right-preconditioned GMRES (flexible form: the
+        preconditioned directions z_j = FD(v_j) are kept), one cycle of at most
+        m steps; each step costs what a Richardson step does (one FD
+        application, one K application) and never reduces the residual less.
+        Stops at `tol`, at stagnation (the estimate fails to halve), or when
+        the Krylov vectors do not fit in device memory (returns None: the
+        caller falls back to Richardson). U is updated in place."""
+        import torch
+
+        N = U.numel()
+        with torch.cuda.device(self.device):
+            free, _ = torch.cuda.mem_get_info()
+            free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+        if (2 * m + 2) * N * 8 > 0.9 * free:
+            return None
+        st = self._stream()
+        if getattr(self, "_dots", None) is None:
+            self._dots = torch.zeros(1, dtype=torch.float64, device=self.device)
+        zero = torch.zeros_like(F)
+        beta = rel0 * fnorm
+        v = self.R.clone()
+        _native.call("kh_dscal", N, 1.0 / beta, v.data_ptr(), st)
+        V, Z = [v], []
+        H = np.zeros((m + 1, m))
+        y = np.zeros(0)
+        est_prev = rel0
+        steps = 0
+        for j in range(m):
+            z = torch.empty_like(U)
+            self.fd_apply(V[j], z)                       # z_j = FD(v_j)
+            self.residual(z, zero)                       # R = -K z_j
+            w = self.R.clone()
+            _native.call("kh_dscal", N, -1.0, w.data_ptr(), st)
+            for i in range(j + 1):                       # modified Gram-Schmidt
+                h = self._dot(w, V[i])
+                H[i, j] = h
+                _native.call("kh_daxpy", N, -h, V[i].data_ptr(), w.data_ptr(), st)
+            hn = float(np.sqrt(max(self._dot(w, w), 0.0)))
+            H[j + 1, j] = hn
+            Z.append(z)
+            steps = j + 1
+            rhs = np.zeros(j + 2)
+            rhs[0] = beta
+            y, *_ = np.linalg.lstsq(H[:j + 2, :j + 1], rhs, rcond=None)
+            est = float(np.linalg.norm(rhs - H[:j + 2, :j + 1] @ y)) / fnorm
+            info["residuals"].append(est)
+            if est <= tol or not est < REFINE_MIN_GAIN * est_prev or hn <= 1e-300 or j + 1 == m:
+                break
+            est_prev = est
+            _native.call("kh_dscal", N, 1.0 / hn, w.data_ptr(), st)
+            V.append(w)
+        for i, yi in enumerate(y):
+            _native.call("kh_daxpy", N, float(yi), Z[i].data_ptr(), U.data_ptr(), st)
+        self.gpu_launches += 4 * steps + steps * (steps + 3) // 2
+        rel = self._rel(self.residual(U, F))             # the true residual of the update
+        info["residuals"].append(rel)
+        return steps, rel
 
     @staticmethod
     def _rel(norms):
