@@ -750,7 +750,10 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
 // blocked_ldlt; the panel and U are then written once, coalesced.
 KH_HD constexpr int packed_elems(int m) { return kh_packed_elems(m); }
 // classes whose residency is bounded by shared memory drop the W buffer
-KH_HD constexpr bool front_has_w(int ms) { return ms != 48; }
+#ifndef KH_NOW_64
+#define KH_NOW_64 0
+#endif
+KH_HD constexpr bool front_has_w(int ms) { return ms != 48 && !(KH_NOW_64 && ms == 64); }
 KH_HD constexpr int front_smem_bytes(int ms) {
   return 16 * (packed_elems(ms) + (front_has_w(ms) ? 8 * (ms + 2) : 0) + 8 + 2 * ms) + 4 * ms + 4 * 4 * ms;
 }
