@@ -104,6 +104,8 @@ struct kh_plan {
   int64_t panel_total = 0, upd_size[2] = {0, 0}, rupd_size[2] = {0, 0};
   // device
   KhDevFront* fronts = nullptr;
+  KhDevFront* lf_fronts = nullptr;
+  KhKid* kids = nullptr;
   int32_t *child_list = nullptr, *relind = nullptr, *cmap = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
   int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
   double *mv = nullptr, *av = nullptr;
@@ -123,6 +125,9 @@ struct kh_plan {
   KhTree tree() const {
     KhTree T;
     T.fronts = fronts;
+    T.lf_fronts = lf_fronts;
+    T.lf_base = level_fronts;
+    T.kids = kids;
     T.child_list = child_list;
     T.relind = relind;
     T.cmap = cmap;
@@ -362,7 +367,8 @@ namespace {
 // Host-side launch schedule derived from the analysis: fronts grouped per
 // level and kernel class, Schur tiles and the large-front block lists.
 struct Sched {
-  std::vector<KhDevFront> df;
+  std::vector<KhDevFront> df, lf_df;
+  std::vector<KhKid> kids;
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
@@ -423,6 +429,16 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     }
     X.cls_off.push_back((int32_t)X.lf.size() - base);
     X.level_off.push_back((int32_t)X.lf.size());
+  }
+  X.lf_df.resize(X.lf.size());
+  for (size_t i = 0; i < X.lf.size(); ++i) {
+    X.lf_df[i] = X.df[X.lf[i]];
+    X.lf_df[i].pad = X.lf[i];
+  }
+  X.kids.resize(S.child_list.size());
+  for (size_t j = 0; j < S.child_list.size(); ++j) {
+    const kh::Front& C = S.fronts[S.child_list[j]];
+    X.kids[j] = {C.upd_off, C.rows_begin, C.rupd_off, C.q, 0};
   }
   X.task_off.push_back(0);
   for (size_t d = 0; d < S.levels.size(); ++d) {
@@ -507,6 +523,8 @@ void carve(kh_plan* p, const kh::Symbolic& S, const Sched& X, Carver& C) {
   C.take(&p->orig_src, S.orig_src.size());
   C.take(&p->orig_dst, S.orig_dst.size());
   C.take(&p->level_fronts, X.lf.size());
+  C.take(&p->lf_fronts, X.lf_df.size());
+  C.take(&p->kids, X.kids.size());
   C.take(&p->tasks, X.tasks.size());
   C.take(&p->btasks, X.bt.size());
   C.take(&p->perm, (size_t)S.n);
@@ -616,6 +634,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     up(p->orig_src, S.orig_src.data(), S.orig_src.size() * 8);
     up(p->orig_dst, X.orig_dst.data(), X.orig_dst.size() * 4);
     up(p->level_fronts, X.lf.data(), X.lf.size() * 4);
+    up(p->lf_fronts, X.lf_df.data(), X.lf_df.size() * sizeof(KhDevFront));
+    up(p->kids, X.kids.data(), X.kids.size() * sizeof(KhKid));
     up(p->tasks, X.tasks.data(), X.tasks.size() * 4);
     up(p->btasks, X.bt.data(), X.bt.size() * 4);
     up(p->perm, S.perm.data(), S.perm.size() * 8);

@@ -36,9 +36,19 @@ constexpr int KC = 16;       // complex K chunk
 constexpr int LDS = TB + 2;  // padded smem row (double2): conflict-free LDS.128 fragments
 constexpr int NB = 32;       // pivot block width
 
+// Complex products in the tile engine: KH_3M = 1 forms each 8x8x4 complex
+// block product with three real DMMAs (Gauss: T1 = (Ar+Ai) Br,
+// T2 = Ar (Bi-Br), T3 = Ai (Br+Bi); re = T1 - T3, im = T1 + T2) instead of
+// four: 25% less FP64 tensor work, one more accumulator set.
+#ifndef KH_3M
+#define KH_3M 1
+#endif
 struct Acc {
   double r[4][2][2];
   double i[4][2][2];
+#if KH_3M
+  double t[4][2][2];
+#endif
 };
 
 // Visit the accumulator: ep(row, col, value) with row, col in [0, 64).
@@ -124,7 +134,12 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) acc.r[a][b][h] = acc.i[a][b][h] = 0.0;
+      for (int h = 0; h < 2; ++h) {
+        acc.r[a][b][h] = acc.i[a][b][h] = 0.0;
+#if KH_3M
+        acc.t[a][b][h] = 0.0;
+#endif
+      }
   const int nch = (K + KC - 1) / KC;
   auto load = [&](int s, int c) {
     CpStage& S = st[s];
@@ -167,6 +182,24 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
         bf[nt] = S.b[(kk + t) * LDS + wj * 16 + nt * 8 + g];
         if (MODE == MODE_SCALED) bf[nt] = cmul(bf[nt], S.d[kk + t]);
       }
+#if KH_3M
+      double bs[2], bd[2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        bs[nt] = bf[nt].x + bf[nt].y;
+        bd[nt] = bf[nt].y - bf[nt].x;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double as = af[mt].x + af[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma884(acc.t[mt][nt][0], acc.t[mt][nt][1], as, bf[nt].x);
+          dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].x, bd[nt]);
+          dmma884(acc.r[mt][nt][0], acc.r[mt][nt][1], af[mt].y, bs[nt]);
+        }
+      }
+#else
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
         const double nai = -af[mt].y;
@@ -178,10 +211,24 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
           dmma884(acc.i[mt][nt][0], acc.i[mt][nt][1], af[mt].y, bf[nt].x);
         }
       }
+#endif
     }
     __syncthreads();
   }
   cp_async_wait<0>();
+#if KH_3M
+  // re = T1 - T3, im = T1 + T2
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double t1 = acc.t[a][b][h];
+        acc.r[a][b][h] = t1 - acc.r[a][b][h];
+        acc.i[a][b][h] = t1 + acc.i[a][b][h];
+      }
+#endif
 }
 
 KH_DEV double2 shfl2(double2 v, int src) {
@@ -221,7 +268,10 @@ KH_DEV double2 warp_sum8(double2 (&v)[8], int lane) {
 // epilogue (the update block is written exactly once: no separate assembly
 // pass over U and no read-modify-write). Tasks are (front, tile row, tile
 // col) triples built on the host.
-__global__ void __launch_bounds__(NT, 2) schur_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
+#ifndef KH_SCHUR_MINB
+#define KH_SCHUR_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                              const double2* __restrict__ panels, double2* upd_cur,
                                                              int64_t upd_stride_cur,
                                                              const double2* __restrict__ upd_child,
@@ -786,11 +836,6 @@ KH_HD constexpr int front_min_blocks(int ms, int nw) {
   return ms <= 32 ? KH_F32_MINB : ((16 / nw) > 1 ? 16 / nw : 1);
 }
 
-struct KidInfo {
-  int64_t upd_off, rows_begin, rupd_off;
-  int32_t q, pad;
-};
-
 // FWD: fused forward solve. The front's right-hand side (y of the pivot
 // rows + the children's rhs updates, pushed in child order during the
 // assembly) is kept in shared memory; after the LDL^T, warp 0 runs the
@@ -805,6 +850,14 @@ struct FwdArgs {
   const double2* ru_child;
   int64_t ru_stride_child;
 };
+
+// child-update columns a warp loads per batch in the push assembly
+#ifndef KH_ASM_CW
+#define KH_ASM_CW 0
+#endif
+KH_HD constexpr int asm_cols(int ms) {
+  return KH_ASM_CW > 0 ? KH_ASM_CW : (ms <= 32 ? 8 : ms <= 48 ? 6 : ms <= 64 ? 4 : ms <= 96 ? 4 : 2);
+}
 
 template <int MS, int NW, bool FWD>
 __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_front_kernel(
@@ -836,24 +889,21 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   auto phase = [](int) {};
 #endif
   const int lane = tid & 31, warp = tid >> 5;
-  const int32_t f = level_fronts[blockIdx.x];
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int32_t f = F.pad;
   const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
   const int p = F.p, q = F.q, m = p + q;
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   const int nkids = F.child_end - F.child_begin;
-  __shared__ KidInfo kinfo[RK];
+  __shared__ KhKid kinfo[RK];
 
   // ---- assembly: zero the front, add the originals (values pre-gathered in
   // front order, destinations pre-packed on the host: one coalesced stream),
   // then push each child's update block through its relind map (coalesced
   // column reads of the child's U, conflict-free within a child; children in
   // order, so the sums are deterministic)
-  if (tid < RK && tid < nkids) {
-    const KhDevFront C = T.fronts[T.child_list[F.child_begin + tid]];
-    kinfo[tid] = {C.upd_off, C.rows_begin, C.rupd_off, C.q, 0};
-  }
+  if (tid < RK && tid < nkids) kinfo[tid] = T.kids[F.child_begin + tid];
   const int ne = packed_elems(m);
   for (int idx = tid; idx < ne; idx += NTH) S[idx] = make_double2(0.0, 0.0);
   for (int c = tid; c < m; c += NTH) cb[c] = kh_packed_col_base(m, c);
@@ -908,7 +958,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
       qk = kinfo[k].q;
       roff = kinfo[k].rupd_off;
     } else {
-      const KhDevFront C = T.fronts[T.child_list[F.child_begin + k]];
+      const KhKid C = T.kids[F.child_begin + k];
       upd_off = C.upd_off;
       rows_begin = C.rows_begin;
       qk = C.q;
@@ -926,12 +976,14 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
     }
     const double2* Uc = upd_child + (int64_t)b * upd_stride_child + upd_off;
     const int32_t* rk = k < RK ? rel + k * MS : T.relind + rows_begin;
-    // warp w takes columns w, w + NW, ... two at a time; lanes walk the rows
-    for (int cj0 = warp; cj0 < qk; cj0 += 2 * NW) {
-      double2 v[2][R];
-      int dst[2][R];
+    // warp w takes columns w, w + NW, ... CW at a time (all their loads in
+    // flight before the adds); lanes walk the rows
+    constexpr int CW = asm_cols(MS);
+    for (int cj0 = warp; cj0 < qk; cj0 += CW * NW) {
+      double2 v[CW][R];
+      int dst[CW][R];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < CW; ++h) {
         const int cj = cj0 + h * NW;
         const int base = cj < qk ? cb[rk[cj]] : 0;
 #pragma unroll
@@ -943,7 +995,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
         }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < CW; ++h)
 #pragma unroll
         for (int u = 0; u < R; ++u)
           if (dst[h][u] >= 0) S[dst[h][u]] = cadd(S[dst[h][u]], v[h][u]);

@@ -31,8 +31,20 @@ __host__ __device__ constexpr int kh_packed_col_base(int m, int c) {
   return off + (c & 7) * kh_packed_ld(m, c >> 3) - 8 * (c >> 3);
 }
 
+// A child as its parent's assembly needs it (parallel to child_list).
+struct KhKid {
+  int64_t upd_off, rows_begin, rupd_off;
+  int32_t q, pad;
+};
+
 struct KhTree {  // device pointers shared by every level kernel
   const KhDevFront* fronts;
+  // fronts in level-launch order (level_fronts), with the front index in
+  // `pad`, and the children's records: one dependent load each instead of
+  // level_fronts -> fronts and child_list -> fronts
+  const KhDevFront* lf_fronts;
+  const int32_t* lf_base;
+  const KhKid* kids;
   const int32_t* child_list;
   const int32_t* relind;
   const int32_t* cmap;

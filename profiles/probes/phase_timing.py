@@ -1,6 +1,6 @@
 """Per-phase cycle counts of factor_front_kernel (clock64, debug builds).
 
-    python profiles/probes/phase_timing.py build          # here: compile variants
+    python profiles/probes/phase_timing.py build [v..]    # here: compile variants
     python profiles/probes/phase_timing.py run <variant>  # GPU box: c3 factor
 
 Variants differ only in compile-time switches; each prints, per front class,
@@ -28,10 +28,12 @@ def lib_path(v):
     return os.path.join(HERE, f"libkh_phase_{v}.so")
 
 
-def build():
+def build(only=()):
     from paper_2008_01996_b200 import build as b
 
     for v, d in VARIANTS.items():
+        if only and v not in only:
+            continue
         b.build(out=lib_path(v), defines=["KH_PHASE_TIMING", *d])
         print("built", lib_path(v))
 
@@ -77,6 +79,6 @@ def run(v):
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build()
+        build(sys.argv[2:])
     else:
         run(sys.argv[2])
