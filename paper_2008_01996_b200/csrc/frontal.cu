@@ -687,12 +687,14 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
     //     diagonal block
     if (!LA) {
       if (s0 < cl) {
+        // tiles task = warp, warp + NW, ...: (bj, rem) advanced incrementally
         const int nrb = (m - s0 + 7) / 8, ncb = (cl - s0 + 7) / 8;
-        for (int task = warp;; task += NW) {
-          int bj = 0, rem = task;
-          while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
-          if (bj >= ncb) break;
+        int bj = 0, rem = warp;
+        while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
+        while (bj < ncb) {
           rank8_tile<HW>(S, cb, W, ldw, dg, kb, w, s0 + 8 * (bj + rem), s0 + 8 * bj, cl, m);
+          rem += NW;
+          while (bj < ncb && rem >= nrb - bj) rem -= nrb - bj++;
         }
       }
     } else if (s0 < cl) {
@@ -726,7 +728,11 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
       tri_index(task, bi, bj);
       const int r0 = p + 8 * bi, c0 = p + 8 * bj;
       const int ra = r0 + g, cv = c0 + g;
-      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      // Gauss 3M form (see KH_3M): T1 = (Ar+Ai) Br, T2 = Ar (Bi-Br),
+      // T3 = Ai (Br+Bi); re = T1 - T3, im = T1 + T2 -- three independent
+      // accumulator chains
+      double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+#pragma unroll 2
       for (int ks = 0; ks < p; ks += 4) {
         const int k = ks + t;
         double2 af = make_double2(0.0, 0.0), bf = make_double2(0.0, 0.0);
@@ -735,10 +741,9 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
           if (ra < m) af = S[ck + ra];
           if (cv < m) bf = cmul(S[ck + cv], dg[k]);
         }
-        dmma884(cr[0], cr[1], af.x, bf.x);
-        dmma884(cr[0], cr[1], -af.y, bf.y);
-        dmma884(ci[0], ci[1], af.x, bf.y);
-        dmma884(ci[0], ci[1], af.y, bf.x);
+        dmma884(t1[0], t1[1], af.x + af.y, bf.x);
+        dmma884(t2[0], t2[1], af.x, bf.y - bf.x);
+        dmma884(t3[0], t3[1], af.y, bf.x + bf.y);
       }
       const int rr = r0 + g;
 #pragma unroll
@@ -746,7 +751,7 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
         const int cc = c0 + 2 * t + h;
         if (rr < m && cc < m && rr >= cc) {
           double2* d = S + cb[cc] + rr;
-          *d = make_double2(d->x - cr[h], d->y - ci[h]);
+          *d = make_double2(d->x - (t1[h] - t3[h]), d->y - (t1[h] + t2[h]));
         }
       }
     }

@@ -20,15 +20,14 @@ struct KhDevFront {
 // roundup8(m - 8b) + 2 (2 mod 8 in 16-byte units: conflict-free DMMA
 // fragment loads). Entry (r, c), r >= c, sits at kh_packed_col_base(m, c) + r.
 __host__ __device__ constexpr int kh_packed_ld(int m, int b) { return ((m - 8 * b + 7) / 8) * 8 + 2; }
+// (closed forms: block b has leading dimension 8 (ceil(m/8) - b) + 2)
 __host__ __device__ constexpr int kh_packed_elems(int m) {
-  int e = 0;
-  for (int b = 0; 8 * b < m; ++b) e += 8 * kh_packed_ld(m, b);
-  return e;
+  const int M8 = (m + 7) / 8;
+  return 32 * M8 * (M8 + 1) + 16 * M8;
 }
 __host__ __device__ constexpr int kh_packed_col_base(int m, int c) {
-  int off = 0;
-  for (int b = 0; b < (c >> 3); ++b) off += 8 * kh_packed_ld(m, b);
-  return off + (c & 7) * kh_packed_ld(m, c >> 3) - 8 * (c >> 3);
+  const int M8 = (m + 7) / 8, b = c >> 3;
+  return 64 * b * M8 - 32 * b * (b - 1) + 16 * b + (c & 7) * kh_packed_ld(m, b) - 8 * b;
 }
 
 // A child as its parent's assembly needs it (parallel to child_list).
