@@ -52,7 +52,28 @@ def parse():
                     help="N>1 back-transform reduce-scatter: fused GEMM + peer-memory scatter, or NCCL")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-GPU driver even with one rank (testing the N>1 path on one GPU)")
+    ap.add_argument("--spawn-check", action="store_true",
+                    help="(tests) each rank prints its rank and world size and exits before touching a GPU")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="reference arm: seconds of full solves after the first (steps are capped to fit)")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`--gpus N` (N > 1) without a torchrun environment: run this script
+    again under torch.distributed.run with N ranks on this node (one process
+    per GPU, rendezvous on 127.0.0.1); rank 0 prints the JSON line. Returns
+    the launcher's exit code, or None when no spawn is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ---- clocks ---------------------------------------------------------------------
@@ -196,20 +217,58 @@ def cpu_fd_sample(system, n_shift_sample, threads=1):
             "t_analyze": t_an, "sample_shifts": int(len(ks)), "n_t": n_t}
 
 
+def cpu_fd_full(system, workers):
+    """One unsampled reference FD solve: the oracle port of solve_fd
+    (solvers.py:348-403; oracle.fd_oracle.solve_fd_parallel) with all N_t
+    SuperLU factor + solves over `workers` processes (the pool is created
+    inside the timed region)."""
+    from oracle import fd_oracle as orc
+
+    tm = {}
+    u, _ = orc.solve_fd_parallel(*orc.system_arrays(system), workers, timings=tm)
+    return dict(tm, u=u, workers=workers, n_t=system.n_t)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def shift_sample_size(cfg):
     return {"c1": 32, "c2": 32, "c3": 12, "c4": 3}.get(cfg, 8)
 
 
 # ---- main -------------------------------------------------------------------------
+def workload_config(args, info, system, world):
+    """The `config` dict, identical in both arms (--impl ours / reference)."""
+    return {"workload": f"{args.config}: {info['mesh']} M_x={system.m_x} N_t={system.n_t} dof={system.dof} "
+                        f"rhs={info['rhs']}",
+            "j_max": info["j_max"],
+            "parallelism": "single GPU" if world == 1 else f"shift-sharded x{world}"}
+
+
 def main():
     args = parse()
-    import torch
-
+    rc = spawn_ranks(args)
+    if rc is not None:
+        sys.exit(rc)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.spawn_check:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        return
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    import torch
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -365,16 +424,15 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {info['mesh']} M_x={n} N_t={nt} dof={dof} rhs={info['rhs']}",
-                       "j_max": info["j_max"], "refine": args.refine, "leaf_size": leaf,
-                       "shifts_solved": int(modal.n_k), "conjugate_pairs": int(modal.n_pairs),
-                       "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
-                           stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
-                       "parallelism": (f"shift-sharded x{world}, back transform + reduce-scatter: "
-                                       + {"p2p": "fused GEMM->peer-memory scatter",
-                                          "nccl": "GEMM + NCCL reduce_scatter",
-                                          "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[coll])
-                       if sharded else "single GPU"},
+            "config": workload_config(args, info, system, world),
+            "knobs": {"refine": args.refine, "leaf_size": leaf,
+                      "shifts_solved": int(modal.n_k), "conjugate_pairs": int(modal.n_pairs),
+                      "l2": "inputs larger than L2 (factors %.1f GB, F %.0f MB)" % (
+                          stats["panel_entries"] * 16 * n_shift_local / 1e9, 8 * dof / 1e6),
+                      "collective": ({"p2p": "fused GEMM->peer-memory scatter",
+                                      "nccl": "GEMM + NCCL reduce_scatter",
+                                      "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[coll]
+                                     if sharded else None)},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),
@@ -393,11 +451,7 @@ def main():
             "kernels": kernels,
         }
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_fd_sample(system, shift_sample_size(args.config))
-            line["cpu_baseline"] = {"value": dof / cb["t_total"], "unit": UNIT, "cores": 1, "kind": "port",
-                                    "sample": (f"oracle port of solve_fd, full pencil/transforms/analysis, "
-                                               f"{cb['sample_shifts']} of {cb['n_t']} SuperLU shift solves "
-                                               f"timed and extrapolated; t_total={cb['t_total']:.2f}s")}
+            line["cpu_baseline"] = cpu_baseline_subprocess(args)
         print(json.dumps(line), flush=True)
     if sharded:
         torch.distributed.barrier()
@@ -533,31 +587,66 @@ def measure_e2e_sharded(system, pencil, args, leaf):
             "residual": rep.residual}
 
 
+def cpu_baseline_subprocess(args):
+    """cpu_baseline of our arm: one unsampled reference solve, timed in a fresh
+    process (no CUDA context in the forking process) by the reference arm's
+    own code (`--impl reference --steps 1 --warmup 0`)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--steps", "1", "--warmup", "0",
+           "--config", args.config]
+    if args.j_max is not None:
+        cmd += ["--j-max", str(args.j_max)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800).stdout.strip().splitlines()
+        ref = json.loads(out[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError) as exc:
+        return {"value": None, "unavailable": f"reference timing failed: {exc}"}
+    return dict(ref["cpu_baseline"])
+
+
 def run_reference(args, world, rank):
-    """The reference's CPU algorithm (oracle port, threads = all host cores),
-    bounded shift sample per step, extrapolated to the full workload."""
+    """The reference's CPU algorithm on this host: the oracle port of
+    solve_fd (same LAPACK / SuperLU calls as the reference) with the N_t shift
+    solves over all host cores. Every timed step is one full, unsampled solve;
+    steps after the first stop once --ref-budget seconds are spent (the line
+    reports the steps actually timed). A 12-shift extrapolation is reported
+    beside it as a cross-check."""
     if rank != 0:
         return
     from paper_2008_01996_b200 import problems
 
     kw = {} if args.j_max is None else {"j_max": args.j_max}
     system, info = problems.build_system(args.config, **kw)
-    threads = os.cpu_count() or 1
-    sample = shift_sample_size(args.config)
+    workers = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_fd_sample(system, max(1, sample // 4), threads)
-    totals = []
-    for _ in range(args.steps):
-        totals.append(cpu_fd_sample(system, sample, threads)["t_total"])
+        cpu_fd_sample(system, 2, 1)
+    totals, spent = [], 0.0
+    for i in range(max(1, args.steps)):
+        if i > 0 and spent + totals[-1] > args.ref_budget:
+            break
+        r = cpu_fd_full(system, workers)
+        totals.append(r["t_total"])
+        spent += r["t_total"]
+    from oracle import fd_oracle as orc
+
+    res = orc.residual(*orc.system_arrays(system), r["u"])
     t = float(np.mean(totals))
     value = system.dof / t
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: {info['mesh']} M_x={system.m_x} N_t={system.n_t} "
-                                   f"dof={system.dof} rhs={info['rhs']}", "j_max": info["j_max"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{sample} of {system.n_t} shifts per step, extrapolated"},
+    cross = cpu_fd_sample(system, shift_sample_size(args.config), 1)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(totals),
+            "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": workload_config(args, info, system, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                             "cpu_model": cpu_model(),
+                             "sample": (f"full solve: oracle port of the reference solve_fd, all {system.n_t} "
+                                        f"SuperLU shift factor+solves over {workers} processes, pencil, "
+                                        f"transforms and MMD analysis included; {len(totals)} solve(s), "
+                                        f"t_total={t:.2f}s")},
+            "residual": res,
+            "phases_s": {k: r[k] for k in ("t_pencil", "t_transform", "t_analyze", "t_spatial")},
+            "extrapolated_sample": {"value": system.dof / cross["t_total"], "cores": 1,
+                                    "sample": f"{cross['sample_shifts']} of {cross['n_t']} shifts, 1 thread, "
+                                              "extrapolated linearly (cross-check only)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -15,6 +15,8 @@
  *                               into the factorization (the first FD application, solvers.py:383-393)
  *   kh_dgemm .................. modal transforms (zgemm)                solvers.py:368-372, :397-400
  *   kh_plan_residual .......... residual / kron_apply_right             solvers.py:428-440, dense.py:264-286
+ *   kh_plan_residual_dd, kh_dgemm_dd, kh_csr_pair_residual_dd
+ *                               the same residual in compensated arithmetic (refinement at c4)
  *   kh_sumsq .................. norms of _discard_imaginary              solvers.py:406-413
  *   kh_dgemm_rowscatter ....... multi-GPU back transform fused with the scatter of its
  *   kh_sum_parts                reduce-scatter (solvers.py:397-400 per rank)
@@ -155,6 +157,14 @@ int kh_plan_level_times(kh_plan* plan, float* ms, int32_t n_levels);
  * R may be NULL. norms2 (device, 2 doubles) receives ||R||_F^2, ||F||_F^2. */
 int kh_plan_residual(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
                      double* R, int64_t ldr, double* norms2, void* stream);
+/* Compensated variant of kh_plan_residual (refinement at fine meshes, where the
+ * fp64 evaluation of f - K u floors the residual): Y2 = U M_t^T given as the
+ * unevaluated sum Y2hi + Y2lo (kh_dgemm_dd), Y1 = U A_t^T in fp64 (ld ldy1);
+ * R = F - (M_x Y1 + A_x Y2) accumulated with error-free products and sums,
+ * rounded once. Replaces the same reference lines as kh_plan_residual. */
+int kh_plan_residual_dd(kh_plan* plan, int64_t nt, const double* Y1, int64_t ldy1, const double* Y2hi,
+                        const double* Y2lo, int64_t ldy2, const double* F, int64_t ldf, double* R, int64_t ldr,
+                        double* norms2, void* stream);
 void kh_plan_free(kh_plan* plan);
 
 /* C = alpha A B + beta C, fp64, column-major, device arrays (DMMA GEMM). */
@@ -165,12 +175,18 @@ int kh_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int
 int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
                          const double* m_vals, const double* a_vals, const double* Y, int64_t ldy,
                          const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2, void* stream);
+/* C_hi + C_lo = A B (m x n, K = k, column-major device arrays) with compensated
+ * products and sums (Dot2): the temporal product U M_t^T of the compensated
+ * residual. */
+int kh_dgemm_dd(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+                double* C_hi, double* C_lo, int64_t ldc, void* stream);
+/* Plan-free kh_plan_residual_dd on a device CSR. */
+int kh_csr_pair_residual_dd(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                            const double* m_vals, const double* a_vals, const double* Y1, int64_t ldy1,
+                            const double* Y2hi, const double* Y2lo, int64_t ldy2, const double* F, int64_t ldf,
+                            double* R, int64_t ldr, double* norms2, void* stream);
 /* y += alpha x over n device doubles (refinement update of a row shard). */
 int kh_daxpy(int64_t n, double alpha, const double* x, double* y, void* stream);
-/* out (device, 1 double) = sum_i x_i y_i (fixed-order partial sums:
- * deterministic); x *= alpha. Device arrays of n doubles (Krylov refinement). */
-int kh_dot(const double* x, const double* y, int64_t n, double* out, void* stream);
-int kh_dscal(int64_t n, double alpha, double* x, void* stream);
 /* out (device, 1 double) = sum_i x_i^2 over n device doubles. */
 int kh_sumsq(const double* x, int64_t n, double* out, void* stream);
 /* Multi-GPU back transform (one process per GPU). C = A B (m x n, K = k,

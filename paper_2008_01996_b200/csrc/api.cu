@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -20,6 +22,22 @@ struct kh_symbolic {
 static std::atomic<long long> g_launches{0};
 void kh_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+cudaError_t kh_smem_optin(const void* kernel, int bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(kernel, dev);
+  const auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -32,6 +50,21 @@ int fail(int status, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(KH_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
+
+// Makes the plan's device current for one ABI call and restores the
+// caller's current device afterwards (the caller's torch state is untouched).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 #define KH_CUDA(call)                                        \
   do {                                                       \
@@ -220,6 +253,29 @@ cudaError_t scratch(double** out) {
 }
 }  // namespace
 
+extern "C" int kh_dgemm_dd(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, void* stream) {
+  if ((m > 0 && n > 0) && (!A || !B || !C_hi || !C_lo)) return fail(KH_ERR_INVALID, "null argument");
+  if (lda < m || ldb < k || ldc < m) return fail(KH_ERR_DIMENSION, "leading dimension too small");
+  KH_CUDA(kh_launch_dgemm_dd(m, n, k, A, lda, B, ldb, C_hi, C_lo, ldc, static_cast<cudaStream_t>(stream)));
+  return KH_OK;
+}
+
+extern "C" int kh_csr_pair_residual_dd(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                       const double* m_vals, const double* a_vals, const double* Y1, int64_t ldy1,
+                                       const double* Y2hi, const double* Y2lo, int64_t ldy2, const double* F,
+                                       int64_t ldf, double* R, int64_t ldr, double* norms2, void* stream) {
+  if (!indptr || !Y1 || !Y2hi || !Y2lo || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
+  if (ldy1 < n || ldy2 < n || ldf < n || (R && ldr < n)) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  KH_CUDA(scratch(&part));
+  KH_CUDA(kh_launch_pair_residual_dd(n, nt, indptr, indices, m_vals, a_vals, Y1, ldy1, Y2hi, Y2lo, ldy2, F, ldf, R,
+                                     ldr, part, kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 2, 0, norms2, st));
+  return KH_OK;
+}
+
 extern "C" int kh_csr_pair_residual(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
                                     const double* m_vals, const double* a_vals, const double* Y, int64_t ldy,
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* norms2,
@@ -248,22 +304,6 @@ extern "C" int kh_sumsq(const double* x, int64_t n, double* out, void* stream) {
   KH_CUDA(scratch(&part));
   KH_CUDA(kh_launch_sumsq(x, n, part, kResidualBlocks, st));
   KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 1, 0, out, st));
-  return KH_OK;
-}
-
-extern "C" int kh_dot(const double* x, const double* y, int64_t n, double* out, void* stream) {
-  if (!out || (n > 0 && (!x || !y))) return fail(KH_ERR_INVALID, "null argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double* part = nullptr;
-  KH_CUDA(scratch(&part));
-  KH_CUDA(kh_launch_dot(x, y, n, part, kResidualBlocks, st));
-  KH_CUDA(kh_launch_rowreduce(part, kResidualBlocks, 1, 0, out, st));
-  return KH_OK;
-}
-
-extern "C" int kh_dscal(int64_t n, double alpha, double* x, void* stream) {
-  if (n > 0 && !x) return fail(KH_ERR_INVALID, "null argument");
-  KH_CUDA(kh_launch_dscal(n, alpha, x, static_cast<cudaStream_t>(stream)));
   return KH_OK;
 }
 
@@ -588,7 +628,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   if (indptr[S.n] != S.nnz) return fail(KH_ERR_DIMENSION, "CSR does not match the analyzed pattern");
   if (S.orig_dst.size() >= (size_t)INT32_MAX)  // assembly tasks carry int32 originals ranges
     return fail(KH_ERR_DIMENSION, "too many original entries for one plan (>= 2^31)");
-  KH_CUDA(cudaSetDevice(device));
+  DeviceGuard dev_guard(device);
+  KH_CUDA(dev_guard.err);
   kh_plan* p = new kh_plan();
   p->device = device;
   plan_sizes(p, S, max_batch, factor_slots);
@@ -660,7 +701,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
 
 int kh_plan_set_values(kh_plan* p, const double* m_vals, const double* a_vals) {
   if (!p || (p->nnz && (!m_vals || !a_vals))) return fail(KH_ERR_INVALID, "null argument");
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   KH_CUDA(cudaMemcpy(p->mv, m_vals, p->nnz * 8, cudaMemcpyHostToDevice));
   KH_CUDA(cudaMemcpy(p->av, a_vals, p->nnz * 8, cudaMemcpyHostToDevice));
   KH_CUDA(kh_launch_gather_orig(p->n_orig, p->orig_src, p->mv, p->av, p->om, p->oa, 0));
@@ -755,7 +797,8 @@ int kh_plan_factor(kh_plan* p, int64_t slot0, int64_t nshift, const double* lamb
   if (!p || (nshift > 0 && !lambda_ri)) return fail(KH_ERR_INVALID, "null argument");
   if (check_batch(p, slot0, nshift) != KH_OK) return KH_ERR_INVALID;
   if (nshift == 0) return KH_OK;
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   return factor_impl(p, slot0, nshift, lambda_ri, static_cast<cudaStream_t>(stream), false);
 }
 
@@ -766,7 +809,8 @@ int kh_plan_factor_fwd(kh_plan* p, int64_t slot0, int64_t nshift, const double* 
   if (ldb < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
   if (nshift == 0 || p->n == 0) return KH_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   KH_CUDA(kh_launch_gather_rhs(p->n, (int32_t)nshift, p->perm, b_re, b_im, ldb, p->y, st));
   return factor_impl(p, slot0, nshift, lambda_ri, st, true);
 }
@@ -777,7 +821,8 @@ int kh_plan_solve_bwd(kh_plan* p, int64_t slot0, int64_t nshift, double* x_re, d
   if (check_batch(p, slot0, nshift) != KH_OK) return KH_ERR_INVALID;
   if (ldx < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
   if (nshift == 0 || p->n == 0) return KH_OK;
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   return solve_bwd_impl(p, slot0, (int32_t)nshift, x_re, x_im, ldx, static_cast<cudaStream_t>(stream));
 }
 
@@ -801,7 +846,8 @@ int kh_plan_level_times(kh_plan* p, float* ms, int32_t n_levels) {
   if (n_levels != p->depth + 1) return fail(KH_ERR_DIMENSION, "n_levels must be the tree depth + 1");
   if (!p->level_timing || p->lvl_ev.size() < (size_t)p->depth + 2)
     return fail(KH_ERR_INVALID, "level timing was not enabled for the last factorization");
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   KH_CUDA(cudaEventSynchronize(p->lvl_ev[p->depth + 1]));
   for (int32_t i = 0; i <= p->depth; ++i) {
     float t = 0.f;
@@ -816,7 +862,8 @@ int kh_plan_pivot_check(kh_plan* p, int64_t slot0, int64_t nshift, double rel_th
   if (!p) return fail(KH_ERR_INVALID, "null argument");
   if (nshift < 0 || slot0 < 0 || slot0 + nshift > p->slots) return fail(KH_ERR_INVALID, "slots out of range");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   std::vector<double> mp(nshift), am(nshift);
   if (nshift) {
     KH_CUDA(cudaMemcpyAsync(mp.data(), p->minpiv + slot0, nshift * 8, cudaMemcpyDeviceToHost, st));
@@ -850,7 +897,8 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   if (ldb < p->n || ldx < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
   if (nshift == 0 || p->n == 0) return KH_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   const KhTree T = p->tree();
   const double2* panels = p->panels + slot0 * p->panel_total;
   const int32_t ns = (int32_t)nshift;
@@ -871,12 +919,28 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   return solve_bwd_impl(p, slot0, ns, x_re, x_im, ldx, st);
 }
 
+int kh_plan_residual_dd(kh_plan* p, int64_t nt, const double* Y1, int64_t ldy1, const double* Y2hi,
+                        const double* Y2lo, int64_t ldy2, const double* F, int64_t ldf, double* R, int64_t ldr,
+                        double* norms2, void* stream) {
+  if (!p || !Y1 || !Y2hi || !Y2lo || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
+  if (ldy1 < p->n || ldy2 < p->n || ldf < p->n || (R && ldr < p->n))
+    return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
+  KH_CUDA(kh_launch_pair_residual_dd(p->n, nt, p->indptr, p->indices, p->mv, p->av, Y1, ldy1, Y2hi, Y2lo, ldy2, F,
+                                     ldf, R, ldr, p->resid_part, kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(p->resid_part, kResidualBlocks, 2, 0, norms2, st));
+  return KH_OK;
+}
+
 int kh_plan_residual(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf, double* R,
                      int64_t ldr, double* norms2, void* stream) {
   if (!p || !Y || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
   if (ldy < p->n || ldf < p->n || (R && ldr < p->n)) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  KH_CUDA(cudaSetDevice(p->device));
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
   KH_CUDA(kh_launch_pair_residual(p->n, nt, p->indptr, p->indices, p->mv, p->av, Y, ldy, F, ldf, R, ldr,
                                   p->resid_part, kResidualBlocks, st));
   KH_CUDA(kh_launch_rowreduce(p->resid_part, kResidualBlocks, 2, 0, norms2, st));
@@ -885,7 +949,7 @@ int kh_plan_residual(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const
 
 void kh_plan_free(kh_plan* p) {
   if (!p) return;
-  cudaSetDevice(p->device);
+  DeviceGuard dev_guard(p->device);
   plan_release(p);
   delete p;
 }

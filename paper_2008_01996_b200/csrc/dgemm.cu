@@ -138,13 +138,8 @@ cudaError_t launch(int64_t M, int64_t N, int64_t K, double alpha, const double* 
                    int64_t ldb, double beta, double* C, int64_t ldc, double* const* dst, int64_t rp, int64_t ldd,
                    cudaStream_t stream, int32_t batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0) {
   if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = kh_smem_optin((const void*)dgemm_kernel<SCATTER>, (int)SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
   dgemm_kernel<SCATTER><<<grid, 256, SMEM_BYTES, stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, dst, rp,
                                                            ldd, sA, sB, sC);

@@ -1726,19 +1726,12 @@ cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_
   return cudaGetLastError();
 }
 
-static cudaError_t set_smem_once(const void* fn, int bytes, bool& done) {
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  done = (e == cudaSuccess);
-  return e;
-}
 
 cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
                                   double2* panels, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  static bool done = false;
   const int smem = (int)(2 * sizeof(CpStage));
-  cudaError_t e = set_smem_once((const void*)big_lupdate_kernel, smem, done);
+  cudaError_t e = kh_smem_optin((const void*)big_lupdate_kernel, smem);
   if (e != cudaSuccess) return e;
   big_lupdate_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
   kh_note_launch();
@@ -1765,9 +1758,8 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
                             const double2* panels, double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
                             int64_t upd_stride_child, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  static bool done = false;
   const int smem = (int)(2 * sizeof(CpStage));
-  cudaError_t e = set_smem_once((const void*)schur_update_kernel, smem, done);
+  cudaError_t e = kh_smem_optin((const void*)schur_update_kernel, smem);
   if (e != cudaSuccess) return e;
   schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,
                                                                  upd_child, upd_stride_child);
@@ -1805,12 +1797,8 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
     return cudaGetLastError();
   }
   const size_t smem = sizeof(double2) * (size_t)max_m;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fwd_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  cudaError_t e = kh_smem_optin((const void*)fwd_top_kernel, (int)smem);
+  if (e != cudaSuccess) return e;
   fwd_top_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
                                                           ru_child, ru_stride_child);
   kh_note_launch();
@@ -1823,14 +1811,8 @@ cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, in
   if (nlev == 0 || batch == 0) return cudaSuccess;
   const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtasBwd;
   const size_t smem = sizeof(double2) * (size_t)max_m;
-  static size_t attr = 0, attr_top = 0;
-  size_t& a = narrow ? attr_top : attr;
-  if (smem > 48 * 1024 && smem > a) {
-    cudaError_t e = cudaFuncSetAttribute(narrow ? (const void*)bwd_top_kernel : (const void*)bwd_level_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    a = smem;
-  }
+  cudaError_t e = kh_smem_optin(narrow ? (const void*)bwd_top_kernel : (const void*)bwd_level_kernel, (int)smem);
+  if (e != cudaSuccess) return e;
   if (narrow) bwd_top_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
   else bwd_level_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y);
   kh_note_launch();
@@ -1888,31 +1870,26 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
   const dim3 grid(nlev, batch);
   FwdArgs fw{};
   if (fwd) fw = {fwd->y, fwd->ru_cur, fwd->ru_stride_cur, fwd->ru_child, fwd->ru_stride_child};
-  auto run = [&](auto kernel, int ms_, int threads, bool& attr) -> cudaError_t {
+  auto run = [&](auto kernel, int ms_, int threads, int) -> cudaError_t {
     const int smem = front_smem_bytes(ms_);
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    cudaError_t e = kh_smem_optin((const void*)kernel, smem);
+    if (e != cudaSuccess) return e;
     kernel<<<grid, threads, smem, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur, upd_child,
                                             upd_stride_child, minpiv, fw);
     kh_note_launch();
     return cudaGetLastError();
   };
-  static bool a[2][5] = {};
-  const int v = fwd ? 1 : 0;
   switch (ms) {
-    case 32: return fwd ? run(factor_front_kernel<32, KH_NW32, true>, 32, 32 * KH_NW32, a[v][0])
-                        : run(factor_front_kernel<32, KH_NW32, false>, 32, 32 * KH_NW32, a[v][0]);
-    case 48: return fwd ? run(factor_front_kernel<48, KH_NW48, true>, 48, 32 * KH_NW48, a[v][1])
-                        : run(factor_front_kernel<48, KH_NW48, false>, 48, 32 * KH_NW48, a[v][1]);
-    case 64: return fwd ? run(factor_front_kernel<64, KH_NW64, true>, 64, 32 * KH_NW64, a[v][2])
-                        : run(factor_front_kernel<64, KH_NW64, false>, 64, 32 * KH_NW64, a[v][2]);
-    case KH_CLASS4: return fwd ? run(factor_front_kernel<KH_CLASS4, KH_NW96, true>, KH_CLASS4, 32 * KH_NW96, a[v][3])
-                        : run(factor_front_kernel<KH_CLASS4, KH_NW96, false>, KH_CLASS4, 32 * KH_NW96, a[v][3]);
-    case 128: return fwd ? run(factor_front_kernel<128, KH_NW128, true>, 128, 32 * KH_NW128, a[v][4])
-                         : run(factor_front_kernel<128, KH_NW128, false>, 128, 32 * KH_NW128, a[v][4]);
+    case 32: return fwd ? run(factor_front_kernel<32, KH_NW32, true>, 32, 32 * KH_NW32, 0)
+                        : run(factor_front_kernel<32, KH_NW32, false>, 32, 32 * KH_NW32, 0);
+    case 48: return fwd ? run(factor_front_kernel<48, KH_NW48, true>, 48, 32 * KH_NW48, 1)
+                        : run(factor_front_kernel<48, KH_NW48, false>, 48, 32 * KH_NW48, 1);
+    case 64: return fwd ? run(factor_front_kernel<64, KH_NW64, true>, 64, 32 * KH_NW64, 2)
+                        : run(factor_front_kernel<64, KH_NW64, false>, 64, 32 * KH_NW64, 2);
+    case KH_CLASS4: return fwd ? run(factor_front_kernel<KH_CLASS4, KH_NW96, true>, KH_CLASS4, 32 * KH_NW96, 3)
+                        : run(factor_front_kernel<KH_CLASS4, KH_NW96, false>, KH_CLASS4, 32 * KH_NW96, 3);
+    case 128: return fwd ? run(factor_front_kernel<128, KH_NW128, true>, 128, 32 * KH_NW128, 4)
+                         : run(factor_front_kernel<128, KH_NW128, false>, 128, 32 * KH_NW128, 4);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -120,11 +120,16 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     const double* mv, const double* av, const double* Y, int64_t ldy,
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
                                     int32_t nblk, cudaStream_t stream);
+// Compensated (double-double) residual pieces (residual.cu).
+cudaError_t kh_launch_dgemm_dd(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                               int64_t ldb, double* Chi, double* Clo, int64_t ldc, cudaStream_t stream);
+cudaError_t kh_launch_pair_residual_dd(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                       const double* mv, const double* av, const double* Y1, int64_t ldy1,
+                                       const double* Y2h, const double* Y2l, int64_t ldy2, const double* F,
+                                       int64_t ldf, double* R, int64_t ldr, double* part, int32_t nblk,
+                                       cudaStream_t stream);
 cudaError_t kh_launch_sumsq(const double* x, int64_t n, double* part, int32_t nblk, cudaStream_t stream);
 cudaError_t kh_launch_daxpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream);
-cudaError_t kh_launch_dot(const double* x, const double* y, int64_t n, double* part, int32_t nblk,
-                          cudaStream_t stream);
-cudaError_t kh_launch_dscal(int64_t n, double alpha, double* x, cudaStream_t stream);
 // Shared-memory DMMA factorization of fronts with m <= ms (ms = 32, 48 or 64).
 // Fused forward solve of the factor kernels (kh_plan_factor_fwd): y holds the
 // gathered rhs of the batch; rhs updates go through the level buffers of the
@@ -147,6 +152,10 @@ cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const doub
 
 // Counts every kernel launch made by the library (kh_launch_count in the ABI).
 void kh_note_launch();
+
+// Dynamic shared memory above 48 KB: the opt-in attribute is per device, so it
+// is cached per (kernel, current device) and raised when a larger size comes.
+cudaError_t kh_smem_optin(const void* kernel, int bytes);
 
 // Temporal H_T assembly (temporal.cu).
 namespace kh_ht {

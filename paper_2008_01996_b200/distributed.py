@@ -129,10 +129,10 @@ class EngineOps:
                         e._stream())
         return e.R, e._rel(e.norms[:2])
 
-    def axpy_(self, y, x):
+    def axpy_(self, y, x, alpha=1.0):
         from . import _native
 
-        _native.call("kh_daxpy", y.numel(), 1.0, x.data_ptr(), y.data_ptr(), self.e._stream())
+        _native.call("kh_daxpy", y.numel(), float(alpha), x.data_ptr(), y.data_ptr(), self.e._stream())
 
 
 class PeerSlots:
@@ -265,6 +265,27 @@ class ShardedFD:
             self.wperm = (torch.from_numpy(np.ascontiguousarray(wperm.T)).to(dev) if dev.type == "cuda"
                           else torch.from_numpy(wperm))
 
+    def close(self):
+        """Teardown of the peer-memory path: unmap the other ranks' receive
+        buffers, then wait until every rank has done so, so no receive
+        buffer is freed while a peer still maps it. Collective over the group
+        (call it on every rank; idempotent)."""
+        if self.peers is None:
+            return
+        import torch.distributed as dist
+
+        self.peers.close()
+        self.peers = None
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
     def rows(self, c):
         r0 = c * self.rp
         return r0, max(0, min(self.n, r0 + self.rp) - r0)
@@ -332,6 +353,10 @@ class ShardedFD:
             steps += 1
             R, new = self._residual()
             info["residuals"].append(new)
+            if not new < rel:
+                # the step did not help (rounding floor): undo it, keep the best iterate
+                self.ops.axpy_(self.U, self.D, -1.0)
+                break
             stalled = not new < REFINE_MIN_GAIN * rel  # stagnation: classic IR stop rule
             rel = new
             if stalled:
@@ -400,14 +425,14 @@ def solve_fd_sharded(system, pencil=None, refine=5, refine_tol=1e-13, leaf_size=
             F = rhs_t.to(dev).view(nt, n)
         symbolic = fut.result()
     report.min_re_lambda = pencil.min_re_lambda
-    report.spectral = pencil.spectral_stats
+    report.spectral_source = solvers.spectral_source(pencil)
     t0 = time.perf_counter()
-    runner = ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
-                       leaf_size=leaf, group=group, collective=collective,
-                       engine_kwargs={"symbolic": symbolic})
-    U, info = runner.solve(F, refine=refine, tol=refine_tol)
-    r0, rows = runner.rows(rank)
-    out = solvers._to_host(U[:, :rows])
+    with ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world, device=dev,
+                   leaf_size=leaf, group=group, collective=collective,
+                   engine_kwargs={"symbolic": symbolic}) as runner:
+        U, info = runner.solve(F, refine=refine, tol=refine_tol)
+        r0, rows = runner.rows(rank)
+        out = solvers._to_host(U[:, :rows])
     report.t_spatial = time.perf_counter() - t0
     report.fd_residual = info["residuals"][0]
     report.refine_steps = info["refine_steps"]

@@ -48,9 +48,9 @@ class ModalPlan:
 
 
 # iterative refinement stops once a step fails to halve the residual (the
-# classic rule: further steps only shuffle rounding errors at the fp64 floor
-# of evaluating f - K u; c4 reaches 3.4e-11 in two steps, then 3.44e-11,
-# 3.43e-11, ... -- SURVEY 8(a) / DESIGN section 7)
+# classic rule: further steps only shuffle rounding errors at the floor of
+# evaluating f - K u); a step that does not lower it at all is undone
+# (FDEngine.refine_step), so the best iterate is returned
 REFINE_MIN_GAIN = 0.5
 
 
@@ -131,6 +131,22 @@ def modal_plan(temporal, pencil):
     weight = np.concatenate([np.full(len(reps), 2.0), np.ones(len(singles))])
     return ModalPlan(n_t=n_t, lam=lam, weight=weight, n_pairs=len(reps), n_single=len(singles),
                      w_in=np.ascontiguousarray(w_in), w_out=np.ascontiguousarray(w_out), kron_b=kron_b)
+
+
+def _on_device(fn):
+    """Run an FDEngine method with the engine's device current (streams,
+    kh_dgemm and the torch allocations then all refer to that device; the
+    caller's current device is restored afterwards)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        import torch
+
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+
+    return wrapper
 
 
 def _fortran(t_np, device):
@@ -228,9 +244,11 @@ class FDEngine:
         if fuse_forward is None:
             fuse_forward = os.environ.get("KH_FUSED_FWD", "0") == "1"
         self.fuse_forward = bool(fuse_forward)
-        # refinement: "richardson" (u += FD(f - K u)) or "gmres" (FD as the
-        # right preconditioner of a short GMRES cycle); KH_REFINE overrides
-        self.refine_method = os.environ.get("KH_REFINE", "richardson")
+        # compensated residual once the fp64 one stagnates above the tolerance
+        # ("auto"), always (True) or never (False); KH_COMPENSATED overrides
+        env = os.environ.get("KH_COMPENSATED")
+        self.compensated = {"1": True, "0": False}.get(env, "auto")
+        self.residual_mode = "fp64"
 
         dev = self.device
         f64 = torch.float64
@@ -254,7 +272,9 @@ class FDEngine:
 
     # ---- primitives -----------------------------------------------------------
     def _stream(self):
-        return _native.stream_handle()
+        import torch
+
+        return _native.stream_handle(torch.cuda.current_stream(self.device))
 
     def _timed(self, name, fn, *args):
         """fn(*args), bracketed by CUDA events on the current stream when
@@ -263,10 +283,11 @@ class FDEngine:
             return fn(*args)
         import torch
 
+        st = torch.cuda.current_stream(self.device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(st)
         out = fn(*args)
-        e1.record()
+        e1.record(st)
         self.timers.setdefault(name, []).append((e0, e1))
         return out
 
@@ -295,6 +316,7 @@ class FDEngine:
         for *_, st in self.pipes:
             main.wait_stream(st)
 
+    @_on_device
     def factor(self, events=None):
         """Factor M_x + lambda_k A_x for every retained shift (no-op otherwise).
 
@@ -304,9 +326,10 @@ class FDEngine:
             return
         import torch
 
+        main = torch.cuda.current_stream(self.device)
         if events is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+            e0.record(main)
 
         def body(plan, k0, k1, b, ts):
             st = _native.stream_handle(ts)
@@ -317,12 +340,13 @@ class FDEngine:
 
         self._run_pipes(body)
         if events is not None:
-            e1.record()
+            e1.record(main)
             events.append((e0, e1))
         for plan, k0, k1, b, st in self.pipes:
             plan.pivot_check(0, k1 - k0, self._stream())
         self.factored = True
 
+    @_on_device
     def _spatial(self):
         """Z[:, k] = (M_x + lambda_k A_x)^-1 G[:, k] for all modes.
 
@@ -385,6 +409,30 @@ class FDEngine:
         if fuse and self.keep_factors:
             self.factored = True
 
+    @_on_device
+    def refine_step(self, U, F, rel, dd=False):
+        """One Richardson step u += FD(f - K u) on the residual held in R.
+        The correction goes to the (then free) G buffer and is added with a
+        daxpy, so a step that fails to lower the residual is undone: returns
+        (new relative residual, residual of the returned U, keep_going).
+        dd: the new residual is evaluated in compensated arithmetic."""
+        import torch
+
+        n, nt = self.n, self.n_t
+        corr = self.G.view(-1)[: n * nt].view(nt, n)  # G is consumed by the first GEMM of fd_apply
+        self.fd_apply(self.R, corr, accumulate=False)
+        st = self._stream()
+        _native.call("kh_daxpy", U.numel(), 1.0, corr.data_ptr(), U.data_ptr(), st)
+        new = self._rel(self.residual(U, F, dd=dd))
+        if not new < rel:
+            # rounding floor reached: undo the step, keep the best iterate
+            _native.call("kh_daxpy", U.numel(), -1.0, corr.data_ptr(), U.data_ptr(), st)
+            self.gpu_launches += 2
+            return new, rel, False
+        self.gpu_launches += 1
+        return new, new, new < REFINE_MIN_GAIN * rel
+
+    @_on_device
     def fd_apply(self, F, U, accumulate=False):
         """U (+)= FD(F): F and U are device column-major n x N_t buffers (torch
         tensors of shape (N_t, n))."""
@@ -396,16 +444,32 @@ class FDEngine:
         self._timed("gemm", self._gemm, n, nt, nk2, 1.0, self.Z.data_ptr(), n, self.w_out.data_ptr(), nk2,
                     1.0 if accumulate else 0.0, U.data_ptr(), n)
 
-    def residual(self, U, F, keep_r=True):
-        """Device: R = F - K U; returns (||R||^2, ||F||^2) as a device tensor slice."""
+    @_on_device
+    def residual(self, U, F, keep_r=True, dd=False):
+        """Device: R = F - K U; returns (||R||^2, ||F||^2) as a device tensor slice.
+
+        dd=True evaluates it in compensated arithmetic (kh_dgemm_dd for
+        U M_t^T, kh_plan_residual_dd): the low parts of U M_t^T go to the
+        Z buffer, which is free between FD applications."""
         n, nt = self.n, self.n_t
-        self._timed("gemm_kron", self._gemm, n, 2 * nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt, 0.0,
-                    self.Y.data_ptr(), n)
-        self._timed("residual", self.plan.residual, nt, self.Y.data_ptr(), n, F.data_ptr(), n,
-                    self.R.data_ptr() if keep_r else None, n, self.norms.data_ptr(), self._stream())
-        self.gpu_launches += 2
+        if not dd:
+            self._timed("gemm_kron", self._gemm, n, 2 * nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt,
+                        0.0, self.Y.data_ptr(), n)
+            self._timed("residual", self.plan.residual, nt, self.Y.data_ptr(), n, F.data_ptr(), n,
+                        self.R.data_ptr() if keep_r else None, n, self.norms.data_ptr(), self._stream())
+            self.gpu_launches += 2
+            return self.norms[:2]
+        st = self._stream()
+        y1, y2 = self.Y.data_ptr(), self.Y.data_ptr() + 8 * n * nt
+        self._timed("gemm_kron", self._gemm, n, nt, nt, 1.0, U.data_ptr(), n, self.kron_b.data_ptr(), nt, 0.0, y1, n)
+        self._timed("gemm_dd", _native.call, "kh_dgemm_dd", n, nt, nt, U.data_ptr(), n,
+                    self.kron_b.data_ptr() + 8 * nt * nt, nt, y2, self.Z.data_ptr(), n, st)
+        self._timed("residual_dd", self.plan.residual_dd, nt, y1, n, y2, self.Z.data_ptr(), n, F.data_ptr(), n,
+                    self.R.data_ptr() if keep_r else None, n, self.norms.data_ptr(), st)
+        self.gpu_launches += 4
         return self.norms[:2]
 
+    @_on_device
     def solve(self, F, U=None, refine=5, tol=1e-13):
         """Full FD solve of K u = f on the device with iterative refinement.
 
@@ -421,87 +485,38 @@ class FDEngine:
         norms = self.residual(U, F).tolist()
         rel = float(np.sqrt(norms[0]) / np.sqrt(norms[1])) if norms[1] > 0 else float(np.sqrt(norms[0]))
         info["residuals"].append(rel)
-        steps = 0
-        if rel > tol and refine > 0 and self.refine_method == "gmres":
-            out = self._gmres(F, U, rel, float(np.sqrt(norms[1])), refine, tol, info)
-            if out is not None:
-                info["refine_steps"], info["residual"] = out
-                return U, info
-        while rel > tol and steps < refine:
-            self.fd_apply(self.R, U, accumulate=True)
-            steps += 1
-            new = self._rel(self.residual(U, F))
-            info["residuals"].append(new)
-            if not new < REFINE_MIN_GAIN * rel:  # stagnation at the rounding floor
-                rel = new
-                break
-            rel = new
+        rel, steps = self.refine(U, F, rel, refine, tol, info["residuals"])
         info["refine_steps"] = steps
         info["residual"] = rel
+        info["residual_mode"] = self.residual_mode
         return U, info
 
-    def _dot(self, x, y):
-        _native.call("kh_dot", x.data_ptr(), y.data_ptr(), x.numel(), self._dots.data_ptr(), self._stream())
-        return float(self._dots.item())
-
-    def _gmres(self, F, U, rel0, fnorm, m, tol, info):
-        """Refinement by FD-right-preconditioned GMRES (flexible form: the
-        preconditioned directions z_j = FD(v_j) are kept), one cycle of at most
-        m steps; each step costs what a Richardson step does (one FD
-        application, one K application) and never reduces the residual less.
-        Stops at `tol`, at stagnation (the estimate fails to halve), or when
-        the Krylov vectors do not fit in device memory (returns None: the
-        caller falls back to Richardson). U is updated in place."""
-        import torch
-
-        N = U.numel()
-        with torch.cuda.device(self.device):
-            free, _ = torch.cuda.mem_get_info()
-            free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
-        if (2 * m + 2) * N * 8 > 0.9 * free:
-            return None
-        st = self._stream()
-        if getattr(self, "_dots", None) is None:
-            self._dots = torch.zeros(1, dtype=torch.float64, device=self.device)
-        zero = torch.zeros_like(F)
-        beta = rel0 * fnorm
-        v = self.R.clone()
-        _native.call("kh_dscal", N, 1.0 / beta, v.data_ptr(), st)
-        V, Z = [v], []
-        H = np.zeros((m + 1, m))
-        y = np.zeros(0)
-        est_prev = rel0
-        steps = 0
-        for j in range(m):
-            z = torch.empty_like(U)
-            self.fd_apply(V[j], z)                       # z_j = FD(v_j)
-            self.residual(z, zero)                       # R = -K z_j
-            w = self.R.clone()
-            _native.call("kh_dscal", N, -1.0, w.data_ptr(), st)
-            for i in range(j + 1):                       # modified Gram-Schmidt
-                h = self._dot(w, V[i])
-                H[i, j] = h
-                _native.call("kh_daxpy", N, -h, V[i].data_ptr(), w.data_ptr(), st)
-            hn = float(np.sqrt(max(self._dot(w, w), 0.0)))
-            H[j + 1, j] = hn
-            Z.append(z)
-            steps = j + 1
-            rhs = np.zeros(j + 2)
-            rhs[0] = beta
-            y, *_ = np.linalg.lstsq(H[:j + 2, :j + 1], rhs, rcond=None)
-            est = float(np.linalg.norm(rhs - H[:j + 2, :j + 1] @ y)) / fnorm
-            info["residuals"].append(est)
-            if est <= tol or not est < REFINE_MIN_GAIN * est_prev or hn <= 1e-300 or j + 1 == m:
-                break
-            est_prev = est
-            _native.call("kh_dscal", N, 1.0 / hn, w.data_ptr(), st)
-            V.append(w)
-        for i, yi in enumerate(y):
-            _native.call("kh_daxpy", N, float(yi), Z[i].data_ptr(), U.data_ptr(), st)
-        self.gpu_launches += 4 * steps + steps * (steps + 3) // 2
-        rel = self._rel(self.residual(U, F))             # the true residual of the update
-        info["residuals"].append(rel)
-        return steps, rel
+    def refine(self, U, F, rel, max_steps, tol, history=None):
+        """Iterative refinement u += FD(f - K u) from the residual held in R
+        (relative value `rel`) until `tol`, `max_steps`, or stagnation. If the
+        fp64 residual stagnates above `tol` (its evaluation floor: fine
+        meshes), the residual is re-evaluated in compensated arithmetic and
+        refinement continues on it (self.compensated: "auto", True, False).
+        Returns (relative residual of U, steps taken)."""
+        steps, dd = 0, self.compensated is True
+        self.residual_mode = "fp64"
+        if dd and rel > tol:
+            rel = self._rel(self.residual(U, F, dd=True))
+            self.residual_mode = "dd"
+        while rel > tol and steps < max_steps:
+            new, rel, go = self.refine_step(U, F, rel, dd=dd)
+            steps += 1
+            if history is not None:
+                history.append(new)
+            if not go:  # stagnation at the evaluation floor (a worse step was undone)
+                if dd or self.compensated is False or rel <= tol:
+                    break
+                dd = True
+                self.residual_mode = "dd"
+                rel = self._rel(self.residual(U, F, dd=True))
+                if history is not None:
+                    history.append(rel)
+        return rel, steps
 
     @staticmethod
     def _rel(norms):

@@ -16,9 +16,9 @@ conjugate eigenpair is solved (the partner is its conjugate), which makes the
 back transform real by construction; and the FD result is polished by
 iterative refinement on the space-time residual (`refine`, default up to 3
 steps to a 1e-13 relative residual). `refine=0` gives the plain FD of the
-reference. The report keeps every reference field and adds `t_refine`,
-`refine_steps`, `imag_residue` and `fd_residual` (the residual before
-refinement).
+reference. The report keeps every reference field (and its t_total
+convention) and adds `t_refine`, `t_solve`, `refine_steps`, `imag_residue`
+and `fd_residual` (the residual before refinement).
 """
 
 import os
@@ -37,7 +37,7 @@ from .dense import (ComplexSchurForm, EigenSvdForm, RealSchurForm, cholesky_lowe
 from .errors import DefectivePencil, DimensionMismatch, ImaginaryResidueTooLarge
 
 FD_IMAG_TOL = 1e-6       # solvers.py:400
-DEFAULT_REFINE = 5  # c3 stops after 1 step (1e-13 reached), c4 needs 4
+DEFAULT_REFINE = 5  # upper bound; the stop rule ends c3 after 1 step, c4 after 3
 DEFAULT_REFINE_TOL = 1e-13
 
 
@@ -123,9 +123,39 @@ class SpaceTimeSolution:
         return full
 
 
+class _LazyStat:
+    """Dataclass field descriptor for sigma_min / sigma_max / kappa2: an
+    ordinary assignable float (reference solvers.py:136-139), which, while
+    unset, is produced on first read from the report's `spectral_source`
+    (a callable returning (sigma_min, sigma_max); see solve_fd)."""
+
+    def __set_name__(self, owner, name):
+        self.name = name
+        self.slot = "_" + name
+
+    def __get__(self, obj, objtype=None):
+        if obj is None:
+            return None  # the dataclass default: "not set"
+        v = obj.__dict__.get(self.slot)
+        if v is None:
+            lo, hi = obj._spectral_pair()
+            v = {"sigma_min": lo, "sigma_max": hi, "kappa2": hi / lo if lo > 0.0 else 0.0}[self.name]
+        return v
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.slot] = None if value is None else float(value)
+
+
 @dataclass
 class SolveReport:
-    """Per-stage wall times and spectral statistics (solvers.py:125-163)."""
+    """Per-stage wall times and spectral statistics (solvers.py:125-163).
+
+    Same fields and `t_total` convention as the reference (decompose +
+    transform_in + spatial + transform_out, solvers.py:146-149); the GPU
+    build adds `t_refine` (iterative refinement, reported separately;
+    `t_solve` = t_total + t_refine is the whole solve), `refine_steps`,
+    `imag_residue`, `fd_residual`, `device` and `phases`.
+    """
 
     variant: str
     dof: int
@@ -137,6 +167,9 @@ class SolveReport:
     t_transform_out: float = 0.0
     residual: float = 0.0
     min_re_lambda: float = 0.0
+    sigma_min: float = _LazyStat()
+    sigma_max: float = _LazyStat()
+    kappa2: float = _LazyStat()
     threads: int = 1
     analyze_calls: int = 0
     fallback: Optional[str] = None
@@ -145,35 +178,31 @@ class SolveReport:
     refine_steps: int = 0
     imag_residue: float = 0.0
     fd_residual: float = 0.0
+    residual_mode: str = "fp64"   # "dd": the refinement finished on the compensated residual
     device: str = ""
     # host-side milestones of solve_fd in seconds since its start (pencil,
     # analyze, host_joined, plan, factored): where the end-to-end time goes
     phases: dict = field(default_factory=dict)
-    # (sigma_min, sigma_max) of X_t, or a callable producing them on first use
-    spectral: object = field(default=(0.0, 0.0), repr=False)
+    # callable -> (sigma_min, sigma_max) of X_t for the unset spectral fields
+    spectral_source: object = field(default=None, repr=False, compare=False)
 
-    def _spectral(self):
-        if callable(self.spectral):
-            self.spectral = tuple(self.spectral())
-        return self.spectral
-
-    @property
-    def sigma_min(self):
-        return self._spectral()[0]
-
-    @property
-    def sigma_max(self):
-        return self._spectral()[1]
-
-    @property
-    def kappa2(self):
-        lo, hi = self._spectral()
-        return hi / lo if lo > 0.0 else 0.0
+    def _spectral_pair(self):
+        if self.spectral_source is None:
+            return 0.0, 0.0
+        key = "_spectral_cache"
+        if key not in self.__dict__:
+            lo, hi = self.spectral_source()
+            self.__dict__[key] = (float(lo), float(hi))
+        return self.__dict__[key]
 
     @property
     def t_total(self):
-        return (self.t_decompose + self.t_transform_in + self.t_spatial + self.t_transform_out
-                + self.t_refine)
+        return self.t_decompose + self.t_transform_in + self.t_spatial + self.t_transform_out
+
+    @property
+    def t_solve(self):
+        """The whole GPU solve: t_total plus the refinement steps."""
+        return self.t_total + self.t_refine
 
     def csv_row(self):
         return (f"{self.dof},{self.n_t},{self.m_x},{self.variant},"
@@ -233,6 +262,19 @@ def build_pencil(temporal, variant, eig="qz"):
     return pencil
 
 
+def spectral_source(pencil):
+    """(sigma_min, sigma_max) producer for a report: this build's pencils
+    carry `spectral_stats` (the reference's dggev statistics); a pencil built
+    by the reference itself (or any object with an eigen-SVD `form`) gives
+    its form's singular values, as the reference's solve_fd does
+    (solvers.py:358-360)."""
+    fn = getattr(pencil, "spectral_stats", None)
+    if callable(fn):
+        return fn
+    form = pencil.form
+    return lambda: (float(form.sigma_min), float(form.sigma_max))
+
+
 def _blas_threads(n):
     try:
         from threadpoolctl import threadpool_limits
@@ -277,7 +319,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     import torch
 
     from . import _native
-    from .engine import REFINE_MIN_GAIN, FDEngine, modal_plan
+    from .engine import FDEngine, modal_plan
 
     _native.require_cuda()
     report = SolveReport(variant="fd", dof=system.dof, n_t=system.n_t, m_x=system.m_x, threads=threads)
@@ -323,7 +365,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
         symbolic = fut.result()
         phases["host_joined"] = time.perf_counter() - t0
     report.min_re_lambda = pencil.min_re_lambda
-    report.spectral = pencil.spectral_stats
+    report.spectral_source = spectral_source(pencil)
 
     # spatial setup: numeric plan + factorization of every shift
     eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev, leaf_size=leaf_size,
@@ -358,15 +400,10 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     t0 = time.perf_counter()
     rel = eng._rel(eng.residual(U, F))
     report.fd_residual = rel
-    steps = 0
-    while rel > refine_tol and steps < refine:
-        eng.fd_apply(eng.R, U, accumulate=True)
-        steps += 1
-        new = eng._rel(eng.residual(U, F))
-        stalled = not new < REFINE_MIN_GAIN * rel  # stagnation: classic IR stop rule
-        rel = new
-        if stalled:
-            break
+    # u += FD(f - K u): a step that does not help is undone; stagnation of the
+    # fp64 residual above refine_tol switches to the compensated residual
+    rel, steps = eng.refine(U, F, rel, refine, refine_tol)
+    report.residual_mode = eng.residual_mode
     coeffs = _to_host(U.reshape(-1))
     report.t_refine = time.perf_counter() - t0
     report.refine_steps = steps
@@ -374,8 +411,12 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     return SpaceTimeSolution(coefficients=coeffs), report
 
 
-def residual(system, coefficients):
-    """Relative residual ||K u - f|| / ||f|| on the GPU (solvers.py:428-440)."""
+def residual(system, coefficients, compensated=False):
+    """Relative residual ||K u - f|| / ||f|| on the GPU (solvers.py:428-440).
+
+    compensated=True evaluates it with error-free products and sums
+    (kh_dgemm_dd + kh_csr_pair_residual_dd): the accurate value at fine
+    meshes, where the fp64 evaluation itself is off by ~1e-11 (config c4)."""
     import torch
 
     from . import _native
@@ -401,9 +442,19 @@ def residual(system, coefficients):
     Y = torch.empty((2 * nt, n), dtype=torch.float64, device=dev)
     norms = torch.zeros(2, dtype=torch.float64, device=dev)
     st = _native.stream_handle()
-    _native.call("kh_dgemm", n, 2 * nt, nt, 1.0, U.data_ptr(), n, kron_b.data_ptr(), nt, 0.0, Y.data_ptr(), n, st)
-    _native.call("kh_csr_pair_residual", n, nt, d_ptr.data_ptr(), d_idx.data_ptr(), d_m.data_ptr(),
-                 d_a.data_ptr(), Y.data_ptr(), n, F.data_ptr(), n, None, n, norms.data_ptr(), st)
+    if compensated:
+        lo = torch.empty((nt, n), dtype=torch.float64, device=dev)
+        y1, y2 = Y.data_ptr(), Y.data_ptr() + 8 * n * nt
+        _native.call("kh_dgemm", n, nt, nt, 1.0, U.data_ptr(), n, kron_b.data_ptr(), nt, 0.0, y1, n, st)
+        _native.call("kh_dgemm_dd", n, nt, nt, U.data_ptr(), n, kron_b.data_ptr() + 8 * nt * nt, nt, y2,
+                     lo.data_ptr(), n, st)
+        _native.call("kh_csr_pair_residual_dd", n, nt, d_ptr.data_ptr(), d_idx.data_ptr(), d_m.data_ptr(),
+                     d_a.data_ptr(), y1, n, y2, lo.data_ptr(), n, F.data_ptr(), n, None, n, norms.data_ptr(), st)
+    else:
+        _native.call("kh_dgemm", n, 2 * nt, nt, 1.0, U.data_ptr(), n, kron_b.data_ptr(), nt, 0.0, Y.data_ptr(), n,
+                     st)
+        _native.call("kh_csr_pair_residual", n, nt, d_ptr.data_ptr(), d_idx.data_ptr(), d_m.data_ptr(),
+                     d_a.data_ptr(), Y.data_ptr(), n, F.data_ptr(), n, None, n, norms.data_ptr(), st)
     r2, f2 = norms.tolist()
     if f2 == 0.0:
         return float(np.sqrt(r2))

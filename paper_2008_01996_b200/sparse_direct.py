@@ -210,6 +210,10 @@ class _Plan:
         _native.call("kh_plan_residual", self.raw, int(nt), Y, int(ldy), F, int(ldf), R, int(ldr), norms2,
                      stream)
 
+    def residual_dd(self, nt, Y1, ldy1, Y2hi, Y2lo, ldy2, F, ldf, R, ldr, norms2, stream):
+        _native.call("kh_plan_residual_dd", self.raw, int(nt), Y1, int(ldy1), Y2hi, Y2lo, int(ldy2), F, int(ldf),
+                     R, int(ldr), norms2, stream)
+
     def __del__(self, _native=_native):
         if getattr(self, "raw", None) and self.raw.value and _native is not None and _native._lib is not None:
             _native._lib.kh_plan_free(self.raw)

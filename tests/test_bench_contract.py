@@ -23,3 +23,28 @@ def test_reference_arm_json_line():
     assert line["e2e"]["value"] == line["value"]
     assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
     assert line["config"]["workload"].startswith("c1")
+    assert line["cpu_baseline"]["sample"].startswith("full solve")
+    assert line["residual"] < 1e-8
+    assert set(line["config"]) == {"workload", "j_max", "parallelism"}
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run, 127.0.0.1); --spawn-check makes each rank report
+    its rank / world size and exit before touching a GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--spawn-check"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    seen = sorted(json.loads(l)["rank"] for l in out.stdout.splitlines() if l.startswith("{"))
+    assert seen == [0, 1]
+    for l in out.stdout.splitlines():
+        if l.startswith("{"):
+            assert json.loads(l)["world"] == 2
+
+
+def test_gpus_flag_must_match_world():
+    env = {**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--spawn-check"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=300, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr

@@ -51,8 +51,8 @@ def test_sharded_fd_world1_nccl(cuda_ok, collective):
         assert rel_diff(U_rows.reshape(-1), ref["bs"]) < 1e-10
         assert rep.residual < 1e-11
     finally:
-        if run is not None and run.peers is not None:
-            run.peers.close()
+        if run is not None:
+            run.close()
         dist.destroy_process_group()
 
 
@@ -103,3 +103,65 @@ def test_ipc_handle_reports_offset_inside_allocation(cuda_ok):
     assert offs[1] - offs[0] == 8 * 1000
     assert offs[2] - offs[0] == 8 * 4096
     assert offs[0] >= 0
+
+
+def _p2p_worker(rank, world, port, out_dir):
+    """One rank of the world-2 p2p check: both ranks on cuda:0 (CUDA IPC is
+    valid within one device), host-side exchange over gloo. The kernels never
+    wait on each other (the ranks synchronize on the host), so two processes on
+    one GPU are safe here."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_01996_b200 import solvers
+    from paper_2008_01996_b200.distributed import ShardedFD
+    from paper_2008_01996_b200.engine import modal_plan
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        system, _ = load_golden("c1")
+        modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
+        with ShardedFD(system.spatial.M_II, system.spatial.A_II, modal, rank, world,
+                       device=torch.device("cuda", 0), collective="p2p") as run:
+            assert run.peers is not None and run.peers.ok, getattr(run.peers, "error", "no peers")
+            assert len(run.peers.mapped) == world - 1
+            F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
+            run.ops.factor(None)
+            out = torch.zeros((system.n_t, run.rp), dtype=torch.float64, device="cuda")
+            run._apply(F, out)   # FD application: local GEMM -> fused row-scatter into peer slots -> slot sum
+            torch.cuda.synchronize()
+            r0, rows = run.rows(rank)
+            np.save(os.path.join(out_dir, f"rank{rank}.npy"), out[:, :rows].cpu().numpy())
+            np.save(os.path.join(out_dir, f"rows{rank}.npy"), np.array([r0, rows]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_world2_on_one_gpu(cuda_ok, tmp_path):
+    """The default-capable p2p collective at world 2: CUDA-IPC mapping of the
+    peer's receive buffer, kh_dgemm_rowscatter writing into it, the ordered
+    slot sum and the teardown; each rank's rows equal the single-rank FD
+    application."""
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2008_01996_b200 import solvers
+    from paper_2008_01996_b200.engine import FDEngine, modal_plan
+
+    mp.spawn(_p2p_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    system, _ = load_golden("c1")
+    modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
+    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=torch.device("cuda", 0))
+    F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
+    U = torch.empty_like(F)
+    eng.fd_apply(F, U)
+    full = U.cpu().numpy()  # (N_t, n): column-major n x N_t
+    covered = 0
+    for r in range(2):
+        r0, rows = np.load(tmp_path / f"rows{r}.npy")
+        got = np.load(tmp_path / f"rank{r}.npy")
+        want = full[:, r0:r0 + rows]
+        assert rel_diff(got, want) < 1e-12
+        covered += rows
+    assert covered == system.m_x

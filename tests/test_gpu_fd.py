@@ -164,18 +164,68 @@ def test_fused_forward_sweep_agrees(cuda_ok, name):
     assert rel_diff(out[1], ref["bs"]) < 1e-10
 
 
-def test_gmres_refinement_option(cuda_ok):
-    """FDEngine.refine_method = "gmres" (FD-preconditioned GMRES cycle)
-    reaches the same solution as the default Richardson refinement."""
-    import torch
+# ---- drop-in: a pencil built by the reference itself ---------------------------
+@dataclasses.dataclass(frozen=True)
+class _RefEigenSvdForm:
+    """The attribute set of the reference's kronheat.dense.EigenSvdForm (dense.py:81-106)."""
 
-    from paper_2008_01996_b200.engine import FDEngine, modal_plan
+    X: np.ndarray
+    D: np.ndarray
+    U: np.ndarray
+    sigma: np.ndarray
+    Vh: np.ndarray
 
-    system, ref = load_golden("c1")
-    modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
-    F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
-    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal)
-    eng.refine_method = "gmres"
-    U, info = eng.solve(F)
-    assert info["residual"] < 1e-12 and info["refine_steps"] >= 1
-    assert rel_diff(U.cpu().numpy().ravel(), ref["bs"]) < 1e-10
+    @property
+    def sigma_min(self):
+        return float(self.sigma[-1])
+
+    @property
+    def sigma_max(self):
+        return float(self.sigma[0])
+
+    @property
+    def kappa2(self):
+        return float(self.sigma[0] / self.sigma[-1])
+
+
+@dataclasses.dataclass(frozen=True)
+class _RefPencil:
+    """The attribute set of kronheat.solvers.PencilFactorization (solvers.py:85-101):
+    no spectral_stats, no temporal operators."""
+
+    variant: str
+    chol_A: np.ndarray
+    form: object
+
+    @property
+    def eigenvalues(self):
+        return self.form.D
+
+    @property
+    def min_re_lambda(self):
+        return float(np.min(self.eigenvalues.real))
+
+
+def _reference_pencil(name):
+    import os
+
+    from conftest import GOLDEN
+
+    z = np.load(os.path.join(GOLDEN, "ref_pencil.npz"))
+    form = _RefEigenSvdForm(*(z[f"{name}_{f}"] for f in ("X", "D", "U", "sigma", "Vh")))
+    return _RefPencil(variant=str(z[f"{name}_variant"]), chol_A=z[f"{name}_chol_A"], form=form)
+
+
+@pytest.mark.parametrize("name", ["lshape0", "c1"])
+def test_fd_accepts_reference_pencil(cuda_ok, name):
+    """The reference's own pencil (tests/golden/make_ref_pencil.py) goes straight
+    into the drop-in solve_fd; the report carries the reference's statistics."""
+    system, ref = load_golden(name)
+    pencil = _reference_pencil(name)
+    sol, rep = solvers.solve_fd(system, pencil=pencil)
+    assert rel_diff(sol.coefficients, ref["bs"]) < 1e-10
+    assert rep.residual < 1e-11
+    assert rep.kappa2 == pytest.approx(float(ref["fd_kappa2"]), rel=1e-12)
+    assert rep.sigma_min == pytest.approx(float(ref["fd_sigma_min"]), rel=1e-12)
+    assert rep.min_re_lambda == pytest.approx(float(ref["fd_min_re_lambda"]), rel=1e-12)
+    assert rep.t_total == pytest.approx(rep.t_decompose + rep.t_transform_in + rep.t_spatial + rep.t_transform_out)

@@ -7,6 +7,7 @@ import pytest
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
+from conftest import load_golden, rel_diff
 from paper_2008_01996_b200 import _native
 from paper_2008_01996_b200 import sparse_direct as sd
 from paper_2008_01996_b200.errors import DimensionMismatch, SingularMatrix
@@ -248,3 +249,66 @@ def test_native_temporal_p2_matches_host(cuda_ok, nodes):
     # product) and device (sincospi) agree to ~1e-13 of the largest entry
     for a, b in ((host.A, dev.A), (host.M, dev.M), (host.C, dev.C)):
         assert np.abs(a - b).max() < 1e-11 * np.abs(a).max()
+
+
+# ---- compensated residual pieces (residual.cu) ---------------------------------
+def test_dgemm_dd_matches_extended_precision(cuda_ok):
+    """kh_dgemm_dd: hi + lo within a few ulps of extended precision relative
+    to |A| |B| even where the fp64 product cancels."""
+    import torch
+
+    from paper_2008_01996_b200 import _native
+
+    rng = np.random.default_rng(0)
+    m, n, k = 300, 70, 513
+    A = rng.standard_normal((m, k))
+    B = rng.standard_normal((k, n))
+    B[:, :35] -= B[:, :35].mean(axis=0)
+    Ad = torch.from_numpy(A.ravel(order="F")).cuda()
+    Bd = torch.from_numpy(B.ravel(order="F")).cuda()
+    hi = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+    lo = torch.zeros_like(hi)
+    _native.call("kh_dgemm_dd", m, n, k, Ad.data_ptr(), m, Bd.data_ptr(), k, hi.data_ptr(), lo.data_ptr(), m,
+                 _native.stream_handle())
+    got = (hi.cpu().numpy().reshape(m, n, order="F").astype(np.longdouble)
+           + lo.cpu().numpy().reshape(m, n, order="F").astype(np.longdouble))
+    want = A.astype(np.longdouble) @ B.astype(np.longdouble)
+    scale = (np.abs(A) @ np.abs(B)).astype(np.longdouble)
+    err = float(np.max(np.abs(got - want) / scale))
+    err64 = float(np.max(np.abs((A @ B) - want) / scale))
+    assert err < 1e-18 and err < 1e-2 * err64, (err, err64)
+
+
+def test_compensated_residual_matches_oracle_on_c1(cuda_ok):
+    """solvers.residual(compensated=True) == the fp64 one (and the oracle's)
+    where fp64 is accurate (c1), for both reference solutions."""
+    from oracle import fd_oracle as orc
+    from paper_2008_01996_b200 import solvers
+
+    system, ref = load_golden("c1")
+    for key in ("fd", "bs"):
+        want = orc.residual(*orc.system_arrays(system), ref[key])
+        got = solvers.residual(system, ref[key], compensated=True)
+        assert got == pytest.approx(want, rel=1e-4, abs=1e-16)
+    rows = np.arange(0, system.m_x, 97)
+    _, rel_ld = orc.residual_rows_longdouble(*orc.system_arrays(system), ref["fd"], rows)
+    _, rel_ld_bs = orc.residual_rows_longdouble(*orc.system_arrays(system), ref["bs"], rows)
+    assert rel_ld > 0 and rel_ld_bs > 0
+
+
+def test_engine_compensated_refinement_c1(cuda_ok):
+    """FDEngine with compensated=True refines on the compensated residual and
+    reaches the reference BS solution."""
+    import torch
+
+    from paper_2008_01996_b200 import solvers
+    from paper_2008_01996_b200.engine import FDEngine, modal_plan
+
+    system, ref = load_golden("c1")
+    modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
+    F = torch.from_numpy(np.ascontiguousarray(system.rhs)).cuda().view(system.n_t, system.m_x)
+    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal)
+    eng.compensated = True
+    U, info = eng.solve(F)
+    assert info["residual_mode"] == "dd" and info["residual"] < 1e-13
+    assert rel_diff(U.cpu().numpy().ravel(), ref["bs"]) < 1e-10

@@ -56,8 +56,8 @@ class _CpuOps:
         self.R = torch.from_numpy(np.ascontiguousarray(R.T))
         return self.R, float(np.linalg.norm(R) / np.linalg.norm(F.numpy()))
 
-    def axpy_(self, y, x):
-        y.add_(x)
+    def axpy_(self, y, x, alpha=1.0):
+        y.add_(x, alpha=alpha)
 
 
 def _worker(rank, world, port, name, out_dir, collective="nccl"):

@@ -94,8 +94,49 @@ def test_reduced_pencil_reports_reference_statistics(name):
     system, ref = load_golden(name)
     p = solvers.build_pencil(system.temporal, "fd", eig="reduced")
     rep = SolveReport(variant="fd", dof=1, n_t=1, m_x=1)
-    rep.spectral = p.spectral_stats
+    rep.spectral_source = solvers.spectral_source(p)
     assert rep.sigma_min == pytest.approx(float(ref["fd_sigma_min"]), rel=1e-12)
     assert rep.sigma_max == pytest.approx(float(ref["fd_sigma_max"]), rel=1e-12)
     assert rep.kappa2 == pytest.approx(float(ref["fd_kappa2"]), rel=1e-12)
-    assert isinstance(rep.spectral, tuple)
+
+
+def test_report_spectral_fields_assignable():
+    """sigma_min / sigma_max / kappa2 are plain fields as in the reference
+    (solvers.py:136-139): constructor arguments, assignable, 0.0 when unset."""
+    from paper_2008_01996_b200.solvers import SolveReport
+
+    rep = SolveReport(variant="fd", dof=4, n_t=2, m_x=2, sigma_min=0.5, kappa2=3.0)
+    assert rep.sigma_min == 0.5 and rep.kappa2 == 3.0 and rep.sigma_max == 0.0
+    rep.sigma_max = 2.0
+    rep.kappa2 = 4.0
+    assert (rep.sigma_max, rep.kappa2) == (2.0, 4.0)
+    blank = SolveReport(variant="fd", dof=1, n_t=1, m_x=1)
+    assert (blank.sigma_min, blank.sigma_max, blank.kappa2) == (0.0, 0.0, 0.0)
+    # an assigned value wins over the lazy source
+    blank.spectral_source = lambda: (1.0, 8.0)
+    assert blank.kappa2 == 8.0
+    blank.kappa2 = 7.0
+    assert blank.kappa2 == 7.0 and blank.sigma_min == 1.0
+    assert "sigma_min=1.0" in repr(blank)
+
+
+def test_report_t_total_reference_convention():
+    """t_total = decompose + transform_in + spatial + transform_out
+    (solvers.py:146-149); refinement is reported separately."""
+    from paper_2008_01996_b200.solvers import SolveReport
+
+    rep = SolveReport(variant="fd", dof=1, n_t=1, m_x=1, t_decompose=1.0, t_transform_in=2.0, t_spatial=3.0,
+                      t_transform_out=4.0, t_refine=5.0)
+    assert rep.t_total == 10.0
+    assert rep.t_solve == 15.0
+    assert rep.csv_row().split(",")[4:8] == ["1.000000", "2.000000", "3.000000", "4.000000"]
+
+
+def test_spectral_source_of_reference_style_pencil():
+    """A pencil without spectral_stats (the reference's own
+    PencilFactorization) reports its form's singular values."""
+    import types
+
+    form = types.SimpleNamespace(sigma_min=0.25, sigma_max=4.0)
+    pencil = types.SimpleNamespace(variant="fd", chol_A=None, form=form)
+    assert solvers.spectral_source(pencil)() == (0.25, 4.0)
