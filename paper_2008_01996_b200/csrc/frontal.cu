@@ -1337,11 +1337,16 @@ constexpr int FWD_CH = KH_FWD_CH;
 #define KH_BWD_L11 16
 #endif
 constexpr int BWD_L11 = KH_BWD_L11;  // bwd_small stages L11 in shared memory for p <= this
-#ifndef KH_SMALL_SOLVE_MINB
-#define KH_SMALL_SOLVE_MINB 4
-#endif  // panel columns per register chunk (fwd_small, bwd L11 rows)
+// resident 256-thread CTAs per SM the warp-per-front solves are compiled for
+// (register caps: 4 -> 64 registers, 3 -> 80, 2 -> 128)
+#ifndef KH_FWD_SOLVE_MINB
+#define KH_FWD_SOLVE_MINB 4
+#endif
+#ifndef KH_BWD_SOLVE_MINB
+#define KH_BWD_SOLVE_MINB 4
+#endif
 
-__global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+__global__ void __launch_bounds__(256, KH_FWD_SOLVE_MINB) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y, double2* ru_cur,
                                                         int64_t ru_stride_cur, const double2* __restrict__ ru_child,
                                                         int64_t ru_stride_child) {
@@ -1396,7 +1401,7 @@ __global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) fwd_small_kernel(KhT
   else if (r1 < m) ru[r1 - p] = x1;
 }
 
-__global__ void __launch_bounds__(256, KH_SMALL_SOLVE_MINB) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
+__global__ void __launch_bounds__(256, KH_BWD_SOLVE_MINB) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
                                                         const double2* __restrict__ panels, double2* y) {
   const int lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
