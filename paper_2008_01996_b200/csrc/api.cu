@@ -110,6 +110,7 @@ struct kh_plan {
   std::vector<int32_t> cls_off;
   const int32_t* classes(int32_t d) const { return cls_off.data() + kClsStride * d; }
   std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
+  std::vector<int32_t> small_panel_max;  // per level: largest lower panel among the warp-solve fronts
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   // large-front schedule: per level an assembly list and per 32-wide pivot
   // block the diag / left-looking / TRSM lists (offsets into btasks, int32s)
@@ -407,6 +408,7 @@ namespace {
 // Host-side launch schedule derived from the analysis: fronts grouped per
 // level and kernel class, Schur tiles and the large-front block lists.
 struct Sched {
+  std::vector<int32_t> small_panel_max;
   std::vector<KhDevFront> df, lf_df;
   std::vector<KhKid> kids;
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
@@ -470,6 +472,15 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     X.cls_off.push_back((int32_t)X.lf.size() - base);
     X.level_off.push_back((int32_t)X.lf.size());
   }
+  for (const auto& lev : S.levels) {
+    int32_t mx = 1;
+    for (int32_t f : lev) {
+      const kh::Front& F = S.fronts[f];
+      if (front_class(F.m()) < kSolveSmallClasses)
+        mx = std::max<int32_t>(mx, F.p * F.m() - F.p * (F.p - 1) / 2);
+    }
+    X.small_panel_max.push_back(mx);
+  }
   X.lf_df.resize(X.lf.size());
   for (size_t i = 0; i < X.lf.size(); ++i) {
     X.lf_df[i] = X.df[X.lf[i]];
@@ -478,7 +489,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   X.kids.resize(S.child_list.size());
   for (size_t j = 0; j < S.child_list.size(); ++j) {
     const kh::Front& C = S.fronts[S.child_list[j]];
-    X.kids[j] = {C.upd_off, C.rows_begin, C.rupd_off, C.q, 0};
+    X.kids[j] = {C.upd_off, C.rows_begin, C.rupd_off, C.cmap_begin, C.q, 0};
   }
   X.task_off.push_back(0);
   for (size_t d = 0; d < S.levels.size(); ++d) {
@@ -640,6 +651,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->level_off = X.level_off;
   p->cls_off = X.cls_off;
   p->task_off = X.task_off;
+  p->small_panel_max = X.small_panel_max;
   p->big = X.big;
   p->kbinfo = X.kbinfo;
   Carver measure;
@@ -782,7 +794,7 @@ int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* 
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->side[0]));
+    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->small_panel_max[d], p->side[0]));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
                                 p->y, st));
     KH_CUDA(join_side(p, st));
@@ -911,7 +923,8 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->side[0]));
+    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->small_panel_max[d],
+                                p->side[0]));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
                                 rch, sch, st));
     KH_CUDA(join_side(p, st));

@@ -1504,6 +1504,157 @@ __global__ void __launch_bounds__(256, KH_BWD_SOLVE_MINB) bwd_small_kernel(KhTre
   if (k1 < p) yy[k1] = t1;
 }
 
+// Forward solve of the fronts with m <= 64, one warp per (front, shift), the
+// panel staged in shared memory by bulk async copies as in bwd_small_tma_kernel;
+// the front's right-hand side (pivot rows of y plus the children's rhs updates)
+// is gathered while the copies are in flight. Lane l owns rows l and l + 32:
+// x_r -= L[r, k] y_k for r > k, y_k broadcast by shuffles.
+#ifndef KH_FWD_TMA
+#define KH_FWD_TMA 1
+#endif
+#ifndef KH_FWD_TMA_NW
+#define KH_FWD_TMA_NW 1
+#endif
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                                int32_t nlev, const double2* __restrict__ panels,
+                                                                double2* y, double2* ru_cur, int64_t ru_stride_cur,
+                                                                const double2* __restrict__ ru_child,
+                                                                int64_t ru_stride_child, int32_t maxe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int idx = blockIdx.x * NW + warp;
+  if (idx >= nlev) return;
+  const int b = blockIdx.y;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + idx];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* Ls = reinterpret_cast<double2*>(smem_raw) + (int64_t)warp * maxe;
+  uint64_t* br = &bar[warp];
+  auto cbase = [m](int c) { return c * m - (c * (c - 1)) / 2; };
+  if (lane == 0) {
+    mbar_init(br, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
+  __syncwarp();
+  for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  const int r0 = lane, r1 = lane + 32;
+  const double2 z = make_double2(0.0, 0.0);
+  double2 x0 = z, x1 = z;
+  for (int c = F.child_begin; c < F.child_end; ++c) {
+    const KhKid C = T.kids[c];
+    const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
+    const int32_t* cm = T.cmap + C.cmap_begin;
+    const int c0 = r0 < m ? cm[r0] : -1;
+    const int c1 = r1 < m ? cm[r1] : -1;
+    if (c0 >= 0) x0 = cadd(x0, rc[c0]);
+    if (c1 >= 0) x1 = cadd(x1, rc[c1]);
+  }
+  if (r0 < p) x0 = cadd(x0, yy[r0]);
+  if (r1 < p) x1 = cadd(x1, yy[r1]);
+  mbar_wait(br, 0);
+  for (int k = 0; k < p; ++k) {
+    const double2* col = Ls + cbase(k) - k;  // L[r, k] = col[r], r >= k
+    const double2 l0 = (r0 > k && r0 < m) ? col[r0] : z;
+    const double2 l1 = (r1 > k && r1 < m) ? col[r1] : z;
+    const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
+    x0 = cfms(x0, l0, yk);
+    x1 = cfms(x1, l1, yk);
+  }
+  if (r0 < p) yy[r0] = x0;
+  else if (r0 < m) ru[r0 - p] = x0;
+  if (r1 < p) yy[r1] = x1;
+  else if (r1 < m) ru[r1 - p] = x1;
+}
+
+// Backward solve of the fronts with m <= 64, one warp per (front, shift), the
+// front's panel (lower part, column by column: column c = rows c..m-1) staged
+// in shared memory by bulk async copies that lanes 0..p-1 issue at kernel
+// start (one TMA-engine transfer per column, completion counted on the warp's
+// mbarrier). The solution values of the update rows and the pivots' rhs are
+// gathered while the copies are in flight, so the front costs one memory
+// round trip for its panel instead of one per register chunk of columns.
+//  t_k = y_k / d_k - sum_a L21[a, k] xu[a]   (column sums: warp_sum8 over 8 columns)
+//  L11^T x = t                               (lane k owns t_k; pivots by shuffles)
+#ifndef KH_BWD_TMA
+#define KH_BWD_TMA 1
+#endif
+#ifndef KH_BWD_TMA_NW
+#define KH_BWD_TMA_NW 1
+#endif
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                                int32_t nlev, const double2* __restrict__ panels,
+                                                                double2* y, int32_t maxe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int idx = blockIdx.x * NW + warp;
+  if (idx >= nlev) return;
+  const int b = blockIdx.y;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + idx];
+  const int p = F.p, q = F.q, m = p + q;
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* Ls = reinterpret_cast<double2*>(smem_raw) + (int64_t)warp * maxe;
+  uint64_t* br = &bar[warp];
+  auto cbase = [m](int c) { return c * m - (c * (c - 1)) / 2; };
+  if (lane == 0) {
+    mbar_init(br, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
+  __syncwarp();
+  for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  const int64_t* urows = T.urows + F.rows_begin;
+  const double2 z = make_double2(0.0, 0.0);
+  const double2 xu0 = lane < q ? yb[urows[lane]] : z;
+  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : z;
+  const int k0 = lane, k1 = lane + 32;
+  const double2 y0 = k0 < p ? yy[k0] : z, y1 = k1 < p ? yy[k1] : z;
+  mbar_wait(br, 0);
+  double2 t0 = z, t1 = z;
+  for (int kc = 0; kc < p; kc += SOLVE_CH) {
+    double2 sv[SOLVE_CH];
+#pragma unroll
+    for (int u = 0; u < SOLVE_CH; ++u) {
+      const int k = kc + u;
+      const double2* col = Ls + cbase(k) + (p - k);  // L21[:, k]
+      const double2 l0 = (k < p && lane < q) ? col[lane] : z;
+      const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
+      sv[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
+    }
+    const double2 v = warp_sum8(sv, lane);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = lane + 32 * h, u = kk - kc;
+      const int src = ((u >> 2) & 1) << 4 | ((u >> 1) & 1) << 3 | (u & 1) << 2;
+      const double2 got = shfl2(v, src & 31);
+      if (u >= 0 && u < SOLVE_CH && kk < p) {
+        if (h == 0) t0 = got;
+        else t1 = got;
+      }
+    }
+  }
+  if (k0 < p) t0 = csub(cmul(y0, cinv(Ls[cbase(k0)])), t0);
+  if (k1 < p) t1 = csub(cmul(y1, cinv(Ls[cbase(k1)])), t1);
+  // L11^T x = t bottom-up (column form: x_i final -> t_k -= L[i, k] x_i, k < i)
+  for (int i = p - 1; i > 0; --i) {
+    const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
+    if (k0 < i) t0 = cfms(t0, Ls[cbase(k0) + i - k0], xi);
+    if (k1 < i) t1 = cfms(t1, Ls[cbase(k1) + i - k1], xi);
+  }
+  if (k0 < p) yy[k0] = t0;
+  if (k1 < p) yy[k1] = t1;
+}
+
 // Backward solve of the large fronts of a narrow level (top of the tree):
 // one CTA per (front, shift), t and x[urows] in shared memory.
 //  1. t_k = y_k / d_k - sum_a L21[a, k] x[urows[a]]: warps over chunks of 8
@@ -1774,8 +1925,19 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
 
 cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
-                                const double2* ru_child, int64_t ru_stride_child, cudaStream_t stream) {
+                                const double2* ru_child, int64_t ru_stride_child, int32_t max_panel,
+                                cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
+  if (KH_FWD_TMA) {
+    constexpr int nw = KH_FWD_TMA_NW;
+    const int smem = 16 * nw * max_panel;
+    cudaError_t e = kh_smem_optin((const void*)fwd_small_tma_kernel<nw>, smem);
+    if (e != cudaSuccess) return e;
+    fwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(
+        T, level_fronts, nlev, panels, y, ru_cur, ru_stride_cur, ru_child, ru_stride_child, max_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   fwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y, ru_cur,
                                                                     ru_stride_cur, ru_child, ru_stride_child);
   kh_note_launch();
@@ -1783,8 +1945,18 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
 }
 
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                const double2* panels, double2* y, cudaStream_t stream) {
+                                const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
+  if (KH_BWD_TMA) {
+    constexpr int nw = KH_BWD_TMA_NW;
+    const int smem = 16 * nw * max_panel;
+    cudaError_t e = kh_smem_optin((const void*)bwd_small_tma_kernel<nw>, smem);
+    if (e != cudaSuccess) return e;
+    bwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(T, level_fronts, nlev,
+                                                                                         panels, y, max_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   bwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y);
   kh_note_launch();
   return cudaGetLastError();
