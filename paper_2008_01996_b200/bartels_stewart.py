@@ -66,6 +66,8 @@ def solve_bs_complex(system, pencil=None, leaf_size=sparse_direct.DEFAULT_LEAF_S
     sym = sparse_direct.analyze((M + A).tocsr(), leaf_size)
     mv, av = sym.align_values(M), sym.align_values(A)
     free, _ = torch.cuda.mem_get_info(dev)
+    # blocks torch has cached but not handed out are free for the plan too
+    free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
     batch = nt
     while batch > 1 and sparse_direct.plan_bytes(sym, batch, nt) > 0.7 * free:
         batch = (batch + 1) // 2

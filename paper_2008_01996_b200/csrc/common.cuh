@@ -8,6 +8,16 @@
 #define KH_DEV __device__ __forceinline__
 #define KH_HD __host__ __device__
 
+// Device-side bounds checks of a checked build (-DKH_CHECKED, e.g.
+// profiles/probes/checked_build.py): index and size invariants of the
+// shared-memory staging and scatter paths; compiled out otherwise.
+#ifdef KH_CHECKED
+#include <cassert>
+#define KH_ASSERT(cond) assert(cond)
+#else
+#define KH_ASSERT(cond) ((void)0)
+#endif
+
 // ---- complex fp64 -----------------------------------------------------------
 KH_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 KH_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }

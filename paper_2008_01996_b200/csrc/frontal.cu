@@ -114,10 +114,16 @@ struct CpStage {
 // on a 64 x (16 NWJ) tile computed by 2 x NWJ warps (64 NWJ threads).
 //  MODE_SCALED: B(j, k) = B[j + k*ldb], s_k = d_k = D[k*ldd] (the pivots on the
 //               panel diagonal): Schur complements and left-looking updates.
-// Two-stage cp.async ring: the next chunk streams in while DMMA consumes the
-// current one; out-of-range operands are zero-filled by the copy itself. The
+// cp.async ring of CP_STAGES chunks: the next ones stream in while DMMA
+// consumes the current one; out-of-range operands are zero-filled by the copy itself. The
 // pivot scaling is applied to the B fragments in registers.
 constexpr int MODE_SCALED = 0;
+// cp.async ring depth of the tile engine (chunks in flight ahead of the one
+// being consumed: KH_CP_STAGES - 1)
+#ifndef KH_CP_STAGES
+#define KH_CP_STAGES 2
+#endif
+constexpr int CP_STAGES = KH_CP_STAGES;
 
 template <int NWJ, int MODE>
 KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t lda, int rowsA,
@@ -164,14 +170,17 @@ KH_DEV void tile_mma_cp(Acc& acc, int K, const double2* __restrict__ A, int64_t 
       cp_async16(&S.d[tid], kk < K ? D + (int64_t)kk * ldd : D, kk < K);
     }
   };
-  if (nch > 0) load(0, 0);
-  cp_async_commit();
-  for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) load((c + 1) & 1, c + 1);
+#pragma unroll
+  for (int s0 = 0; s0 < CP_STAGES - 1; ++s0) {
+    if (s0 < nch) load(s0, s0);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int c = 0; c < nch; ++c) {
+    if (c + CP_STAGES - 1 < nch) load((c + CP_STAGES - 1) % CP_STAGES, c + CP_STAGES - 1);
+    cp_async_commit();
+    cp_async_wait<CP_STAGES - 1>();
     __syncthreads();
-    const CpStage& S = st[c & 1];
+    const CpStage& S = st[c % CP_STAGES];
 #pragma unroll
     for (int kk = 0; kk < (idle ? 0 : KC); kk += 4) {
       double2 af[4], bf[2];
@@ -408,6 +417,7 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
   for (int64_t e = olo + tid; e < ohi; e += NT) {
     const int d = T.orig_dst[e];
     const double av = T.oa[e];
+    KH_ASSERT(d >= 0 && d < m * p);
     P[d] = cadd(P[d], make_double2(fma(L.x, av, T.om[e]), L.y * av));
   }
 }
@@ -910,6 +920,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   // order, so the sums are deterministic)
   if (tid < RK && tid < nkids) kinfo[tid] = T.kids[F.child_begin + tid];
   const int ne = packed_elems(m);
+  KH_ASSERT(m <= MS && ne <= packed_elems(MS));
   for (int idx = tid; idx < ne; idx += NTH) S[idx] = make_double2(0.0, 0.0);
   for (int c = tid; c < m; c += NTH) cb[c] = kh_packed_col_base(m, c);
   // FWD: the pivot rows' rhs, loaded now and stored to xs after the assembly
@@ -941,6 +952,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
     for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += NTH) {
       const int d = T.orig_dst[e];
       const double av = T.oa[e];
+      KH_ASSERT(d >= 0 && d < ne);
       S[d] = cadd(S[d], make_double2(fma(Lm.x, av, T.om[e]), Lm.y * av));
     }
   }
@@ -1003,7 +1015,10 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
       for (int h = 0; h < CW; ++h)
 #pragma unroll
         for (int u = 0; u < R; ++u)
-          if (dst[h][u] >= 0) S[dst[h][u]] = cadd(S[dst[h][u]], v[h][u]);
+          if (dst[h][u] >= 0) {
+            KH_ASSERT(dst[h][u] < ne);
+            S[dst[h][u]] = cadd(S[dst[h][u]], v[h][u]);
+          }
     }
     if (FWD) {  // the child's rhs update (rows distinct within a child)
 #pragma unroll
@@ -1538,6 +1553,7 @@ __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const 
     mbar_fence_init();
   }
   __syncwarp();
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 64);
   if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
   __syncwarp();
   for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
@@ -1608,6 +1624,7 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
     mbar_fence_init();
   }
   __syncwarp();
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 64);
   if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
   __syncwarp();
   for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
@@ -1886,7 +1903,7 @@ cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_
 cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
                                   double2* panels, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  const int smem = (int)(2 * sizeof(CpStage));
+  const int smem = (int)(CP_STAGES * sizeof(CpStage));
   cudaError_t e = kh_smem_optin((const void*)big_lupdate_kernel, smem);
   if (e != cudaSuccess) return e;
   big_lupdate_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
@@ -1914,7 +1931,7 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
                             const double2* panels, double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
                             int64_t upd_stride_child, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  const int smem = (int)(2 * sizeof(CpStage));
+  const int smem = (int)(CP_STAGES * sizeof(CpStage));
   cudaError_t e = kh_smem_optin((const void*)schur_update_kernel, smem);
   if (e != cudaSuccess) return e;
   schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,

@@ -136,14 +136,17 @@ def modal_plan(temporal, pencil):
 def _on_device(fn):
     """Run an FDEngine method with the engine's device current (streams,
     kh_dgemm and the torch allocations then all refer to that device; the
-    caller's current device is restored afterwards)."""
+    caller's current device is restored afterwards), inside an NVTX range
+    "kh.<method>" (engine phases in ncu --nvtx / Nsight timelines)."""
     import functools
+
+    name = "kh." + fn.__name__.lstrip("_")
 
     @functools.wraps(fn)
     def wrapper(self, *args, **kwargs):
         import torch
 
-        with torch.cuda.device(self.device):
+        with torch.cuda.device(self.device), torch.cuda.nvtx.range(name):
             return fn(self, *args, **kwargs)
 
     return wrapper

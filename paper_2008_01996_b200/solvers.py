@@ -345,6 +345,8 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     # while the host computes the pencil); a pageable one after the pencil
     rhs_t = torch.from_numpy(np.ascontiguousarray(np.asarray(system.rhs, dtype=np.float64)))
     F = rhs_t.to(dev, non_blocking=True).view(nt, n) if rhs_t.is_pinned() else None
+    nvtx = torch.cuda.nvtx
+    nvtx.range_push("kh.solve_fd.host")
     with ThreadPoolExecutor(max_workers=1) as pool:
         fut = pool.submit(_analyze)
         # few BLAS threads: dgeev / the SVD of an N_t <= 512 matrix gain
@@ -367,9 +369,12 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     report.min_re_lambda = pencil.min_re_lambda
     report.spectral_source = spectral_source(pencil)
 
+    nvtx.range_pop()
     # spatial setup: numeric plan + factorization of every shift
+    nvtx.range_push("kh.solve_fd.plan")
     eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev, leaf_size=leaf_size,
                    max_batch=max_batch, keep_factors=keep_factors, symbolic=symbolic)
+    nvtx.range_pop()
     phases["plan"] = time.perf_counter() - t0
     report.analyze_calls = sparse_direct.analyze_call_count() - analyze_before
     t_setup = time.perf_counter() - t0 - report.t_decompose
@@ -404,7 +409,8 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     # fp64 residual above refine_tol switches to the compensated residual
     rel, steps = eng.refine(U, F, rel, refine, refine_tol)
     report.residual_mode = eng.residual_mode
-    coeffs = _to_host(U.reshape(-1))
+    with nvtx.range("kh.solve_fd.d2h"):
+        coeffs = _to_host(U.reshape(-1))
     report.t_refine = time.perf_counter() - t0
     report.refine_steps = steps
     report.residual = rel
