@@ -111,6 +111,9 @@ struct kh_plan {
   const int32_t* classes(int32_t d) const { return cls_off.data() + kClsStride * d; }
   std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
   std::vector<int32_t> small_panel_max;  // per level: largest lower panel among the warp-solve fronts
+  // per level: largest lower panel and m among the other fronts when they all
+  // fit the bulk-copy staged solve kernels' shared memory (else 0)
+  std::vector<int32_t> mid_panel_max, mid_m_max;
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   // large-front schedule: per level an assembly list and per 32-wide pivot
   // block the diag / left-looking / TRSM lists (offsets into btasks, int32s)
@@ -407,8 +410,15 @@ namespace {
 
 // Host-side launch schedule derived from the analysis: fronts grouped per
 // level and kernel class, Schur tiles and the large-front block lists.
+// shared-memory budget (complex entries: panel + front vector) of the
+// bulk-copy staged solve kernels for fronts with m > 64 (c3: 4500-8000 give
+// 39.47 ms/step, 13000 -- one 208 KB CTA per SM on depth 6 -- 41.5, off 39.74)
+#ifndef KH_MID_MAX_ENTRIES
+#define KH_MID_MAX_ENTRIES 8000
+#endif
+
 struct Sched {
-  std::vector<int32_t> small_panel_max;
+  std::vector<int32_t> small_panel_max, mid_panel_max, mid_m_max;
   std::vector<KhDevFront> df, lf_df;
   std::vector<KhKid> kids;
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
@@ -480,6 +490,17 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
         mx = std::max<int32_t>(mx, F.p * F.m() - F.p * (F.p - 1) / 2);
     }
     X.small_panel_max.push_back(mx);
+    int32_t pm = 0, mm = 0;
+    for (int32_t f : lev) {
+      const kh::Front& F = S.fronts[f];
+      if (front_class(F.m()) >= kSolveSmallClasses) {
+        pm = std::max<int32_t>(pm, F.p * F.m() - F.p * (F.p - 1) / 2);
+        mm = std::max<int32_t>(mm, F.m());
+      }
+    }
+    const bool fits = pm > 0 && pm + mm <= KH_MID_MAX_ENTRIES;
+    X.mid_panel_max.push_back(fits ? pm : 0);
+    X.mid_m_max.push_back(fits ? mm : 0);
   }
   X.lf_df.resize(X.lf.size());
   for (size_t i = 0; i < X.lf.size(); ++i) {
@@ -652,6 +673,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->cls_off = X.cls_off;
   p->task_off = X.task_off;
   p->small_panel_max = X.small_panel_max;
+  p->mid_panel_max = X.mid_panel_max;
+  p->mid_m_max = X.mid_m_max;
   p->big = X.big;
   p->kbinfo = X.kbinfo;
   Carver measure;
@@ -796,7 +819,7 @@ int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* 
     const int32_t* co = p->classes(d);
     KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->small_panel_max[d], p->side[0]));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
-                                p->y, st));
+                                p->y, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));
   }
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
@@ -926,7 +949,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->small_panel_max[d],
                                 p->side[0]));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
-                                rch, sch, st));
+                                rch, sch, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));
   }
   return solve_bwd_impl(p, slot0, ns, x_re, x_im, ldx, st);

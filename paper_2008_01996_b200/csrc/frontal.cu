@@ -1808,6 +1808,160 @@ __global__ void __launch_bounds__(NT, 2) bwd_top_kernel(KhTree T, const int32_t*
   for (int k = tid; k < p; k += NT) yy[k] = ts[k];
 }
 
+// ---- solves of the fronts with m > 64 on wide levels, panel staged by bulk copies
+// One CTA per (front, shift) whose whole lower panel fits in shared memory
+// (the host picks these kernels per level): warp 0 issues one bulk async copy
+// per panel column at kernel start, the right-hand side / update-row values
+// are gathered meanwhile, and after one mbarrier wait every operand of the
+// sweep is on chip (the level kernels above take a global round trip per
+// 32-pivot block for the block and another for the rows below it).
+// Shared memory: the packed panel (column c = rows c..m-1 at c m - c(c-1)/2,
+// `maxe` entries reserved) followed by the front's vector (m entries).
+#ifndef KH_MID_TMA
+#define KH_MID_TMA 1
+#endif
+constexpr int MID_NW = 4, MID_NT = 32 * MID_NW;
+KH_DEV void mid_stage_panel(const double2* P, int p, int m, double2* Ls, uint64_t* bar) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid < 32) {
+    if (lane == 0) mbar_arrive_expect_tx(bar, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
+    __syncwarp();
+    for (int c = lane; c < p; c += 32)
+      bulk_g2s(Ls + (c * m - (c * (c - 1)) / 2), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), bar);
+  }
+}
+
+__global__ void __launch_bounds__(MID_NT) fwd_mid_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                            const double2* __restrict__ panels, double2* y,
+                                                            double2* ru_cur, int64_t ru_stride_cur,
+                                                            const double2* __restrict__ ru_child,
+                                                            int64_t ru_stride_child, int32_t maxe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  double2* Ls = reinterpret_cast<double2*>(smem_raw);
+  double2* xs = Ls + maxe;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int b = blockIdx.y;
+  const int p = F.p, q = F.q, m = p + q;
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe);
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  mid_stage_panel(P, p, m, Ls, &bar);
+  // the front's rhs: pivot rows of y plus the children's updates (fixed child order)
+  const int nk = F.child_end - F.child_begin;
+  for (int r = tid; r < m; r += MID_NT) {
+    double2 v = r < p ? yy[r] : make_double2(0.0, 0.0);
+    for (int k = 0; k < nk; ++k) {
+      const KhKid C = T.kids[F.child_begin + k];
+      const int ci = T.cmap[C.cmap_begin + r];
+      if (ci >= 0) v = cadd(v, ru_child[(int64_t)b * ru_stride_child + C.rupd_off + ci]);
+    }
+    xs[r] = v;
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  auto L = [&](int r, int c) { return Ls[c * m - (c * (c - 1)) / 2 + r - c]; };  // r >= c
+  for (int kb = 0; kb < p; kb += NB) {
+    const int w = min(NB, p - kb);
+    if (warp == 0) {
+      const int i = lane;
+      double2 xi = i < w ? xs[kb + i] : make_double2(0.0, 0.0);
+#pragma unroll 8
+      for (int k = 0; k < w; ++k) {
+        const double2 l = (i > k && i < w) ? L(kb + i, kb + k) : make_double2(0.0, 0.0);
+        const double2 xk = shfl2(xi, k);
+        xi = cfms(xi, l, xk);
+      }
+      if (i < w) xs[kb + i] = xi;
+    }
+    __syncthreads();
+    for (int r = kb + w + tid; r < m; r += MID_NT) {
+      double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+#pragma unroll 4
+      for (int k = 0; k < w; k += 2) {
+        s0 = cadd(s0, cmul(L(r, kb + k), xs[kb + k]));
+        if (k + 1 < w) s1 = cadd(s1, cmul(L(r, kb + k + 1), xs[kb + k + 1]));
+      }
+      xs[r] = csub(xs[r], cadd(s0, s1));
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < m; r += MID_NT) {
+    if (r < p) yy[r] = xs[r];
+    else ru[r - p] = xs[r];
+  }
+}
+
+__global__ void __launch_bounds__(MID_NT) bwd_mid_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                            const double2* __restrict__ panels, double2* y,
+                                                            int32_t maxe) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  double2* Ls = reinterpret_cast<double2*>(smem_raw);
+  double2* ts = Ls + maxe;  // p entries, then xu: q entries
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int b = blockIdx.y;
+  const int p = F.p, q = F.q, m = p + q;
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe);
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  double2* xu = ts + p;
+  const int64_t* urows = T.urows + F.rows_begin;
+  mid_stage_panel(P, p, m, Ls, &bar);
+  for (int a = tid; a < q; a += MID_NT) xu[a] = yb[urows[a]];
+  for (int k = tid; k < p; k += MID_NT) ts[k] = yy[k];
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  auto L = [&](int r, int c) { return Ls[c * m - (c * (c - 1)) / 2 + r - c]; };  // r >= c
+  // t_k = y_k / d_k - sum_a L21[a, k] xu[a]   (warp per column k)
+  for (int k = warp; k < p; k += MID_NW) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int a = lane; a < q; a += 32) s = cadd(s, cmul(L(p + a, k), xu[a]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    if (lane == 0) ts[k] = csub(cmul(ts[k], cinv(L(k, k))), s);
+  }
+  __syncthreads();
+  const int nblk = (p + NB - 1) / NB;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * NB, w = min(NB, p - kb);
+    if (warp == 0) {  // L_blk^T x = t_blk: lane i owns t_{kb+i}
+      double2 t = lane < w ? ts[kb + lane] : make_double2(0.0, 0.0);
+      for (int i = w - 1; i > 0; --i) {
+        const double2 l = lane < i ? L(kb + i, kb + lane) : make_double2(0.0, 0.0);
+        const double2 xi = shfl2(t, i);
+        t = cfms(t, l, xi);
+      }
+      if (lane < w) ts[kb + lane] = t;
+    }
+    __syncthreads();
+    // earlier pivots k < kb: t_k -= sum_i L[kb+i, k] x_{kb+i}   (warp per column)
+    for (int k = warp; k < kb; k += MID_NW) {
+      double2 s = lane < w ? cmul(L(kb + lane, k), ts[kb + lane]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      if (lane == 0) ts[k] = csub(ts[k], s);
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < p; k += MID_NT) yy[k] = ts[k];
+}
+
 // ---- backward solve: x <- L^{-T} D^{-1} y, fronts top-down -------------------
 __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                        const double2* __restrict__ panels, double2* y) {
@@ -2033,8 +2187,18 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
                                 int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
+  if (KH_MID_TMA && mid_panel > 0 && (int64_t)nlev * batch > kNarrowLevelCtas) {
+    const int smem = 16 * (mid_panel + mid_m);
+    cudaError_t e = kh_smem_optin((const void*)fwd_mid_tma_kernel, smem);
+    if (e != cudaSuccess) return e;
+    fwd_mid_tma_kernel<<<dim3(nlev, batch), MID_NT, smem, stream>>>(T, level_fronts, panels, y, ru_cur,
+                                                                    ru_stride_cur, ru_child, ru_stride_child,
+                                                                    mid_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   if ((int64_t)nlev * batch > kNarrowLevelCtas) {
     fwd_level_kernel<<<dim3(nlev, batch), NT, 0, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
                                                            ru_child, ru_stride_child);
@@ -2052,9 +2216,17 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
 
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtasBwd;
+  if (KH_MID_TMA && mid_panel > 0 && !narrow) {
+    const int smem = 16 * (mid_panel + mid_m);
+    cudaError_t e = kh_smem_optin((const void*)bwd_mid_tma_kernel, smem);
+    if (e != cudaSuccess) return e;
+    bwd_mid_tma_kernel<<<dim3(nlev, batch), MID_NT, smem, stream>>>(T, level_fronts, panels, y, mid_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(double2) * (size_t)max_m;
   cudaError_t e = kh_smem_optin(narrow ? (const void*)bwd_top_kernel : (const void*)bwd_level_kernel, (int)smem);
   if (e != cudaSuccess) return e;

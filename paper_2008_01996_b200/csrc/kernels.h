@@ -73,10 +73,13 @@ cudaError_t kh_launch_dgemm_rowscatter(int64_t M, int64_t N, int64_t K, const do
                                        cudaStream_t stream);
 cudaError_t kh_launch_sum_parts(int32_t g, const double* parts, int64_t len, double* out, cudaStream_t stream);
 
+// mid_panel > 0: every front of the launch has a lower panel of at most
+// mid_panel entries and m <= mid_m, small enough for the bulk-copy staged
+// kernels on a wide level (0: the level kernels).
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
                                 int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
-                                cudaStream_t stream);
+                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0);
 // Level-synchronous kernels for the large fronts (see frontal.cu). Tasks are
 // (front, index) int32 pairs; schur tasks are (front, tile row, tile col).
 #ifndef KH_ASM_CHUNK_DEF
@@ -110,7 +113,7 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
                                 const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream);
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
-                                cudaStream_t stream);
+                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0);
 cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
                                  const double* g_im, int64_t ldg, double2* y, cudaStream_t stream);
 cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm, const double2* y,
