@@ -56,6 +56,10 @@ def parse():
                     help="(tests) each rank prints its rank and world size and exits before touching a GPU")
     ap.add_argument("--ref-budget", type=float, default=240.0,
                     help="reference arm: seconds of full solves after the first (steps are capped to fit)")
+    ap.add_argument("--ref-processes", action="store_true",
+                    help="reference arm: time the shift solves over a process pool instead of threads")
+    ap.add_argument("--ref-quick", action="store_true",
+                    help="reference arm: skip the process-pool and sampled cross-checks")
     return ap.parse_args()
 
 
@@ -217,15 +221,16 @@ def cpu_fd_sample(system, n_shift_sample, threads=1):
             "t_analyze": t_an, "sample_shifts": int(len(ks)), "n_t": n_t}
 
 
-def cpu_fd_full(system, workers):
+def cpu_fd_full(system, workers, mode):
     """One unsampled reference FD solve: the oracle port of solve_fd
     (solvers.py:348-403; oracle.fd_oracle.solve_fd_parallel) with all N_t
-    SuperLU factor + solves over `workers` processes (the pool is created
-    inside the timed region)."""
+    SuperLU factor + solves over `workers` threads (mode "threads": the
+    reference's own thread pool) or processes (the pool is created inside
+    the timed region)."""
     from oracle import fd_oracle as orc
 
     tm = {}
-    u, _ = orc.solve_fd_parallel(*orc.system_arrays(system), workers, timings=tm)
+    u, _ = orc.solve_fd_parallel(*orc.system_arrays(system), workers, timings=tm, mode=mode)
     return dict(tm, u=u, workers=workers, n_t=system.n_t)
 
 
@@ -401,6 +406,15 @@ def main():
                                         "work": "R = F - (M_x Y1 + A_x Y2): Y (2 N_t), F, R columns + CSR once"}
         if ms_of("factor_solve") > 0:
             kernels["factor_plus_solve_ms_per_step"] = ms_of("factor_solve")
+        if ms_of("gemm_dd") > 0:
+            # compensated U M_t^T: one TwoProd + TwoSum (~9 fp64 ops) per multiply-add
+            madd = calls.get("gemm_dd", 0) * float(n) * nt * nt
+            kernels["compensated_residual"] = {
+                "ms_per_step": ms_of("gemm_dd") + ms_of("residual_dd"), "calls_per_step": calls.get("gemm_dd", 0),
+                "gemm_dd_ms": ms_of("gemm_dd"),
+                "gemm_dd_gmadd_per_s": madd / (ms_of("gemm_dd") / 1e3) / 1e9,
+                "work": "kh_dgemm_dd (U M_t^T as hi + lo, Dot2) + kh_plan_residual_dd; used once the fp64 "
+                        "residual nears its rounding floor"}
 
     # the e2e runs build their own plans: release this one's device memory
     # first (at c4 its retained factors take 136 GB of the 180)
@@ -434,6 +448,8 @@ def main():
                                       "alltoall": "NCCL all-to-all of Z by rows + local GEMM"}[coll]
                                      if sharded else None)},
             "residual": infos[-1]["residual"], "refine_steps": infos[-1]["refine_steps"],
+            "residual_mode": infos[-1].get("residual_mode", "fp64"),
+            "residual_history": infos[-1]["residuals"],
             "fd_residual": infos[-1]["residuals"][0],
             "gpu_launches": int(launches),
             "clocks": ck,
@@ -588,11 +604,12 @@ def measure_e2e_sharded(system, pencil, args, leaf):
 
 
 def cpu_baseline_subprocess(args):
-    """cpu_baseline of our arm: one unsampled reference solve, timed in a fresh
-    process (no CUDA context in the forking process) by the reference arm's
-    own code (`--impl reference --steps 1 --warmup 0`)."""
+    """cpu_baseline of our arm: one unsampled reference solve with its shifts
+    over a process pool (~10 s at c3 on 16 cores), timed in a fresh process
+    (no CUDA context in the forking process) by the reference arm's own code
+    (`--impl reference --steps 1 --warmup 0 --ref-processes`)."""
     cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--steps", "1", "--warmup", "0",
-           "--config", args.config]
+           "--config", args.config, "--ref-processes", "--ref-quick"]
     if args.j_max is not None:
         cmd += ["--j-max", str(args.j_max)]
     try:
@@ -605,11 +622,15 @@ def cpu_baseline_subprocess(args):
 
 def run_reference(args, world, rank):
     """The reference's CPU algorithm on this host: the oracle port of
-    solve_fd (same LAPACK / SuperLU calls as the reference) with the N_t shift
-    solves over all host cores. Every timed step is one full, unsampled solve;
+    solve_fd (same LAPACK / SuperLU calls as the reference). Every timed step
+    is one full, unsampled solve with the reference's own parallelism, a
+    thread pool of all host cores over the shifts (solvers.py:387-390);
     steps after the first stop once --ref-budget seconds are spent (the line
-    reports the steps actually timed). A 12-shift extrapolation is reported
-    beside it as a cross-check."""
+    reports the steps actually timed). Reported beside it: the same solve
+    with the shifts over a process pool (what the host cores give the
+    algorithm without the GIL) and a 12-shift single-thread extrapolation
+    (cross-check). --ref-processes makes the process pool the timed steps
+    (our arm's cpu_baseline)."""
     if rank != 0:
         return
     from paper_2008_01996_b200 import problems
@@ -617,13 +638,14 @@ def run_reference(args, world, rank):
     kw = {} if args.j_max is None else {"j_max": args.j_max}
     system, info = problems.build_system(args.config, **kw)
     workers = os.cpu_count() or 1
+    mode = "processes" if args.ref_processes else "threads"
     for _ in range(args.warmup):
         cpu_fd_sample(system, 2, 1)
     totals, spent = [], 0.0
     for i in range(max(1, args.steps)):
         if i > 0 and spent + totals[-1] > args.ref_budget:
             break
-        r = cpu_fd_full(system, workers)
+        r = cpu_fd_full(system, workers, mode)
         totals.append(r["t_total"])
         spent += r["t_total"]
     from oracle import fd_oracle as orc
@@ -631,7 +653,7 @@ def run_reference(args, world, rank):
     res = orc.residual(*orc.system_arrays(system), r["u"])
     t = float(np.mean(totals))
     value = system.dof / t
-    cross = cpu_fd_sample(system, shift_sample_size(args.config), 1)
+    what = "processes" if mode == "processes" else "threads (the reference's ThreadPoolExecutor)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(totals),
             "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -639,15 +661,21 @@ def run_reference(args, world, rank):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                              "cpu_model": cpu_model(),
                              "sample": (f"full solve: oracle port of the reference solve_fd, all {system.n_t} "
-                                        f"SuperLU shift factor+solves over {workers} processes, pencil, "
+                                        f"SuperLU shift factor+solves over {workers} {what}, pencil, "
                                         f"transforms and MMD analysis included; {len(totals)} solve(s), "
                                         f"t_total={t:.2f}s")},
             "residual": res,
             "phases_s": {k: r[k] for k in ("t_pencil", "t_transform", "t_analyze", "t_spatial")},
-            "extrapolated_sample": {"value": system.dof / cross["t_total"], "cores": 1,
-                                    "sample": f"{cross['sample_shifts']} of {cross['n_t']} shifts, 1 thread, "
-                                              "extrapolated linearly (cross-check only)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if mode == "threads" and not args.ref_quick:
+        rp = cpu_fd_full(system, workers, "processes")
+        line["process_pool"] = {"value": system.dof / rp["t_total"], "cores": workers,
+                                "sample": f"the same full solve, shifts over {workers} processes (no GIL), "
+                                          f"t_total={rp['t_total']:.2f}s"}
+        cross = cpu_fd_sample(system, shift_sample_size(args.config), 1)
+        line["extrapolated_sample"] = {"value": system.dof / cross["t_total"], "cores": 1,
+                                       "sample": f"{cross['sample_shifts']} of {cross['n_t']} shifts, 1 thread, "
+                                                 "extrapolated linearly (cross-check only)"}
     print(json.dumps(line), flush=True)
 
 

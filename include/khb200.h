@@ -157,6 +157,12 @@ int kh_plan_level_times(kh_plan* plan, float* ms, int32_t n_levels);
  * R may be NULL. norms2 (device, 2 doubles) receives ||R||_F^2, ||F||_F^2. */
 int kh_plan_residual(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
                      double* R, int64_t ldr, double* norms2, void* stream);
+/* norms2 (device, 2 doubles) = (|| |F| + |M_x| |Y1| + |A_x| |Y2| ||^2, ||F||^2): the
+ * magnitude of the terms the residual cancels, whose eps multiple is the
+ * rounding floor of evaluating kh_plan_residual in fp64 (decides when
+ * refinement needs the compensated residual). Same Y / F layout. */
+int kh_plan_residual_scale(kh_plan* plan, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
+                           double* norms2, void* stream);
 /* Compensated variant of kh_plan_residual (refinement at fine meshes, where the
  * fp64 evaluation of f - K u floors the residual): Y2 = U M_t^T given as the
  * unevaluated sum Y2hi + Y2lo (kh_dgemm_dd), Y1 = U A_t^T in fp64 (ld ldy1);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "kh_plan_set_level_timing": (ctypes.c_int, [_vp, _i32]),
     "kh_plan_level_times": (ctypes.c_int, [_vp, _vp, _i32]),
     "kh_plan_residual": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "kh_plan_residual_scale": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "kh_plan_residual_dd": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "kh_dgemm_dd": (ctypes.c_int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp]),
     "kh_csr_pair_residual_dd": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64,

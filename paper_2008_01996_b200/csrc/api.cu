@@ -955,6 +955,19 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   return solve_bwd_impl(p, slot0, ns, x_re, x_im, ldx, st);
 }
 
+int kh_plan_residual_scale(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
+                           double* norms2, void* stream) {
+  if (!p || !Y || !F || !norms2) return fail(KH_ERR_INVALID, "null argument");
+  if (ldy < p->n || ldf < p->n) return fail(KH_ERR_DIMENSION, "leading dimension smaller than n");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceGuard dev_guard(p->device);
+  KH_CUDA(dev_guard.err);
+  KH_CUDA(kh_launch_residual_scale(p->n, nt, p->indptr, p->indices, p->mv, p->av, Y, ldy, F, ldf, p->resid_part,
+                                   kResidualBlocks, st));
+  KH_CUDA(kh_launch_rowreduce(p->resid_part, kResidualBlocks, 2, 0, norms2, st));
+  return KH_OK;
+}
+
 int kh_plan_residual_dd(kh_plan* p, int64_t nt, const double* Y1, int64_t ldy1, const double* Y2hi,
                         const double* Y2lo, int64_t ldy2, const double* F, int64_t ldf, double* R, int64_t ldr,
                         double* norms2, void* stream) {

@@ -126,6 +126,11 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     const double* mv, const double* av, const double* Y, int64_t ldy,
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
                                     int32_t nblk, cudaStream_t stream);
+// ||(|f| + |M_x| |Y1| + |A_x| |Y2|)||^2 and ||f||^2 (the scale of the terms the
+// fp64 residual cancels: its evaluation floor is ~eps times that norm).
+cudaError_t kh_launch_residual_scale(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                     const double* mv, const double* av, const double* Y, int64_t ldy,
+                                     const double* F, int64_t ldf, double* part, int32_t nblk, cudaStream_t stream);
 // Compensated (double-double) residual pieces (residual.cu).
 cudaError_t kh_launch_dgemm_dd(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                                int64_t ldb, double* Chi, double* Clo, int64_t ldc, cudaStream_t stream);

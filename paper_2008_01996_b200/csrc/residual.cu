@@ -22,6 +22,10 @@ namespace {
 #define KH_RES_TCH 16
 #endif
 constexpr int RES_TCH = KH_RES_TCH, RES_ROWNZ = 8;
+// ABS: instead of R, the magnitude |f| + sum |m y1| + sum |a y2| of the terms
+// whose cancellation the fp64 residual evaluates (its rounding floor is
+// ~eps times the norm of that); R is not written.
+template <bool ABS = false>
 __global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t nt, const int64_t* __restrict__ indptr,
                                                             const int64_t* __restrict__ indices,
                                                             const double* __restrict__ mv,
@@ -54,17 +58,27 @@ __global__ void __launch_bounds__(256) pair_residual_kernel(int64_t n, int64_t n
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < RES_ROWNZ; ++k) {
-        s = fma(mm[k], y1[col[k]], s);
-        s = fma(aa[k], y2[col[k]], s);
+        if (ABS) {
+          s = fma(fabs(mm[k]), fabs(y1[col[k]]), s);
+          s = fma(fabs(aa[k]), fabs(y2[col[k]]), s);
+        } else {
+          s = fma(mm[k], y1[col[k]], s);
+          s = fma(aa[k], y2[col[k]], s);
+        }
       }
       for (int64_t e = e0 + RES_ROWNZ; e < e1; ++e) {  // rows longer than RES_ROWNZ
         const int64_t j = indices[e];
-        s = fma(mv[e], y1[j], s);
-        s = fma(av[e], y2[j], s);
+        if (ABS) {
+          s = fma(fabs(mv[e]), fabs(y1[j]), s);
+          s = fma(fabs(av[e]), fabs(y2[j]), s);
+        } else {
+          s = fma(mv[e], y1[j], s);
+          s = fma(av[e], y2[j], s);
+        }
       }
       const double f = F[i + t * ldf];
-      const double r = f - s;
-      if (R) R[i + t * ldr] = r;
+      const double r = ABS ? fabs(f) + s : f - s;
+      if (!ABS && R) R[i + t * ldr] = r;
       rr = fma(r, r, rr);
       ff = fma(f, f, ff);
     }
@@ -277,7 +291,16 @@ cudaError_t kh_launch_pair_residual(int64_t n, int64_t nt, const int64_t* indptr
                                     const double* mv, const double* av, const double* Y, int64_t ldy,
                                     const double* F, int64_t ldf, double* R, int64_t ldr, double* part,
                                     int32_t nblk, cudaStream_t stream) {
-  pair_residual_kernel<<<nblk, 256, 0, stream>>>(n, nt, indptr, indices, mv, av, Y, ldy, F, ldf, R, ldr, part);
+  pair_residual_kernel<false><<<nblk, 256, 0, stream>>>(n, nt, indptr, indices, mv, av, Y, ldy, F, ldf, R, ldr, part);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_residual_scale(int64_t n, int64_t nt, const int64_t* indptr, const int64_t* indices,
+                                     const double* mv, const double* av, const double* Y, int64_t ldy,
+                                     const double* F, int64_t ldf, double* part, int32_t nblk, cudaStream_t stream) {
+  pair_residual_kernel<true><<<nblk, 256, 0, stream>>>(n, nt, indptr, indices, mv, av, Y, ldy, F, ldf, nullptr, 0,
+                                                       part);
   kh_note_launch();
   return cudaGetLastError();
 }

@@ -52,6 +52,10 @@ class ModalPlan:
 # evaluating f - K u); a step that does not lower it at all is undone
 # (FDEngine.refine_step), so the best iterate is returned
 REFINE_MIN_GAIN = 0.5
+# refinement on the compensated residual (fp64 evaluation floor above the
+# tolerance: fine meshes, config c4) stops at this relative residual, one
+# decade under the 1e-11 bar of BASELINE.json
+DD_TOL = 1e-12
 
 
 def conjugate_pairs(D, X):
@@ -494,31 +498,53 @@ class FDEngine:
         info["residual_mode"] = self.residual_mode
         return U, info
 
+    @_on_device
+    def eval_floor(self):
+        """Relative rounding floor of the fp64 residual of the U whose K U the
+        last residual() left in Y: eps || |f| + |M_x| |Y1| + |A_x| |Y2| || / ||f||,
+        times a small safety factor."""
+        self.plan.residual_scale(self.n_t, self.Y.data_ptr(), self.n, self._F.data_ptr(), self.n,
+                                 self.norms[2:].data_ptr(), self._stream())
+        self.gpu_launches += 2
+        s2, f2 = self.norms[2:4].tolist()
+        return 4.0 * 2.0 ** -52 * float(np.sqrt(s2) / np.sqrt(f2)) if f2 > 0 else 0.0
+
     def refine(self, U, F, rel, max_steps, tol, history=None):
         """Iterative refinement u += FD(f - K u) from the residual held in R
-        (relative value `rel`) until `tol`, `max_steps`, or stagnation. If the
-        fp64 residual stagnates above `tol` (its evaluation floor: fine
-        meshes), the residual is re-evaluated in compensated arithmetic and
-        refinement continues on it (self.compensated: "auto", True, False).
-        Returns (relative residual of U, steps taken)."""
+        (relative value `rel`, evaluated for this U: K U is still in Y) until
+        `tol`, `max_steps`, or stagnation. Compensated residual
+        (self.compensated): True -- always; False -- never; "auto" -- once the
+        fp64 residual is within 100x of its own rounding floor (eval_floor)
+        while still above `tol`, or stagnates above `tol`; refinement on the
+        compensated residual stops at max(tol, DD_TOL). Returns (relative
+        residual of U, steps taken)."""
         steps, dd = 0, self.compensated is True
         self.residual_mode = "fp64"
+        floor = 0.0
+        if self.compensated == "auto" and rel > tol:
+            self._F = F
+            floor = self.eval_floor()
+        if not dd and floor > 0.0 and tol < rel < 100.0 * floor:
+            dd = True
         if dd and rel > tol:
             rel = self._rel(self.residual(U, F, dd=True))
             self.residual_mode = "dd"
-        while rel > tol and steps < max_steps:
+        while rel > (max(tol, DD_TOL) if dd else tol) and steps < max_steps:
             new, rel, go = self.refine_step(U, F, rel, dd=dd)
             steps += 1
             if history is not None:
                 history.append(new)
-            if not go:  # stagnation at the evaluation floor (a worse step was undone)
-                if dd or self.compensated is False or rel <= tol:
-                    break
+            switch = not dd and self.compensated == "auto" and (not go or rel < 100.0 * floor)
+            if not go and not switch:  # stagnation at the evaluation floor (a worse step was undone)
+                break
+            if switch and rel > tol:
                 dd = True
                 self.residual_mode = "dd"
                 rel = self._rel(self.residual(U, F, dd=True))
                 if history is not None:
                     history.append(rel)
+            elif not go:
+                break
         return rel, steps
 
     @staticmethod

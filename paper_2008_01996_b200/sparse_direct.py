@@ -210,6 +210,9 @@ class _Plan:
         _native.call("kh_plan_residual", self.raw, int(nt), Y, int(ldy), F, int(ldf), R, int(ldr), norms2,
                      stream)
 
+    def residual_scale(self, nt, Y, ldy, F, ldf, norms2, stream):
+        _native.call("kh_plan_residual_scale", self.raw, int(nt), Y, int(ldy), F, int(ldf), norms2, stream)
+
     def residual_dd(self, nt, Y1, ldy1, Y2hi, Y2lo, ldy2, F, ldf, R, ldr, norms2, stream):
         _native.call("kh_plan_residual_dd", self.raw, int(nt), Y1, int(ldy1), Y2hi, Y2lo, int(ldy2), F, int(ldf),
                      R, int(ldr), norms2, stream)
