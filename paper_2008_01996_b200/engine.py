@@ -56,6 +56,9 @@ REFINE_MIN_GAIN = 0.5
 # tolerance: fine meshes, config c4) stops at this relative residual, one
 # decade under the 1e-11 bar of BASELINE.json
 DD_TOL = 1e-12
+# ... entered once the fp64 residual is within this factor of its estimated
+# rounding floor (c4: after two steps; c3, c5: never)
+FLOOR_MARGIN = 10.0
 
 
 def conjugate_pairs(D, X):
@@ -514,18 +517,14 @@ class FDEngine:
         (relative value `rel`, evaluated for this U: K U is still in Y) until
         `tol`, `max_steps`, or stagnation. Compensated residual
         (self.compensated): True -- always; False -- never; "auto" -- once the
-        fp64 residual is within 100x of its own rounding floor (eval_floor)
-        while still above `tol`, or stagnates above `tol`; refinement on the
-        compensated residual stops at max(tol, DD_TOL). Returns (relative
-        residual of U, steps taken)."""
+        fp64 residual is within FLOOR_MARGIN of its own rounding floor
+        (eval_floor, estimated after the first step) while still above `tol`,
+        or stagnates above `tol`; refinement on the compensated residual stops
+        at max(tol, DD_TOL). Returns (relative residual of U, steps taken)."""
         steps, dd = 0, self.compensated is True
         self.residual_mode = "fp64"
-        floor = 0.0
-        if self.compensated == "auto" and rel > tol:
-            self._F = F
-            floor = self.eval_floor()
-        if not dd and floor > 0.0 and tol < rel < 100.0 * floor:
-            dd = True
+        floor = None  # estimated after the first step, if refinement goes on
+        self._F = F
         if dd and rel > tol:
             rel = self._rel(self.residual(U, F, dd=True))
             self.residual_mode = "dd"
@@ -534,7 +533,9 @@ class FDEngine:
             steps += 1
             if history is not None:
                 history.append(new)
-            switch = not dd and self.compensated == "auto" and (not go or rel < 100.0 * floor)
+            if floor is None and not dd and self.compensated == "auto" and go and rel > tol:
+                floor = self.eval_floor()  # Y holds K U of the new iterate
+            switch = not dd and self.compensated == "auto" and (not go or rel < FLOOR_MARGIN * (floor or 0.0))
             if not go and not switch:  # stagnation at the evaluation floor (a worse step was undone)
                 break
             if switch and rel > tol:
