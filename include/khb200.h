@@ -151,6 +151,10 @@ int kh_plan_solve_bwd(kh_plan* plan, int64_t slot0, int64_t nshift, double* x_re
  * every level boundary on the caller's stream; kh_plan_level_times waits for
  * the last one and returns the milliseconds of each level of the most recent
  * factorization, indexed by tree depth (0 = root), n_levels = depth + 1. */
+/* Device address of the retained factor storage (slot-major, panel_total
+ * complex entries per slot; front panels column-major m x p in front order)
+ * for diagnostics and tests. */
+int kh_plan_factor_storage(const kh_plan* plan, void** panels, int64_t* panel_total);
 int kh_plan_set_level_timing(kh_plan* plan, int32_t on);
 int kh_plan_level_times(kh_plan* plan, float* ms, int32_t n_levels);
 /* R = F - (M Y[:, :nt] + A Y[:, nt:2nt]) on the plan's CSR (device arrays);

@@ -77,6 +77,7 @@ SIGNATURES = {
     "kh_plan_factor_solve": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp]),
     "kh_plan_factor_fwd": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
     "kh_plan_solve_bwd": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp]),
+    "kh_plan_factor_storage": (ctypes.c_int, [_vp, _P(_vp), _P(_i64)]),
     "kh_plan_set_level_timing": (ctypes.c_int, [_vp, _i32]),
     "kh_plan_level_times": (ctypes.c_int, [_vp, _vp, _i32]),
     "kh_plan_residual": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libkhb200.so")
-SOURCES = ["api.cu", "dgemm.cu", "frontal.cu", "residual.cu", "temporal.cu", "symbolic.cpp"]
+SOURCES = ["api.cu", "dgemm.cu", "frontal.cu", "warpfront.cu", "residual.cu", "temporal.cu", "symbolic.cpp"]
 HEADERS = ["common.cuh", "kernels.h", "symbolic.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -80,6 +80,9 @@ constexpr int kSmallClasses = 5;
 #define KH_CLASS4 96
 #endif
 constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, KH_CLASS4, 128};
+#ifndef KH_WARP_CLASSES
+#define KH_WARP_CLASSES 1
+#endif
 // the warp-per-front solve kernels take the classes with m <= 64
 #ifndef KH_SOLVE_SMALL_CLASSES
 #define KH_SOLVE_SMALL_CLASSES 3
@@ -144,6 +147,9 @@ struct kh_plan {
   KhDevFront* lf_fronts = nullptr;
   KhKid* kids = nullptr;
   int32_t *child_list = nullptr, *relind = nullptr, *cmap = nullptr, *orig_dst = nullptr, *level_fronts = nullptr;
+  int32_t* wdst = nullptr;  // originals' slots in the warp-front kernels' dense image
+  // per small class: register-resident warp kernel tile count (0: shared-memory kernel)
+  int warp_mt[kSmallClasses] = {};
   int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
   double *mv = nullptr, *av = nullptr;
   double *om = nullptr, *oa = nullptr;  // values in front-original order (gathered on the device)
@@ -422,6 +428,8 @@ struct Sched {
   std::vector<KhDevFront> df, lf_df;
   std::vector<KhKid> kids;
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
+  std::vector<int32_t> wdst;      // warp-front image slots (-1 outside the warp classes)
+  int warp_mt[kSmallClasses] = {};
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
   std::vector<kh_plan::KbInfo> kbinfo;
@@ -469,6 +477,22 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     for (int64_t e = F.orig_begin; e < F.orig_end; ++e) {
       const int32_t d = X.orig_dst[e], c = d / m, r = d - c * m;
       X.orig_dst[e] = kh_packed_col_base(m, c) + r;
+    }
+  }
+  // register-resident warp kernels for the classes m <= 32 and m <= 48
+  // (KH_WARP_CLASSES: bit c enables class c; default: m <= 32 only)
+  int warp_mask = KH_WARP_CLASSES;
+  if (const char* env = std::getenv("KH_WARP_CLASSES")) warp_mask = std::atoi(env);
+  for (int c = 0; c < kSmallClasses; ++c)
+    X.warp_mt[c] = ((warp_mask >> c) & 1) && kClassMax[c] <= 48 ? kClassMax[c] / 8 : 0;
+  X.wdst.assign(S.orig_dst.size(), -1);
+  for (int32_t f = 0; f < nf; ++f) {
+    const kh::Front& F = S.fronts[f];
+    const int32_t m = F.m(), c = front_class(m);
+    if (c >= kSmallClasses || !X.warp_mt[c]) continue;
+    for (int64_t e = F.orig_begin; e < F.orig_end; ++e) {
+      const int32_t d = S.orig_dst[e], cc = d / m, r = d - cc * m;
+      X.wdst[e] = kh_warp_front_slot(m, F.p, r, cc);
     }
   }
   X.level_off.push_back(0);
@@ -594,6 +618,7 @@ void carve(kh_plan* p, const kh::Symbolic& S, const Sched& X, Carver& C) {
   C.take(&p->urows, S.urows.size());
   C.take(&p->orig_src, S.orig_src.size());
   C.take(&p->orig_dst, S.orig_dst.size());
+  C.take(&p->wdst, X.wdst.size());
   C.take(&p->level_fronts, X.lf.size());
   C.take(&p->lf_fronts, X.lf_df.size());
   C.take(&p->kids, X.kids.size());
@@ -675,6 +700,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->small_panel_max = X.small_panel_max;
   p->mid_panel_max = X.mid_panel_max;
   p->mid_m_max = X.mid_m_max;
+  for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
   p->big = X.big;
   p->kbinfo = X.kbinfo;
   Carver measure;
@@ -709,6 +735,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     up(p->urows, S.urows.data(), S.urows.size() * 8);
     up(p->orig_src, S.orig_src.data(), S.orig_src.size() * 8);
     up(p->orig_dst, X.orig_dst.data(), X.orig_dst.size() * 4);
+    up(p->wdst, X.wdst.data(), X.wdst.size() * 4);
     up(p->level_fronts, X.lf.data(), X.lf.size() * 4);
     up(p->lf_fronts, X.lf_df.data(), X.lf_df.size() * sizeof(KhDevFront));
     up(p->kids, X.kids.data(), X.kids.size() * sizeof(KhKid));
@@ -770,9 +797,14 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
     const int64_t sc = p->upd_size[d & 1], sch = p->upd_size[(d + 1) & 1];
     const int32_t ns = (int32_t)nshift;
     const KhFwd fw{p->y, p->rupd[d & 1], p->rupd_size[d & 1], p->rupd[(d + 1) & 1], p->rupd_size[(d + 1) & 1]};
-    for (int c = 0; c < kSmallClasses; ++c)
-      KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                     uch, sch, p->minpiv_work, p->side[c], fwd ? &fw : nullptr));
+    for (int c = 0; c < kSmallClasses; ++c) {
+      if (p->warp_mt[c] && !fwd)
+        KH_CUDA(kh_launch_warp_front(p->warp_mt[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
+                                     uch, sch, p->minpiv_work, p->wdst, p->side[c]));
+      else
+        KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
+                                       uch, sch, p->minpiv_work, p->side[c], fwd ? &fw : nullptr));
+    }
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
@@ -868,6 +900,13 @@ int kh_plan_factor_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double
   const int rc = kh_plan_factor_fwd(p, slot0, nshift, lambda_ri, b_re, b_im, ldb, stream);
   if (rc != KH_OK) return rc;
   return kh_plan_solve_bwd(p, slot0, nshift, x_re, x_im, ldx, stream);
+}
+
+int kh_plan_factor_storage(const kh_plan* p, void** panels, int64_t* panel_total) {
+  if (!p || !panels || !panel_total) return fail(KH_ERR_INVALID, "null argument");
+  *panels = p->panels;
+  *panel_total = p->panel_total;
+  return KH_OK;
 }
 
 int kh_plan_set_level_timing(kh_plan* p, int32_t on) {

@@ -1285,7 +1285,7 @@ __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t*
                                                           const double2* __restrict__ ru_child,
                                                           int64_t ru_stride_child) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* xs = reinterpret_cast<double2*>(smem_raw);  // m entries
+  double2* xs = reinterpret_cast<double2*>(smem_raw);  // m + FWD_W entries
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t f = level_fronts[blockIdx.x];
   const int b = blockIdx.y;
@@ -1305,6 +1305,9 @@ __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t*
     kcm[tid] = T.cmap + C.cmap_begin;
   }
   __syncthreads();
+  // xs[m, m + FWD_W) is zeroed: the GEMV below multiplies the L columns past the
+  // block width (zeros) with xs entries up to kb + FWD_W, which must be finite
+  for (int r = m + tid; r < m + FWD_W; r += NT) xs[r] = z;
   for (int r = tid; r < m; r += NT) {
     double2 v = r < p ? yy[r] : z;
     for (int k = 0; k < nk; ++k) {
@@ -2205,7 +2208,7 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
     kh_note_launch();
     return cudaGetLastError();
   }
-  const size_t smem = sizeof(double2) * (size_t)max_m;
+  const size_t smem = sizeof(double2) * (size_t)(max_m + FWD_W);
   cudaError_t e = kh_smem_optin((const void*)fwd_top_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   fwd_top_kernel<<<dim3(nlev, batch), NT, smem, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,

@@ -157,6 +157,15 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
                                    cudaStream_t stream, const KhFwd* fwd = nullptr);
 
+// Register-resident warp-per-(front, shift) factorization of the fronts with
+// m <= 8 mt (warpfront.cu; mt = 4, 5 or 6): wdst[e] is the slot of original e
+// in the CTA's dense originals image (kh_warp_front_slot).
+int kh_warp_front_slot(int32_t m, int32_t p, int32_t r, int32_t c);
+cudaError_t kh_launch_warp_front(int mt, const KhTree& T, const int32_t* level_fronts, int32_t nlev,
+                                 int32_t batch, const double2* lam, double2* panels, double2* upd_cur,
+                                 int64_t upd_stride_cur, const double2* upd_child, int64_t upd_stride_child,
+                                 double* minpiv, const int32_t* wdst, cudaStream_t stream);
+
 // om[e] = mv[src[e]], oa[e] = av[src[e]] (values in the order the fronts read them).
 cudaError_t kh_launch_gather_orig(int64_t n_orig, const int64_t* src, const double* mv, const double* av, double* om,
                                   double* oa, cudaStream_t stream);

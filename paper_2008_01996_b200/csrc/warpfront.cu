@@ -1,0 +1,315 @@
+// Register-resident fronts: one warp per (front, shift) for the small fronts
+// (m <= 8 MT), the whole partial LDL^T in the DMMA accumulator layout.
+//
+// Replaces, for the deep levels of the dissection tree, the per-shift SuperLU
+// factorization of the reference (solvers.py:383-393 -> sparse_direct.py:155-188)
+// like factor_front_kernel does, but without shared memory for the front and
+// without CTA barriers: the front's lower triangle lives in registers as
+// 8 x 8 tiles in the C/D fragment layout of mma.sync m8n8k4 f64 (lane
+// (g, t) holds rows g, columns 2t and 2t+1 of every tile), so a warp carries
+// its front from assembly to write-out with shuffles only.
+//
+// Index permutation inside each 8-block. Rows and columns of a tile are stored
+// in the order phys = rho(logical) with rho(k) = 2 (k & 3) + (k >> 2), i.e.
+// lane (g, t) holds the logical entries (pi(g), t) and (pi(g), t + 4),
+// pi = rho^-1 = [0, 4, 1, 5, 2, 6, 3, 7]. Its two accumulator registers are
+// then exactly the A fragment of the tile for the K-slices {0..3} and
+// {4..7}, and -- scaled by the pivots -- its B fragment: the rank-8 trailing
+// updates S_IJ -= X_I D X_J^T run on DMMA straight from the registers that
+// hold the panel, with no shuffles and no shared-memory round trip. The pivot
+// order itself is the logical one (the permutation only changes where an
+// entry is stored), so the factors are the same LDL^T as factor_front_kernel's
+// up to rounding order.
+//
+// Per 8-pivot block:
+//  (a) the diagonal tile is factored in place with shuffles; the same row
+//      operations applied to an identity tile give L11^-1 in the same layout
+//      (Gauss-Jordan style), so M = L11^-T D^-1 is a per-lane product, again
+//      without shuffles;
+//  (b) panel tiles: X = A M on DMMA (A fragment = the lane's own registers);
+//  (c) trailing tiles: S_IJ -= X_I (X_J D)^T on DMMA (4 real MMAs per K-slice,
+//      accumulating in place).
+// Assembly pulls each child's update block through the child's parent-row map
+// (cmap): one independent load per register entry, children in order
+// (deterministic sums); the originals (M + lambda A on the pivot columns)
+// come from a per-CTA dense shared-memory image built from the front's
+// original-entry list, shared by the CTA's four shifts.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int WF_WARPS = 4;  // shifts per CTA (one warp each)
+
+KH_DEV int perm8(int g) { return (g >> 1) + 4 * (g & 1); }           // phys -> logical
+KH_HD constexpr int rho8(int k) { return 2 * (k & 3) + (k >> 2); }   // logical -> phys
+
+KH_DEV double2 shfl2w(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+KH_HD constexpr int tix(int I, int J) { return I * (I + 1) / 2 + J; }
+
+template <int MT>
+__global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_kernel(
+    KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
+    double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
+    double* minpiv, const int32_t* __restrict__ wdst, int32_t nshift) {
+  constexpr int NTL = MT * (MT + 1) / 2;
+  extern __shared__ __align__(16) double2 O[];  // originals image: [panel tile][h][lane] = (M, A)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int f = F.pad, p = F.p, q = F.q, m = p + q;
+  const int M8 = (m + 7) >> 3, PJ = (p + 7) >> 3;
+  KH_ASSERT(m <= 8 * MT);
+  // ---- originals image (shared by the CTA's shifts)
+  const int ntile = PJ * M8 - PJ * (PJ - 1) / 2;
+  for (int i = tid; i < ntile * 64; i += 32 * WF_WARPS) O[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int64_t e = F.orig_begin + tid; e < F.orig_end; e += 32 * WF_WARPS) {
+    const int d = wdst[e];
+    KH_ASSERT(d >= 0 && d < ntile * 64);
+    O[d] = make_double2(T.om[e], T.oa[e]);
+  }
+  __syncthreads();
+  const int b = blockIdx.y * WF_WARPS + warp;
+  if (b >= nshift) return;
+
+  const int rl = perm8(g);  // logical row of this lane inside every 8-block
+  double2 S[NTL][2];
+  {
+    const double2 L = lam[b];
+#pragma unroll
+    for (int I = 0; I < MT; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double2 v = make_double2(0.0, 0.0);
+          if (J < PJ && I < M8) {
+            const double2 o = O[(J * M8 - J * (J - 1) / 2 + I - J) * 64 + h * 32 + lane];
+            v = make_double2(fma(L.x, o.y, o.x), L.y * o.y);
+          }
+          S[tix(I, J)][h] = v;
+        }
+  }
+  // ---- children: pull through cmap (child-local index of each parent row)
+  const int nkids = F.child_end - F.child_begin;
+  for (int k = 0; k < nkids; ++k) {
+    const KhKid C = T.kids[F.child_begin + k];
+    const double2* __restrict__ U = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
+    const int32_t* __restrict__ cm = T.cmap + C.cmap_begin;
+    const int qk = C.q;
+    int ri[MT], cj[MT][2];
+#pragma unroll
+    for (int I = 0; I < MT; ++I) {
+      const int r = 8 * I + rl;
+      ri[I] = r < m ? __ldg(cm + r) : -1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * I + t + 4 * h;
+        cj[I][h] = c < m ? __ldg(cm + c) : -1;
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < MT; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool ok = ri[I] >= 0 && cj[J][h] >= 0 && (J < I || rl >= t + 4 * h);
+          if (ok) {
+            const double2 u = __ldg(U + ri[I] + (int64_t)cj[J][h] * qk);
+            S[tix(I, J)][h] = cadd(S[tix(I, J)][h], u);
+          }
+        }
+  }
+
+  // ---- blocked LDL^T over the p pivots
+  double minp = DBL_MAX;  // min |d|^2 (-1: non-finite pivot)
+#pragma unroll
+  for (int KB = 0; KB < MT; ++KB) {
+    if (8 * KB < p) {
+      const int w = min(8, p - 8 * KB);
+      double2(&Dg)[2] = S[tix(KB, KB)];
+      // E: identity in the same layout; receives the row operations -> L11^-1
+      double2 E[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) E[h] = make_double2(rl == t + 4 * h ? 1.0 : 0.0, 0.0);
+      double2 dk[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // d_{t}, d_{t+4}
+      double2 dinv_row = make_double2(0.0, 0.0);                           // 1 / d_{rl}
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < w) {
+          const int rk = rho8(k), sk = rk & 1, qk4 = rk >> 1;  // phys index, slot, quad lane
+          const double2 d = shfl2w(Dg[sk], rk * 4 + qk4);
+          const double2 colk = shfl2w(Dg[sk], (lane & ~3) | qk4);  // S[rl][k]
+          double2 sc[2], ek[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            sc[h] = shfl2w(Dg[sk], (2 * t + h) * 4 + qk4);  // S[t + 4h][k]
+            ek[h] = shfl2w(E[h], rk * 4 + t);               // E[k][t + 4h]
+          }
+          const double2 di = cinv(d);
+          const double2 l = cmul(colk, di);
+          const bool below = rl > k;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = t + 4 * h;
+            if (below && c > k && rl >= c) Dg[h] = cfms(Dg[h], l, sc[h]);
+            if (below) E[h] = cfms(E[h], l, ek[h]);
+          }
+          if (below && t == qk4) Dg[sk] = l;
+          if (t == (k & 3)) dk[k >> 2] = d;
+          if (rl == k) dinv_row = di;
+          const double a2 = cabs2(d);
+          minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
+        }
+      }
+      // M = L11^-T D^-1 as B fragments: lane (g, t), slice s holds
+      // M[t + 4s][rl] = L11^-1[rl][t + 4s] / d_rl (zero outside the w pivots)
+      double Mr[2], Mi[2], nMi[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const bool ok = rl < w && t + 4 * s < w;
+        const double2 v = ok ? cmul(E[s], dinv_row) : make_double2(0.0, 0.0);
+        Mr[s] = v.x;
+        Mi[s] = v.y;
+        nMi[s] = -v.y;
+      }
+      // B fragments of the diagonal tile's Schur rows (partial block only):
+      // L[rl][t + 4s] d_{t+4s} for t + 4s < w
+      const bool partial = w < 8;
+      double2 Bd[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        Bd[s] = (partial && t + 4 * s < w) ? cmul(Dg[s], dk[s]) : make_double2(0.0, 0.0);
+      // (b) panel tiles I > KB: X = A M; columns >= w keep A and get the
+      //     Schur update by the block's first w pivots
+#pragma unroll
+      for (int I = KB + 1; I < MT; ++I) {
+        if (I < M8) {
+          double2(&A)[2] = S[tix(I, KB)];
+          double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            dmma884(xr[0], xr[1], A[s].x, Mr[s]);
+            dmma884(xr[0], xr[1], A[s].y, nMi[s]);
+            dmma884(xi[0], xi[1], A[s].x, Mi[s]);
+            dmma884(xi[0], xi[1], A[s].y, Mr[s]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (t + 4 * h < w) A[h] = make_double2(xr[h], xi[h]);
+          if (partial) {
+            // A[:, w:] -= X[:, :w] (L[w:, :w] D)^T
+            double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const bool ks = t + 4 * s < w;
+              const double ar = ks ? A[s].x : 0.0, ai = ks ? A[s].y : 0.0;
+              dmma884(zr[0], zr[1], ar, Bd[s].x);
+              dmma884(zr[0], zr[1], -ai, Bd[s].y);
+              dmma884(zi[0], zi[1], ar, Bd[s].y);
+              dmma884(zi[0], zi[1], ai, Bd[s].x);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (t + 4 * h >= w) A[h] = make_double2(A[h].x - zr[h], A[h].y - zi[h]);
+          }
+        }
+      }
+      // (c) trailing tiles (I, J), KB < J <= I: S_IJ -= X_I (X_J D)^T,
+      //     accumulated in place: re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
+#pragma unroll
+      for (int J = KB + 1; J < MT; ++J) {
+        if (J < M8) {
+          double nBr[2], Bi[2], nBi[2];
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const bool ks = t + 4 * s < w;
+            const double2 bx = ks ? cmul(S[tix(J, KB)][s], dk[s]) : make_double2(0.0, 0.0);
+            nBr[s] = -bx.x;
+            Bi[s] = bx.y;
+            nBi[s] = -bx.y;
+          }
+#pragma unroll
+          for (int I = J; I < MT; ++I) {
+            if (I < M8) {
+              double2(&C)[2] = S[tix(I, J)];
+              double cr[2] = {C[0].x, C[1].x}, ci[2] = {C[0].y, C[1].y};
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                const bool ks = t + 4 * s < w;
+                const double ar = ks ? S[tix(I, KB)][s].x : 0.0, ai = ks ? S[tix(I, KB)][s].y : 0.0;
+                dmma884(cr[0], cr[1], ar, nBr[s]);
+                dmma884(cr[0], cr[1], ai, Bi[s]);
+                dmma884(ci[0], ci[1], ar, nBi[s]);
+                dmma884(ci[0], ci[1], ai, nBr[s]);
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) C[h] = make_double2(cr[h], ci[h]);
+            }
+          }
+        }
+      }
+    }
+  }
+
+  // ---- write the panel (m x p, column-major) and the update block (q x q)
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* Uo = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+#pragma unroll
+  for (int I = 0; I < MT; ++I)
+#pragma unroll
+    for (int J = 0; J <= I; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * I + rl, c = 8 * J + t + 4 * h;
+        if (r < m && r >= c) {
+          if (c < p) P[r + (int64_t)c * m] = S[tix(I, J)][h];
+          else Uo[(r - p) + (int64_t)(c - p) * q] = S[tix(I, J)][h];
+        }
+      }
+  if (lane == 0) minpiv[(int64_t)b * T.nf + f] = minp < 0.0 ? -1.0 : sqrt(minp);
+}
+
+}  // namespace
+
+// shared-memory bytes of the originals image for a front class
+static int warp_front_smem(int mt) { return 16 * 64 * (mt * (mt + 1) / 2); }
+
+int kh_warp_front_slot(int32_t m, int32_t p, int32_t r, int32_t c) {
+  // destination of the original entry (r, c), r >= c, c < p, in the image
+  const int M8 = (m + 7) >> 3, I = r >> 3, J = c >> 3;
+  const int pr = rho8(r & 7), pc = rho8(c & 7);
+  const int lane = pr * 4 + (pc >> 1), h = pc & 1;
+  (void)p;
+  return (J * M8 - J * (J - 1) / 2 + I - J) * 64 + h * 32 + lane;
+}
+
+cudaError_t kh_launch_warp_front(int mt, const KhTree& T, const int32_t* level_fronts, int32_t nlev,
+                                 int32_t batch, const double2* lam, double2* panels, double2* upd_cur,
+                                 int64_t upd_stride_cur, const double2* upd_child, int64_t upd_stride_child,
+                                 double* minpiv, const int32_t* wdst, cudaStream_t stream) {
+  if (nlev == 0 || batch == 0) return cudaSuccess;
+  const dim3 grid(nlev, (batch + WF_WARPS - 1) / WF_WARPS);
+  auto run = [&](auto kernel) -> cudaError_t {
+    const int smem = warp_front_smem(mt);
+    cudaError_t e = kh_smem_optin((const void*)kernel, smem);
+    if (e != cudaSuccess) return e;
+    kernel<<<grid, 32 * WF_WARPS, smem, stream>>>(T, level_fronts, lam, panels, upd_cur, upd_stride_cur,
+                                                   upd_child, upd_stride_child, minpiv, wdst, batch);
+    kh_note_launch();
+    return cudaGetLastError();
+  };
+  switch (mt) {
+    case 4: return run(warp_front_kernel<4>);
+    case 5: return run(warp_front_kernel<5>);
+    case 6: return run(warp_front_kernel<6>);
+    default: return cudaErrorInvalidValue;
+  }
+}

@@ -18,6 +18,7 @@ There is no CPU fallback.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -165,6 +166,8 @@ class _Plan:
         # it without cudaMalloc/cudaFree (which would synchronize the device)
         nbytes = plan_bytes(symbolic, self.max_batch, self.slots)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", int(device)))
+        if os.environ.get("KH_POISON"):  # debugging: NaN-fill the workspace (uninitialized reads show up)
+            self.workspace.fill_(255)
         _native.call("kh_plan_create", symbolic.handle.raw, int(device), _native.ptr(symbolic.indptr),
                      _native.ptr(symbolic.indices), _native.ptr(mv), _native.ptr(av), self.max_batch,
                      self.slots, self.workspace.data_ptr(), nbytes, ctypes.byref(self.raw))

@@ -144,21 +144,28 @@ def test_rhs_dimension_check(cuda_ok):
         num.solve(np.ones(5))
 
 
-@pytest.mark.parametrize("mesh,small_max,leaf", [
-    (("square", 40), None, None), (("lshape", 4), None, None), (("square", 128), None, None),
+@pytest.mark.parametrize("mesh,small_max,leaf,warp", [
+    (("square", 40), None, None, None), (("lshape", 4), None, None, None), (("square", 128), None, None, None),
     # every front through the level-synchronous large-front kernels
-    (("square", 64), "0", None), (("lshape", 4), "0", None),
+    (("square", 64), "0", None, None), (("lshape", 4), "0", None, None),
     # fused classes capped at m <= 64 / leaves large enough for the 96 and 128 classes
-    (("square", 64), "64", None), (("square", 96), None, 80), (("square", 64), None, 8)])
-def test_batched_shifts_match_superlu(cuda_ok, monkeypatch, mesh, small_max, leaf):
+    (("square", 64), "64", None, None), (("square", 96), None, 80, None), (("square", 64), None, 8, None),
+    # m <= 48 through the shared-memory fused kernel instead of the register-resident warp kernel
+    (("square", 64), None, None, "0"), (("lshape", 4), None, 16, "0"),
+    # warp kernels with small leaves (partial 8-pivot blocks, p < 8)
+    (("square", 64), None, 5, None), (("lshape", 4), None, 11, None)])
+def test_batched_shifts_match_superlu(cuda_ok, monkeypatch, mesh, small_max, leaf, warp):
     """Many complex shifts M + lam_k A in one batched factorization vs SuperLU,
-    through every front-class code path (KH_SMALL_MAX caps the fused classes)."""
+    through every front-class code path (KH_SMALL_MAX caps the fused classes,
+    KH_WARP_CLASSES selects the register-resident warp kernels)."""
     import torch
 
     from paper_2008_01996_b200 import fem, problems
 
     if small_max is not None:
         monkeypatch.setenv("KH_SMALL_MAX", small_max)
+    if warp is not None:
+        monkeypatch.setenv("KH_WARP_CLASSES", warp)
     ops = fem.assemble_p1(problems.spatial_mesh(*mesh))
     M, A = ops.M_II.tocsr(), ops.A_II.tocsr()
     n = M.shape[0]
