@@ -81,7 +81,7 @@ constexpr int kSmallClasses = 5;
 #endif
 constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, KH_CLASS4, 128};
 #ifndef KH_WARP_CLASSES
-#define KH_WARP_CLASSES 1
+#define KH_WARP_CLASSES 3
 #endif
 // the warp-per-front solve kernels take the classes with m <= 64
 #ifndef KH_SOLVE_SMALL_CLASSES
@@ -480,7 +480,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     }
   }
   // register-resident warp kernels for the classes m <= 32 and m <= 48
-  // (KH_WARP_CLASSES: bit c enables class c; default: m <= 32 only)
+  // (KH_WARP_CLASSES: bit c enables class c; default 0b011)
   int warp_mask = KH_WARP_CLASSES;
   if (const char* env = std::getenv("KH_WARP_CLASSES")) warp_mask = std::atoi(env);
   for (int c = 0; c < kSmallClasses; ++c)

@@ -10,7 +10,8 @@
 //
 // Per front (m = p + q rows, p pivots):
 //   panel P (m x p, column-major, ld m) in the retained factor storage,
-//   update U (q x q, lower) in a depth-parity buffer consumed by the parent.
+//   update U (q x q lower, packed by columns: kh_upk) in a depth-parity buffer
+//   consumed by the parent.
 // Fronts with m <= 128 (factor_front_kernel): the whole front is assembled in
 //   shared memory (packed block-column layout, push extend-add of the
 //   children), factored by blocked_ldlt (8-pivot blocks, DMMA trailing
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (ri[a] >= 0 && cj[nt][h] >= 0)
-              cacc[a][nt][h] = cadd(cacc[a][nt][h], C.U[ri[a] + (int64_t)cj[nt][h] * C.q]);
+              cacc[a][nt][h] = cadd(cacc[a][nt][h], C.U[kh_upk(C.q, ri[a], cj[nt][h])]);
     }
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
           const int mt = 2 * half + a;
           const int r = i0 + wi * 32 + mt * 8 + g, c = j0 + wj * 16 + nt * 8 + 2 * t + h;
           if (r < q && c < q && r >= c)
-            U[r + (int64_t)c * q] = csub(cacc[a][nt][h], make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
+            U[kh_upk(q, r, c)] = csub(cacc[a][nt][h], make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
         }
   }
 }
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
     for (int u = 0; u < ASM_CHUNK / NT; ++u) {
       if (idx0 + tid + u * NT < total && rr[u] >= cc[u]) {
         const int ci = C.cmap[rr[u]], cj = C.cmap[cc[u]];
-        if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[ci + (int64_t)cj * C.q]);
+        if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[kh_upk(C.q, ci, cj)]);
       }
     }
   }
@@ -991,7 +992,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   // warm L2 with the children's update blocks (read after the originals)
   for (int k = 0; k < nkids && k < RK; ++k) {
     const char* base = reinterpret_cast<const char*>(upd_child + (int64_t)b * upd_stride_child + kinfo[k].upd_off);
-    const int lines = (kinfo[k].q * kinfo[k].q * 16 + 127) >> 7;
+    const int lines = (kinfo[k].q * (kinfo[k].q + 1) * 8 + 127) >> 7;
     for (int l = tid; l < lines; l += NTH) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
   }
   for (int idx = tid; idx < RK * MS; idx += NTH) {
@@ -1058,7 +1059,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
         for (int u = 0; u < R; ++u) {
           const int ci = cj + lane + 32 * u;
           const bool ok = cj < qk && ci < qk;
-          v[h][u] = ok ? Uc[ci + (int64_t)cj * qk] : make_double2(0.0, 0.0);
+          v[h][u] = ok ? Uc[kh_upk(qk, ci, cj)] : make_double2(0.0, 0.0);
           dst[h][u] = ok ? base + rk[ci] : -1;
         }
       }
@@ -1141,7 +1142,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
       } else {
         const int cc = c - p;
         src = S + cb[c] + c;
-        dst = U + cc + (int64_t)cc * q;
+        dst = U + kh_upk(q, cc, cc);
         rows = q - cc;
       }
       const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(src));
@@ -1159,7 +1160,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   }
   for (int c = warp; c < q; c += NW) {
     const int base = cb[p + c] + p;
-    for (int r = c + lane; r < q; r += 32) U[r + (int64_t)c * q] = S[base + r];
+    for (int r = c + lane; r < q; r += 32) U[kh_upk(q, r, c)] = S[base + r];
   }
 #endif
   if (FWD) {

@@ -15,6 +15,11 @@ struct KhDevFront {
   int32_t depth, pad;
 };
 
+// Update (Schur complement) blocks are stored packed: the lower triangle of
+// the q x q block column by column, entry (i, j), i >= j, at kh_upk(q, i, j)
+// (one contiguous q(q+1)/2 array per front: a single bulk copy moves it).
+__host__ __device__ inline int64_t kh_upk(int q, int i, int j) { return i + (int64_t)j * (2 * q - j - 1) / 2; }
+
 // Packed block-column layout of a fused front (m <= 128) in shared memory:
 // the 8-column block b stores rows 8b..m-1 with leading dimension
 // roundup8(m - 8b) + 2 (2 mod 8 in 16-byte units: conflict-free DMMA

@@ -476,7 +476,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       Front& F = S.fronts[f];
       F.upd_off = uo;
       F.rupd_off = ru;
-      uo += (int64_t)F.q * F.q;
+      uo += (int64_t)F.q * (F.q + 1) / 2;  // packed lower (kh_upk)
       ru += F.q;
     }
     S.upd_size[d & 1] = std::max(S.upd_size[d & 1], uo);

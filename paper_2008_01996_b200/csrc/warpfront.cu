@@ -30,8 +30,10 @@
 //  (c) trailing tiles: S_IJ -= X_I (X_J D)^T on DMMA (4 real MMAs per K-slice,
 //      accumulating in place).
 // Assembly pulls each child's update block through the child's parent-row map
-// (cmap): one independent load per register entry, children in order
-// (deterministic sums); the originals (M + lambda A on the pivot columns)
+// (cmap), children in order (deterministic sums): the child's lower update
+// block is first staged in a per-warp shared-memory buffer by cp.async (the
+// whole block in flight at once without holding registers), then read by
+// one LDS per register entry; the originals (M + lambda A on the pivot columns)
 // come from a per-CTA dense shared-memory image built from the front's
 // original-entry list, shared by the CTA's four shifts.
 #include <cfloat>
@@ -42,6 +44,9 @@
 namespace {
 
 constexpr int WF_WARPS = 4;  // shifts per CTA (one warp each)
+// per-warp child staging buffer: packed lower triangle of a q <= 8 MT update
+// block followed by a zero slot
+KH_HD constexpr int WF_CHILD_MAX(int mt) { return 4 * mt * (8 * mt + 1) + 2; }  // + zero slot (+ pad)
 
 KH_DEV int perm8(int g) { return (g >> 1) + 4 * (g & 1); }           // phys -> logical
 KH_HD constexpr int rho8(int k) { return 2 * (k & 3) + (k >> 2); }   // logical -> phys
@@ -59,7 +64,10 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
     double* minpiv, const int32_t* __restrict__ wdst, int32_t nshift) {
   constexpr int NTL = MT * (MT + 1) / 2;
   extern __shared__ __align__(16) double2 O[];  // originals image: [panel tile][h][lane] = (M, A)
+  __shared__ __align__(8) uint64_t wbar[WF_WARPS];  // per-warp child-staging barriers
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < WF_WARPS) mbar_init(&wbar[tid], 1);
+  mbar_fence_init();
   const int g = lane >> 2, t = lane & 3;
   const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
   const int f = F.pad, p = F.p, q = F.q, m = p + q;
@@ -96,183 +104,227 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
           S[tix(I, J)][h] = v;
         }
   }
-  // ---- children: pull through cmap (child-local index of each parent row)
+  // ---- children: the child's packed update block (one contiguous array) is
+  // staged in the warp's shared-memory buffer by one bulk async copy, then
+  // pulled through cmap (child-local index of each parent row)
+  double2* cs = O + NTL * 64 + warp * WF_CHILD_MAX(MT);
   const int nkids = F.child_end - F.child_begin;
+  uint32_t phase = 0;
   for (int k = 0; k < nkids; ++k) {
     const KhKid C = T.kids[F.child_begin + k];
     const double2* __restrict__ U = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
     const int32_t* __restrict__ cm = T.cmap + C.cmap_begin;
     const int qk = C.q;
-    int ri[MT], cj[MT][2];
+    KH_ASSERT(qk <= 8 * MT);
+    __syncwarp();  // the previous child's pulls are done
+    if (lane == 0 && qk > 0) {
+      // order the generic-proxy reads of the buffer before the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = 8u * (uint32_t)(qk * (qk + 1));
+      mbar_arrive_expect_tx(&wbar[warp], bytes);
+      bulk_g2s(cs, U, bytes, &wbar[warp]);
+    }
+    // child-local row / packed column base of every parent row / column this
+    // lane touches; rows or columns outside the child get a huge sentinel so
+    // the sum of the two lands past ZSLOT and min() routes it to the zero slot
+    // (branch-free pulls; upper entries of diagonal tiles are don't-care and
+    // may receive any child entry)
+    constexpr int SENT = 1 << 24;
+    const int zslot = qk * (qk + 1) / 2;  // a zero entry right after the child block
+    int ri[MT], cbase[MT][2];
 #pragma unroll
     for (int I = 0; I < MT; ++I) {
       const int r = 8 * I + rl;
-      ri[I] = r < m ? __ldg(cm + r) : -1;
+      const int v = r < m ? __ldg(cm + r) : -1;
+      ri[I] = v >= 0 ? v : SENT;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = 8 * I + t + 4 * h;
-        cj[I][h] = c < m ? __ldg(cm + c) : -1;
+        const int cj = c < m ? __ldg(cm + c) : -1;
+        cbase[I][h] = cj >= 0 ? cj * (2 * qk - cj - 1) / 2 : SENT;
       }
     }
+    if (lane == 0) cs[zslot] = make_double2(0.0, 0.0);
+    if (qk > 0) {
+      mbar_wait(&wbar[warp], phase);
+      phase ^= 1u;
+    }
+    __syncwarp();
 #pragma unroll
     for (int I = 0; I < MT; ++I)
 #pragma unroll
       for (int J = 0; J <= I; ++J)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const bool ok = ri[I] >= 0 && cj[J][h] >= 0 && (J < I || rl >= t + 4 * h);
-          if (ok) {
-            const double2 u = __ldg(U + ri[I] + (int64_t)cj[J][h] * qk);
-            S[tix(I, J)][h] = cadd(S[tix(I, J)][h], u);
-          }
-        }
+        for (int h = 0; h < 2; ++h) S[tix(I, J)][h] = cadd(S[tix(I, J)][h], cs[min(cbase[J][h] + ri[I], zslot)]);
   }
 
-  // ---- blocked LDL^T over the p pivots
+  // ---- blocked LDL^T over the p pivots, one 8-pivot block per iteration of a
+  // runtime loop: the body works on the tile triangle relative to the current
+  // diagonal tile (S[tix(0, 0)]); after a block its finished tile column is
+  // written out and the triangle shifts up-left by one tile (register moves),
+  // so the kernel holds one copy of the block code instead of MT.
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* Uo = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   double minp = DBL_MAX;  // min |d|^2 (-1: non-finite pivot)
+  int kb = 0;
+#pragma unroll 1
+  for (; kb < p; kb += 8) {
+    const int w = min(8, p - kb);
+    const int nt = M8 - (kb >> 3);  // tile rows left (>= 1)
+    double2(&Dg)[2] = S[0];
+    // E: identity in the same layout; receives the row operations -> L11^-1
+    double2 E[2];
 #pragma unroll
-  for (int KB = 0; KB < MT; ++KB) {
-    if (8 * KB < p) {
-      const int w = min(8, p - 8 * KB);
-      double2(&Dg)[2] = S[tix(KB, KB)];
-      // E: identity in the same layout; receives the row operations -> L11^-1
-      double2 E[2];
+    for (int h = 0; h < 2; ++h) E[h] = make_double2(rl == t + 4 * h ? 1.0 : 0.0, 0.0);
+    double2 dk[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // d_{t}, d_{t+4}
+    double2 dinv_row = make_double2(0.0, 0.0);                           // 1 / d_{rl}
 #pragma unroll
-      for (int h = 0; h < 2; ++h) E[h] = make_double2(rl == t + 4 * h ? 1.0 : 0.0, 0.0);
-      double2 dk[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // d_{t}, d_{t+4}
-      double2 dinv_row = make_double2(0.0, 0.0);                           // 1 / d_{rl}
+    for (int k = 0; k < 8; ++k) {
+      if (k < w) {
+        const int rk = rho8(k), sk = rk & 1, qk4 = rk >> 1;  // phys index, slot, quad lane
+        const double2 d = shfl2w(Dg[sk], rk * 4 + qk4);
+        const double2 colk = shfl2w(Dg[sk], (lane & ~3) | qk4);  // S[rl][k]
+        double2 sc[2], ek[2];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (k < w) {
-          const int rk = rho8(k), sk = rk & 1, qk4 = rk >> 1;  // phys index, slot, quad lane
-          const double2 d = shfl2w(Dg[sk], rk * 4 + qk4);
-          const double2 colk = shfl2w(Dg[sk], (lane & ~3) | qk4);  // S[rl][k]
-          double2 sc[2], ek[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            sc[h] = shfl2w(Dg[sk], (2 * t + h) * 4 + qk4);  // S[t + 4h][k]
-            ek[h] = shfl2w(E[h], rk * 4 + t);               // E[k][t + 4h]
-          }
-          const double2 di = cinv(d);
-          const double2 l = cmul(colk, di);
-          const bool below = rl > k;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = t + 4 * h;
-            if (below && c > k && rl >= c) Dg[h] = cfms(Dg[h], l, sc[h]);
-            if (below) E[h] = cfms(E[h], l, ek[h]);
-          }
-          if (below && t == qk4) Dg[sk] = l;
-          if (t == (k & 3)) dk[k >> 2] = d;
-          if (rl == k) dinv_row = di;
-          const double a2 = cabs2(d);
-          minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
+        for (int h = 0; h < 2; ++h) {
+          sc[h] = shfl2w(Dg[sk], (2 * t + h) * 4 + qk4);  // S[t + 4h][k]
+          ek[h] = shfl2w(E[h], rk * 4 + t);               // E[k][t + 4h]
         }
-      }
-      // M = L11^-T D^-1 as B fragments: lane (g, t), slice s holds
-      // M[t + 4s][rl] = L11^-1[rl][t + 4s] / d_rl (zero outside the w pivots)
-      double Mr[2], Mi[2], nMi[2];
+        const double2 di = cinv(d);
+        const double2 l = cmul(colk, di);
+        const bool below = rl > k;
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const bool ok = rl < w && t + 4 * s < w;
-        const double2 v = ok ? cmul(E[s], dinv_row) : make_double2(0.0, 0.0);
-        Mr[s] = v.x;
-        Mi[s] = v.y;
-        nMi[s] = -v.y;
-      }
-      // B fragments of the diagonal tile's Schur rows (partial block only):
-      // L[rl][t + 4s] d_{t+4s} for t + 4s < w
-      const bool partial = w < 8;
-      double2 Bd[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-        Bd[s] = (partial && t + 4 * s < w) ? cmul(Dg[s], dk[s]) : make_double2(0.0, 0.0);
-      // (b) panel tiles I > KB: X = A M; columns >= w keep A and get the
-      //     Schur update by the block's first w pivots
-#pragma unroll
-      for (int I = KB + 1; I < MT; ++I) {
-        if (I < M8) {
-          double2(&A)[2] = S[tix(I, KB)];
-          double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            dmma884(xr[0], xr[1], A[s].x, Mr[s]);
-            dmma884(xr[0], xr[1], A[s].y, nMi[s]);
-            dmma884(xi[0], xi[1], A[s].x, Mi[s]);
-            dmma884(xi[0], xi[1], A[s].y, Mr[s]);
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (t + 4 * h < w) A[h] = make_double2(xr[h], xi[h]);
-          if (partial) {
-            // A[:, w:] -= X[:, :w] (L[w:, :w] D)^T
-            double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const bool ks = t + 4 * s < w;
-              const double ar = ks ? A[s].x : 0.0, ai = ks ? A[s].y : 0.0;
-              dmma884(zr[0], zr[1], ar, Bd[s].x);
-              dmma884(zr[0], zr[1], -ai, Bd[s].y);
-              dmma884(zi[0], zi[1], ar, Bd[s].y);
-              dmma884(zi[0], zi[1], ai, Bd[s].x);
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              if (t + 4 * h >= w) A[h] = make_double2(A[h].x - zr[h], A[h].y - zi[h]);
-          }
+        for (int h = 0; h < 2; ++h) {
+          const int c = t + 4 * h;
+          if (below && c > k && rl >= c) Dg[h] = cfms(Dg[h], l, sc[h]);
+          if (below) E[h] = cfms(E[h], l, ek[h]);
         }
+        if (below && t == qk4) Dg[sk] = l;
+        if (t == (k & 3)) dk[k >> 2] = d;
+        if (rl == k) dinv_row = di;
+        const double a2 = cabs2(d);
+        minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
       }
-      // (c) trailing tiles (I, J), KB < J <= I: S_IJ -= X_I (X_J D)^T,
-      //     accumulated in place: re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
+    }
+    // M = L11^-T D^-1 as B fragments: lane (g, t), slice s holds
+    // M[t + 4s][rl] = L11^-1[rl][t + 4s] / d_rl (zero outside the w pivots)
+    double Mr[2], Mi[2], nMi[2];
 #pragma unroll
-      for (int J = KB + 1; J < MT; ++J) {
-        if (J < M8) {
-          double nBr[2], Bi[2], nBi[2];
+    for (int s = 0; s < 2; ++s) {
+      const bool ok = rl < w && t + 4 * s < w;
+      const double2 v = ok ? cmul(E[s], dinv_row) : make_double2(0.0, 0.0);
+      Mr[s] = v.x;
+      Mi[s] = v.y;
+      nMi[s] = -v.y;
+    }
+    // B fragments of the diagonal tile's Schur rows (partial block only):
+    // L[rl][t + 4s] d_{t+4s} for t + 4s < w
+    const bool partial = w < 8;
+    double2 Bd[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      Bd[s] = (partial && t + 4 * s < w) ? cmul(Dg[s], dk[s]) : make_double2(0.0, 0.0);
+    // (b) panel tiles I >= 1: X = A M; columns >= w keep A and get the Schur
+    //     update by the block's first w pivots
+#pragma unroll
+    for (int I = 1; I < MT; ++I) {
+      if (I < nt) {
+        double2(&A)[2] = S[tix(I, 0)];
+        double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          dmma884(xr[0], xr[1], A[s].x, Mr[s]);
+          dmma884(xr[0], xr[1], A[s].y, nMi[s]);
+          dmma884(xi[0], xi[1], A[s].x, Mi[s]);
+          dmma884(xi[0], xi[1], A[s].y, Mr[s]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (t + 4 * h < w) A[h] = make_double2(xr[h], xi[h]);
+        if (partial) {
+          // A[:, w:] -= X[:, :w] (L[w:, :w] D)^T
+          double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const bool ks = t + 4 * s < w;
-            const double2 bx = ks ? cmul(S[tix(J, KB)][s], dk[s]) : make_double2(0.0, 0.0);
-            nBr[s] = -bx.x;
-            Bi[s] = bx.y;
-            nBi[s] = -bx.y;
+            const double ar = ks ? A[s].x : 0.0, ai = ks ? A[s].y : 0.0;
+            dmma884(zr[0], zr[1], ar, Bd[s].x);
+            dmma884(zr[0], zr[1], -ai, Bd[s].y);
+            dmma884(zi[0], zi[1], ar, Bd[s].y);
+            dmma884(zi[0], zi[1], ai, Bd[s].x);
           }
 #pragma unroll
-          for (int I = J; I < MT; ++I) {
-            if (I < M8) {
-              double2(&C)[2] = S[tix(I, J)];
-              double cr[2] = {C[0].x, C[1].x}, ci[2] = {C[0].y, C[1].y};
+          for (int h = 0; h < 2; ++h)
+            if (t + 4 * h >= w) A[h] = make_double2(A[h].x - zr[h], A[h].y - zi[h]);
+        }
+      }
+    }
+    // (c) trailing tiles (I, J), 1 <= J <= I: S_IJ -= X_I (X_J D)^T, accumulated
+    //     in place: re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
 #pragma unroll
-              for (int s = 0; s < 2; ++s) {
-                const bool ks = t + 4 * s < w;
-                const double ar = ks ? S[tix(I, KB)][s].x : 0.0, ai = ks ? S[tix(I, KB)][s].y : 0.0;
-                dmma884(cr[0], cr[1], ar, nBr[s]);
-                dmma884(cr[0], cr[1], ai, Bi[s]);
-                dmma884(ci[0], ci[1], ar, nBi[s]);
-                dmma884(ci[0], ci[1], ai, nBr[s]);
-              }
+    for (int J = 1; J < MT; ++J) {
+      if (J < nt) {
+        double nBr[2], Bi[2], nBi[2];
 #pragma unroll
-              for (int h = 0; h < 2; ++h) C[h] = make_double2(cr[h], ci[h]);
+        for (int s = 0; s < 2; ++s) {
+          const bool ks = t + 4 * s < w;
+          const double2 bx = ks ? cmul(S[tix(J, 0)][s], dk[s]) : make_double2(0.0, 0.0);
+          nBr[s] = -bx.x;
+          Bi[s] = bx.y;
+          nBi[s] = -bx.y;
+        }
+#pragma unroll
+        for (int I = J; I < MT; ++I) {
+          if (I < nt) {
+            double2(&C)[2] = S[tix(I, J)];
+            double cr[2] = {C[0].x, C[1].x}, ci[2] = {C[0].y, C[1].y};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const bool ks = t + 4 * s < w;
+              const double ar = ks ? S[tix(I, 0)][s].x : 0.0, ai = ks ? S[tix(I, 0)][s].y : 0.0;
+              dmma884(cr[0], cr[1], ar, nBr[s]);
+              dmma884(cr[0], cr[1], ai, Bi[s]);
+              dmma884(ci[0], ci[1], ar, nBi[s]);
+              dmma884(ci[0], ci[1], ai, nBr[s]);
             }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) C[h] = make_double2(cr[h], ci[h]);
           }
         }
       }
     }
+    // (d) the finished tile column: pivot columns to the panel, the Schur
+    //     columns of a partial block to the update block
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = kb + t + 4 * h;
+      double2* pc = P + (int64_t)c * m;
+#pragma unroll
+      for (int I = 0; I < MT; ++I) {
+        const int r = kb + 8 * I + rl;
+        if (I < nt && r < m && (I > 0 || rl >= t + 4 * h)) {
+          if (c < p) pc[r] = S[tix(I, 0)][h];
+          else Uo[kh_upk(q, r - p, c - p)] = S[tix(I, 0)][h];
+        }
+      }
+    }
+    // (e) shift the trailing triangle to the origin
+#pragma unroll
+    for (int I = 1; I < MT; ++I)
+#pragma unroll
+      for (int J = 1; J <= I; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) S[tix(I - 1, J - 1)][h] = S[tix(I, J)][h];
   }
-
-  // ---- write the panel (m x p, column-major) and the update block (q x q)
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* Uo = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
+  // ---- the rest is the update block (rows and columns >= kb >= p)
 #pragma unroll
   for (int I = 0; I < MT; ++I)
 #pragma unroll
     for (int J = 0; J <= I; ++J)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = 8 * I + rl, c = 8 * J + t + 4 * h;
-        if (r < m && r >= c) {
-          if (c < p) P[r + (int64_t)c * m] = S[tix(I, J)][h];
-          else Uo[(r - p) + (int64_t)(c - p) * q] = S[tix(I, J)][h];
-        }
+        const int r = kb + 8 * I + rl, c = kb + 8 * J + t + 4 * h;
+        if (r < m && r >= c) Uo[kh_upk(q, r - p, c - p)] = S[tix(I, J)][h];
       }
   if (lane == 0) minpiv[(int64_t)b * T.nf + f] = minp < 0.0 ? -1.0 : sqrt(minp);
 }
@@ -280,7 +332,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
 }  // namespace
 
 // shared-memory bytes of the originals image for a front class
-static int warp_front_smem(int mt) { return 16 * 64 * (mt * (mt + 1) / 2); }
+static int warp_front_smem(int mt) { return 16 * (64 * (mt * (mt + 1) / 2) + WF_WARPS * WF_CHILD_MAX(mt)); }
 
 int kh_warp_front_slot(int32_t m, int32_t p, int32_t r, int32_t c) {
   // destination of the original entry (r, c), r >= c, c < p, in the image
