@@ -44,6 +44,9 @@
 namespace {
 
 constexpr int WF_WARPS = 4;  // shifts per CTA (one warp each)
+constexpr int WF_KMAP = 4;   // children whose pull maps are tabulated in shared memory
+// packed (lower, by columns) update-block index in 32-bit arithmetic (q <= 64)
+KH_DEV int upk32(int q, int i, int j) { return i + j * (2 * q - j - 1) / 2; }
 // per-warp child staging buffer: packed lower triangle of a q <= 8 MT update
 // block followed by a zero slot
 KH_HD constexpr int WF_CHILD_MAX(int mt) { return 4 * mt * (8 * mt + 1) + 2; }  // + zero slot (+ pad)
@@ -73,6 +76,58 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
   const int f = F.pad, p = F.p, q = F.q, m = p + q;
   const int M8 = (m + 7) >> 3, PJ = (p + 7) >> 3;
   KH_ASSERT(m <= 8 * MT);
+  const int b = blockIdx.y * WF_WARPS + warp;
+  const int nkids = F.child_end - F.child_begin;
+  double2* cs = O + NTL * 64 + warp * WF_CHILD_MAX(MT);  // this warp's child buffer
+  // the first child's update block starts streaming in right away
+  auto stage_child = [&](int k) {
+    const KhKid C = T.kids[F.child_begin + k];
+    if (lane == 0 && C.q > 0) {
+      // order earlier generic-proxy reads of the buffer before the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = 8u * (uint32_t)(C.q * (C.q + 1));
+      mbar_arrive_expect_tx(&wbar[warp], bytes);
+      bulk_g2s(cs, upd_child + (int64_t)b * upd_stride_child + C.upd_off, bytes, &wbar[warp]);
+    }
+  };
+  __syncthreads();  // barriers initialized
+  if (b < nshift && nkids > 0) stage_child(0);
+  // child maps for the pulls, per lane (shared by the CTA's shifts, built once
+  // by warp k for child k < WF_KMAP): child-local row of each parent row the
+  // lane holds and packed column base of each parent column; entries outside
+  // the child get a huge sentinel so that the sum of the two lands past the
+  // zero slot and min() routes it there (branch-free pulls; the upper entries
+  // of diagonal tiles are don't-care and may receive any child entry)
+  constexpr int SENT = 1 << 24;
+  int32_t* kmap = reinterpret_cast<int32_t*>(O + NTL * 64 + WF_WARPS * WF_CHILD_MAX(MT));
+  auto child_maps = [&](int k, int (&ri)[MT], int (&cbase)[MT][2]) {
+    const KhKid C = T.kids[F.child_begin + k];
+    const int32_t* __restrict__ cm = T.cmap + C.cmap_begin;
+    const int rl_ = perm8(g);
+#pragma unroll
+    for (int I = 0; I < MT; ++I) {
+      const int r = 8 * I + rl_;
+      const int v = r < m ? __ldg(cm + r) : -1;
+      ri[I] = v >= 0 ? v : SENT;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * I + t + 4 * h;
+        const int cj = c < m ? __ldg(cm + c) : -1;
+        cbase[I][h] = cj >= 0 ? cj * (2 * C.q - cj - 1) / 2 : SENT;
+      }
+    }
+  };
+  if (warp < nkids && warp < WF_KMAP) {
+    int ri[MT], cbase[MT][2];
+    child_maps(warp, ri, cbase);
+    int32_t* km = kmap + warp * 3 * MT * 32 + lane;
+#pragma unroll
+    for (int I = 0; I < MT; ++I) {
+      km[(3 * I) * 32] = ri[I];
+      km[(3 * I + 1) * 32] = cbase[I][0];
+      km[(3 * I + 2) * 32] = cbase[I][1];
+    }
+  }
   // ---- originals image (shared by the CTA's shifts)
   const int ntile = PJ * M8 - PJ * (PJ - 1) / 2;
   for (int i = tid; i < ntile * 64; i += 32 * WF_WARPS) O[i] = make_double2(0.0, 0.0);
@@ -83,7 +138,6 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
     O[d] = make_double2(T.om[e], T.oa[e]);
   }
   __syncthreads();
-  const int b = blockIdx.y * WF_WARPS + warp;
   if (b >= nshift) return;
 
   const int rl = perm8(g);  // logical row of this lane inside every 8-block
@@ -104,46 +158,30 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
           S[tix(I, J)][h] = v;
         }
   }
-  // ---- children: the child's packed update block (one contiguous array) is
+  // ---- children: each child's packed update block (one contiguous array) is
   // staged in the warp's shared-memory buffer by one bulk async copy, then
-  // pulled through cmap (child-local index of each parent row)
-  double2* cs = O + NTL * 64 + warp * WF_CHILD_MAX(MT);
-  const int nkids = F.child_end - F.child_begin;
+  // pulled through the child maps
   uint32_t phase = 0;
   for (int k = 0; k < nkids; ++k) {
-    const KhKid C = T.kids[F.child_begin + k];
-    const double2* __restrict__ U = upd_child + (int64_t)b * upd_stride_child + C.upd_off;
-    const int32_t* __restrict__ cm = T.cmap + C.cmap_begin;
-    const int qk = C.q;
+    const int qk = T.kids[F.child_begin + k].q;
     KH_ASSERT(qk <= 8 * MT);
-    __syncwarp();  // the previous child's pulls are done
-    if (lane == 0 && qk > 0) {
-      // order the generic-proxy reads of the buffer before the async-proxy writes
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t bytes = 8u * (uint32_t)(qk * (qk + 1));
-      mbar_arrive_expect_tx(&wbar[warp], bytes);
-      bulk_g2s(cs, U, bytes, &wbar[warp]);
+    if (k > 0) {
+      __syncwarp();  // the previous child's pulls are done
+      stage_child(k);
     }
-    // child-local row / packed column base of every parent row / column this
-    // lane touches; rows or columns outside the child get a huge sentinel so
-    // the sum of the two lands past ZSLOT and min() routes it to the zero slot
-    // (branch-free pulls; upper entries of diagonal tiles are don't-care and
-    // may receive any child entry)
-    constexpr int SENT = 1 << 24;
-    const int zslot = qk * (qk + 1) / 2;  // a zero entry right after the child block
     int ri[MT], cbase[MT][2];
+    if (k < WF_KMAP) {
+      const int32_t* km = kmap + k * 3 * MT * 32 + lane;
 #pragma unroll
-    for (int I = 0; I < MT; ++I) {
-      const int r = 8 * I + rl;
-      const int v = r < m ? __ldg(cm + r) : -1;
-      ri[I] = v >= 0 ? v : SENT;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 8 * I + t + 4 * h;
-        const int cj = c < m ? __ldg(cm + c) : -1;
-        cbase[I][h] = cj >= 0 ? cj * (2 * qk - cj - 1) / 2 : SENT;
+      for (int I = 0; I < MT; ++I) {
+        ri[I] = km[(3 * I) * 32];
+        cbase[I][0] = km[(3 * I + 1) * 32];
+        cbase[I][1] = km[(3 * I + 2) * 32];
       }
+    } else {
+      child_maps(k, ri, cbase);
     }
+    const int zslot = qk * (qk + 1) / 2;  // a zero entry right after the child block
     if (lane == 0) cs[zslot] = make_double2(0.0, 0.0);
     if (qk > 0) {
       mbar_wait(&wbar[warp], phase);
@@ -304,7 +342,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
         const int r = kb + 8 * I + rl;
         if (I < nt && r < m && (I > 0 || rl >= t + 4 * h)) {
           if (c < p) pc[r] = S[tix(I, 0)][h];
-          else Uo[kh_upk(q, r - p, c - p)] = S[tix(I, 0)][h];
+          else Uo[upk32(q, r - p, c - p)] = S[tix(I, 0)][h];
         }
       }
     }
@@ -324,7 +362,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = kb + 8 * I + rl, c = kb + 8 * J + t + 4 * h;
-        if (r < m && r >= c) Uo[kh_upk(q, r - p, c - p)] = S[tix(I, J)][h];
+        if (r < m && r >= c) Uo[upk32(q, r - p, c - p)] = S[tix(I, J)][h];
       }
   if (lane == 0) minpiv[(int64_t)b * T.nf + f] = minp < 0.0 ? -1.0 : sqrt(minp);
 }
@@ -332,7 +370,9 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
 }  // namespace
 
 // shared-memory bytes of the originals image for a front class
-static int warp_front_smem(int mt) { return 16 * (64 * (mt * (mt + 1) / 2) + WF_WARPS * WF_CHILD_MAX(mt)); }
+static int warp_front_smem(int mt) {
+  return 16 * (64 * (mt * (mt + 1) / 2) + WF_WARPS * WF_CHILD_MAX(mt)) + 4 * WF_KMAP * 3 * mt * 32;
+}
 
 int kh_warp_front_slot(int32_t m, int32_t p, int32_t r, int32_t c) {
   // destination of the original entry (r, c), r >= c, c < p, in the image
