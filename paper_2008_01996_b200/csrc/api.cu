@@ -125,7 +125,10 @@ struct kh_plan {
   };
   struct BigLevel {
     int32_t asm_off, asm_n, kb_off, nkb;
+    int32_t piv_off, piv_n, psol_off, psol_n;  // p <= kh_piv_max(): pivot-block and panel-solve tasks
   };
+  double2* minv = nullptr;     // [max_batch][minv_size]: B images of a level's pivot blocks (pivot_block_kernel)
+  int64_t minv_size = 1;
   std::vector<BigLevel> big;
   std::vector<KbInfo> kbinfo;
   int32_t* btasks = nullptr;
@@ -434,6 +437,7 @@ struct Sched {
   std::vector<kh_plan::BigLevel> big;
   std::vector<kh_plan::KbInfo> kbinfo;
   int32_t max_p = 0, max_m = 0;
+  int64_t minv_size = 1;
 };
 
 void build_schedule(const kh::Symbolic& S, Sched& X) {
@@ -463,6 +467,9 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   // (0 disables them, for A/B measurements)
   int small_max = 128;
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
+  // large fronts with p <= kh_piv_max() take the pivot-block + panel-solve path
+  bool panel_inv = true;
+  if (const char* env = std::getenv("KH_PANEL_INV")) panel_inv = std::atoi(env) != 0;
   auto front_class = [&](int32_t m) {
     for (int c = 0; c < kSmallClasses; ++c)
       if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
@@ -549,6 +556,9 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     X.task_off.push_back((int32_t)(X.tasks.size() / 3));
     kh_plan::BigLevel L{};
     L.asm_off = (int32_t)X.bt.size();
+    // fronts whose pivot block fits the two-launch panel path (KH_PANEL_INV=0: none)
+    auto inv_path = [&](int32_t f) { return panel_inv && S.fronts[f].p <= kh_piv_max(); };
+    auto img_tiles = [](int32_t p) { const int64_t pt = (p + 7) / 8; return pt * (pt + 1) / 2; };
     int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
@@ -563,9 +573,29 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
         while (e < F.orig_end && S.orig_dst[e] < end) ++e;
         X.bt.insert(X.bt.end(), {f, idx0, (int32_t)lo, (int32_t)e});
       }
-      nkb = std::max(nkb, (F.p + 31) / 32);
+      if (!inv_path(f)) nkb = std::max(nkb, (F.p + 31) / 32);
     }
     L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 4;
+    {
+      int64_t off = 0;
+      L.piv_off = (int32_t)X.bt.size();
+      for (int32_t f : large)
+        if (inv_path(f)) {
+          X.bt.insert(X.bt.end(), {f, (int32_t)off});
+          off += 64 * img_tiles(S.fronts[f].p);
+        }
+      L.piv_n = ((int32_t)X.bt.size() - L.piv_off) / 2;
+      X.minv_size = std::max(X.minv_size, off);
+      off = 0;
+      L.psol_off = (int32_t)X.bt.size();
+      for (int32_t f : large)
+        if (inv_path(f)) {
+          const kh::Front& F = S.fronts[f];
+          for (int32_t i0 = F.p; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, (int32_t)off});
+          off += 64 * img_tiles(F.p);
+        }
+      L.psol_n = ((int32_t)X.bt.size() - L.psol_off) / 3;
+    }
     L.kb_off = (int32_t)X.kbinfo.size();
     L.nkb = nkb;
     for (int32_t kbi = 0; kbi < nkb; ++kbi) {
@@ -573,20 +603,20 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
       kh_plan::KbInfo K{};
       K.diag_off = (int32_t)X.bt.size();
       for (int32_t f : large)
-        if (S.fronts[f].p > kb) X.bt.push_back(f);
+        if (S.fronts[f].p > kb && !inv_path(f)) X.bt.push_back(f);
       K.diag_n = (int32_t)X.bt.size() - K.diag_off;
       K.lupd_off = (int32_t)X.bt.size();
       if (kb > 0)
         for (int32_t f : large) {
           const kh::Front& F = S.fronts[f];
-          if (F.p <= kb) continue;
+          if (F.p <= kb || inv_path(f)) continue;
           for (int32_t i0 = (kb / 64) * 64; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0});
         }
       K.lupd_n = ((int32_t)X.bt.size() - K.lupd_off) / 2;
       K.trsm_off = (int32_t)X.bt.size();
       for (int32_t f : large) {
         const kh::Front& F = S.fronts[f];
-        if (F.p <= kb) continue;
+        if (F.p <= kb || inv_path(f)) continue;
         const int32_t start = kb + std::min(32, F.p - kb);
         for (int32_t i0 = start; i0 < F.m(); i0 += KH_TRSM_ROWS) X.bt.insert(X.bt.end(), {f, i0});
       }
@@ -637,6 +667,7 @@ void carve(kh_plan* p, const kh::Symbolic& S, const Sched& X, Carver& C) {
     C.take(&p->rupd[k], (size_t)(p->max_batch * p->rupd_size[k]));
   }
   C.take(&p->y, (size_t)(p->max_batch * S.n));
+  C.take(&p->minv, (size_t)(p->max_batch * p->minv_size));
   C.take(&p->lam, (size_t)p->max_batch);
   C.take(&p->minpiv_work, (size_t)(p->max_batch * (int64_t)X.df.size()));
   C.take(&p->absmax_work, (size_t)(p->max_batch * kAbsmaxBlocks));
@@ -669,6 +700,7 @@ int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots,
   Sched X;
   build_schedule(s->S, X);
   plan_sizes(&tmp, s->S, max_batch, factor_slots);
+  tmp.minv_size = X.minv_size;
   Carver C;
   carve(&tmp, s->S, X, C);
   *bytes = (int64_t)C.off;
@@ -703,6 +735,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
   p->big = X.big;
   p->kbinfo = X.kbinfo;
+  p->minv_size = X.minv_size;
   Carver measure;
   carve(p, S, X, measure);
   cudaError_t e = cudaSuccess;
@@ -807,6 +840,9 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
     }
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
+    KH_CUDA(kh_launch_pivot_block(T, p->btasks + B.piv_off, B.piv_n, ns, panels, p->minpiv_work, p->minv,
+                                  p->minv_size, st));
+    KH_CUDA(kh_launch_panel_solve(T, p->btasks + B.psol_off, B.psol_n, ns, panels, p->minv, p->minv_size, st));
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
       const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
       const int kb = 32 * kbi;

@@ -860,6 +860,177 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
   }
 }
 
+// ---- large fronts with p <= PIV_MAX: two launches for the whole panel ----------
+// Instead of lupdate / diag / trsm per 32-pivot block:
+//   pivot_block_kernel (front, shift): the p x p pivot block of the assembled
+//     panel is loaded into shared memory, factored by blocked_ldlt (8-pivot
+//     blocks, DMMA trailing updates) and written back; it also writes the
+//     block's "B image": for every 8 x 8 tile pair (j, k), k < j, of L11 the
+//     DMMA B fragments of D_k L_jk^T, and for k = j those of
+//     M_j = L_jj^-T D_j^-1 (from the 8 x 8 unit-lower inverse), in lane order;
+//   panel_trsm_kernel (front, 64-row tile of L21, shift): a warp per 8 rows
+//     solves X = A21 L11^-T D^-1 by blocks of 8 columns,
+//     X_j = (A_j - sum_{k<j} X_k D_k L_jk^T) M_j, on DMMA with its rows held in
+//     registers in the permuted accumulator layout of warpfront.cu (lane
+//     (g, t) holds logical rows pi(g), columns t and t + 4 of every tile, so
+//     a finished X_k is directly an A fragment) and the B image staged in
+//     shared memory by one bulk copy.
+constexpr int PIV_MAX = 64, PIV_NW = 4, PIV_LD = PIV_MAX + 2, PIV_PT = PIV_MAX / 8;
+constexpr int PIV_IMG = 64 * PIV_PT * (PIV_PT + 1) / 2;  // B image entries (double2) at p = PIV_MAX
+KH_HD constexpr int piv_smem_bytes() { return 16 * (kh_packed_elems(PIV_MAX) + 8 * PIV_LD + 8 + PIV_MAX + 64 * PIV_PT) + 4 * PIV_MAX; }
+KH_DEV int piv_perm8(int g) { return (g >> 1) + 4 * (g & 1); }  // phys -> logical inside an 8-block
+KH_HD constexpr int piv_tp(int j, int k) { return j * (j + 1) / 2 + k; }
+
+__global__ void __launch_bounds__(32 * PIV_NW) pivot_block_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                                  double2* panels, double* minpiv, double2* img,
+                                                                  int64_t img_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // packed p x p (L11, D)
+  double2* W = S + kh_packed_elems(PIV_MAX);
+  double2* dinv = W + 8 * PIV_LD;
+  double2* dg = dinv + 8;
+  double2* Ld = dg + PIV_MAX;  // inverses of the diagonal 8 x 8 blocks: Ld[j][i][c] = L_jj^-1[i][c]
+  int32_t* cb = reinterpret_cast<int32_t*>(Ld + 64 * PIV_PT);
+  __shared__ int ctr;
+  constexpr int NTH = 32 * PIV_NW;
+  const int tid = threadIdx.x;
+  const int32_t f = tasks[2 * blockIdx.x];
+  const int64_t off = tasks[2 * blockIdx.x + 1];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, PT = (p + 7) >> 3;
+  KH_ASSERT(p <= PIV_MAX);
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  for (int c = tid; c < p; c += NTH) cb[c] = kh_packed_col_base(p, c);
+  __syncthreads();
+  for (int e = tid; e < p * p; e += NTH) {
+    const int c = e / p, r = e - c * p;
+    if (r >= c) S[cb[c] + r] = P[r + (int64_t)c * m];
+  }
+  __syncthreads();
+  const double minp = blocked_ldlt<PIV_NW, false>(S, cb, W, PIV_LD, dinv, dg, &ctr, p, p);
+  for (int e = tid; e < p * p; e += NTH) {
+    const int c = e / p, r = e - c * p;
+    if (r >= c) P[r + (int64_t)c * m] = S[cb[c] + r];
+  }
+  // unit-lower inverses of the diagonal blocks, thread per (block, column)
+  for (int e = tid; e < 8 * PT; e += NTH) {
+    const int j = e >> 3, c = e & 7, base = 8 * j;
+    double2 y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+      if (i > c && base + i < p) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < i; ++k)
+          if (k >= c) acc = cfms(acc, S[cb[base + k] + base + i], y[k]);
+        y[i] = acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Ld[j * 64 + i * 8 + c] = y[i];
+  }
+  __syncthreads();
+  // B image: tile pair (j, k), slice s, lane (g, t) at [(tp * 2 + s) * 32 + lane]
+  double2* im = img + (int64_t)b * img_stride + off;
+  const int ntp = PT * (PT + 1) / 2;
+  for (int e = tid; e < ntp * 64; e += NTH) {
+    const int tp = e >> 6, s = (e >> 5) & 1, lane = e & 31;
+    int j = 0;
+    while (piv_tp(j + 1, 0) <= tp) ++j;
+    const int k = tp - piv_tp(j, 0);
+    const int g = lane >> 2, t = lane & 3;
+    const int n = piv_perm8(g), kk = t + 4 * s;  // logical row of block j / column of block k
+    const int rn = 8 * j + n, ck = 8 * k + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (rn < p && ck < p) {
+      if (k < j) v = cmul(S[cb[ck] + rn], dg[ck]);                                    // d_k L_jk[n][kk]
+      else if (kk <= n) v = cmul(Ld[j * 64 + n * 8 + kk], cinv(dg[rn]));             // L_jj^-1[n][kk] / d_n
+    }
+    im[e] = v;
+  }
+  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+}
+
+constexpr int PTR_NW = 8;  // warps (8-row slabs) per panel_trsm CTA
+__global__ void __launch_bounds__(32 * PTR_NW) panel_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                                 double2* panels, const double2* __restrict__ img,
+                                                                 int64_t img_stride) {
+  __shared__ __align__(16) double2 Bs[PIV_IMG];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int32_t f = tasks[3 * blockIdx.x];
+  const int i0 = tasks[3 * blockIdx.x + 1];
+  const int64_t off = tasks[3 * blockIdx.x + 2];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q, PT = (p + 7) >> 3;
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    const uint32_t bytes = 16u * 64u * (uint32_t)(PT * (PT + 1) / 2);
+    mbar_arrive_expect_tx(&bar, bytes);
+    bulk_g2s(Bs, img + (int64_t)b * img_stride + off, bytes, &bar);
+  }
+  // this warp's 8 rows of A21, all p columns, in the permuted accumulator layout
+  const int r = i0 + 8 * warp + piv_perm8(g);
+  double2 a[PIV_PT][2];
+#pragma unroll
+  for (int j = 0; j < PIV_PT; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 8 * j + t + 4 * h;
+      a[j][h] = (j < PT && r < m && c < p) ? P[r + (int64_t)c * m] : make_double2(0.0, 0.0);
+    }
+  __syncthreads();  // barrier initialized before anyone waits on it
+  mbar_wait(&bar, 0);
+  if (i0 + 8 * warp >= m) return;
+  const double2* B2 = Bs + lane;
+#pragma unroll
+  for (int j = 0; j < PIV_PT; ++j) {
+    if (j < PT) {
+      double cr[2] = {a[j][0].x, a[j][1].x}, ci[2] = {a[j][0].y, a[j][1].y};
+      // A_j - sum_{k<j} X_k (D_k L_jk^T): re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
+#pragma unroll
+      for (int k = 0; k < j; ++k) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const double2 bv = B2[(piv_tp(j, k) * 2 + s) * 32];
+          dmma884(cr[0], cr[1], a[k][s].x, -bv.x);
+          dmma884(cr[0], cr[1], a[k][s].y, bv.y);
+          dmma884(ci[0], ci[1], a[k][s].x, -bv.y);
+          dmma884(ci[0], ci[1], a[k][s].y, -bv.x);
+        }
+      }
+      // X_j = (.) M_j
+      double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double2 mv = B2[(piv_tp(j, j) * 2 + s) * 32];
+        dmma884(xr[0], xr[1], cr[s], mv.x);
+        dmma884(xr[0], xr[1], ci[s], -mv.y);
+        dmma884(xi[0], xi[1], cr[s], mv.y);
+        dmma884(xi[0], xi[1], ci[s], mv.x);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) a[j][h] = make_double2(xr[h], xi[h]);
+    }
+  }
+  if (r < m) {
+#pragma unroll
+    for (int j = 0; j < PIV_PT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * j + t + 4 * h;
+        if (j < PT && c < p) P[r + (int64_t)c * m] = a[j][h];
+      }
+  }
+}
+
 // ---- fused fronts (m <= MS): assemble + factor + Schur complement in one CTA ----
 // The front's lower triangle lives in shared memory in the packed block-column
 // layout of kernels.h (a 128-row front needs 140 KB instead of 260 KB). The
@@ -2132,6 +2303,26 @@ cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t nt
                                double2* panels, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
   big_trsm_kernel<<<dim3(ntasks, batch), TRSM_ROWS, 0, stream>>>(T, tasks, kb, panels);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+                                 double2* panels, double* minpiv, double2* img, int64_t img_stride,
+                                 cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  const int smem = piv_smem_bytes();
+  cudaError_t e = kh_smem_optin((const void*)pivot_block_kernel, smem);
+  if (e != cudaSuccess) return e;
+  pivot_block_kernel<<<dim3(ntasks, batch), 32 * PIV_NW, smem, stream>>>(T, tasks, panels, minpiv, img, img_stride);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_panel_solve(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+                                  double2* panels, const double2* img, int64_t img_stride, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  panel_trsm_kernel<<<dim3(ntasks, batch), 32 * PTR_NW, 0, stream>>>(T, tasks, panels, img, img_stride);
   kh_note_launch();
   return cudaGetLastError();
 }
