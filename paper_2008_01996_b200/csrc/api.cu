@@ -125,8 +125,9 @@ struct kh_plan {
   };
   struct BigLevel {
     int32_t asm_off, asm_n, kb_off, nkb;
-    int32_t piv_off, piv_n, psol_off, psol_n;  // p <= kh_piv_max(): pivot-block and panel-solve tasks
+    int32_t sb_off, nsb;  // 64-pivot super-blocks (sbinfo): pivot block, panel TRSM, panel update
   };
+  std::vector<KbInfo> sbinfo;
   double2* minv = nullptr;     // [max_batch][minv_size]: B images of a level's pivot blocks (pivot_block_kernel)
   int64_t minv_size = 1;
   std::vector<BigLevel> big;
@@ -435,7 +436,7 @@ struct Sched {
   int warp_mt[kSmallClasses] = {};
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
-  std::vector<kh_plan::KbInfo> kbinfo;
+  std::vector<kh_plan::KbInfo> kbinfo, sbinfo;
   int32_t max_p = 0, max_m = 0;
   int64_t minv_size = 1;
 };
@@ -556,8 +557,8 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     X.task_off.push_back((int32_t)(X.tasks.size() / 3));
     kh_plan::BigLevel L{};
     L.asm_off = (int32_t)X.bt.size();
-    // fronts whose pivot block fits the two-launch panel path (KH_PANEL_INV=0: none)
-    auto inv_path = [&](int32_t f) { return panel_inv && S.fronts[f].p <= kh_piv_max(); };
+    // the panel by 64-pivot super-blocks (KH_PANEL_INV=0: the per-32-block chain)
+    auto inv_path = [&](int32_t) { return panel_inv; };
     auto img_tiles = [](int32_t p) { const int64_t pt = (p + 7) / 8; return pt * (pt + 1) / 2; };
     int32_t nkb = 0;
     for (int32_t f : large) {
@@ -576,25 +577,46 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
       if (!inv_path(f)) nkb = std::max(nkb, (F.p + 31) / 32);
     }
     L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 4;
-    {
+    // super-block sbi (pivots c0 = 64 sbi .. c0 + w): pivot block (front, image
+    // offset) -> TRSM of the rows below (front, row, offset) -> right-looking
+    // update of the later pivot columns (front, row tile, column tile)
+    constexpr int32_t SB = kh_piv_max();
+    int32_t nsb = 0;
+    for (int32_t f : large)
+      if (inv_path(f)) nsb = std::max(nsb, (S.fronts[f].p + SB - 1) / SB);
+    L.sb_off = (int32_t)X.sbinfo.size();
+    L.nsb = nsb;
+    for (int32_t sbi = 0; sbi < nsb; ++sbi) {
+      const int32_t c0 = SB * sbi;
+      kh_plan::KbInfo K{};
       int64_t off = 0;
-      L.piv_off = (int32_t)X.bt.size();
+      K.diag_off = (int32_t)X.bt.size();
       for (int32_t f : large)
-        if (inv_path(f)) {
+        if (inv_path(f) && S.fronts[f].p > c0) {
           X.bt.insert(X.bt.end(), {f, (int32_t)off});
-          off += 64 * img_tiles(S.fronts[f].p);
+          off += 64 * img_tiles(std::min(SB, S.fronts[f].p - c0));
         }
-      L.piv_n = ((int32_t)X.bt.size() - L.piv_off) / 2;
+      K.diag_n = ((int32_t)X.bt.size() - K.diag_off) / 2;
       X.minv_size = std::max(X.minv_size, off);
       off = 0;
-      L.psol_off = (int32_t)X.bt.size();
-      for (int32_t f : large)
-        if (inv_path(f)) {
-          const kh::Front& F = S.fronts[f];
-          for (int32_t i0 = F.p; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, (int32_t)off});
-          off += 64 * img_tiles(F.p);
-        }
-      L.psol_n = ((int32_t)X.bt.size() - L.psol_off) / 3;
+      K.trsm_off = (int32_t)X.bt.size();
+      for (int32_t f : large) {
+        const kh::Front& F = S.fronts[f];
+        if (!inv_path(f) || F.p <= c0) continue;
+        const int32_t w = std::min(SB, F.p - c0);
+        for (int32_t i0 = c0 + w; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, (int32_t)off});
+        off += 64 * img_tiles(w);
+      }
+      K.trsm_n = ((int32_t)X.bt.size() - K.trsm_off) / 3;
+      K.lupd_off = (int32_t)X.bt.size();
+      for (int32_t f : large) {
+        const kh::Front& F = S.fronts[f];
+        if (!inv_path(f) || F.p <= c0 + SB) continue;
+        for (int32_t j0 = c0 + SB; j0 < F.p; j0 += 64)
+          for (int32_t i0 = j0; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, j0});
+      }
+      K.lupd_n = ((int32_t)X.bt.size() - K.lupd_off) / 3;
+      X.sbinfo.push_back(K);
     }
     L.kb_off = (int32_t)X.kbinfo.size();
     L.nkb = nkb;
@@ -735,6 +757,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
   p->big = X.big;
   p->kbinfo = X.kbinfo;
+  p->sbinfo = X.sbinfo;
   p->minv_size = X.minv_size;
   Carver measure;
   carve(p, S, X, measure);
@@ -840,9 +863,14 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
     }
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
-    KH_CUDA(kh_launch_pivot_block(T, p->btasks + B.piv_off, B.piv_n, ns, panels, p->minpiv_work, p->minv,
-                                  p->minv_size, st));
-    KH_CUDA(kh_launch_panel_solve(T, p->btasks + B.psol_off, B.psol_n, ns, panels, p->minv, p->minv_size, st));
+    for (int32_t sbi = 0; sbi < B.nsb; ++sbi) {
+      const kh_plan::KbInfo& K = p->sbinfo[B.sb_off + sbi];
+      const int c0 = kh_piv_max() * sbi;
+      KH_CUDA(kh_launch_pivot_block(T, p->btasks + K.diag_off, K.diag_n, c0, ns, panels, p->minpiv_work, p->minv,
+                                    p->minv_size, st));
+      KH_CUDA(kh_launch_panel_solve(T, p->btasks + K.trsm_off, K.trsm_n, c0, ns, panels, p->minv, p->minv_size, st));
+      KH_CUDA(kh_launch_panel_update(T, p->btasks + K.lupd_off, K.lupd_n, c0, ns, panels, st));
+    }
     for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
       const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
       const int kb = 32 * kbi;

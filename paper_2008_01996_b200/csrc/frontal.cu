@@ -882,8 +882,8 @@ KH_DEV int piv_perm8(int g) { return (g >> 1) + 4 * (g & 1); }  // phys -> logic
 KH_HD constexpr int piv_tp(int j, int k) { return j * (j + 1) / 2 + k; }
 
 __global__ void __launch_bounds__(32 * PIV_NW) pivot_block_kernel(KhTree T, const int32_t* __restrict__ tasks,
-                                                                  double2* panels, double* minpiv, double2* img,
-                                                                  int64_t img_stride) {
+                                                                  int c0, double2* panels, double* minpiv,
+                                                                  double2* img, int64_t img_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* S = reinterpret_cast<double2*>(smem_raw);  // packed p x p (L11, D)
   double2* W = S + kh_packed_elems(PIV_MAX);
@@ -898,9 +898,10 @@ __global__ void __launch_bounds__(32 * PIV_NW) pivot_block_kernel(KhTree T, cons
   const int64_t off = tasks[2 * blockIdx.x + 1];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, PT = (p + 7) >> 3;
-  KH_ASSERT(p <= PIV_MAX);
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  const int m = F.p + F.q;
+  const int p = min(PIV_MAX, F.p - c0), PT = (p + 7) >> 3;  // this super-block's pivots
+  // the super-block's diagonal block at (c0, c0): P[r + c m] below is entry (c0 + r, c0 + c)
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off + c0 + (int64_t)c0 * m;
   for (int c = tid; c < p; c += NTH) cb[c] = kh_packed_col_base(p, c);
   __syncthreads();
   for (int e = tid; e < p * p; e += NTH) {
@@ -951,13 +952,16 @@ __global__ void __launch_bounds__(32 * PIV_NW) pivot_block_kernel(KhTree T, cons
     }
     im[e] = v;
   }
-  if (tid == 0) minpiv[(int64_t)b * T.nf + f] = minp;
+  if (tid == 0) {
+    double* mp = minpiv + (int64_t)b * T.nf + f;
+    *mp = c0 == 0 ? minp : fmin(*mp, minp);
+  }
 }
 
 constexpr int PTR_NW = 8;  // warps (8-row slabs) per panel_trsm CTA
 __global__ void __launch_bounds__(32 * PTR_NW) panel_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks,
-                                                                 double2* panels, const double2* __restrict__ img,
-                                                                 int64_t img_stride) {
+                                                                 int c0, double2* panels,
+                                                                 const double2* __restrict__ img, int64_t img_stride) {
   __shared__ __align__(16) double2 Bs[PIV_IMG];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -967,8 +971,10 @@ __global__ void __launch_bounds__(32 * PTR_NW) panel_trsm_kernel(KhTree T, const
   const int64_t off = tasks[3 * blockIdx.x + 2];
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, PT = (p + 7) >> 3;
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  const int m = F.p + F.q;
+  const int p = min(PIV_MAX, F.p - c0), PT = (p + 7) >> 3;  // this super-block's pivots
+  // columns c0 .. c0 + p of the panel (rows keep their front numbering)
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off + (int64_t)c0 * m;
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_fence_init();
@@ -1029,6 +1035,35 @@ __global__ void __launch_bounds__(32 * PTR_NW) panel_trsm_kernel(KhTree T, const
         if (j < PT && c < p) P[r + (int64_t)c * m] = a[j][h];
       }
   }
+}
+
+// Right-looking update of the pivot columns after a super-block: for the 64 x 64
+// tile (i0, j0) of the panel (j0 >= c0 + 64, rows i0.. >= j0, columns j0..< p),
+// P[r][c] -= sum_{c0 <= k < c0 + 64} L[r][k] d_k L[c][k].
+__global__ void __launch_bounds__(NT, KH_SCHUR_MINB) panel_update_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                                        int c0, double2* panels) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
+  const int32_t f = tasks[3 * blockIdx.x];
+  const int i0 = tasks[3 * blockIdx.x + 1], j0 = tasks[3 * blockIdx.x + 2];
+  const int b = blockIdx.y;
+  const KhDevFront F = T.fronts[f];
+  const int p = F.p, m = p + F.q;
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  const int wrp = threadIdx.x >> 5, r0w = i0 + (wrp & 1) * 32, c0w = j0 + (wrp >> 1) * 16;
+  const bool idle = c0w > r0w + 31 || r0w >= m || c0w >= p;
+  Acc acc;
+  __shared__ __align__(8) uint64_t bars[CP_STAGES];
+  const int64_t kc = (int64_t)c0 * m;
+  tile_mma_cp<4, MODE_SCALED>(acc, PIV_MAX, P + i0 + kc, m, m - i0, P + j0 + kc, m, p - j0, P + c0 + kc, m + 1, st,
+                              idle, bars);
+  tile_epilogue(acc, [&](int i, int j, double2 v) {
+    const int r = i0 + i, c = j0 + j;
+    if (r < m && c < p && r >= c) {
+      double2* d = P + r + (int64_t)c * m;
+      *d = csub(*d, v);
+    }
+  });
 }
 
 // ---- fused fronts (m <= MS): assemble + factor + Schur complement in one CTA ----
@@ -2307,22 +2342,34 @@ cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t nt
   return cudaGetLastError();
 }
 
-cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                  double2* panels, double* minpiv, double2* img, int64_t img_stride,
                                  cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
   const int smem = piv_smem_bytes();
   cudaError_t e = kh_smem_optin((const void*)pivot_block_kernel, smem);
   if (e != cudaSuccess) return e;
-  pivot_block_kernel<<<dim3(ntasks, batch), 32 * PIV_NW, smem, stream>>>(T, tasks, panels, minpiv, img, img_stride);
+  pivot_block_kernel<<<dim3(ntasks, batch), 32 * PIV_NW, smem, stream>>>(T, tasks, c0, panels, minpiv, img,
+                                                                         img_stride);
   kh_note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t kh_launch_panel_solve(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+cudaError_t kh_launch_panel_solve(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                   double2* panels, const double2* img, int64_t img_stride, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  panel_trsm_kernel<<<dim3(ntasks, batch), 32 * PTR_NW, 0, stream>>>(T, tasks, panels, img, img_stride);
+  panel_trsm_kernel<<<dim3(ntasks, batch), 32 * PTR_NW, 0, stream>>>(T, tasks, c0, panels, img, img_stride);
+  kh_note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t kh_launch_panel_update(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
+                                   double2* panels, cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  const int smem = (int)(CP_STAGES * sizeof(CpStage));
+  cudaError_t e = kh_smem_optin((const void*)panel_update_kernel, smem);
+  if (e != cudaSuccess) return e;
+  panel_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, c0, panels);
   kh_note_launch();
   return cudaGetLastError();
 }

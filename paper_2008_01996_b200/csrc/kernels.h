@@ -162,15 +162,18 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
                                    const double2* upd_child, int64_t upd_stride_child, double* minpiv,
                                    cudaStream_t stream, const KhFwd* fwd = nullptr);
 
-// Large fronts with p <= 64 (frontal.cu): pivot-block LDL^T writing the block's
-// DMMA B image (tasks: front, scratch offset), then the blocked TRSM
-// L21 = A21 L11^-T D^-1 by 8-row warps (tasks: front, row, offset).
+// Large fronts (frontal.cu), per 64-pivot super-block at column c0: pivot-block
+// LDL^T writing the block's DMMA B image (tasks: front, scratch offset), the
+// blocked TRSM of the rows below by 8-row warps (tasks: front, row, offset),
+// the right-looking update of the later pivot columns (tasks: front, row, col).
 constexpr int kh_piv_max() { return 64; }
-cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                  double2* panels, double* minpiv, double2* img, int64_t img_stride,
                                  cudaStream_t stream);
-cudaError_t kh_launch_panel_solve(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
+cudaError_t kh_launch_panel_solve(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                   double2* panels, const double2* img, int64_t img_stride, cudaStream_t stream);
+cudaError_t kh_launch_panel_update(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
+                                   double2* panels, cudaStream_t stream);
 // Register-resident warp-per-(front, shift) factorization of the fronts with
 // m <= 8 mt (warpfront.cu; mt = 4, 5 or 6): wdst[e] is the slot of original e
 // in the CTA's dense originals image (kh_warp_front_slot).
