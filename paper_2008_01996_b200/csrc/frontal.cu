@@ -346,8 +346,6 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
   const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* U = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   load_kids(T, F, upd_child, upd_stride_child, b, kids);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3, wi = warp & 1, wj = warp >> 1;
   Acc acc;
   // warps whose 32 x 16 sub-tile lies strictly above the diagonal (diagonal
   // tiles) or beyond row/column q skip their MMAs
@@ -355,54 +353,41 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
   const bool idle = c0w > r0w + 31 || r0w >= q || c0w >= q;
   __shared__ __align__(8) uint64_t bars[CP_STAGES];
   tile_mma_cp<4, MODE_SCALED>(acc, p, P + p + i0, m, q - i0, P + p + j0, m, q - j0, P, m + 1, st, idle, bars);
-  __syncthreads();  // kids visible even when p = 0
-  // epilogue: this thread's 16 tile entries (rows wi*32+mt*8+g, cols
-  // wj*16+nt*8+2t+h), in two halves of rows to bound register pressure;
-  // children pulled in order (deterministic sums)
+  // epilogue: the product goes to shared memory (the operand ring is free:
+  // tile_mma_cp ends on a barrier after its last chunk), then the CTA pulls the
+  // children's extend-add column by column -- a warp covers 32 consecutive
+  // rows of one tile column, so both the child reads (rows of a child column
+  // stay in order under cmap) and the U writes are coalesced; children in
+  // order (deterministic sums)
+  double2* Ct = reinterpret_cast<double2*>(smem_raw);  // [64 columns][TB + 1]
+  tile_epilogue(acc, [&](int i, int j, double2 v) { Ct[j * (TB + 1) + i] = v; });
+  __syncthreads();  // kids visible even when p = 0; the product tile complete
+  // thread: tile row i (fixed), columns jb, jb + 4, ..., jb + 60
+  const int i = threadIdx.x & (TB - 1), jb = threadIdx.x >> 6;
+  const int r = i0 + i;
+  double2 v[TB / 4];
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    double2 cacc[2][2][2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) cacc[a][nt][h] = make_double2(0.0, 0.0);
+  for (int u = 0; u < TB / 4; ++u) v[u] = make_double2(0.0, 0.0);
+  if (r < q) {
     for (int k = 0; k < kids.n; ++k) {
       const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-      int ri[2], cj[2][2];
+      const int ci = C.cmap[p + r];
+      if (ci < 0) continue;
+      int cj[TB / 4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int r = i0 + wi * 32 + (2 * half + a) * 8 + g;
-        ri[a] = r < q ? C.cmap[p + r] : -1;
+      for (int u = 0; u < TB / 4; ++u) {
+        const int c = j0 + jb + 4 * u;
+        cj[u] = c <= r ? C.cmap[p + c] : -1;
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = j0 + wj * 16 + nt * 8 + 2 * t + h;
-          cj[nt][h] = c < q ? C.cmap[p + c] : -1;
-        }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (ri[a] >= 0 && cj[nt][h] >= 0)
-              cacc[a][nt][h] = cadd(cacc[a][nt][h], C.U[kh_upk(C.q, ri[a], cj[nt][h])]);
+      for (int u = 0; u < TB / 4; ++u)
+        if (cj[u] >= 0) v[u] = cadd(v[u], C.U[kh_upk32(C.q, ci, cj[u])]);
     }
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int mt = 2 * half + a;
-          const int r = i0 + wi * 32 + mt * 8 + g, c = j0 + wj * 16 + nt * 8 + 2 * t + h;
-          if (r < q && c < q && r >= c)
-            U[kh_upk(q, r, c)] = csub(cacc[a][nt][h], make_double2(acc.r[mt][nt][h], acc.i[mt][nt][h]));
-        }
+    for (int u = 0; u < TB / 4; ++u) {
+      const int j = jb + 4 * u, c = j0 + j;
+      if (c <= r) U[kh_upk32(q, r, c)] = csub(v[u], Ct[j * (TB + 1) + i]);
+    }
   }
 }
 
@@ -453,7 +438,7 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
     for (int u = 0; u < ASM_CHUNK / NT; ++u) {
       if (idx0 + tid + u * NT < total && rr[u] >= cc[u]) {
         const int ci = C.cmap[rr[u]], cj = C.cmap[cc[u]];
-        if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[kh_upk(C.q, ci, cj)]);
+        if (ci >= 0 && cj >= 0) v[u] = cadd(v[u], C.U[kh_upk32(C.q, ci, cj)]);
       }
     }
   }
@@ -1265,7 +1250,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
         for (int u = 0; u < R; ++u) {
           const int ci = cj + lane + 32 * u;
           const bool ok = cj < qk && ci < qk;
-          v[h][u] = ok ? Uc[kh_upk(qk, ci, cj)] : make_double2(0.0, 0.0);
+          v[h][u] = ok ? Uc[kh_upk32(qk, ci, cj)] : make_double2(0.0, 0.0);
           dst[h][u] = ok ? base + rk[ci] : -1;
         }
       }
@@ -1348,7 +1333,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
       } else {
         const int cc = c - p;
         src = S + cb[c] + c;
-        dst = U + kh_upk(q, cc, cc);
+        dst = U + kh_upk32(q, cc, cc);
         rows = q - cc;
       }
       const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(src));
@@ -1366,7 +1351,7 @@ __global__ void __launch_bounds__(32 * NW, front_min_blocks(MS, NW)) factor_fron
   }
   for (int c = warp; c < q; c += NW) {
     const int base = cb[p + c] + p;
-    for (int r = c + lane; r < q; r += 32) U[kh_upk(q, r, c)] = S[base + r];
+    for (int r = c + lane; r < q; r += 32) U[kh_upk32(q, r, c)] = S[base + r];
   }
 #endif
   if (FWD) {

@@ -19,6 +19,8 @@ struct KhDevFront {
 // the q x q block column by column, entry (i, j), i >= j, at kh_upk(q, i, j)
 // (one contiguous q(q+1)/2 array per front: a single bulk copy moves it).
 __host__ __device__ inline int64_t kh_upk(int q, int i, int j) { return i + (int64_t)j * (2 * q - j - 1) / 2; }
+// 32-bit form for q < 46341 (every front here; kh_analyze caps local offsets at 2^31)
+__host__ __device__ inline int kh_upk32(int q, int i, int j) { return i + j * (2 * q - j - 1) / 2; }
 
 // Packed block-column layout of a fused front (m <= 128) in shared memory:
 // the 8-column block b stores rows 8b..m-1 with leading dimension

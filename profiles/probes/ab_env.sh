@@ -1,5 +1,5 @@
-# bench A/B over an environment switch: bash profiles/probes/ab_env.sh VAR "v1 v2 ..."
-for v in $2; do
-  env $1=$v python bench.py --no-cpu-baseline --no-e2e > gpurun_out/ab.log 2>&1
-  python -c "import json,sys;d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]);print(sys.argv[1], d['ms_per_step'], d['roofline']['ms_per_step'], d['residual'])" "$1=$v"
+# A/B of env knobs on the c3 bench: bash profiles/probes/ab_env.sh "VAR=a VAR2=b" "VAR=c" ...
+for cfg in "$@"; do
+  env $cfg timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/ab.log 2>&1
+  tail -n 1 gpurun_out/ab.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$cfg', round(d['ms_per_step'],2), round(r['ms_per_step'],2), round(r['frac'],3), [round(l['ms'],3) for l in r['levels']])" || tail -n 3 gpurun_out/ab.log
 done
