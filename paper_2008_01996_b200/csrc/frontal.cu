@@ -860,7 +860,10 @@ __global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const 
 //     (g, t) holds logical rows pi(g), columns t and t + 4 of every tile, so
 //     a finished X_k is directly an A fragment) and the B image staged in
 //     shared memory by one bulk copy.
-constexpr int PIV_MAX = 64, PIV_NW = 4, PIV_LD = PIV_MAX + 2, PIV_PT = PIV_MAX / 8;
+#ifndef KH_PIV_NW
+#define KH_PIV_NW 4
+#endif
+constexpr int PIV_MAX = 64, PIV_NW = KH_PIV_NW, PIV_LD = PIV_MAX + 2, PIV_PT = PIV_MAX / 8;
 constexpr int PIV_IMG = 64 * PIV_PT * (PIV_PT + 1) / 2;  // B image entries (double2) at p = PIV_MAX
 KH_HD constexpr int piv_smem_bytes() { return 16 * (kh_packed_elems(PIV_MAX) + 8 * PIV_LD + 8 + PIV_MAX + 64 * PIV_PT) + 4 * PIV_MAX; }
 KH_DEV int piv_perm8(int g) { return (g >> 1) + 4 * (g & 1); }  // phys -> logical inside an 8-block
@@ -894,7 +897,7 @@ __global__ void __launch_bounds__(32 * PIV_NW) pivot_block_kernel(KhTree T, cons
     if (r >= c) S[cb[c] + r] = P[r + (int64_t)c * m];
   }
   __syncthreads();
-  const double minp = blocked_ldlt<PIV_NW, false>(S, cb, W, PIV_LD, dinv, dg, &ctr, p, p);
+  const double minp = blocked_ldlt<PIV_NW, kLookAhead(PIV_NW)>(S, cb, W, PIV_LD, dinv, dg, &ctr, p, p);
   for (int e = tid; e < p * p; e += NTH) {
     const int c = e / p, r = e - c * p;
     if (r >= c) P[r + (int64_t)c * m] = S[cb[c] + r];
