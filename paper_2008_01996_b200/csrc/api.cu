@@ -120,18 +120,17 @@ struct kh_plan {
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   // large-front schedule: per level an assembly list and per 32-wide pivot
   // block the diag / left-looking / TRSM lists (offsets into btasks, int32s)
-  struct KbInfo {
-    int32_t diag_off, diag_n, lupd_off, lupd_n, trsm_off, trsm_n;
+  struct SuperBlock {  // one 64-pivot super-block of a level's large fronts: task lists in btasks
+    int32_t piv_off, piv_n, trsm_off, trsm_n, upd_off, upd_n;
   };
   struct BigLevel {
-    int32_t asm_off, asm_n, kb_off, nkb;
+    int32_t asm_off, asm_n;
     int32_t sb_off, nsb;  // 64-pivot super-blocks (sbinfo): pivot block, panel TRSM, panel update
   };
-  std::vector<KbInfo> sbinfo;
+  std::vector<SuperBlock> sbinfo;
   double2* minv = nullptr;     // [max_batch][minv_size]: B images of a level's pivot blocks (pivot_block_kernel)
   int64_t minv_size = 1;
   std::vector<BigLevel> big;
-  std::vector<KbInfo> kbinfo;
   int32_t* btasks = nullptr;
   char* owned = nullptr;           // workspace allocated by the plan (null if caller-provided)
   // side streams: the fused-front kernels of a level run there (one stream
@@ -436,7 +435,7 @@ struct Sched {
   int warp_mt[kSmallClasses] = {};
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
-  std::vector<kh_plan::KbInfo> kbinfo, sbinfo;
+  std::vector<kh_plan::SuperBlock> sbinfo;
   int32_t max_p = 0, max_m = 0;
   int64_t minv_size = 1;
 };
@@ -468,9 +467,6 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   // (0 disables them, for A/B measurements)
   int small_max = 128;
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
-  // large fronts with p <= kh_piv_max() take the pivot-block + panel-solve path
-  bool panel_inv = true;
-  if (const char* env = std::getenv("KH_PANEL_INV")) panel_inv = std::atoi(env) != 0;
   auto front_class = [&](int32_t m) {
     for (int c = 0; c < kSmallClasses; ++c)
       if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
@@ -557,10 +553,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     X.task_off.push_back((int32_t)(X.tasks.size() / 3));
     kh_plan::BigLevel L{};
     L.asm_off = (int32_t)X.bt.size();
-    // the panel by 64-pivot super-blocks (KH_PANEL_INV=0: the per-32-block chain)
-    auto inv_path = [&](int32_t) { return panel_inv; };
     auto img_tiles = [](int32_t p) { const int64_t pt = (p + 7) / 8; return pt * (pt + 1) / 2; };
-    int32_t nkb = 0;
     for (int32_t f : large) {
       const kh::Front& F = S.fronts[f];
       // (front, chunk start, originals range of the chunk): the originals of
@@ -574,7 +567,6 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
         while (e < F.orig_end && S.orig_dst[e] < end) ++e;
         X.bt.insert(X.bt.end(), {f, idx0, (int32_t)lo, (int32_t)e});
       }
-      if (!inv_path(f)) nkb = std::max(nkb, (F.p + 31) / 32);
     }
     L.asm_n = ((int32_t)X.bt.size() - L.asm_off) / 4;
     // super-block sbi (pivots c0 = 64 sbi .. c0 + w): pivot block (front, image
@@ -583,67 +575,40 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     constexpr int32_t SB = kh_piv_max();
     int32_t nsb = 0;
     for (int32_t f : large)
-      if (inv_path(f)) nsb = std::max(nsb, (S.fronts[f].p + SB - 1) / SB);
+      nsb = std::max(nsb, (S.fronts[f].p + SB - 1) / SB);
     L.sb_off = (int32_t)X.sbinfo.size();
     L.nsb = nsb;
     for (int32_t sbi = 0; sbi < nsb; ++sbi) {
       const int32_t c0 = SB * sbi;
-      kh_plan::KbInfo K{};
+      kh_plan::SuperBlock K{};
       int64_t off = 0;
-      K.diag_off = (int32_t)X.bt.size();
+      K.piv_off = (int32_t)X.bt.size();
       for (int32_t f : large)
-        if (inv_path(f) && S.fronts[f].p > c0) {
+        if (S.fronts[f].p > c0) {
           X.bt.insert(X.bt.end(), {f, (int32_t)off});
           off += 64 * img_tiles(std::min(SB, S.fronts[f].p - c0));
         }
-      K.diag_n = ((int32_t)X.bt.size() - K.diag_off) / 2;
+      K.piv_n = ((int32_t)X.bt.size() - K.piv_off) / 2;
       X.minv_size = std::max(X.minv_size, off);
       off = 0;
       K.trsm_off = (int32_t)X.bt.size();
       for (int32_t f : large) {
         const kh::Front& F = S.fronts[f];
-        if (!inv_path(f) || F.p <= c0) continue;
+        if (F.p <= c0) continue;
         const int32_t w = std::min(SB, F.p - c0);
         for (int32_t i0 = c0 + w; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, (int32_t)off});
         off += 64 * img_tiles(w);
       }
       K.trsm_n = ((int32_t)X.bt.size() - K.trsm_off) / 3;
-      K.lupd_off = (int32_t)X.bt.size();
+      K.upd_off = (int32_t)X.bt.size();
       for (int32_t f : large) {
         const kh::Front& F = S.fronts[f];
-        if (!inv_path(f) || F.p <= c0 + SB) continue;
+        if (F.p <= c0 + SB) continue;
         for (int32_t j0 = c0 + SB; j0 < F.p; j0 += 64)
           for (int32_t i0 = j0; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0, j0});
       }
-      K.lupd_n = ((int32_t)X.bt.size() - K.lupd_off) / 3;
+      K.upd_n = ((int32_t)X.bt.size() - K.upd_off) / 3;
       X.sbinfo.push_back(K);
-    }
-    L.kb_off = (int32_t)X.kbinfo.size();
-    L.nkb = nkb;
-    for (int32_t kbi = 0; kbi < nkb; ++kbi) {
-      const int32_t kb = 32 * kbi;
-      kh_plan::KbInfo K{};
-      K.diag_off = (int32_t)X.bt.size();
-      for (int32_t f : large)
-        if (S.fronts[f].p > kb && !inv_path(f)) X.bt.push_back(f);
-      K.diag_n = (int32_t)X.bt.size() - K.diag_off;
-      K.lupd_off = (int32_t)X.bt.size();
-      if (kb > 0)
-        for (int32_t f : large) {
-          const kh::Front& F = S.fronts[f];
-          if (F.p <= kb || inv_path(f)) continue;
-          for (int32_t i0 = (kb / 64) * 64; i0 < F.m(); i0 += 64) X.bt.insert(X.bt.end(), {f, i0});
-        }
-      K.lupd_n = ((int32_t)X.bt.size() - K.lupd_off) / 2;
-      K.trsm_off = (int32_t)X.bt.size();
-      for (int32_t f : large) {
-        const kh::Front& F = S.fronts[f];
-        if (F.p <= kb || inv_path(f)) continue;
-        const int32_t start = kb + std::min(32, F.p - kb);
-        for (int32_t i0 = start; i0 < F.m(); i0 += KH_TRSM_ROWS) X.bt.insert(X.bt.end(), {f, i0});
-      }
-      K.trsm_n = ((int32_t)X.bt.size() - K.trsm_off) / 2;
-      X.kbinfo.push_back(K);
     }
     X.big.push_back(L);
   }
@@ -756,7 +721,6 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->mid_m_max = X.mid_m_max;
   for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
   p->big = X.big;
-  p->kbinfo = X.kbinfo;
   p->sbinfo = X.sbinfo;
   p->minv_size = X.minv_size;
   Carver measure;
@@ -864,19 +828,12 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
     const kh_plan::BigLevel& B = p->big[d];
     KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
     for (int32_t sbi = 0; sbi < B.nsb; ++sbi) {
-      const kh_plan::KbInfo& K = p->sbinfo[B.sb_off + sbi];
+      const kh_plan::SuperBlock& K = p->sbinfo[B.sb_off + sbi];
       const int c0 = kh_piv_max() * sbi;
-      KH_CUDA(kh_launch_pivot_block(T, p->btasks + K.diag_off, K.diag_n, c0, ns, panels, p->minpiv_work, p->minv,
+      KH_CUDA(kh_launch_pivot_block(T, p->btasks + K.piv_off, K.piv_n, c0, ns, panels, p->minpiv_work, p->minv,
                                     p->minv_size, st));
       KH_CUDA(kh_launch_panel_solve(T, p->btasks + K.trsm_off, K.trsm_n, c0, ns, panels, p->minv, p->minv_size, st));
-      KH_CUDA(kh_launch_panel_update(T, p->btasks + K.lupd_off, K.lupd_n, c0, ns, panels, st));
-    }
-    for (int32_t kbi = 0; kbi < B.nkb; ++kbi) {
-      const kh_plan::KbInfo& K = p->kbinfo[B.kb_off + kbi];
-      const int kb = 32 * kbi;
-      if (kb > 0) KH_CUDA(kh_launch_big_lupdate(T, p->btasks + K.lupd_off, K.lupd_n, kb, ns, panels, st));
-      KH_CUDA(kh_launch_big_diag(T, p->btasks + K.diag_off, K.diag_n, kb, ns, panels, p->minpiv_work, st));
-      KH_CUDA(kh_launch_big_trsm(T, p->btasks + K.trsm_off, K.trsm_n, kb, ns, panels, st));
+      KH_CUDA(kh_launch_panel_update(T, p->btasks + K.upd_off, K.upd_n, c0, ns, panels, st));
     }
     if (fwd) {  // the level's large fronts: panels are final after their trsm;
                 // their forward sweep runs on a side stream beside the Schur kernel

@@ -458,70 +458,6 @@ __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_
   }
 }
 
-__global__ void __launch_bounds__(128) big_lupdate_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
-                                                          double2* panels) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  CpStage* st = reinterpret_cast<CpStage*>(smem_raw);
-  const int32_t f = tasks[2 * blockIdx.x];
-  const int i0 = tasks[2 * blockIdx.x + 1];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  Acc acc;
-  // warps whose 32 rows all lie above the block (r < kb) or past m skip their MMAs
-  const int r0w = i0 + ((threadIdx.x >> 5) & 1) * 32;
-  const bool idle = r0w + 31 < kb || r0w >= m;
-  __shared__ __align__(8) uint64_t bars[CP_STAGES];
-  tile_mma_cp<2, MODE_SCALED>(acc, kb, P + i0, m, m - i0, P + kb, m, w, P, m + 1, st, idle, bars);
-  tile_epilogue(acc, [&](int i, int j, double2 v) {
-    const int r = i0 + i, c = kb + j;
-    if (r < m && j < w && r >= c) {
-      double2* d = P + r + (int64_t)c * m;
-      *d = csub(*d, v);
-    }
-  });
-}
-
-// Rows below the factored diagonal block: one thread per row r solves
-// v_j = a_rj - sum_{k<j} v_k L[kb+j][kb+k], L[r][kb+j] = v_j / d_j (the
-// block L and 1/d staged in shared memory, read as broadcasts).
-constexpr int TRSM_ROWS = KH_TRSM_ROWS;
-__global__ void __launch_bounds__(TRSM_ROWS) big_trsm_kernel(KhTree T, const int32_t* __restrict__ tasks, int kb,
-                                                             double2* panels) {
-  __shared__ double2 sL[NB][NB + 1];
-  __shared__ double2 sdi[NB];
-  const int32_t f = tasks[2 * blockIdx.x];
-  const int i0 = tasks[2 * blockIdx.x + 1];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
-  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  const double2* Bk = P + kb + (int64_t)kb * m;
-  for (int e = threadIdx.x; e < NB * NB; e += TRSM_ROWS) {
-    const int r = e % NB, c = e / NB;
-    sL[r][c] = (r < w && c < r) ? Bk[r + (int64_t)c * m] : make_double2(0.0, 0.0);
-  }
-  if (threadIdx.x < NB) sdi[threadIdx.x] = threadIdx.x < w ? cinv(Bk[threadIdx.x * (int64_t)(m + 1)]) : make_double2(0.0, 0.0);
-  __syncthreads();
-  const int r = i0 + threadIdx.x;
-  if (r < kb + w || r >= m) return;
-  double2* row = P + r + (int64_t)kb * m;
-  double2 v[NB];
-#pragma unroll
-  for (int jj = 0; jj < NB; ++jj) v[jj] = jj < w ? row[(int64_t)jj * m] : make_double2(0.0, 0.0);
-#pragma unroll
-  for (int jj = 1; jj < NB; ++jj) {
-    double2 x = v[jj];
-#pragma unroll
-    for (int k = 0; k < jj; ++k) x = cfms(x, v[k], sL[jj][k]);
-    v[jj] = x;
-  }
-#pragma unroll
-  for (int jj = 0; jj < NB; ++jj)
-    if (jj < w) row[(int64_t)jj * m] = cmul(v[jj], sdi[jj]);
-}
-
 // Lower-triangle tile index -> (bi, bj), bj <= bi, tiles numbered row by row.
 KH_DEV void tri_index(int t, int& bi, int& bj) {
   int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
@@ -806,43 +742,6 @@ KH_DEV double blocked_ldlt(double2* S, const int32_t* cb, double2* W, int ldw, d
     sub(6);
   }
   return minp < 0.0 ? -1.0 : sqrt(minp);  // min |d|
-}
-
-// LDL^T of the w x w diagonal block at kb of a large front: one 64-thread CTA
-// per (front, shift), the block staged in shared memory and factored by
-// blocked_ldlt (8-pivot blocks, DMMA trailing updates).
-#ifndef KH_DIAG_NW
-#define KH_DIAG_NW 2
-#endif
-constexpr int DIAG_NW = KH_DIAG_NW, DIAG_LD = NB + 2;
-__global__ void __launch_bounds__(32 * DIAG_NW) big_diag_kernel(KhTree T, const int32_t* __restrict__ fronts,
-                                                                int nfr, int kb, double2* panels, double* minpiv) {
-  __shared__ double2 S[NB * DIAG_LD];
-  __shared__ double2 W[8 * DIAG_LD];
-  __shared__ double2 dinv[8];
-  __shared__ int32_t cb[NB];
-  __shared__ double2 dg[NB];
-  __shared__ int ctr;
-  if (threadIdx.x < NB) cb[threadIdx.x] = threadIdx.x * DIAG_LD;
-  const int32_t f = fronts[blockIdx.x];
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[f];
-  const int p = F.p, m = p + F.q, w = min(NB, p - kb);
-  double2* B = panels + (int64_t)b * T.panel_total + F.panel_off + kb + (int64_t)kb * m;
-  for (int e = threadIdx.x; e < w * w; e += 32 * DIAG_NW) {
-    const int c = e / w, r = e - c * w;
-    if (r >= c) S[c * DIAG_LD + r] = B[r + (int64_t)c * m];
-  }
-  __syncthreads();
-  const double minp = blocked_ldlt<DIAG_NW, false>(S, cb, W, DIAG_LD, dinv, dg, &ctr, w, w);
-  for (int e = threadIdx.x; e < w * w; e += 32 * DIAG_NW) {
-    const int c = e / w, r = e - c * w;
-    if (r >= c) B[r + (int64_t)c * m] = S[c * DIAG_LD + r];
-  }
-  if (threadIdx.x == 0) {
-    double* mp = minpiv + (int64_t)b * T.nf + f;
-    *mp = kb == 0 ? minp : fmin(*mp, minp);
-  }
 }
 
 // ---- large fronts with p <= PIV_MAX: two launches for the whole panel ----------
@@ -1589,193 +1488,9 @@ __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t*
 
 // ---- warp-per-front solves for fronts with m <= 64 ------------------------------
 // Lane l owns front rows l and l + 32. No block barriers: pivots are broadcast
-// with shuffles. The panel is streamed in chunks of 8 columns loaded into
-// registers before use (the first chunk while the rhs is gathered), so the
-// loads of a chunk are in flight together instead of one round trip per column.
+// with shuffles.
 constexpr int SOLVE_CH = 8;   // columns per warp_sum8 reduction (bwd)
-#ifndef KH_FWD_CH
-#define KH_FWD_CH 4
-#endif
-constexpr int FWD_CH = KH_FWD_CH;
-#ifndef KH_BWD_L11
-#define KH_BWD_L11 16
-#endif
-constexpr int BWD_L11 = KH_BWD_L11;  // bwd_small stages L11 in shared memory for p <= this
-// resident 256-thread CTAs per SM the warp-per-front solves are compiled for
-// (register caps: 4 -> 64 registers, 3 -> 80, 2 -> 128)
-#ifndef KH_FWD_SOLVE_MINB
-#define KH_FWD_SOLVE_MINB 4
-#endif
-#ifndef KH_BWD_SOLVE_MINB
-#define KH_BWD_SOLVE_MINB 4
-#endif
 
-__global__ void __launch_bounds__(256, KH_FWD_SOLVE_MINB) fwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
-                                                        const double2* __restrict__ panels, double2* y, double2* ru_cur,
-                                                        int64_t ru_stride_cur, const double2* __restrict__ ru_child,
-                                                        int64_t ru_stride_child) {
-  const int lane = threadIdx.x & 31;
-  const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (idx >= nlev) return;
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[level_fronts[idx]];
-  const int p = F.p, q = F.q, m = p + q;
-  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* yy = y + (int64_t)b * T.n + F.first;
-  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
-  const int r0 = lane, r1 = lane + 32;
-  const double2 z = make_double2(0.0, 0.0);
-  auto load_chunk = [&](int k0, double2* c0, double2* c1) {
-#pragma unroll
-    for (int u = 0; u < FWD_CH; ++u) {
-      const int k = k0 + u;
-      c0[u] = (k < p && r0 > k && r0 < m) ? P[r0 + (int64_t)k * m] : z;
-      c1[u] = (k < p && r1 > k && r1 < m) ? P[r1 + (int64_t)k * m] : z;
-    }
-  };
-  double2 a0[FWD_CH], a1[FWD_CH];
-  load_chunk(0, a0, a1);  // first panel chunk streams in during the rhs gather
-  double2 x0 = z, x1 = z;
-  for (int c = F.child_begin; c < F.child_end; ++c) {
-    const KhDevFront C = T.fronts[T.child_list[c]];
-    const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
-    const int32_t* cm = T.cmap + C.cmap_begin;
-    const int c0 = r0 < m ? cm[r0] : -1;
-    const int c1 = r1 < m ? cm[r1] : -1;
-    if (c0 >= 0) x0 = cadd(x0, rc[c0]);
-    if (c1 >= 0) x1 = cadd(x1, rc[c1]);
-  }
-  if (r0 < p) x0 = cadd(x0, yy[r0]);
-  if (r1 < p) x1 = cadd(x1, yy[r1]);
-  for (int k0 = 0; k0 < p; k0 += FWD_CH) {
-    if (k0 > 0) load_chunk(k0, a0, a1);
-#pragma unroll
-    for (int u = 0; u < FWD_CH; ++u) {
-      const int k = k0 + u;
-      if (k < p) {
-        const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
-        x0 = cfms(x0, a0[u], yk);
-        x1 = cfms(x1, a1[u], yk);
-      }
-    }
-  }
-  if (r0 < p) yy[r0] = x0;
-  else if (r0 < m) ru[r0 - p] = x0;
-  if (r1 < p) yy[r1] = x1;
-  else if (r1 < m) ru[r1 - p] = x1;
-}
-
-__global__ void __launch_bounds__(256, KH_BWD_SOLVE_MINB) bwd_small_kernel(KhTree T, const int32_t* __restrict__ level_fronts, int32_t nlev,
-                                                        const double2* __restrict__ panels, double2* y) {
-  const int lane = threadIdx.x & 31;
-  const int idx = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (idx >= nlev) return;
-  const int b = blockIdx.y;
-  const KhDevFront F = T.fronts[level_fronts[idx]];
-  const int p = F.p, q = F.q, m = p + q;
-  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
-  double2* yb = y + (int64_t)b * T.n;
-  double2* yy = yb + F.first;
-  const int64_t* urows = T.urows + F.rows_begin;
-  const double2 z = make_double2(0.0, 0.0);
-  // the L11 block (p <= BWD_L11) streams into shared memory with cp.async
-  // right away, so the serial L11^T chain at the end reads it on-chip
-  __shared__ __align__(16) double2 l11s[8][BWD_L11 * (BWD_L11 + 1)];
-  double2* Ls = l11s[threadIdx.x >> 5];
-  const bool stage = p <= BWD_L11;
-  if (stage) {
-    for (int e = lane; e < p * p; e += 32) {
-      const int k = e / p, i = e - k * p;
-      cp_async16(Ls + k * (BWD_L11 + 1) + i, P + i + (int64_t)k * m, true);
-    }
-    cp_async_commit();
-  }
-  // solution values of the update rows (already final: ancestors are done);
-  // lane a holds xu[a] and xu[a + 32]
-  const double2 xu0 = lane < q ? yb[urows[lane]] : z;
-  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : z;
-  // independent of the column sums: issue the rhs and pivot loads up front
-  const int k0 = lane, k1 = lane + 32;
-  const double2 y0 = k0 < p ? yy[k0] : z, y1 = k1 < p ? yy[k1] : z;
-  const double2 d0 = k0 < p ? P[k0 + (int64_t)k0 * m] : make_double2(1.0, 0.0);
-  const double2 d1 = k1 < p ? P[k1 + (int64_t)k1 * m] : make_double2(1.0, 0.0);
-  // t_k = y_k / d_k - sum_a L21[a, k] xu[a]: lane a reads rows p+a of column k
-  // (coalesced); the column sums are warp reductions, SOLVE_CH columns at a
-  // time so their shuffle trees overlap; lane k & 31 keeps the result
-  double2 t0 = z, t1 = z;
-  for (int k0 = 0; k0 < p; k0 += SOLVE_CH) {
-    double2 s[SOLVE_CH];
-#pragma unroll
-    for (int u = 0; u < SOLVE_CH; ++u) {
-      const int k = k0 + u;
-      const double2* col = P + p + (int64_t)k * m;
-      const double2 l0 = (k < p && lane < q) ? col[lane] : z;
-      const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
-      s[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
-    }
-    // transpose-reduce the 8 column sums over the warp (9 exchanges instead
-    // of 40): afterwards lane l holds the full sum of column u(l) =
-    // 4*bit4(l) + 2*bit3(l) + bit2(l)
-    const double2 v = warp_sum8(s, lane);
-    // the owner lane of column k0 + u fetches it from a lane holding u
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int kk = lane + 32 * h, u = kk - k0;
-      const int src = ((u >> 2) & 1) << 4 | ((u >> 1) & 1) << 3 | (u & 1) << 2;
-      const double2 got = shfl2(v, src & 31);
-      if (u >= 0 && u < SOLVE_CH && kk < p) {
-        if (h == 0) t0 = got;
-        else t1 = got;
-      }
-    }
-  }
-  if (k0 < p) t0 = csub(cmul(y0, cinv(d0)), t0);
-  if (k1 < p) t1 = csub(cmul(y1, cinv(d1)), t1);
-  if (stage) {
-    // L11^T x = t from shared memory (p <= BWD_L11: lane k owns column k)
-    cp_async_wait<0>();
-    __syncwarp();
-    for (int i = p - 1; i > 0; --i) {
-      const double2 xi = shfl2(t0, i);
-      if (k0 < i) t0 = cfms(t0, Ls[k0 * (BWD_L11 + 1) + i], xi);
-    }
-    if (k0 < p) yy[k0] = t0;
-    return;
-  }
-  // L11^T x = t bottom-up, column form: x_i final -> t_j -= L[i, j] x_i for
-  // j < i; the L11 rows of a chunk of SOLVE_CH steps are loaded into
-  // registers first (independent of x), so the serial chain waits on one
-  // load round trip per chunk instead of one per pivot
-  for (int i1 = p - 1; i1 > 0; i1 -= FWD_CH) {
-    double2 l0[FWD_CH], l1[FWD_CH];
-#pragma unroll
-    for (int u = 0; u < FWD_CH; ++u) {
-      const int i = i1 - u;
-      l0[u] = (i > 0 && k0 < i) ? P[i + (int64_t)k0 * m] : z;
-      l1[u] = (i > 0 && k1 < i) ? P[i + (int64_t)k1 * m] : z;
-    }
-#pragma unroll
-    for (int u = 0; u < FWD_CH; ++u) {
-      const int i = i1 - u;
-      if (i > 0) {
-        const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
-        if (k0 < i) t0 = cfms(t0, l0[u], xi);
-        if (k1 < i) t1 = cfms(t1, l1[u], xi);
-      }
-    }
-  }
-  if (k0 < p) yy[k0] = t0;
-  if (k1 < p) yy[k1] = t1;
-}
-
-// Forward solve of the fronts with m <= 64, one warp per (front, shift), the
-// panel staged in shared memory by bulk async copies as in bwd_small_tma_kernel;
-// the front's right-hand side (pivot rows of y plus the children's rhs updates)
-// is gathered while the copies are in flight. Lane l owns rows l and l + 32:
-// x_r -= L[r, k] y_k for r > k, y_k broadcast by shuffles.
-#ifndef KH_FWD_TMA
-#define KH_FWD_TMA 1
-#endif
 #ifndef KH_FWD_TMA_NW
 #define KH_FWD_TMA_NW 1
 #endif
@@ -1846,9 +1561,6 @@ __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const 
 // round trip for its panel instead of one per register chunk of columns.
 //  t_k = y_k / d_k - sum_a L21[a, k] xu[a]   (column sums: warp_sum8 over 8 columns)
 //  L11^T x = t                               (lane k owns t_k; pivots by shuffles)
-#ifndef KH_BWD_TMA
-#define KH_BWD_TMA 1
-#endif
 #ifndef KH_BWD_TMA_NW
 #define KH_BWD_TMA_NW 1
 #endif
@@ -2303,33 +2015,6 @@ cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_
 }
 
 
-cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
-                                  double2* panels, cudaStream_t stream) {
-  if (ntasks == 0 || batch == 0) return cudaSuccess;
-  const int smem = (int)(CP_STAGES * sizeof(CpStage));
-  cudaError_t e = kh_smem_optin((const void*)big_lupdate_kernel, smem);
-  if (e != cudaSuccess) return e;
-  big_lupdate_kernel<<<dim3(ntasks, batch), 128, smem, stream>>>(T, tasks, kb, panels);
-  kh_note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t nfr, int kb, int32_t batch,
-                               double2* panels, double* minpiv, cudaStream_t stream) {
-  if (nfr == 0 || batch == 0) return cudaSuccess;
-  big_diag_kernel<<<dim3(nfr, batch), 32 * DIAG_NW, 0, stream>>>(T, fronts, nfr, kb, panels, minpiv);
-  kh_note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
-                               double2* panels, cudaStream_t stream) {
-  if (ntasks == 0 || batch == 0) return cudaSuccess;
-  big_trsm_kernel<<<dim3(ntasks, batch), TRSM_ROWS, 0, stream>>>(T, tasks, kb, panels);
-  kh_note_launch();
-  return cudaGetLastError();
-}
-
 cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                  double2* panels, double* minpiv, double2* img, int64_t img_stride,
                                  cudaStream_t stream) {
@@ -2380,18 +2065,12 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
                                 const double2* ru_child, int64_t ru_stride_child, int32_t max_panel,
                                 cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  if (KH_FWD_TMA) {
-    constexpr int nw = KH_FWD_TMA_NW;
-    const int smem = 16 * nw * max_panel;
-    cudaError_t e = kh_smem_optin((const void*)fwd_small_tma_kernel<nw>, smem);
-    if (e != cudaSuccess) return e;
-    fwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(
-        T, level_fronts, nlev, panels, y, ru_cur, ru_stride_cur, ru_child, ru_stride_child, max_panel);
-    kh_note_launch();
-    return cudaGetLastError();
-  }
-  fwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y, ru_cur,
-                                                                    ru_stride_cur, ru_child, ru_stride_child);
+  constexpr int nw = KH_FWD_TMA_NW;
+  const int smem = 16 * nw * max_panel;
+  cudaError_t e = kh_smem_optin((const void*)fwd_small_tma_kernel<nw>, smem);
+  if (e != cudaSuccess) return e;
+  fwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(
+      T, level_fronts, nlev, panels, y, ru_cur, ru_stride_cur, ru_child, ru_stride_child, max_panel);
   kh_note_launch();
   return cudaGetLastError();
 }
@@ -2399,17 +2078,12 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
-  if (KH_BWD_TMA) {
-    constexpr int nw = KH_BWD_TMA_NW;
-    const int smem = 16 * nw * max_panel;
-    cudaError_t e = kh_smem_optin((const void*)bwd_small_tma_kernel<nw>, smem);
-    if (e != cudaSuccess) return e;
-    bwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(T, level_fronts, nlev,
-                                                                                         panels, y, max_panel);
-    kh_note_launch();
-    return cudaGetLastError();
-  }
-  bwd_small_kernel<<<dim3((nlev + 7) / 8, batch), 256, 0, stream>>>(T, level_fronts, nlev, panels, y);
+  constexpr int nw = KH_BWD_TMA_NW;
+  const int smem = 16 * nw * max_panel;
+  cudaError_t e = kh_smem_optin((const void*)bwd_small_tma_kernel<nw>, smem);
+  if (e != cudaSuccess) return e;
+  bwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(T, level_fronts, nlev,
+                                                                                       panels, y, max_panel);
   kh_note_launch();
   return cudaGetLastError();
 }

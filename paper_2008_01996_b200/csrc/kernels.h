@@ -93,19 +93,9 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
 #define KH_ASM_CHUNK_DEF 512
 #endif
 constexpr int KH_ASM_CHUNK = KH_ASM_CHUNK_DEF;
-#ifndef KH_TRSM_ROWS_DEF
-#define KH_TRSM_ROWS_DEF 128
-#endif
-constexpr int KH_TRSM_ROWS = KH_TRSM_ROWS_DEF;  // rows per TRSM task
 cudaError_t kh_launch_big_assemble(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
                                    const double2* lam, double2* panels, const double2* upd_child,
                                    int64_t upd_stride_child, cudaStream_t stream);
-cudaError_t kh_launch_big_lupdate(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
-                                  double2* panels, cudaStream_t stream);
-cudaError_t kh_launch_big_diag(const KhTree& T, const int32_t* fronts, int32_t nfr, int kb, int32_t batch,
-                               double2* panels, double* minpiv, cudaStream_t stream);
-cudaError_t kh_launch_big_trsm(const KhTree& T, const int32_t* tasks, int32_t ntasks, int kb, int32_t batch,
-                               double2* panels, cudaStream_t stream);
 cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntasks, int32_t batch,
                             const double2* panels, double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
                             int64_t upd_stride_child, cudaStream_t stream);
