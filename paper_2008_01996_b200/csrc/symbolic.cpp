@@ -23,14 +23,63 @@
 
 namespace kh {
 namespace {
+std::atomic<long long> g_sep_ns[8];
 
 struct Graph {
   int64_t n = 0;
   std::vector<int64_t> xadj, adj;
 };
 
+// rows [0, n) split over up to 8 threads: fn(r0, r1)
+template <class F>
+void parallel_rows(int64_t n, F fn) {
+  const int nth = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < 4096 || nth == 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nth; ++t) th.emplace_back(fn, n * t / nth, n * (t + 1) / nth);
+  fn((int64_t)0, n / nth);
+  for (auto& x : th) x.join();
+}
+
+// Fast path of build_graph: a canonical (rows sorted, no duplicates) and
+// structurally symmetric pattern -- what scipy hands over for M + A -- is its
+// own graph minus the diagonal. Returns false if the pattern is not of that kind.
+bool graph_from_symmetric(int64_t n, const int64_t* indptr, const int64_t* indices, Graph& g) {
+  std::atomic<bool> ok{true};
+  parallel_rows(n, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1 && ok.load(std::memory_order_relaxed); ++i)
+      for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+        const int64_t j = indices[e];
+        if (e > indptr[i] && indices[e - 1] >= j) { ok = false; break; }
+        if (j == i) continue;
+        if (!std::binary_search(indices + indptr[j], indices + indptr[j + 1], i)) { ok = false; break; }
+      }
+  });
+  if (!ok) return false;
+  g.n = n;
+  g.xadj.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t d = indptr[i + 1] - indptr[i];
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) d -= indices[e] == i;
+    g.xadj[i + 1] = g.xadj[i] + d;
+  }
+  g.adj.resize(g.xadj[n]);
+  parallel_rows(n, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t w = g.xadj[i];
+      for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e)
+        if (indices[e] != i) g.adj[w++] = indices[e];
+    }
+  });
+  return true;
+}
+
 Graph build_graph(int64_t n, const int64_t* indptr, const int64_t* indices) {
   Graph g;
+  if (graph_from_symmetric(n, indptr, indices, g)) return g;
   g.n = n;
   std::vector<int64_t> deg(n, 0);
   for (int64_t i = 0; i < n; ++i)
@@ -77,9 +126,9 @@ struct Shared {
   const Graph& g;
   int32_t leaf;
   std::vector<std::atomic<int32_t>> in_set;
-  std::vector<int32_t> dist;
+  std::vector<int32_t> dist, dist2;  // two level structures per vertex set (both ends of the diameter)
   std::atomic<int32_t> stamp{0};
-  Shared(const Graph& gr, int32_t lf) : g(gr), leaf(lf), in_set(gr.n), dist(gr.n, -1) {
+  Shared(const Graph& gr, int32_t lf) : g(gr), leaf(lf), in_set(gr.n), dist(gr.n, -1), dist2(gr.n, -1) {
     for (auto& x : in_set) x.store(0, std::memory_order_relaxed);
   }
 };
@@ -96,22 +145,41 @@ struct Builder {
 
   // BFS restricted to vertices stamped s; fills queue and level starts.
   int64_t bfs(int64_t root, int32_t s, std::vector<int64_t>& lvl_start) {
+    return bfs_into(root, s, lvl_start, queue, sh.dist);
+  }
+  int64_t bfs_into(int64_t root, int32_t s, std::vector<int64_t>& lvl_start, std::vector<int64_t>& q,
+                   std::vector<int32_t>& dist) {
     lvl_start.clear();
     int64_t head = 0, tail = 0;
-    queue[tail++] = root;
-    sh.dist[root] = 0;
+    q[tail++] = root;
+    dist[root] = 0;
     int32_t cur = -1;
     while (head < tail) {
-      int64_t v = queue[head];
-      if (sh.dist[v] != cur) { cur = sh.dist[v]; lvl_start.push_back(head); }
+      int64_t v = q[head];
+      const int32_t dv = dist[v];
+      if (dv != cur) { cur = dv; lvl_start.push_back(head); }
       ++head;
       for (int64_t e = g.xadj[v]; e < g.xadj[v + 1]; ++e) {
         int64_t u = g.adj[e];
-        if (in(u) == s && sh.dist[u] < 0) { sh.dist[u] = sh.dist[v] + 1; queue[tail++] = u; }
+        if (dist[u] < 0 && in(u) == s) { dist[u] = dv + 1; q[tail++] = u; }
       }
     }
     lvl_start.push_back(tail);
     return tail;
+  }
+
+  // A rooted level structure of the current set: BFS order, level starts and
+  // per-vertex levels (in one of the two shared dist arrays).
+  struct Levels {
+    std::vector<int64_t> order, ls;
+    std::vector<int32_t>* dist = nullptr;
+    int64_t N = 0;
+  };
+  Levels lv[2];  // per-thread level-structure slots
+  void levels(int64_t root, int32_t s, const std::vector<int64_t>& V, Levels& L) {
+    if (L.order.size() < V.size()) L.order.resize(V.size());
+    for (int64_t v : V) (*L.dist)[v] = -1;
+    L.N = bfs_into(root, s, L.ls, L.order, *L.dist);
   }
 
   void reset_dist(const std::vector<int64_t>& V) {
@@ -131,15 +199,15 @@ struct Builder {
     double ratio = 1e30;
   };
 
-  // Separator from the BFS level structure rooted at `root`.
-  Cut cut_from(int64_t root, int32_t s, const std::vector<int64_t>& V) {
+  // Separator from a rooted BFS level structure.
+  Cut cut_from(const Levels& L, int32_t s) {
     Cut c;
-    std::vector<int64_t> ls;
-    reset_dist(V);
-    int64_t N = bfs(root, s, ls);
+    const std::vector<int64_t>& ls = L.ls;
+    const std::vector<int64_t>& order = L.order;
+    const std::vector<int32_t>& dist = *L.dist;
+    const int64_t N = L.N;
     int64_t e = (int64_t)ls.size() - 2;  // eccentricity
     if (e < 2) return c;
-    std::vector<int64_t> order(queue.begin(), queue.begin() + N);
     int64_t best = -1;
     for (int64_t l = 1; l < e; ++l) {
       int64_t below = ls[l], size = ls[l + 1] - ls[l], above = N - ls[l + 1];
@@ -163,7 +231,7 @@ struct Builder {
       bool up = false;
       for (int64_t a = g.xadj[v]; a < g.xadj[v + 1] && !up; ++a) {
         int64_t u = g.adj[a];
-        up = (in(u) == s && sh.dist[u] == best + 1);
+        up = (in(u) == s && dist[u] == best + 1);
       }
       if (up) c.sep.push_back(v);
     }
@@ -172,18 +240,25 @@ struct Builder {
     return c;
   }
 
-  // Connected components of the set stamped `s` (in V order).
+  // Connected components of the set stamped `s` (components in order of their
+  // first vertex in V; each keeps V's order, so sorted V gives sorted parts):
+  // BFS labels, then one distributing pass over V (no per-part sort).
   std::vector<std::vector<int64_t>> components(const std::vector<int64_t>& V, int32_t s) {
     std::vector<std::vector<int64_t>> parts;
     reset_dist(V);
-    std::vector<int64_t> ls;
+    std::vector<int64_t> ls, sizes;
+    std::vector<int32_t>& lab = sh.dist2;
     for (int64_t v : V) {
       if (in(v) != s || sh.dist[v] >= 0) continue;
-      int64_t N = bfs(v, s, ls);
-      std::vector<int64_t> part(queue.begin(), queue.begin() + N);
-      std::sort(part.begin(), part.end());
-      parts.push_back(std::move(part));
+      const int64_t N = bfs(v, s, ls);
+      const int32_t id = (int32_t)sizes.size();
+      for (int64_t k = 0; k < N; ++k) lab[queue[k]] = id;
+      sizes.push_back(N);
     }
+    parts.resize(sizes.size());
+    for (size_t k = 0; k < sizes.size(); ++k) parts[k].reserve(sizes[k]);
+    for (int64_t v : V)
+      if (in(v) == s) parts[lab[v]].push_back(v);
     return parts;
   }
 
@@ -199,31 +274,43 @@ struct Builder {
   // the tree are dissected by separate threads (each with its own Builder).
   Sub nd(std::vector<int64_t> V, int depth) {
     if ((int64_t)V.size() <= sh.leaf) return leaf_sub(std::move(V));
+    auto T0 = std::chrono::steady_clock::now();
     if (queue.size() < V.size()) queue.resize(V.size());
     int32_t s = ++sh.stamp;
     for (int64_t v : V) mark(v, s);
-    // pseudo-peripheral pair
+    // pseudo-peripheral pair (a, b); the level structures rooted at both are
+    // kept (two slots) and reused by the cuts below instead of recomputed
     int64_t r = V[0];
-    int64_t ecc = -1, a = r, b = r;
-    std::vector<int64_t> ls;
+    int64_t ecc = -1, b = r;
+    lv[0].dist = &sh.dist;
+    lv[1].dist = &sh.dist2;
+    int cur = 0, sa = -1, sb = -1;  // slot of the last BFS; slots rooted at a and at b
     for (int it = 0; it < 4; ++it) {
-      reset_dist(V);
-      int64_t N = bfs(r, s, ls);
+      levels(r, s, V, lv[cur]);
+      const std::vector<int64_t>& ls = lv[cur].ls;
       int64_t e = (int64_t)ls.size() - 2;
-      if (e <= ecc) break;
+      if (e <= ecc) {  // the BFS from b did not go further: it is b's structure
+        sb = cur;
+        break;
+      }
       ecc = e;
-      a = r;
+      sa = cur;
       int64_t bestv = -1, bestd = 0;
-      for (int64_t k = ls[e]; k < N; ++k) {
-        int64_t v = queue[k];
+      for (int64_t k = ls[e]; k < lv[cur].N; ++k) {
+        int64_t v = lv[cur].order[k];
         int64_t d = deg_in(v, s);
         if (bestv < 0 || d < bestd) { bestv = v; bestd = d; }
       }
       b = bestv;
       r = bestv;
+      cur ^= 1;
     }
-    Cut ca = cut_from(a, s, V);
-    Cut cb = cut_from(b, s, V);
+    if (sb < 0) {  // four improving rounds: b not yet searched
+      sb = sa ^ 1;
+      levels(b, s, V, lv[sb]);
+    }
+    Cut ca = cut_from(lv[sa], s);
+    Cut cb = cut_from(lv[sb], s);
     Cut* c = nullptr;
     if (ca.ok && cb.ok) {
       bool a_bal = ca.ratio <= 2.0, b_bal = cb.ratio <= 2.0;
@@ -240,6 +327,7 @@ struct Builder {
     for (int64_t v : V) mark(v, s2);
     for (int64_t v : sep) mark(v, 0);
     auto parts = components(V, s2);
+    if (depth < 8) g_sep_ns[depth] += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - T0).count();
     const size_t nV = V.size();
     std::vector<int64_t>().swap(V);
     std::vector<Sub> subs(parts.size());
@@ -338,6 +426,7 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
       for (auto& kk : sb.kids) kids.push_back(std::move(kk));
     }
   }
+  if (timing) for (int d = 0; d < 8; ++d) std::fprintf(stderr, "  sep depth %d: %.2f ms (sum over subproblems)\n", d, g_sep_ns[d].exchange(0) * 1e-6);
   lap("dissection");
   const int32_t nf = (int32_t)piv.size();
   S.iperm.assign(n, -1);
@@ -434,25 +523,44 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
     }
   }
   S.panel_total = panel;
-  for (int32_t f = 0; f < nf; ++f) {
-    const Front& F = S.fronts[f];
-    if (F.parent < 0) continue;
-    const Front& P = S.fronts[F.parent];
-    const int64_t plast = P.first + P.p - 1;
-    const int64_t* prow = S.urows.data() + P.rows_begin;
-    for (int32_t a = 0; a < F.q; ++a) {
-      int64_t r = S.urows[F.rows_begin + a];
-      int32_t loc;
-      if (r <= plast) {
-        if (r < P.first) return "internal: update row below parent pivots";
-        loc = (int32_t)(r - P.first);
-      } else {
-        const int64_t* it = std::lower_bound(prow, prow + P.q, r);
-        if (it == prow + P.q || *it != r) return "internal: update row missing in parent";
-        loc = P.p + (int32_t)(it - prow);
+  {
+    // relind: fronts are independent (contiguous front ranges per thread);
+    // both row lists are sorted, so a merge walk finds each row in the parent
+    std::vector<std::string> rerr(nth);
+    auto rel = [&](int t) {
+      const int32_t f0 = (int32_t)((int64_t)nf * t / nth), f1 = (int32_t)((int64_t)nf * (t + 1) / nth);
+      for (int32_t f = f0; f < f1; ++f) {
+        const Front& F = S.fronts[f];
+        if (F.parent < 0) continue;
+        const Front& P = S.fronts[F.parent];
+        const int64_t plast = P.first + P.p - 1;
+        const int64_t* prow = S.urows.data() + P.rows_begin;
+        int32_t j = 0;
+        for (int32_t a = 0; a < F.q; ++a) {
+          int64_t r = S.urows[F.rows_begin + a];
+          int32_t loc;
+          if (r <= plast) {
+            if (r < P.first) { rerr[t] = "internal: update row below parent pivots"; return; }
+            loc = (int32_t)(r - P.first);
+          } else {
+            while (j < P.q && prow[j] < r) ++j;
+            if (j == P.q || prow[j] != r) { rerr[t] = "internal: update row missing in parent"; return; }
+            loc = P.p + j;
+          }
+          S.relind[F.relind_begin + a] = loc;
+        }
       }
-      S.relind[F.relind_begin + a] = loc;
+    };
+    if (nf < 256) {
+      for (int t = 0; t < nth; ++t) rel(t);
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 1; t < nth; ++t) th.emplace_back(rel, t);
+      rel(0);
+      for (auto& x : th) x.join();
     }
+    for (auto& e : rerr)
+      if (!e.empty()) return e;
   }
   lap("relind");
   // pull maps: for child c of P, cmap[c][r] = a with relind_c[a] = r (r < m_P), else -1
