@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -17,6 +18,12 @@
 
 struct kh_symbolic {
   kh::Symbolic S;
+  // launch schedule derived from S (built once per analysis: kh_plan_bytes
+  // and kh_plan_create of the same symbolic share it), keyed by the schedule
+  // environment knobs
+  mutable std::mutex sched_mu;
+  mutable std::shared_ptr<const void> sched;
+  mutable std::string sched_key;
 };
 
 static std::atomic<long long> g_launches{0};
@@ -677,6 +684,24 @@ void plan_sizes(kh_plan* p, const kh::Symbolic& S, int64_t max_batch, int64_t sl
   }
 }
 
+// The symbolic's schedule, built on first use (thread-safe).
+std::shared_ptr<const Sched> schedule_of(const kh_symbolic* s) {
+  std::string key;
+  for (const char* v : {"KH_SMALL_MAX", "KH_WARP_CLASSES"}) {
+    const char* e = std::getenv(v);
+    key += e ? e : "-";
+    key += ';';
+  }
+  std::lock_guard<std::mutex> lock(s->sched_mu);
+  if (!s->sched || s->sched_key != key) {
+    auto X = std::make_shared<Sched>();
+    build_schedule(s->S, *X);
+    s->sched = X;
+    s->sched_key = key;
+  }
+  return std::static_pointer_cast<const Sched>(s->sched);
+}
+
 }  // namespace
 
 extern "C" {
@@ -684,8 +709,7 @@ extern "C" {
 int kh_plan_bytes(const kh_symbolic* s, int64_t max_batch, int64_t factor_slots, int64_t* bytes) {
   if (!s || !bytes) return fail(KH_ERR_INVALID, "null argument");
   kh_plan tmp;
-  Sched X;
-  build_schedule(s->S, X);
+  const Sched& X = *schedule_of(s);
   plan_sizes(&tmp, s->S, max_batch, factor_slots);
   tmp.minv_size = X.minv_size;
   Carver C;
@@ -709,8 +733,8 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   kh_plan* p = new kh_plan();
   p->device = device;
   plan_sizes(p, S, max_batch, factor_slots);
-  Sched X;
-  build_schedule(S, X);
+  const std::shared_ptr<const Sched> Xp = schedule_of(s);
+  const Sched& X = *Xp;
   p->max_p = X.max_p;
   p->max_m = X.max_m;
   p->level_off = X.level_off;

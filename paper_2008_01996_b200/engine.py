@@ -19,6 +19,7 @@ DESIGN.md). All kernels are in libkhb200.so; torch only allocates memory.
 """
 
 import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -81,6 +82,18 @@ def conjugate_pairs(D, X):
             singles.append(j)
             j += 1
     return np.array(reps, dtype=np.int64), np.array(singles, dtype=np.int64)
+
+
+def modal_stub(n_t, D, X):
+    """The shifts of a modal plan (same order as `modal_plan`: conjugate-pair
+    representatives, then the real eigenvalues) without its transforms: what
+    an FDEngine needs to factor before the SVD of X is done
+    (FDEngine.attach_modal supplies the rest)."""
+    reps, singles = conjugate_pairs(D, X)
+    lam = np.concatenate([np.asarray(D)[reps], np.asarray(D)[singles].real.astype(np.complex128)])
+    weight = np.concatenate([np.full(len(reps), 2.0), np.ones(len(singles))])
+    return ModalPlan(n_t=n_t, lam=np.ascontiguousarray(lam, dtype=np.complex128), weight=weight,
+                     n_pairs=len(reps), n_single=len(singles), w_in=None, w_out=None, kron_b=None)
 
 
 def modal_plan(temporal, pencil):
@@ -159,13 +172,18 @@ def _on_device(fn):
     return wrapper
 
 
-def _fortran(t_np, device):
+def _fortran(t_np, device, async_copy=False):
     """Host (rows x cols) array -> device column-major buffer (as a torch tensor
-    of shape (cols, rows), i.e. the transpose view, contiguous)."""
+    of shape (cols, rows), i.e. the transpose view, contiguous).
+    async_copy: stage through pinned memory and copy without blocking the host
+    (the copy is queued behind the stream's work, e.g. a factorization)."""
     import torch
 
     a = np.asarray(t_np, dtype=np.float64)
-    return torch.from_numpy(np.ascontiguousarray(a.T)).to(device)
+    t = torch.from_numpy(np.ascontiguousarray(a.T))
+    if async_copy:
+        return t.pin_memory().to(device, non_blocking=True)
+    return t.to(device)
 
 
 class FDEngine:
@@ -235,6 +253,7 @@ class FDEngine:
                 batch = (batch + 1) // 2
         self.keep_factors = bool(keep_factors)
         self.batch = int(batch)
+        self.t_memplan = time.perf_counter()
         self.pipes = []
         for i in range(npipe):
             k0, k1 = bounds[i], bounds[i + 1]
@@ -242,8 +261,10 @@ class FDEngine:
             plan = sparse_direct._Plan(self.sym, mv, av, b, (k1 - k0 if self.keep_factors else b) or 1,
                                        self.device.index)
             self.pipes.append((plan, k0, k1, b, torch.cuda.Stream(device=self.device)))
+        self.t_plans = time.perf_counter()
         self.plan = self.pipes[0][0]   # residual kernels (CSR of M, A) and single-pipe callers
         self.factored = False
+        self.unchecked = []  # (plan, slot, count) factored without their pivot check yet
         # first application with retained factors: factor with the forward
         # sweep fused (kh_plan_factor_fwd) or factor, then sweep. Measured
         # equal at c3 (42.02 ms/step either way: the in-kernel sweep costs
@@ -262,9 +283,9 @@ class FDEngine:
 
         dev = self.device
         f64 = torch.float64
-        self.w_in = _fortran(modal.w_in, dev)        # (2N_k, N_t) storage of N_t x 2N_k
-        self.w_out = _fortran(modal.w_out, dev)      # (N_t, 2N_k) storage of 2N_k x N_t
-        self.kron_b = _fortran(modal.kron_b, dev)    # (2N_t, N_t) storage of N_t x 2N_t
+        self.w_in = self.w_out = self.kron_b = None
+        if modal.w_in is not None:
+            self.attach_modal(modal)
         n, nt, nk2 = self.n, self.n_t, 2 * self.n_k
         self.G = torch.empty((nk2, n), dtype=f64, device=dev)   # column-major n x 2N_k
         self.Z = torch.empty((nk2, n), dtype=f64, device=dev)
@@ -279,6 +300,19 @@ class FDEngine:
         self.event_log = None
         # optional per-phase CUDA-event timers (bench.py's per-kernel rooflines)
         self.timers = None
+
+    def attach_modal(self, modal):
+        """Upload the modal transforms (W_in, W_out, [A_t^T | M_t^T]) of `modal`,
+        whose shifts must be the ones the engine was built for (an engine built
+        from `modal_stub` factors before the transforms exist)."""
+        if not np.array_equal(np.asarray(modal.lam), self.lam if hasattr(self, "lam") else modal.lam):
+            raise DimensionMismatch("modal plan shifts differ from the engine's")
+        dev = self.device
+        self.modal = modal
+        # pinned, non-blocking: the host does not wait for work already queued
+        self.w_in = _fortran(modal.w_in, dev, True)        # (2N_k, N_t) storage of N_t x 2N_k
+        self.w_out = _fortran(modal.w_out, dev, True)      # (N_t, 2N_k) storage of 2N_k x N_t
+        self.kron_b = _fortran(modal.kron_b, dev, True)    # (2N_t, N_t) storage of N_t x 2N_t
 
     # ---- primitives -----------------------------------------------------------
     def _stream(self):
@@ -327,11 +361,13 @@ class FDEngine:
             main.wait_stream(st)
 
     @_on_device
-    def factor(self, events=None):
+    def factor(self, events=None, check=True):
         """Factor M_x + lambda_k A_x for every retained shift (no-op otherwise).
 
         `events`: optional list that receives a (start, end) CUDA-event pair
-        bracketing the factorization launches (for the roofline)."""
+        bracketing the factorization launches (for the roofline). The pivot
+        guard synchronizes with the host; check=False defers it to the next
+        application (`_spatial`), so that its solves are queued first."""
         if not self.keep_factors:
             return
         import torch
@@ -352,8 +388,11 @@ class FDEngine:
         if events is not None:
             e1.record(main)
             events.append((e0, e1))
-        for plan, k0, k1, b, st in self.pipes:
-            plan.pivot_check(0, k1 - k0, self._stream())
+        if check:
+            for plan, k0, k1, b, st in self.pipes:
+                plan.pivot_check(0, k1 - k0, self._stream())
+        else:
+            self.unchecked = [(plan, 0, k1 - k0) for plan, k0, k1, b, st in self.pipes]
         self.factored = True
 
     @_on_device
@@ -414,6 +453,8 @@ class FDEngine:
             e1.record(main)
             log.append((e0, e1))
         self._join_pipes()
+        checks += self.unchecked
+        self.unchecked = []
         for plan, slot, cnt in checks:
             plan.pivot_check(slot, cnt, self._stream())
         if fuse and self.keep_factors:

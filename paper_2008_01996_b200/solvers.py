@@ -22,6 +22,7 @@ and `fd_residual` (the residual before refinement).
 """
 
 import os
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -217,7 +218,7 @@ class SolveReport:
                 "t_transform_out,residual,minReLambda,kappa2,threads")
 
 
-def build_pencil(temporal, variant, eig="qz"):
+def build_pencil(temporal, variant, eig="qz", on_eigenvalues=None):
     """Decompose the temporal pencil on the host (solvers.py:166-206).
 
     ``eig`` picks the "fd" eigensolver: "qz" (default) is the reference's
@@ -232,6 +233,9 @@ def build_pencil(temporal, variant, eig="qz"):
     (tests/test_pencil.py). `solve_fd` uses "reduced" when it builds the
     pencil itself; its report still carries the reference's statistics
     (`PencilFactorization.spectral_stats`, computed when first read).
+    ``on_eigenvalues(vals, vecs)`` ("fd" only) is called as soon as the
+    eigenpairs have passed the residual check, before the SVD of X (solve_fd
+    starts factoring the shifts there).
     """
     L = cholesky_lower(temporal.A)
     P = spd_solve(L, temporal.M)
@@ -245,11 +249,15 @@ def build_pencil(temporal, variant, eig="qz"):
             vals, vecs = eig_pencil_reduced(temporal.M, temporal.A, L)
             if pencil_residual(P, vecs, vals) > 1e-8 * scale:
                 raise DefectivePencil("eigenvector residual above tolerance")
+            if on_eigenvalues is not None:
+                on_eigenvalues(vals, vecs)
             form = svd_of_eigenvectors_real(vecs, vals)
         elif eig == "qz":
             vals, vecs = eig_pencil(temporal.M, temporal.A)
             if np.linalg.norm(P @ vecs - vecs * vals[None, :], "fro") > 1e-8 * scale:
                 raise DefectivePencil("eigenvector residual above tolerance")
+            if on_eigenvalues is not None:
+                on_eigenvalues(vals, vecs)
             form = svd_of_eigenvectors(vecs, vals)
         else:
             raise ValueError(f"unknown eigensolver: {eig!r}")
@@ -309,6 +317,18 @@ def _to_host(t):
     return out.numpy()
 
 
+def _publish_modes(box, ready, n_t, vals, vecs):
+    """Hand the shifts of the FD solve (one representative per conjugate pair,
+    then the real eigenvalues: the order of engine.modal_plan) to the worker
+    thread that factors them, as soon as the pencil's eigenpairs exist."""
+    from .engine import modal_stub
+
+    if np.min(np.real(vals)) <= 0.0:
+        return  # build_pencil raises DefectivePencil; nothing is factored
+    box["stub"] = modal_stub(n_t, vals, vecs)
+    ready.set()
+
+
 def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=DEFAULT_REFINE_TOL,
              leaf_size=sparse_direct.DEFAULT_LEAF_SIZE, max_batch=None, keep_factors=None):
     """Fast diagonalization on the GPU: independent complex spatial solves.
@@ -327,19 +347,53 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     report.device = torch.cuda.get_device_name(dev)
     n, nt = system.m_x, system.n_t
 
-    # The spatial symbolic analysis (host C++, releases the GIL) runs on a
-    # worker thread while this thread builds the modal plan and uploads f:
-    # the two host phases and the H2D copy overlap instead of adding up.
+    # Host pipeline. A worker thread runs the spatial symbolic analysis (host
+    # C++, releases the GIL), aligns M_x and A_x on its pattern, and -- as
+    # soon as this thread has the eigenvalues of the temporal pencil -- builds
+    # the numeric plan and launches the factorization of every shift. This
+    # thread meanwhile finishes the pencil (SVD of the eigenvectors) and the
+    # modal transforms, which only the GEMMs after the factorization need:
+    # the GPU factors while the host completes the pencil.
     t0 = time.perf_counter()
     analyze_before = sparse_direct.analyze_call_count()
     phases = report.phases
+    lam_box = {}
+    lam_ready = threading.Event()   # main -> worker: the shifts are known
+    queued = threading.Event()      # worker -> main: factorization queued (or the worker is done)
 
-    def _analyze():
-        a0 = time.perf_counter()
-        pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
-        out = sparse_direct.analyze(pattern, leaf_size)
-        phases["analyze"] = time.perf_counter() - a0
-        return out
+    def _spatial_setup():
+        try:
+            a0 = time.perf_counter()
+            pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
+            symbolic = sparse_direct.analyze(pattern, leaf_size)
+            phases["analyze"] = time.perf_counter() - a0
+            aligned = (symbolic.align_values(system.spatial.M_II), symbolic.align_values(system.spatial.A_II))
+            sparse_direct.plan_bytes(symbolic, 1, 1)  # builds the launch schedule (cached on the symbolic)
+            phases["aligned"] = time.perf_counter() - t0
+            lam_ready.wait()
+            if "stub" not in lam_box:  # the pencil failed on the main thread
+                return None
+            with torch.cuda.device(dev), nvtx.range("kh.solve_fd.plan"):
+                eng = FDEngine(system.spatial.M_II, system.spatial.A_II, lam_box["stub"], device=dev,
+                               leaf_size=leaf_size, max_batch=max_batch, keep_factors=keep_factors,
+                               symbolic=symbolic, aligned=aligned)
+                phases["plan"] = time.perf_counter() - t0
+                phases["memplan"] = eng.t_memplan - t0
+                phases["plans_created"] = eng.t_plans - t0
+                eng.factor(check=False)  # retained factors: queued now, checked after the solves are queued
+            phases["factor_queued"] = time.perf_counter() - t0
+            return eng
+        finally:
+            queued.set()
+
+    def _on_eigenvalues(vals, vecs):
+        # publish the shifts, then let the worker build the plan and queue the
+        # factorization before this thread's Python-heavy rest of the pencil
+        # competes with it for the GIL: the GPU starts as early as possible
+        phases["eigenvalues"] = time.perf_counter() - t0
+        _publish_modes(lam_box, lam_ready, nt, vals, vecs)
+        if lam_ready.is_set():
+            queued.wait()
 
     # a pinned rhs goes up asynchronously right away (the copy engine works
     # while the host computes the pencil); a pageable one after the pencil
@@ -347,14 +401,19 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     F = rhs_t.to(dev, non_blocking=True).view(nt, n) if rhs_t.is_pinned() else None
     nvtx = torch.cuda.nvtx
     nvtx.range_push("kh.solve_fd.host")
-    with ThreadPoolExecutor(max_workers=1) as pool:
-        fut = pool.submit(_analyze)
+    pool = ThreadPoolExecutor(max_workers=1)
+    fut = pool.submit(_spatial_setup)
+    try:
         # few BLAS threads: dgeev / the SVD of an N_t <= 512 matrix gain
         # nothing from more, and the dissection threads of the analysis
         # need the cores
         with _blas_threads(int(os.environ.get("KH_PENCIL_THREADS", 1 if nt <= 512 else 4))):
             if pencil is None:
-                pencil = build_pencil(system.temporal, "fd", eig="reduced")
+                pencil = build_pencil(system.temporal, "fd", eig="reduced", on_eigenvalues=_on_eigenvalues)
+            else:
+                form = pencil.form
+                if getattr(form, "X", None) is not None and getattr(form, "D", None) is not None:
+                    _publish_modes(lam_box, lam_ready, nt, np.asarray(form.D), np.asarray(form.X))
             phases["pencil"] = time.perf_counter() - t0
             form = pencil.form
             if not (isinstance(form, EigenSvdForm)
@@ -364,18 +423,17 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
         report.t_decompose = time.perf_counter() - t0
         if F is None:
             F = rhs_t.to(dev).view(nt, n)
-        symbolic = fut.result()
-        phases["host_joined"] = time.perf_counter() - t0
+    finally:
+        lam_ready.set()  # a failed pencil releases the worker (it then returns None)
+        eng = fut.result()
+        pool.shutdown()
+    if not np.array_equal(eng.lam, modal.lam):
+        raise DimensionMismatch("internal: factored shifts differ from the modal plan's")
+    eng.attach_modal(modal)
+    phases["host_joined"] = time.perf_counter() - t0
     report.min_re_lambda = pencil.min_re_lambda
     report.spectral_source = spectral_source(pencil)
-
     nvtx.range_pop()
-    # spatial setup: numeric plan + factorization of every shift
-    nvtx.range_push("kh.solve_fd.plan")
-    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev, leaf_size=leaf_size,
-                   max_batch=max_batch, keep_factors=keep_factors, symbolic=symbolic)
-    nvtx.range_pop()
-    phases["plan"] = time.perf_counter() - t0
     report.analyze_calls = sparse_direct.analyze_call_count() - analyze_before
     t_setup = time.perf_counter() - t0 - report.t_decompose
 
