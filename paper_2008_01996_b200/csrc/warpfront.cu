@@ -60,6 +60,12 @@ KH_DEV double2 shfl2w(double2 v, int src) {
 
 KH_HD constexpr int tix(int I, int J) { return I * (I + 1) / 2 + J; }
 
+#ifdef KH_PHASE_TIMING
+// debug builds only (profiles/probes/phase_timing.py): clock64 cycles per phase
+// of warp_front_kernel, summed over warps, [MT][phase], phase 7 = warp count
+__device__ unsigned long long g_wphase[8 * 8];
+#endif
+
 template <int MT>
 __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_kernel(
     KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
@@ -69,6 +75,19 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
   extern __shared__ __align__(16) double2 O[];  // originals image: [panel tile][h][lane] = (M, A)
   __shared__ __align__(8) uint64_t wbar[WF_WARPS];  // per-warp child-staging barriers
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef KH_PHASE_TIMING
+  long long tph = clock64();
+  auto wphase = [&](int i) {
+    if (lane == 0) {
+      const long long t1 = clock64();
+      atomicAdd(&g_wphase[MT * 8 + i], (unsigned long long)(t1 - tph));
+      if (i == 0) atomicAdd(&g_wphase[MT * 8 + 7], 1ull);
+      tph = t1;
+    }
+  };
+#else
+  auto wphase = [](int) {};
+#endif
   if (tid < WF_WARPS) mbar_init(&wbar[tid], 1);
   mbar_fence_init();
   const int g = lane >> 2, t = lane & 3;
@@ -139,6 +158,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
   }
   __syncthreads();
   if (b >= nshift) return;
+  wphase(0);
 
   const int rl = perm8(g);  // logical row of this lane inside every 8-block
   double2 S[NTL][2];
@@ -158,6 +178,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
           S[tix(I, J)][h] = v;
         }
   }
+  wphase(1);
   // ---- children: each child's packed update block (one contiguous array) is
   // staged in the warp's shared-memory buffer by one bulk async copy, then
   // pulled through the child maps
@@ -196,6 +217,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
         for (int h = 0; h < 2; ++h) S[tix(I, J)][h] = cadd(S[tix(I, J)][h], cs[min(cbase[J][h] + ri[I], zslot)]);
   }
 
+  wphase(2);
   // ---- blocked LDL^T over the p pivots, one 8-pivot block per iteration of a
   // runtime loop: the body works on the tile triangle relative to the current
   // diagonal tile (S[tix(0, 0)]); after a block its finished tile column is
@@ -342,7 +364,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
         const int r = kb + 8 * I + rl;
         if (I < nt && r < m && (I > 0 || rl >= t + 4 * h)) {
           if (c < p) pc[r] = S[tix(I, 0)][h];
-          else Uo[upk32(q, r - p, c - p)] = S[tix(I, 0)][h];
+          else cs[upk32(q, r - p, c - p)] = S[tix(I, 0)][h];  // update block: staged, see below
         }
       }
     }
@@ -354,6 +376,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
 #pragma unroll
         for (int h = 0; h < 2; ++h) S[tix(I - 1, J - 1)][h] = S[tix(I, J)][h];
   }
+  wphase(3);
   // ---- the rest is the update block (rows and columns >= kb >= p)
 #pragma unroll
   for (int I = 0; I < MT; ++I)
@@ -362,12 +385,35 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_k
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = kb + 8 * I + rl, c = kb + 8 * J + t + 4 * h;
-        if (r < m && r >= c) Uo[upk32(q, r - p, c - p)] = S[tix(I, J)][h];
+        if (r < m && r >= c) cs[upk32(q, r - p, c - p)] = S[tix(I, J)][h];
       }
-  if (lane == 0) minpiv[(int64_t)b * T.nf + f] = minp < 0.0 ? -1.0 : sqrt(minp);
+  // the packed update block is contiguous in global memory: it was assembled
+  // in the warp's (now free) child buffer and leaves with one bulk copy
+  __syncwarp();
+  if (lane == 0 && q > 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(Uo),
+                 "r"(smem_u32(cs)), "r"(8u * (uint32_t)(q * (q + 1)))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (lane == 0) {
+    minpiv[(int64_t)b * T.nf + f] = minp < 0.0 ? -1.0 : sqrt(minp);
+    // shared memory must outlive the bulk copy's reads of it
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  wphase(4);
 }
 
 }  // namespace
+
+#ifdef KH_PHASE_TIMING
+extern "C" int kh_debug_wphase_cycles(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, g_wphase, sizeof(unsigned long long) * 64) != cudaSuccess) return 4;
+  static const unsigned long long zero[64] = {};
+  return cudaMemcpyToSymbol(g_wphase, zero, sizeof zero) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 // shared-memory bytes of the originals image for a front class
 static int warp_front_smem(int mt) {

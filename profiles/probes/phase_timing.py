@@ -56,6 +56,9 @@ def run(v):
     modal = modal_plan(system.temporal, solvers.build_pencil(system.temporal, "fd"))
     eng = FDEngine(system.spatial.M_II, system.spatial.A_II, modal, device=dev)
     buf = np.zeros(72, dtype=np.uint64)
+    wbuf = np.zeros(64, dtype=np.uint64)
+    wfn = lib.kh_debug_wphase_cycles
+    wfn.argtypes = [ctypes.c_void_p]
     times = []
     for it in range(4):
         eng.factored = False
@@ -65,7 +68,9 @@ def run(v):
         times.append(ev[0][0].elapsed_time(ev[0][1]))
         if it == 0:
             fn(buf.ctypes.data)  # discard warm-up counts
+            wfn(wbuf.ctypes.data)
     fn(buf.ctypes.data)
+    wfn(wbuf.ctypes.data)
     print(f"variant {v}: factor ms/step {np.mean(times[1:]):.2f}")
     names = ["staging", "assembly", "ldlt", "write", "(a)", "(b)", "(c)"]
     for ms in (2, 3, 4, 6, 8):
@@ -75,6 +80,14 @@ def run(v):
             continue
         parts = " ".join(f"{nm}={row[i] / n:6.0f}" for i, nm in enumerate(names))
         print(f"  MS={ms * 16:3d} CTAs={int(n):7d} cycles/CTA: {parts} total={row[:4].sum() / n:8.0f}")
+    wnames = ["setup", "originals", "children", "ldlt", "write"]
+    for mt in (4, 5, 6):
+        row = wbuf[mt * 8: mt * 8 + 8].astype(float)
+        n = row[7]
+        if n == 0:
+            continue
+        parts = " ".join(f"{nm}={row[i] / n:6.0f}" for i, nm in enumerate(wnames))
+        print(f"  warp MT={mt} warps={int(n):7d} cycles/warp: {parts} total={row[:5].sum() / n:8.0f}")
 
 
 if __name__ == "__main__":
