@@ -24,21 +24,24 @@ def main():
             continue
         if rec[0] == "Line No":
             col = rec.index("Warp Stall Sampling (All Samples)")
+            icol = rec.index("Instructions Executed") if "Instructions Executed" in rec else None
             continue
         if col is None or not rec[0]:
             continue
         try:
             s = int(rec[col] or 0)
+            ins = int(rec[icol] or 0) if icol is not None else 0
         except ValueError:
             continue
-        if s:
-            rows.append((s, fname.split("/")[-1], int(rec[0]), rec[1].strip()[:110]))
+        if s or ins:
+            rows.append((s, ins, fname.split("/")[-1], int(rec[0]), rec[1].strip()[:100]))
     tot = sum(r[0] for r in rows) or 1
-    print(f"total samples {tot}")
-    for s, f, ln, src in sorted(rows, reverse=True)[:top]:
+    itot = sum(r[1] for r in rows) or 1
+    print(f"total samples {tot}, warp instructions executed {itot}")
+    for s, ins, f, ln, src in sorted(rows, reverse=True)[:top]:
         if sub and sub not in f:
             continue
-        print(f"{100 * s / tot:5.1f}%  {f}:{ln}  {src}")
+        print(f"{100 * s / tot:5.1f}% stalls {100 * ins / itot:5.1f}% instr  {f}:{ln}  {src}")
 
 
 if __name__ == "__main__":
