@@ -7,17 +7,19 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.max.sm,clocks.sm,power.limit --format=csv > gpurun_out/${T}_box_gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_out/${T}_box_gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${T}_gpu_tests.txt 2>&1
-python bench.py > gpurun_out/${T}_bench_c3.log 2>&1; tail -1 gpurun_out/${T}_bench_c3.log > gpurun_out/${T}_bench_c3.json
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_ref.log 2>&1; tail -1 gpurun_out/${T}_ref.log > gpurun_out/${T}_bench_c3_reference_arm.json
+python bench.py > gpurun_out/${T}_bench_c3.log 2>&1; tail -n 1 gpurun_out/${T}_bench_c3.log > gpurun_out/${T}_bench_c3.json
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_ref.log 2>&1; tail -n 1 gpurun_out/${T}_ref.log > gpurun_out/${T}_bench_c3_reference_arm.json
 for c in c1 c2 c5; do
-  python bench.py --config $c --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; tail -1 gpurun_out/${T}_bench_$c.log > gpurun_out/${T}_bench_$c.json
+  python bench.py --config $c --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; tail -n 1 gpurun_out/${T}_bench_$c.log > gpurun_out/${T}_bench_$c.json
 done
-timeout 1500 python bench.py --config c4 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_bench_c4.log 2>&1; tail -1 gpurun_out/${T}_bench_c4.log > gpurun_out/${T}_bench_c4.json
+timeout 1500 python bench.py --config c4 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_bench_c4.log 2>&1; tail -n 1 gpurun_out/${T}_bench_c4.log > gpurun_out/${T}_bench_c4.json
 bash profiles/launch_list_dram.sh $T
+python profiles/level_breakdown.py gpurun_out/launches_dram_$T.csv > gpurun_out/${T}_level_breakdown.txt 2>&1
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-levels"
-for spec in "schur_update_kernel 13 schur" "front_kernel<.int.48 14 f48" "front_kernel<.int.128 8 f128" "bwd_small_tma 29 bwdsmall" "fwd_mid_tma 10 fwdmid" "dgemm_kernel 8 dgemm"; do
+for spec in "schur_update_kernel 11 schur" "warp_front_kernel<.int.6 7 wf6" "warp_front_kernel<.int.4 5 wf4" "front_kernel<.int.96 4 f96" "pivot_block_kernel 8 pivot" "panel_trsm_kernel 8 ptrsm" "bwd_small_tma 29 bwdsmall" "dgemm_kernel 8 dgemm"; do
   set -- $spec
   timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$1" --launch-skip $2 -c 1 -f -o gpurun_out/ncu_${T}_$3 $B > gpurun_out/ncu_${T}_$3.log 2>&1
   python profiles/ncu_summary.py gpurun_out/ncu_${T}_$3.ncu-rep "$3 (c3, $B)" > gpurun_out/${T}_ncu_$3.txt 2>&1
+  python profiles/ncu_lines.py gpurun_out/ncu_${T}_$3.ncu-rep "" 25 >> gpurun_out/${T}_ncu_$3.txt 2>&1
 done
 ls -la gpurun_out | grep $T
