@@ -134,9 +134,11 @@ int kh_plan_pivot_check(kh_plan* plan, int64_t slot0, int64_t nshift, double rel
 int kh_plan_solve(kh_plan* plan, int64_t slot0, int64_t nshift, const double* b_re, const double* b_im,
                   int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream);
 /* kh_plan_factor + kh_plan_solve in one pass: the forward sweep runs inside
- * the factorization kernels (the rhs is assembled as a border row of every
- * front), so the factors are read back only once, by the backward sweep.
- * Same arguments and results as the two calls (rounding aside). */
+ * the shared-memory factorization kernels (each front's rhs segment sits
+ * beside it in shared memory and is swept after its LDL^T) and beside the
+ * large fronts' Schur kernels, so the factors are read back only once, by the
+ * backward sweep. Same arguments and results as the two calls (rounding
+ * aside). */
 int kh_plan_factor_solve(kh_plan* plan, int64_t slot0, int64_t nshift, const double* lambda_ri, const double* b_re,
                          const double* b_im, int64_t ldb, double* x_re, double* x_im, int64_t ldx, void* stream);
 /* The two halves of kh_plan_factor_solve: factorization + forward sweep

@@ -82,17 +82,17 @@ struct DeviceGuard {
 constexpr int32_t kDefaultLeaf = 24;
 // fronts with m <= kClassMax[c] use the register-resident kernels; the rest
 // ("large", class kSmallClasses) the level-synchronous DMMA kernels
-constexpr int kSmallClasses = 5;
+constexpr int kSmallClasses = 6;
 #ifndef KH_CLASS4
 #define KH_CLASS4 96
 #endif
-constexpr int32_t kClassMax[kSmallClasses] = {32, 48, 64, KH_CLASS4, 128};
+constexpr int32_t kClassMax[kSmallClasses] = {32, 40, 48, 64, KH_CLASS4, 128};
 #ifndef KH_WARP_CLASSES
-#define KH_WARP_CLASSES 3
+#define KH_WARP_CLASSES 7
 #endif
 // the warp-per-front solve kernels take the classes with m <= 64
 #ifndef KH_SOLVE_SMALL_CLASSES
-#define KH_SOLVE_SMALL_CLASSES 3
+#define KH_SOLVE_SMALL_CLASSES 4
 #endif
 constexpr int kSolveSmallClasses = KH_SOLVE_SMALL_CLASSES;  // classes m <= 64: warp-per-front solves
 constexpr int kClsStride = kSmallClasses + 2;
@@ -115,7 +115,7 @@ struct kh_plan {
   int64_t n = 0, nnz = 0, max_batch = 0, slots = 0;
   int32_t nf = 0, max_p = 0, max_m = 0;
   std::vector<int32_t> level_off;  // levels d -> [level_off[d], level_off[d+1]) in level_fronts
-  // kClsStride per level: starts of the front classes (m <= 32, 48, 64, large)
+  // kClsStride per level: starts of the front classes (m <= 32, 40, 48, 64, 96, 128, large)
   // relative to level_off[d], plus the end
   std::vector<int32_t> cls_off;
   const int32_t* classes(int32_t d) const { return cls_off.data() + kClsStride * d; }
@@ -491,7 +491,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     }
   }
   // register-resident warp kernels for the classes m <= 32 and m <= 48
-  // (KH_WARP_CLASSES: bit c enables class c; default 0b011)
+  // (KH_WARP_CLASSES: bit c enables class c; default 0b111: m <= 32, 40, 48)
   int warp_mask = KH_WARP_CLASSES;
   if (const char* env = std::getenv("KH_WARP_CLASSES")) warp_mask = std::atoi(env);
   for (int c = 0; c < kSmallClasses; ++c)

@@ -1,5 +1,5 @@
 // Batched multifrontal complex-symmetric LDL^T (pivot-free) and its
-// triangular solves, one CTA per (front, shift).
+// triangular solves (the register-resident m <= 48 fronts: warpfront.cu).
 //
 // Replaces the reference's per-shift SuperLU path
 //   K = (Mc + lam[k] Ac).tocsr(); sparse_direct.factorize(sym, K).solve(G[:,k])
@@ -15,13 +15,13 @@
 // Fronts with m <= 128 (factor_front_kernel): the whole front is assembled in
 //   shared memory (packed block-column layout, push extend-add of the
 //   children), factored by blocked_ldlt (8-pivot blocks, DMMA trailing
-//   updates) and written out once.
+//   updates) and written out once (m <= 48: warp_front_kernel instead).
 // Larger fronts (level-synchronous kernels): big_assemble (panel), then per
-//   32-pivot block big_lupdate / big_diag / big_trsm, then
+//   64-pivot super-block pivot_block / panel_trsm / panel_update, then
 //   schur_update_kernel, which pulls the children's contributions into its
 //   64 x 64 tiles of U in the epilogue.
-// Every GEMM-shaped step runs on DMMA (mma.sync m8n8k4 f64) with complex
-// products built from four real MMAs.
+// Every GEMM-shaped step runs on DMMA (mma.sync m8n8k4 f64); complex products
+// use three real MMAs in the tile engine (KH_3M) and four elsewhere.
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -392,17 +392,15 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
 }
 
 // ---- large fronts, level-synchronous batched kernels ------------------------------
-// For the fronts with m > 64 of one level, the factorization is a sequence of
+// For the fronts with m > 128 of one level, the factorization is a sequence of
 // launches, each covering every (front, shift) of the level at once:
-//   big_assemble   (front, 2048-entry chunk): P = pulled children + originals
-//   for each 32-wide pivot block kb:
-//     big_lupdate  (front, 64-row tile): P[:, kb:kb+w] -= L[:, :kb] D L[kb:kb+w, :kb]^T   (DMMA, K = kb)
-//     big_diag     warp per (front, shift): LDL^T of the w x w diagonal block in shared
-//                  memory; L and D in place, L^-1 (strict part) transposed into the
-//                  otherwise unused upper triangle of the block
-//     big_trsm     (front, 64-row tile): L[r, kb:kb+w] = (A[r, kb:kb+w] L^-T) D^-1   (DMMA)
-//   schur_update   (front, 64x64 tile of U): U = pulled children - L21 D L21^T       (DMMA)
-// Tasks are int32 pairs (front, index) prepared on the host per level and block.
+//   big_assemble        (front, 512-entry chunk): P = pulled children + originals
+//   for each 64-pivot super-block at column c0 (see pivot_block_kernel below):
+//     pivot_block       (front, shift): LDL^T of the diagonal block + its DMMA B image
+//     panel_trsm        (front, 64-row tile): rows below, X = A L^-T D^-1      (DMMA)
+//     panel_update      (front, 64x64 tile): later pivot columns -= X D X^T   (DMMA)
+//   schur_update        (front, 64x64 tile of U): U = pulled children - L21 D L21^T (DMMA)
+// Tasks are int32 tuples prepared on the host per level and super-block.
 constexpr int ASM_CHUNK = KH_ASM_CHUNK;
 
 __global__ void __launch_bounds__(NT) big_assemble_kernel(KhTree T, const int32_t* __restrict__ tasks,
@@ -2203,6 +2201,7 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
   switch (ms) {
     case 32: return fwd ? run(factor_front_kernel<32, KH_NW32, true>, 32, 32 * KH_NW32, 0)
                         : run(factor_front_kernel<32, KH_NW32, false>, 32, 32 * KH_NW32, 0);
+    case 40:  // the shared-memory kernel of the m <= 48 class serves m <= 40 too
     case 48: return fwd ? run(factor_front_kernel<48, KH_NW48, true>, 48, 32 * KH_NW48, 1)
                         : run(factor_front_kernel<48, KH_NW48, false>, 48, 32 * KH_NW48, 1);
     case 64: return fwd ? run(factor_front_kernel<64, KH_NW64, true>, 64, 32 * KH_NW64, 2)

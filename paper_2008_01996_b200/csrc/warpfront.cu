@@ -67,7 +67,7 @@ __device__ unsigned long long g_wphase[8 * 8];
 #endif
 
 template <int MT>
-__global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 4 ? 3 : 2)) warp_front_kernel(
+__global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_kernel(
     KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
     double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
     double* minpiv, const int32_t* __restrict__ wdst, int32_t nshift) {
