@@ -83,6 +83,11 @@ const char* kh_last_error(void);
  * structurally symmetric pattern (duplicates and self loops allowed).
  * `leaf_size` <= 0 selects the default. */
 int kh_analyze(int64_t n, const int64_t* indptr, const int64_t* indices, int32_t leaf_size, kh_symbolic** out);
+/* kh_analyze of the union of two patterns (the FD path analyzes M_x + A_x:
+ * solvers.py:216-223, _union_symbolic) without forming the sum on the host
+ * first; rows are merged in parallel. */
+int kh_analyze_union(int64_t n, const int64_t* indptr1, const int64_t* indices1, const int64_t* indptr2,
+                     const int64_t* indices2, int32_t leaf_size, kh_symbolic** out);
 int kh_symbolic_stats_get(const kh_symbolic* s, kh_symbolic_stats* out);
 /* perm[k] = original index eliminated k-th (host array of n). */
 int kh_symbolic_perm(const kh_symbolic* s, int64_t* perm);

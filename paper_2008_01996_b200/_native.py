@@ -61,6 +61,7 @@ SIGNATURES = {
     "kh_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "kh_last_error": (ctypes.c_char_p, []),
     "kh_analyze": (ctypes.c_int, [_i64, _vp, _vp, _i32, _P(_vp)]),
+    "kh_analyze_union": (ctypes.c_int, [_i64, _vp, _vp, _vp, _vp, _i32, _P(_vp)]),
     "kh_symbolic_stats_get": (ctypes.c_int, [_vp, _P(SymbolicStats)]),
     "kh_symbolic_perm": (ctypes.c_int, [_vp, _vp]),
     "kh_symbolic_fronts": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),

@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/khb200.h"
@@ -348,6 +349,48 @@ int kh_analyze(int64_t n, const int64_t* indptr, const int64_t* indices, int32_t
   }
   *out = s;
   return KH_OK;
+}
+
+int kh_analyze_union(int64_t n, const int64_t* indptr1, const int64_t* indices1, const int64_t* indptr2,
+                     const int64_t* indices2, int32_t leaf_size, kh_symbolic** out) {
+  if (!out || (n > 0 && (!indptr1 || !indices1 || !indptr2 || !indices2))) return fail(KH_ERR_INVALID, "null argument");
+  if (n < 0) return fail(KH_ERR_DIMENSION, "negative dimension");
+  // row-wise union of the two patterns (merge of sorted rows; rows that are
+  // not sorted are concatenated and left to kh_analyze's symmetrization)
+  std::vector<int64_t> ptr(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + (indptr1[i + 1] - indptr1[i]) + (indptr2[i + 1] - indptr2[i]);
+  std::vector<int64_t> idx(ptr[n]);
+  std::vector<int64_t> len(n);
+  auto merge_rows = [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      const int64_t *a = indices1 + indptr1[i], *ae = indices1 + indptr1[i + 1];
+      const int64_t *b = indices2 + indptr2[i], *be = indices2 + indptr2[i + 1];
+      int64_t* o = idx.data() + ptr[i];
+      const bool sorted = std::is_sorted(a, ae) && std::is_sorted(b, be);
+      if (sorted) {
+        int64_t* e = std::set_union(a, ae, b, be, o);
+        len[i] = std::unique(o, e) - o;
+      } else {
+        int64_t* e = std::copy(b, be, std::copy(a, ae, o));
+        len[i] = e - o;
+      }
+    }
+  };
+  const int nth = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < 4096 || nth == 1) {
+    merge_rows(0, n);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(merge_rows, n * t / nth, n * (t + 1) / nth);
+    merge_rows(0, n / nth);
+    for (auto& x : th) x.join();
+  }
+  // compact
+  std::vector<int64_t> cptr(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) cptr[i + 1] = cptr[i] + len[i];
+  std::vector<int64_t> cidx(cptr[n]);
+  for (int64_t i = 0; i < n; ++i) std::copy(idx.begin() + ptr[i], idx.begin() + ptr[i] + len[i], cidx.begin() + cptr[i]);
+  return kh_analyze(n, cptr.data(), cidx.data(), leaf_size, out);
 }
 
 int kh_symbolic_stats_get(const kh_symbolic* s, kh_symbolic_stats* o) {

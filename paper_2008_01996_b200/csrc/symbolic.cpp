@@ -391,15 +391,17 @@ std::string analyze(int64_t n, const int64_t* indptr, const int64_t* indices,
   S.pat_ptr.assign(n + 1, 0);
   for (int64_t i = 0; i < n; ++i) S.pat_ptr[i + 1] = S.pat_ptr[i] + (g.xadj[i + 1] - g.xadj[i]) + 1;
   S.pat_idx.resize(S.pat_ptr[n]);
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t w = S.pat_ptr[i];
-    bool diag = false;
-    for (int64_t e = g.xadj[i]; e < g.xadj[i + 1]; ++e) {
-      if (!diag && g.adj[e] > i) { S.pat_idx[w++] = i; diag = true; }
-      S.pat_idx[w++] = g.adj[e];
+  parallel_rows(n, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t w = S.pat_ptr[i];
+      bool diag = false;
+      for (int64_t e = g.xadj[i]; e < g.xadj[i + 1]; ++e) {
+        if (!diag && g.adj[e] > i) { S.pat_idx[w++] = i; diag = true; }
+        S.pat_idx[w++] = g.adj[e];
+      }
+      if (!diag) S.pat_idx[w++] = i;
     }
-    if (!diag) S.pat_idx[w++] = i;
-  }
+  });
   S.nnz = S.pat_ptr[n];
   indptr = S.pat_ptr.data();   // the originals below index the analyzed CSR
   indices = S.pat_idx.data();

@@ -364,8 +364,7 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     def _spatial_setup():
         try:
             a0 = time.perf_counter()
-            pattern = (sp.csr_matrix(system.spatial.M_II) + sp.csr_matrix(system.spatial.A_II)).tocsr()
-            symbolic = sparse_direct.analyze(pattern, leaf_size)
+            symbolic = sparse_direct.analyze(system.spatial.M_II, leaf_size, union_with=system.spatial.A_II)
             phases["analyze"] = time.perf_counter() - a0
             aligned = (symbolic.align_values(system.spatial.M_II), symbolic.align_values(system.spatial.A_II))
             sparse_direct.plan_bytes(symbolic, 1, 1)  # builds the launch schedule (cached on the symbolic)

@@ -119,8 +119,12 @@ class SymbolicFactorization:
         return outs[0]
 
 
-def analyze(pattern, leaf_size=DEFAULT_LEAF_SIZE):
-    """Symbolic analysis of a sparsity pattern (symmetrized by union first)."""
+def analyze(pattern, leaf_size=DEFAULT_LEAF_SIZE, union_with=None):
+    """Symbolic analysis of a sparsity pattern (symmetrized by union first).
+
+    ``union_with``: a second pattern of the same shape; the analysis is then of
+    the union of both (the FD path's M_x + A_x, solvers.py:216-223), merged
+    natively instead of summed on the host."""
     global _analyze_calls
     # the native analysis symmetrizes the pattern itself (A | A^T, diagonal
     # added, duplicates merged) and returns that canonical CSR
@@ -132,8 +136,17 @@ def analyze(pattern, leaf_size=DEFAULT_LEAF_SIZE):
     in_idx = np.ascontiguousarray(A.indices, dtype=np.int64)
     lib = _native.load()
     raw = ctypes.c_void_p()
-    _native.check(lib.kh_analyze(n, _native.ptr(in_ptr), _native.ptr(in_idx), int(leaf_size),
-                                 ctypes.byref(raw)))
+    if union_with is None:
+        _native.check(lib.kh_analyze(n, _native.ptr(in_ptr), _native.ptr(in_idx), int(leaf_size),
+                                     ctypes.byref(raw)))
+    else:
+        B = sp.csr_matrix(union_with)
+        if B.shape != A.shape:
+            raise DimensionMismatch("patterns differ in shape")
+        b_ptr = np.ascontiguousarray(B.indptr, dtype=np.int64)
+        b_idx = np.ascontiguousarray(B.indices, dtype=np.int64)
+        _native.check(lib.kh_analyze_union(n, _native.ptr(in_ptr), _native.ptr(in_idx), _native.ptr(b_ptr),
+                                           _native.ptr(b_idx), int(leaf_size), ctypes.byref(raw)))
     handle = _Handle(raw.value)
     st = _native.SymbolicStats()
     _native.check(lib.kh_symbolic_stats_get(handle.raw, ctypes.byref(st)))
