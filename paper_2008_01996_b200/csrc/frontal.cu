@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(32 * PTR_NW) panel_trsm_kernel(KhTree T, const
   const int b = blockIdx.y;
   const KhDevFront F = T.fronts[f];
   const int m = F.p + F.q;
-  const int p = min(PIV_MAX, F.p - c0), PT = (p + 7) >> 3;  // this super-block's pivots
+  const int p = min(kh_piv_max(), F.p - c0), PT = (p + 7) >> 3;  // this super-block's pivots
   // columns c0 .. c0 + p of the panel (rows keep their front numbering)
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off + (int64_t)c0 * m;
   if (tid == 0) {
@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) panel_update_kernel(KhTree 
   Acc acc;
   __shared__ __align__(8) uint64_t bars[CP_STAGES];
   const int64_t kc = (int64_t)c0 * m;
-  tile_mma_cp<4, MODE_SCALED>(acc, PIV_MAX, P + i0 + kc, m, m - i0, P + j0 + kc, m, p - j0, P + c0 + kc, m + 1, st,
+  tile_mma_cp<4, MODE_SCALED>(acc, kh_piv_max(), P + i0 + kc, m, m - i0, P + j0 + kc, m, p - j0, P + c0 + kc, m + 1, st,
                               idle, bars);
   tile_epilogue(acc, [&](int i, int j, double2 v) {
     const int r = i0 + i, c = j0 + j;
@@ -2017,6 +2017,7 @@ cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t
                                  double2* panels, double* minpiv, double2* img, int64_t img_stride,
                                  cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
+  if (KH_PIVOT_WARP) return kh_launch_pivot_warp(T, tasks, ntasks, c0, batch, panels, minpiv, img, img_stride, stream);
   const int smem = piv_smem_bytes();
   cudaError_t e = kh_smem_optin((const void*)pivot_block_kernel, smem);
   if (e != cudaSuccess) return e;

@@ -158,7 +158,15 @@ cudaError_t kh_launch_factor_small(int ms, const KhTree& T, const int32_t* level
 // LDL^T writing the block's DMMA B image (tasks: front, scratch offset), the
 // blocked TRSM of the rows below by 8-row warps (tasks: front, row, offset),
 // the right-looking update of the later pivot columns (tasks: front, row, col).
-constexpr int kh_piv_max() { return 64; }
+// super-block width: 48 with the register-resident pivot kernel
+// (KH_PIVOT_WARP, default), 64 with the shared-memory one
+#ifndef KH_PIVOT_WARP
+#define KH_PIVOT_WARP 1
+#endif
+__host__ __device__ constexpr int kh_piv_max() { return KH_PIVOT_WARP ? 48 : 64; }
+cudaError_t kh_launch_pivot_warp(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
+                                 double2* panels, double* minpiv, double2* img, int64_t img_stride,
+                                 cudaStream_t stream);
 cudaError_t kh_launch_pivot_block(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
                                  double2* panels, double* minpiv, double2* img, int64_t img_stride,
                                  cudaStream_t stream);

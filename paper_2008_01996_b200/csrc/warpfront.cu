@@ -60,6 +60,160 @@ KH_DEV double2 shfl2w(double2 v, int src) {
 
 KH_HD constexpr int tix(int I, int J) { return I * (I + 1) / 2 + J; }
 
+// Blocked LDL^T of the register-resident tile triangle S (lower, MT x MT
+// tiles in the permuted accumulator layout) over its first p of m rows, one
+// 8-pivot block per iteration of a runtime loop: the body works on the
+// triangle relative to the current diagonal tile (S[tix(0, 0)]); after a
+// block, col(kb, nt, w, dk, Mr, Mi) writes out the finished tile column
+// (tiles S[tix(I, 0)], I < nt: L with D on the diagonal; dk = the lane's
+// pivots d_t, d_{t+4}; Mr / Mi = the block's M_j B fragments) and the
+// triangle shifts up-left by one tile (register moves): one copy of the
+// block code instead of MT. Returns the first index not eliminated (the
+// trailing triangle is then the Schur complement); minp = min |d|^2 or -1.
+template <int MT, class ColFn>
+KH_DEV int tile_ldlt(double2 (&S)[MT * (MT + 1) / 2][2], int p, int m, double& minp, ColFn col) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int rl = perm8(g);
+  const int M8 = (m + 7) >> 3;
+  int kb = 0;
+#pragma unroll 1
+  for (; kb < p; kb += 8) {
+    const int w = min(8, p - kb);
+    const int nt = M8 - (kb >> 3);  // tile rows left (>= 1)
+    double2(&Dg)[2] = S[0];
+    // E: identity in the same layout; receives the row operations -> L11^-1
+    double2 E[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) E[h] = make_double2(rl == t + 4 * h ? 1.0 : 0.0, 0.0);
+    double2 dk[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // d_{t}, d_{t+4}
+    double2 dinv_row = make_double2(0.0, 0.0);                           // 1 / d_{rl}
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < w) {
+        const int rk = rho8(k), sk = rk & 1, qk4 = rk >> 1;  // phys index, slot, quad lane
+        const double2 d = shfl2w(Dg[sk], rk * 4 + qk4);
+        const double2 colk = shfl2w(Dg[sk], (lane & ~3) | qk4);  // S[rl][k]
+        double2 sc[2], ek[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          sc[h] = shfl2w(Dg[sk], (2 * t + h) * 4 + qk4);  // S[t + 4h][k]
+          ek[h] = shfl2w(E[h], rk * 4 + t);               // E[k][t + 4h]
+        }
+        const double2 di = cinv(d);
+        const double2 l = cmul(colk, di);
+        const bool below = rl > k;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = t + 4 * h;
+          if (below && c > k && rl >= c) Dg[h] = cfms(Dg[h], l, sc[h]);
+          if (below) E[h] = cfms(E[h], l, ek[h]);
+        }
+        if (below && t == qk4) Dg[sk] = l;
+        if (t == (k & 3)) dk[k >> 2] = d;
+        if (rl == k) dinv_row = di;
+        const double a2 = cabs2(d);
+        minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
+      }
+    }
+    // M = L11^-T D^-1 as B fragments: lane (g, t), slice s holds
+    // M[t + 4s][rl] = L11^-1[rl][t + 4s] / d_rl (zero outside the w pivots)
+    double Mr[2], Mi[2], nMi[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const bool ok = rl < w && t + 4 * s < w;
+      const double2 v = ok ? cmul(E[s], dinv_row) : make_double2(0.0, 0.0);
+      Mr[s] = v.x;
+      Mi[s] = v.y;
+      nMi[s] = -v.y;
+    }
+    // B fragments of the diagonal tile's Schur rows (partial block only):
+    // L[rl][t + 4s] d_{t+4s} for t + 4s < w
+    const bool partial = w < 8;
+    double2 Bd[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      Bd[s] = (partial && t + 4 * s < w) ? cmul(Dg[s], dk[s]) : make_double2(0.0, 0.0);
+    // (b) panel tiles I >= 1: X = A M; columns >= w keep A and get the Schur
+    //     update by the block's first w pivots
+#pragma unroll
+    for (int I = 1; I < MT; ++I) {
+      if (I < nt) {
+        double2(&A)[2] = S[tix(I, 0)];
+        double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          dmma884(xr[0], xr[1], A[s].x, Mr[s]);
+          dmma884(xr[0], xr[1], A[s].y, nMi[s]);
+          dmma884(xi[0], xi[1], A[s].x, Mi[s]);
+          dmma884(xi[0], xi[1], A[s].y, Mr[s]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (t + 4 * h < w) A[h] = make_double2(xr[h], xi[h]);
+        if (partial) {
+          // A[:, w:] -= X[:, :w] (L[w:, :w] D)^T
+          double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const bool ks = t + 4 * s < w;
+            const double ar = ks ? A[s].x : 0.0, ai = ks ? A[s].y : 0.0;
+            dmma884(zr[0], zr[1], ar, Bd[s].x);
+            dmma884(zr[0], zr[1], -ai, Bd[s].y);
+            dmma884(zi[0], zi[1], ar, Bd[s].y);
+            dmma884(zi[0], zi[1], ai, Bd[s].x);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (t + 4 * h >= w) A[h] = make_double2(A[h].x - zr[h], A[h].y - zi[h]);
+        }
+      }
+    }
+    // (c) trailing tiles (I, J), 1 <= J <= I: S_IJ -= X_I (X_J D)^T, accumulated
+    //     in place: re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
+#pragma unroll
+    for (int J = 1; J < MT; ++J) {
+      if (J < nt) {
+        double nBr[2], Bi[2], nBi[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const bool ks = t + 4 * s < w;
+          const double2 bx = ks ? cmul(S[tix(J, 0)][s], dk[s]) : make_double2(0.0, 0.0);
+          nBr[s] = -bx.x;
+          Bi[s] = bx.y;
+          nBi[s] = -bx.y;
+        }
+#pragma unroll
+        for (int I = J; I < MT; ++I) {
+          if (I < nt) {
+            double2(&C)[2] = S[tix(I, J)];
+            double cr[2] = {C[0].x, C[1].x}, ci[2] = {C[0].y, C[1].y};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const bool ks = t + 4 * s < w;
+              const double ar = ks ? S[tix(I, 0)][s].x : 0.0, ai = ks ? S[tix(I, 0)][s].y : 0.0;
+              dmma884(cr[0], cr[1], ar, nBr[s]);
+              dmma884(cr[0], cr[1], ai, Bi[s]);
+              dmma884(ci[0], ci[1], ar, nBi[s]);
+              dmma884(ci[0], ci[1], ai, nBr[s]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) C[h] = make_double2(cr[h], ci[h]);
+          }
+        }
+      }
+    }
+    col(kb, nt, w, dk, Mr, Mi);
+    // (e) shift the trailing triangle to the origin
+#pragma unroll
+    for (int I = 1; I < MT; ++I)
+#pragma unroll
+      for (int J = 1; J <= I; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) S[tix(I - 1, J - 1)][h] = S[tix(I, J)][h];
+  }
+  return kb;
+}
+
 #ifdef KH_PHASE_TIMING
 // debug builds only (profiles/probes/phase_timing.py): clock64 cycles per phase
 // of warp_front_kernel, summed over warps, [MT][phase], phase 7 = warp count
@@ -218,143 +372,14 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_k
   }
 
   wphase(2);
-  // ---- blocked LDL^T over the p pivots, one 8-pivot block per iteration of a
-  // runtime loop: the body works on the tile triangle relative to the current
-  // diagonal tile (S[tix(0, 0)]); after a block its finished tile column is
-  // written out and the triangle shifts up-left by one tile (register moves),
-  // so the kernel holds one copy of the block code instead of MT.
+  // ---- blocked LDL^T over the p pivots (tile_ldlt); the finished tile columns
+  // go to the panel, the Schur columns of a partial block to the staged update
+  // block
   double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
   double2* Uo = upd_cur + (int64_t)b * upd_stride_cur + F.upd_off;
   double minp = DBL_MAX;  // min |d|^2 (-1: non-finite pivot)
-  int kb = 0;
-#pragma unroll 1
-  for (; kb < p; kb += 8) {
-    const int w = min(8, p - kb);
-    const int nt = M8 - (kb >> 3);  // tile rows left (>= 1)
-    double2(&Dg)[2] = S[0];
-    // E: identity in the same layout; receives the row operations -> L11^-1
-    double2 E[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) E[h] = make_double2(rl == t + 4 * h ? 1.0 : 0.0, 0.0);
-    double2 dk[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // d_{t}, d_{t+4}
-    double2 dinv_row = make_double2(0.0, 0.0);                           // 1 / d_{rl}
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k < w) {
-        const int rk = rho8(k), sk = rk & 1, qk4 = rk >> 1;  // phys index, slot, quad lane
-        const double2 d = shfl2w(Dg[sk], rk * 4 + qk4);
-        const double2 colk = shfl2w(Dg[sk], (lane & ~3) | qk4);  // S[rl][k]
-        double2 sc[2], ek[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          sc[h] = shfl2w(Dg[sk], (2 * t + h) * 4 + qk4);  // S[t + 4h][k]
-          ek[h] = shfl2w(E[h], rk * 4 + t);               // E[k][t + 4h]
-        }
-        const double2 di = cinv(d);
-        const double2 l = cmul(colk, di);
-        const bool below = rl > k;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = t + 4 * h;
-          if (below && c > k && rl >= c) Dg[h] = cfms(Dg[h], l, sc[h]);
-          if (below) E[h] = cfms(E[h], l, ek[h]);
-        }
-        if (below && t == qk4) Dg[sk] = l;
-        if (t == (k & 3)) dk[k >> 2] = d;
-        if (rl == k) dinv_row = di;
-        const double a2 = cabs2(d);
-        minp = (a2 != a2 || minp < 0.0) ? -1.0 : fmin(minp, a2);
-      }
-    }
-    // M = L11^-T D^-1 as B fragments: lane (g, t), slice s holds
-    // M[t + 4s][rl] = L11^-1[rl][t + 4s] / d_rl (zero outside the w pivots)
-    double Mr[2], Mi[2], nMi[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const bool ok = rl < w && t + 4 * s < w;
-      const double2 v = ok ? cmul(E[s], dinv_row) : make_double2(0.0, 0.0);
-      Mr[s] = v.x;
-      Mi[s] = v.y;
-      nMi[s] = -v.y;
-    }
-    // B fragments of the diagonal tile's Schur rows (partial block only):
-    // L[rl][t + 4s] d_{t+4s} for t + 4s < w
-    const bool partial = w < 8;
-    double2 Bd[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-      Bd[s] = (partial && t + 4 * s < w) ? cmul(Dg[s], dk[s]) : make_double2(0.0, 0.0);
-    // (b) panel tiles I >= 1: X = A M; columns >= w keep A and get the Schur
-    //     update by the block's first w pivots
-#pragma unroll
-    for (int I = 1; I < MT; ++I) {
-      if (I < nt) {
-        double2(&A)[2] = S[tix(I, 0)];
-        double xr[2] = {0.0, 0.0}, xi[2] = {0.0, 0.0};
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          dmma884(xr[0], xr[1], A[s].x, Mr[s]);
-          dmma884(xr[0], xr[1], A[s].y, nMi[s]);
-          dmma884(xi[0], xi[1], A[s].x, Mi[s]);
-          dmma884(xi[0], xi[1], A[s].y, Mr[s]);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (t + 4 * h < w) A[h] = make_double2(xr[h], xi[h]);
-        if (partial) {
-          // A[:, w:] -= X[:, :w] (L[w:, :w] D)^T
-          double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const bool ks = t + 4 * s < w;
-            const double ar = ks ? A[s].x : 0.0, ai = ks ? A[s].y : 0.0;
-            dmma884(zr[0], zr[1], ar, Bd[s].x);
-            dmma884(zr[0], zr[1], -ai, Bd[s].y);
-            dmma884(zi[0], zi[1], ar, Bd[s].y);
-            dmma884(zi[0], zi[1], ai, Bd[s].x);
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (t + 4 * h >= w) A[h] = make_double2(A[h].x - zr[h], A[h].y - zi[h]);
-        }
-      }
-    }
-    // (c) trailing tiles (I, J), 1 <= J <= I: S_IJ -= X_I (X_J D)^T, accumulated
-    //     in place: re += Ar (-Br) + Ai Bi, im += Ar (-Bi) + Ai (-Br)
-#pragma unroll
-    for (int J = 1; J < MT; ++J) {
-      if (J < nt) {
-        double nBr[2], Bi[2], nBi[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const bool ks = t + 4 * s < w;
-          const double2 bx = ks ? cmul(S[tix(J, 0)][s], dk[s]) : make_double2(0.0, 0.0);
-          nBr[s] = -bx.x;
-          Bi[s] = bx.y;
-          nBi[s] = -bx.y;
-        }
-#pragma unroll
-        for (int I = J; I < MT; ++I) {
-          if (I < nt) {
-            double2(&C)[2] = S[tix(I, J)];
-            double cr[2] = {C[0].x, C[1].x}, ci[2] = {C[0].y, C[1].y};
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const bool ks = t + 4 * s < w;
-              const double ar = ks ? S[tix(I, 0)][s].x : 0.0, ai = ks ? S[tix(I, 0)][s].y : 0.0;
-              dmma884(cr[0], cr[1], ar, nBr[s]);
-              dmma884(cr[0], cr[1], ai, Bi[s]);
-              dmma884(ci[0], ci[1], ar, nBi[s]);
-              dmma884(ci[0], ci[1], ai, nBr[s]);
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) C[h] = make_double2(cr[h], ci[h]);
-          }
-        }
-      }
-    }
-    // (d) the finished tile column: pivot columns to the panel, the Schur
-    //     columns of a partial block to the update block
+  const int kb = tile_ldlt<MT>(S, p, m, minp, [&](int kb, int nt, int, const double2 (&)[2], const double (&)[2],
+                                              const double (&)[2]) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = kb + t + 4 * h;
@@ -368,14 +393,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_k
         }
       }
     }
-    // (e) shift the trailing triangle to the origin
-#pragma unroll
-    for (int I = 1; I < MT; ++I)
-#pragma unroll
-      for (int J = 1; J <= I; ++J)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) S[tix(I - 1, J - 1)][h] = S[tix(I, J)][h];
-  }
+  });
   wphase(3);
   // ---- the rest is the update block (rows and columns >= kb >= p)
 #pragma unroll
@@ -405,6 +423,75 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_k
   wphase(4);
 }
 
+// Pivot block of a large front's super-block (see pivot_block_kernel in
+// frontal.cu for the shared-memory version and panel_trsm_kernel for the
+// consumer): one warp per (front, shift), four shifts per CTA. The w x w
+// diagonal block at (c0, c0) of the assembled panel (w <= 8 MT) is loaded
+// into registers in the permuted accumulator layout, factored by tile_ldlt,
+// and written back (L with D on the diagonal) together with the block's DMMA
+// B image: for tile pair (j, k < j) the lane's own L_jk values times d_k, for
+// (j, j) the M_j fragments of the Gauss-Jordan inverse -- both are already in
+// the B-fragment layout in registers, so the image costs one store per value.
+template <int MT>
+__global__ void __launch_bounds__(32 * WF_WARPS, 2) pivot_warp_kernel(KhTree T, const int32_t* __restrict__ tasks,
+                                                                     int c0, double2* panels, double* minpiv,
+                                                                     double2* img, int64_t img_stride,
+                                                                     int32_t nshift) {
+  constexpr int NTL = MT * (MT + 1) / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3, rl = perm8(g);
+  const int32_t f = tasks[2 * blockIdx.x];
+  const int64_t off = tasks[2 * blockIdx.x + 1];
+  const int b = blockIdx.y * WF_WARPS + warp;
+  if (b >= nshift) return;
+  const KhDevFront F = T.fronts[f];
+  const int mf = F.p + F.q, w = min(8 * MT, F.p - c0);
+  double2* P = panels + (int64_t)b * T.panel_total + F.panel_off + c0 + (int64_t)c0 * mf;
+  double2 S[NTL][2];
+#pragma unroll
+  for (int I = 0; I < MT; ++I)
+#pragma unroll
+    for (int J = 0; J <= I; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * I + rl, c = 8 * J + t + 4 * h;
+        S[tix(I, J)][h] = (r < w && r >= c) ? P[r + (int64_t)c * mf] : make_double2(0.0, 0.0);
+      }
+  double2* im = img + (int64_t)b * img_stride + off + lane;
+  double minp = DBL_MAX;
+  tile_ldlt<MT>(S, w, w, minp, [&](int kb, int nt, int wb, const double2 (&dk)[2], const double (&Mr)[2],
+                                   const double (&Mi)[2]) {
+    const int KB = kb >> 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = kb + t + 4 * h;
+      double2* pc = P + (int64_t)c * mf;
+#pragma unroll
+      for (int I = 0; I < MT; ++I) {
+        const int r = kb + 8 * I + rl;
+        if (I < nt && r < w && c < w && (I > 0 || rl >= t + 4 * h)) pc[r] = S[tix(I, 0)][h];
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < MT; ++I) {
+      if (I < nt) {
+        const int tp = (KB + I) * (KB + I + 1) / 2 + KB;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          double2 v = make_double2(0.0, 0.0);
+          if (t + 4 * s < wb) v = I == 0 ? make_double2(Mr[s], Mi[s]) : cmul(S[tix(I, 0)][s], dk[s]);
+          im[(tp * 2 + s) * 32] = v;
+        }
+      }
+    }
+  });
+  if (lane == 0) {
+    double* mp = minpiv + (int64_t)b * T.nf + f;
+    const double v = minp < 0.0 ? -1.0 : sqrt(minp);
+    *mp = c0 == 0 ? v : fmin(*mp, v);
+  }
+}
+
 }  // namespace
 
 #ifdef KH_PHASE_TIMING
@@ -427,6 +514,16 @@ int kh_warp_front_slot(int32_t m, int32_t p, int32_t r, int32_t c) {
   const int lane = pr * 4 + (pc >> 1), h = pc & 1;
   (void)p;
   return (J * M8 - J * (J - 1) / 2 + I - J) * 64 + h * 32 + lane;
+}
+
+cudaError_t kh_launch_pivot_warp(const KhTree& T, const int32_t* tasks, int32_t ntasks, int c0, int32_t batch,
+                                 double2* panels, double* minpiv, double2* img, int64_t img_stride,
+                                 cudaStream_t stream) {
+  if (ntasks == 0 || batch == 0) return cudaSuccess;
+  const dim3 grid(ntasks, (batch + WF_WARPS - 1) / WF_WARPS);
+  pivot_warp_kernel<6><<<grid, 32 * WF_WARPS, 0, stream>>>(T, tasks, c0, panels, minpiv, img, img_stride, batch);
+  kh_note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t kh_launch_warp_front(int mt, const KhTree& T, const int32_t* level_fronts, int32_t nlev,
