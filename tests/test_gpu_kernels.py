@@ -150,6 +150,8 @@ def test_rhs_dimension_check(cuda_ok):
     (("square", 64), "0", None, None), (("lshape", 4), "0", None, None),
     # fused classes capped at m <= 64 / leaves large enough for the 96 and 128 classes
     (("square", 64), "64", None, None), (("square", 96), None, 80, None), (("square", 64), None, 8, None),
+    # the fused m <= 128 class (off by default: those fronts take the large-front path)
+    (("square", 96), "128", 80, None),
     # m <= 48 through the shared-memory fused kernel instead of the register-resident warp kernel
     (("square", 64), None, None, "0"), (("lshape", 4), None, 16, "0"),
     # warp kernels with small leaves (partial 8-pivot blocks, p < 8)
