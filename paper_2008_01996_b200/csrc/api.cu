@@ -121,7 +121,8 @@ struct kh_plan {
   std::vector<int32_t> cls_off;
   const int32_t* classes(int32_t d) const { return cls_off.data() + kClsStride * d; }
   std::vector<int32_t> task_off;   // Schur-update tasks of level d: [task_off[d], task_off[d+1])
-  std::vector<int32_t> small_panel_max;  // per level: largest lower panel among the warp-solve fronts
+  // per level and warp-solve class: largest lower panel (the class's shared-memory size)
+  std::vector<int32_t> small_panel_max;
   // per level: largest lower panel and m among the other fronts when they all
   // fit the bulk-copy staged solve kernels' shared memory (else 0)
   std::vector<int32_t> mid_panel_max, mid_m_max;
@@ -563,13 +564,16 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     X.level_off.push_back((int32_t)X.lf.size());
   }
   for (const auto& lev : S.levels) {
-    int32_t mx = 1;
+    // per class: the solve kernels of a class are launched with that class's
+    // largest panel as shared memory (occupancy of the small classes)
+    int32_t mx[kSolveSmallClasses];
+    for (int c = 0; c < kSolveSmallClasses; ++c) mx[c] = 1;
     for (int32_t f : lev) {
       const kh::Front& F = S.fronts[f];
-      if (front_class(F.m()) < kSolveSmallClasses)
-        mx = std::max<int32_t>(mx, F.p * F.m() - F.p * (F.p - 1) / 2);
+      const int c = front_class(F.m());
+      if (c < kSolveSmallClasses) mx[c] = std::max<int32_t>(mx[c], F.p * F.m() - F.p * (F.p - 1) / 2);
     }
-    X.small_panel_max.push_back(mx);
+    for (int c = 0; c < kSolveSmallClasses; ++c) X.small_panel_max.push_back(mx[c]);
     int32_t pm = 0, mm = 0;
     for (int32_t f : lev) {
       const kh::Front& F = S.fronts[f];
@@ -939,7 +943,9 @@ int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* 
   for (int32_t d = 0; d <= p->depth; ++d) {
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
-    KH_CUDA(kh_launch_bwd_small(T, lev, co[L], ns, panels, p->y, p->small_panel_max[d], p->side[0]));
+    for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
+      KH_CUDA(kh_launch_bwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y,
+                                  p->small_panel_max[L * d + c], p->side[c]));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
                                 p->y, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));
@@ -1075,8 +1081,9 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     const int32_t* co = p->classes(d);
     double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    KH_CUDA(kh_launch_fwd_small(T, lev, co[L], ns, panels, p->y, rc, sc, rch, sch, p->small_panel_max[d],
-                                p->side[0]));
+    for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
+      KH_CUDA(kh_launch_fwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y, rc, sc, rch, sch,
+                                  p->small_panel_max[L * d + c], p->side[c]));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
                                 rch, sch, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));
