@@ -33,7 +33,10 @@ namespace {
 
 constexpr int NT = 256;      // threads per CTA
 constexpr int TB = 64;       // complex tile edge
-constexpr int KC = 16;       // complex K chunk
+#ifndef KH_TILE_KC
+#define KH_TILE_KC 8
+#endif
+constexpr int KC = KH_TILE_KC;  // complex K chunk of the tile engine
 constexpr int LDS = TB + 2;  // padded smem row (double2): conflict-free LDS.128 fragments
 constexpr int NB = 32;       // pivot block width
 
@@ -122,7 +125,7 @@ constexpr int MODE_SCALED = 0;
 // cp.async ring depth of the tile engine (chunks in flight ahead of the one
 // being consumed: KH_CP_STAGES - 1)
 #ifndef KH_CP_STAGES
-#define KH_CP_STAGES 2
+#define KH_CP_STAGES 4
 #endif
 constexpr int CP_STAGES = KH_CP_STAGES;
 
@@ -2050,7 +2053,8 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
                             const double2* panels, double2* upd_cur, int64_t upd_stride_cur, const double2* upd_child,
                             int64_t upd_stride_child, cudaStream_t stream) {
   if (ntasks == 0 || batch == 0) return cudaSuccess;
-  const int smem = (int)(CP_STAGES * sizeof(CpStage));
+  // the operand ring, reused by the epilogue's 64 x 65 product tile
+  const int smem = (int)std::max(CP_STAGES * sizeof(CpStage), sizeof(double2) * TB * (TB + 1));
   cudaError_t e = kh_smem_optin((const void*)schur_update_kernel, smem);
   if (e != cudaSuccess) return e;
   schur_update_kernel<<<dim3(ntasks, batch), NT, smem, stream>>>(T, tasks, panels, upd_cur, upd_stride_cur,

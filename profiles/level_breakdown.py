@@ -13,7 +13,7 @@ for r in rows[1:]:
     key = r[hdr["ID"]]
     d = launch.setdefault(key, {"name": r[hdr["Kernel Name"]], "grid": r[hdr["Grid Size"]]})
     d[r[hdr["Metric Name"]]] = float(r[hdr["Metric Value"]].replace(",", ""))
-FACT = re.compile(r"(warp_front|factor_front|big_|schur_update|pivot_block|panel_)")
+FACT = re.compile(r"(warp_front|factor_front|big_|schur_update|pivot_|panel_)")
 seq = [v for v in launch.values()]
 # first factorization: from the first FACT launch to the rowreduce after it
 i0 = next(i for i, v in enumerate(seq) if FACT.search(v["name"]))
