@@ -365,30 +365,54 @@ __global__ void __launch_bounds__(NT, KH_SCHUR_MINB) schur_update_kernel(KhTree 
   double2* Ct = reinterpret_cast<double2*>(smem_raw);  // [64 columns][TB + 1]
   tile_epilogue(acc, [&](int i, int j, double2 v) { Ct[j * (TB + 1) + i] = v; });
   __syncthreads();  // kids visible even when p = 0; the product tile complete
-  // thread: tile row i (fixed), columns jb, jb + 4, ..., jb + 60
+  // packed column base of every tile column in every (cached) child, once per CTA
+  __shared__ int cbs[MAXC][TB];
+  const int nkc = min(kids.n, MAXC);
+  for (int e = threadIdx.x; e < nkc * TB; e += NT) {
+    const int k = e / TB, j = e - k * TB, c = j0 + j;
+    const ChildRef C = kids.c[k];
+    const int cj = c < q ? C.cmap[p + c] : -1;
+    cbs[k][j] = cj >= 0 ? cj * (2 * C.q - cj - 1) / 2 : -1;
+  }
+  __syncthreads();
+  // thread: tile row i (fixed), columns jb, jb + 4, ..., jb + 60, in two passes
+  // of 8; children two at a time with all their loads issued before the adds
+  // (which stay in child order: deterministic sums)
   const int i = threadIdx.x & (TB - 1), jb = threadIdx.x >> 6;
   const int r = i0 + i;
-  double2 v[TB / 4];
+  if (r >= q) return;
+  constexpr int HU = TB / 8;
+  auto colbase = [&](int k, int j) -> int {
+    if (k < MAXC) return cbs[k][j];
+    const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+    const int c = j0 + j, cj = c < q ? C.cmap[p + c] : -1;
+    return cj >= 0 ? cj * (2 * C.q - cj - 1) / 2 : -1;
+  };
 #pragma unroll
-  for (int u = 0; u < TB / 4; ++u) v[u] = make_double2(0.0, 0.0);
-  if (r < q) {
-    for (int k = 0; k < kids.n; ++k) {
-      const ChildRef C = kid(T, F, upd_child, upd_stride_child, b, kids, k);
-      const int ci = C.cmap[p + r];
-      if (ci < 0) continue;
-      int cj[TB / 4];
+  for (int half = 0; half < 2; ++half) {
+    double2 v[HU];
 #pragma unroll
-      for (int u = 0; u < TB / 4; ++u) {
-        const int c = j0 + jb + 4 * u;
-        cj[u] = c <= r ? C.cmap[p + c] : -1;
+    for (int u = 0; u < HU; ++u) v[u] = make_double2(0.0, 0.0);
+    for (int k = 0; k < kids.n; k += 2) {
+      const ChildRef C0 = kid(T, F, upd_child, upd_stride_child, b, kids, k);
+      const bool two = k + 1 < kids.n;
+      const ChildRef C1 = two ? kid(T, F, upd_child, upd_stride_child, b, kids, k + 1) : C0;
+      const int ci0 = C0.cmap[p + r], ci1 = two ? C1.cmap[p + r] : -1;
+      double2 a0[HU], a1[HU];
+#pragma unroll
+      for (int u = 0; u < HU; ++u) {
+        const int j = jb + 4 * (half * HU + u), c = j0 + j;
+        const int b0 = ci0 >= 0 && c <= r ? colbase(k, j) : -1;
+        const int b1 = ci1 >= 0 && c <= r ? colbase(k + 1, j) : -1;
+        a0[u] = b0 >= 0 ? C0.U[b0 + ci0] : make_double2(0.0, 0.0);
+        a1[u] = b1 >= 0 ? C1.U[b1 + ci1] : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < TB / 4; ++u)
-        if (cj[u] >= 0) v[u] = cadd(v[u], C.U[kh_upk32(C.q, ci, cj[u])]);
+      for (int u = 0; u < HU; ++u) v[u] = cadd(cadd(v[u], a0[u]), a1[u]);
     }
 #pragma unroll
-    for (int u = 0; u < TB / 4; ++u) {
-      const int j = jb + 4 * u, c = j0 + j;
+    for (int u = 0; u < HU; ++u) {
+      const int j = jb + 4 * (half * HU + u), c = j0 + j;
       if (c <= r) U[kh_upk32(q, r, c)] = csub(v[u], Ct[j * (TB + 1) + i]);
     }
   }
