@@ -945,7 +945,7 @@ int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* 
     const int32_t* co = p->classes(d);
     for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
       KH_CUDA(kh_launch_bwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y,
-                                  p->small_panel_max[L * d + c], p->side[c]));
+                                  p->small_panel_max[L * d + c], p->side[c], kClassMax[c]));
     KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
                                 p->y, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));
@@ -1083,7 +1083,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
     const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
     for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
       KH_CUDA(kh_launch_fwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y, rc, sc, rch, sch,
-                                  p->small_panel_max[L * d + c], p->side[c]));
+                                  p->small_panel_max[L * d + c], p->side[c], kClassMax[c]));
     KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
                                 rch, sch, st, p->mid_panel_max[d], p->mid_m_max[d]));
     KH_CUDA(join_side(p, st));

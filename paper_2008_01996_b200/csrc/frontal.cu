@@ -1519,7 +1519,9 @@ constexpr int SOLVE_CH = 8;   // columns per warp_sum8 reduction (bwd)
 #ifndef KH_FWD_TMA_NW
 #define KH_FWD_TMA_NW 1
 #endif
-template <int NW>
+// R = 2: lanes own rows lane and lane + 32 (m <= 64); R = 1: m <= 32, one row
+// per lane (the m <= 32 class: no work on rows that cannot exist).
+template <int NW, int R>
 __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                                 int32_t nlev, const double2* __restrict__ panels,
                                                                 double2* y, double2* ru_cur, int64_t ru_stride_cur,
@@ -1551,30 +1553,37 @@ __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const 
   const int r0 = lane, r1 = lane + 32;
   const double2 z = make_double2(0.0, 0.0);
   double2 x0 = z, x1 = z;
+  KH_ASSERT(R == 2 || m <= 32);
   for (int c = F.child_begin; c < F.child_end; ++c) {
     const KhKid C = T.kids[c];
     const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
     const int32_t* cm = T.cmap + C.cmap_begin;
     const int c0 = r0 < m ? cm[r0] : -1;
-    const int c1 = r1 < m ? cm[r1] : -1;
     if (c0 >= 0) x0 = cadd(x0, rc[c0]);
-    if (c1 >= 0) x1 = cadd(x1, rc[c1]);
+    if (R == 2) {
+      const int c1 = r1 < m ? cm[r1] : -1;
+      if (c1 >= 0) x1 = cadd(x1, rc[c1]);
+    }
   }
   if (r0 < p) x0 = cadd(x0, yy[r0]);
-  if (r1 < p) x1 = cadd(x1, yy[r1]);
+  if (R == 2 && r1 < p) x1 = cadd(x1, yy[r1]);
   mbar_wait(br, 0);
   for (int k = 0; k < p; ++k) {
     const double2* col = Ls + cbase(k) - k;  // L[r, k] = col[r], r >= k
     const double2 l0 = (r0 > k && r0 < m) ? col[r0] : z;
-    const double2 l1 = (r1 > k && r1 < m) ? col[r1] : z;
-    const double2 yk = shfl2(k < 32 ? x0 : x1, k & 31);
+    const double2 yk = shfl2(R == 1 || k < 32 ? x0 : x1, k & 31);
     x0 = cfms(x0, l0, yk);
-    x1 = cfms(x1, l1, yk);
+    if (R == 2) {
+      const double2 l1 = (r1 > k && r1 < m) ? col[r1] : z;
+      x1 = cfms(x1, l1, yk);
+    }
   }
   if (r0 < p) yy[r0] = x0;
   else if (r0 < m) ru[r0 - p] = x0;
-  if (r1 < p) yy[r1] = x1;
-  else if (r1 < m) ru[r1 - p] = x1;
+  if (R == 2) {
+    if (r1 < p) yy[r1] = x1;
+    else if (r1 < m) ru[r1 - p] = x1;
+  }
 }
 
 // Backward solve of the fronts with m <= 64, one warp per (front, shift), the
@@ -1589,7 +1598,7 @@ __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const 
 #ifndef KH_BWD_TMA_NW
 #define KH_BWD_TMA_NW 1
 #endif
-template <int NW>
+template <int NW, int R>
 __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                                 int32_t nlev, const double2* __restrict__ panels,
                                                                 double2* y, int32_t maxe) {
@@ -1619,9 +1628,10 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
   const int64_t* urows = T.urows + F.rows_begin;
   const double2 z = make_double2(0.0, 0.0);
   const double2 xu0 = lane < q ? yb[urows[lane]] : z;
-  const double2 xu1 = lane + 32 < q ? yb[urows[lane + 32]] : z;
+  const double2 xu1 = R == 2 && lane + 32 < q ? yb[urows[lane + 32]] : z;
   const int k0 = lane, k1 = lane + 32;
-  const double2 y0 = k0 < p ? yy[k0] : z, y1 = k1 < p ? yy[k1] : z;
+  const double2 y0 = k0 < p ? yy[k0] : z, y1 = R == 2 && k1 < p ? yy[k1] : z;
+  KH_ASSERT(R == 2 || m <= 32);
   mbar_wait(br, 0);
   double2 t0 = z, t1 = z;
   for (int kc = 0; kc < p; kc += SOLVE_CH) {
@@ -1631,12 +1641,16 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
       const int k = kc + u;
       const double2* col = Ls + cbase(k) + (p - k);  // L21[:, k]
       const double2 l0 = (k < p && lane < q) ? col[lane] : z;
-      const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
-      sv[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
+      if (R == 2) {
+        const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
+        sv[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
+      } else {
+        sv[u] = cmul(l0, xu0);
+      }
     }
     const double2 v = warp_sum8(sv, lane);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < R; ++h) {
       const int kk = lane + 32 * h, u = kk - kc;
       const int src = ((u >> 2) & 1) << 4 | ((u >> 1) & 1) << 3 | (u & 1) << 2;
       const double2 got = shfl2(v, src & 31);
@@ -1647,15 +1661,15 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
     }
   }
   if (k0 < p) t0 = csub(cmul(y0, cinv(Ls[cbase(k0)])), t0);
-  if (k1 < p) t1 = csub(cmul(y1, cinv(Ls[cbase(k1)])), t1);
+  if (R == 2 && k1 < p) t1 = csub(cmul(y1, cinv(Ls[cbase(k1)])), t1);
   // L11^T x = t bottom-up (column form: x_i final -> t_k -= L[i, k] x_i, k < i)
   for (int i = p - 1; i > 0; --i) {
-    const double2 xi = shfl2(i < 32 ? t0 : t1, i & 31);
+    const double2 xi = shfl2(R == 1 || i < 32 ? t0 : t1, i & 31);
     if (k0 < i) t0 = cfms(t0, Ls[cbase(k0) + i - k0], xi);
-    if (k1 < i) t1 = cfms(t1, Ls[cbase(k1) + i - k1], xi);
+    if (R == 2 && k1 < i) t1 = cfms(t1, Ls[cbase(k1) + i - k1], xi);
   }
   if (k0 < p) yy[k0] = t0;
-  if (k1 < p) yy[k1] = t1;
+  if (R == 2 && k1 < p) yy[k1] = t1;
 }
 
 // Backward solve of the large fronts of a narrow level (top of the tree):
@@ -2090,29 +2104,36 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
 cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
                                 const double2* ru_child, int64_t ru_stride_child, int32_t max_panel,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int32_t max_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   constexpr int nw = KH_FWD_TMA_NW;
   const int smem = 16 * nw * max_panel;
-  cudaError_t e = kh_smem_optin((const void*)fwd_small_tma_kernel<nw>, smem);
-  if (e != cudaSuccess) return e;
-  fwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(
-      T, level_fronts, nlev, panels, y, ru_cur, ru_stride_cur, ru_child, ru_stride_child, max_panel);
-  kh_note_launch();
-  return cudaGetLastError();
+  auto run = [&](auto kernel) -> cudaError_t {
+    cudaError_t e = kh_smem_optin((const void*)kernel, smem);
+    if (e != cudaSuccess) return e;
+    kernel<<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(
+        T, level_fronts, nlev, panels, y, ru_cur, ru_stride_cur, ru_child, ru_stride_child, max_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  };
+  return max_m <= 32 ? run(fwd_small_tma_kernel<nw, 1>) : run(fwd_small_tma_kernel<nw, 2>);
 }
 
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream) {
+                                const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream,
+                                int32_t max_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
   constexpr int nw = KH_BWD_TMA_NW;
   const int smem = 16 * nw * max_panel;
-  cudaError_t e = kh_smem_optin((const void*)bwd_small_tma_kernel<nw>, smem);
-  if (e != cudaSuccess) return e;
-  bwd_small_tma_kernel<nw><<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(T, level_fronts, nlev,
-                                                                                       panels, y, max_panel);
-  kh_note_launch();
-  return cudaGetLastError();
+  auto run = [&](auto kernel) -> cudaError_t {
+    cudaError_t e = kh_smem_optin((const void*)kernel, smem);
+    if (e != cudaSuccess) return e;
+    kernel<<<dim3((nlev + nw - 1) / nw, batch), 32 * nw, smem, stream>>>(T, level_fronts, nlev, panels, y,
+                                                                         max_panel);
+    kh_note_launch();
+    return cudaGetLastError();
+  };
+  return max_m <= 32 ? run(bwd_small_tma_kernel<nw, 1>) : run(bwd_small_tma_kernel<nw, 2>);
 }
 
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,

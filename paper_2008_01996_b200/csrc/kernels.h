@@ -103,11 +103,12 @@ cudaError_t kh_launch_schur(const KhTree& T, const int32_t* tasks, int32_t ntask
 cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 const double2* panels, double2* y, double2* ru_cur, int64_t ru_stride_cur,
                                 const double2* ru_child, int64_t ru_stride_child, int32_t max_panel,
-                                cudaStream_t stream);
+                                cudaStream_t stream, int32_t max_m = 64);
 // max_panel: largest lower-panel entry count p m - p (p - 1) / 2 among the fronts
 // (sizes the shared-memory staging of the bulk-copy variant)
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
-                                const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream);
+                                const double2* panels, double2* y, int32_t max_panel, cudaStream_t stream,
+                                int32_t max_m = 64);
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
                                 cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0);
