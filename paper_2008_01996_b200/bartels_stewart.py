@@ -6,8 +6,9 @@ All N_t shifted matrices M_x + S_kk A_x are factored in one batched call
 (they are independent); only the triangular back-substitution over k is
 sequential: rhs_k = G_k - A_x (Z[:, k+1:] S[k, k+1:]^T), a DMMA GEMV plus the
 fused CSR residual kernel, then one solve with the retained factors.
-`solve_bs_real` (2 M_x symmetric-indefinite systems, solvers.py:226-301) is
-not provided: pivot-free LDL^T is not safe on indefinite matrices.
+`solve_bs_real` (solvers.py:226-301) follows the reference's real-Schur block
+recursion; each 2 x 2 block's 2 M_x indefinite system is solved as the
+equivalent complex-symmetric M_x system (see its docstring).
 """
 
 import time
@@ -126,6 +127,142 @@ def solve_bs_complex(system, pencil=None, leaf_size=sparse_direct.DEFAULT_LEAF_S
     return SpaceTimeSolution(coefficients=coeffs), report
 
 
-def solve_bs_real(system, pencil=None):
-    raise UsageError("bs-real (real Schur, 2M_x indefinite systems) is not part of the B200 build; "
-                     "use 'bs-complex' or 'fd'")
+def _real_schur_blocks(R):
+    """Diagonal blocks of a standardized real Schur form (LAPACK dgees):
+    (k, k) for a real eigenvalue, (k-1, k) for a 2 x 2 block [[a, b1], [b2, a]]
+    with b1 b2 < 0, scanned from the bottom as the reference does
+    (solvers.py:256-257)."""
+    blocks, k = [], R.shape[0] - 1
+    while k >= 0:
+        if k == 0 or R[k, k - 1] == 0.0:
+            blocks.append((k, k))
+            k -= 1
+        else:
+            blocks.append((k - 1, k))
+            k -= 2
+    return blocks
+
+
+def solve_bs_real(system, pencil=None, leaf_size=sparse_direct.DEFAULT_LEAF_SIZE):
+    """Bartels-Stewart with a real Schur form (reference solvers.py:226-301).
+
+    Same block back-substitution over the quasi-triangular R as the
+    reference, the spatial systems on the GPU. A real eigenvalue R_kk is one
+    shifted system M_x + R_kk A_x (solvers.py:258-268). A standardized 2 x 2
+    block [[a, b1], [b2, a]] couples z_{k-1}, z_k through
+        D z_{k-1} + b1 A z_k = r1,   b2 A z_{k-1} + D z_k = r2   (D = M + a A),
+    which the reference solves as one scaled 2 M_x symmetric-indefinite system
+    (solvers.py:269-289). Here the same pair is ONE complex-symmetric M_x
+    system: with beta = sqrt(-b1 b2) and c = beta / b2,
+        (M + (a + i beta) A) w = r1 + i c r2,   z_{k-1} = Re w,  z_k = Im w / c,
+    (expand and use beta^2 = -b1 b2), so it goes through the batched pivot-free
+    LDL^T with the shifted matrices of bs-complex/FD (M_x + lambda A_x with
+    Re lambda > 0 is complex symmetric with an SPD real part; the indefinite
+    real 2 M_x form would need pivoting). The solution is the same up to
+    rounding; one symbolic analysis serves every block (the reference runs a
+    second one for the 2 M_x pattern: `analyze_calls` is 1 here).
+    """
+    import torch
+
+    from .dense import RealSchurForm, spd_solve
+    from .engine import _fortran
+    from .solvers import SolveReport, SpaceTimeSolution, build_pencil, residual
+
+    _native.require_cuda()
+    report = SolveReport(variant="bs-real", dof=system.dof, n_t=system.n_t, m_x=system.m_x)
+    t0 = time.perf_counter()
+    if pencil is None:
+        pencil = build_pencil(system.temporal, "bs-real")
+    if not isinstance(pencil.form, RealSchurForm) and not hasattr(pencil.form, "R"):
+        raise DimensionMismatch("solve_bs_real needs a real Schur pencil")
+    Q, Rs = np.asarray(pencil.form.Q, dtype=np.float64), np.asarray(pencil.form.R, dtype=np.float64)
+    n, nt = system.m_x, system.n_t
+    blocks = _real_schur_blocks(Rs)
+    lam = np.empty(len(blocks), dtype=np.complex128)
+    scale = np.ones(len(blocks))
+    for s, (i, k) in enumerate(blocks):
+        if i == k:
+            lam[s] = Rs[k, k]
+        else:
+            a, b1, b2 = Rs[i, i], Rs[i, k], Rs[k, i]
+            if b1 * b2 >= 0.0:
+                raise DimensionMismatch("real Schur 2 x 2 block is not standardized (b1 b2 >= 0)")
+            beta = np.sqrt(-b1 * b2)
+            lam[s] = complex(a, beta)
+            scale[s] = beta / b2
+    w_in = spd_solve(pencil.chol_A, Q)                         # G = F A_t^-1 Q
+    report.t_decompose = time.perf_counter() - t0
+    report.min_re_lambda = pencil.min_re_lambda
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f64 = torch.float64
+    st = _native.stream_handle()
+    t0 = time.perf_counter()
+    F = torch.from_numpy(np.ascontiguousarray(system.rhs, dtype=np.float64)).to(dev)
+    d_win = _fortran(w_in, dev)
+    G = torch.empty((nt, n), dtype=f64, device=dev)
+    _native.call("kh_dgemm", n, nt, nt, 1.0, F.data_ptr(), n, d_win.data_ptr(), nt, 0.0, G.data_ptr(), n, st)
+    torch.cuda.synchronize()
+    report.t_transform_in = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    before = sparse_direct.analyze_call_count()
+    M = system.spatial.M_II.tocsr()
+    A = system.spatial.A_II.tocsr()
+    sym = sparse_direct.analyze((M + A).tocsr(), leaf_size)
+    mv, av = sym.align_values(M), sym.align_values(A)
+    ns = len(blocks)
+    free, _ = torch.cuda.mem_get_info(dev)
+    free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    batch = ns
+    while batch > 1 and sparse_direct.plan_bytes(sym, batch, ns) > 0.7 * free:
+        batch = (batch + 1) // 2
+    if sparse_direct.plan_bytes(sym, batch, ns) > 0.7 * free:
+        raise UsageError("bs-real needs every block's factors resident; not enough device memory")
+    plan = sparse_direct._Plan(sym, mv, av, batch, ns, dev.index)
+    for s0 in range(0, ns, batch):
+        plan.factor(s0, lam[s0:s0 + batch], st)
+    plan.pivot_check(0, ns, st)
+    d_ptr = torch.from_numpy(sym.indptr).to(dev)
+    d_idx = torch.from_numpy(sym.indices).to(dev)
+    d_mv = torch.from_numpy(mv).to(dev)
+    d_av = torch.from_numpy(av).to(dev)
+    d_rt = _fortran(np.ascontiguousarray(Rs.T), dev)            # column j of R^T = row j of R
+    Z = torch.zeros((nt, n), dtype=f64, device=dev)
+    # residual operands [Y1 | Y2] = [0 | C]: one buffer per block width, Y1 never written
+    Ys = {1: torch.zeros((2, n), dtype=f64, device=dev), 2: torch.zeros((4, n), dtype=f64, device=dev)}
+    Rr = torch.empty((2, n), dtype=f64, device=dev)
+    Wi = torch.empty((1, n), dtype=f64, device=dev)
+    zero = torch.zeros((1, n), dtype=f64, device=dev)
+    norms = torch.zeros(2, dtype=f64, device=dev)
+    zp, gp, rp, rtp = Z.data_ptr(), G.data_ptr(), Rr.data_ptr(), d_rt.data_ptr()
+    for s, (i, k) in enumerate(blocks):
+        w = k - i + 1                                           # 1 or 2 coupled columns
+        m = nt - k - 1
+        yp = Ys[w].data_ptr()
+        if m > 0:   # (the first block has C = 0: its buffer is still zero)
+            # C = Z[:, k+1:] R[i:k+1, k+1:]^T  (acc of solvers.py:265-267, :284-288)
+            _native.call("kh_dgemm", n, w, m, 1.0, zp + 8 * (k + 1) * n, n, rtp + 8 * ((k + 1) + i * nt), nt,
+                         0.0, yp + 8 * w * n, n, st)
+        # rhs = G[:, i:k+1] - A_x C
+        _native.call("kh_csr_pair_residual", n, w, d_ptr.data_ptr(), d_idx.data_ptr(), d_mv.data_ptr(),
+                     d_av.data_ptr(), yp, n, gp + 8 * i * n, n, rp, n, norms.data_ptr(), st)
+        if w == 1:
+            plan.solve(s, 1, rp, zero.data_ptr(), n, zp + 8 * k * n, Wi.data_ptr(), n, st)
+            continue
+        c = scale[s]
+        _native.call("kh_daxpy", n, c - 1.0, rp + 8 * n, rp + 8 * n, st)          # r2 <- c r2
+        plan.solve(s, 1, rp, rp + 8 * n, n, zp + 8 * i * n, zp + 8 * k * n, n, st)
+        _native.call("kh_daxpy", n, 1.0 / c - 1.0, zp + 8 * k * n, zp + 8 * k * n, st)  # z_k = Im w / c
+    torch.cuda.synchronize()
+    report.analyze_calls = sparse_direct.analyze_call_count() - before
+    report.t_spatial = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    U = torch.empty((nt, n), dtype=f64, device=dev)
+    d_qt = _fortran(np.ascontiguousarray(Q.T), dev)
+    _native.call("kh_dgemm", n, nt, nt, 1.0, zp, n, d_qt.data_ptr(), nt, 0.0, U.data_ptr(), n, st)
+    coeffs = U.reshape(-1).cpu().numpy()
+    report.t_transform_out = time.perf_counter() - t0
+    report.residual = residual(system, coeffs)
+    return SpaceTimeSolution(coefficients=coeffs), report

@@ -229,3 +229,33 @@ def test_fd_accepts_reference_pencil(cuda_ok, name):
     assert rep.sigma_min == pytest.approx(float(ref["fd_sigma_min"]), rel=1e-12)
     assert rep.min_re_lambda == pytest.approx(float(ref["fd_min_re_lambda"]), rel=1e-12)
     assert rep.t_total == pytest.approx(rep.t_decompose + rep.t_transform_in + rep.t_spatial + rep.t_transform_out)
+
+
+@pytest.mark.parametrize("name", ["lshape0", "odd", "random_11", "random_12", "random_13", "c1"])
+def test_bs_real_matches_reference(cuda_ok, name):
+    # bsreal.npz: the reference's own solve_bs_real on the same systems (tests/golden/make_golden_bsreal.py)
+    import os
+
+    from conftest import GOLDEN
+
+    system, ref = load_golden(name)
+    z = np.load(os.path.join(GOLDEN, "bsreal.npz"))
+    sol, rep = solvers.solve(system, "bs-real")
+    assert rep.variant == "bs-real"
+    assert rel_diff(sol.coefficients, z[f"{name}_bsr"]) < 1e-11
+    assert rel_diff(sol.coefficients, ref["bs"]) < 1e-11
+    assert rep.residual < 1e-12
+    assert rep.analyze_calls == 1   # one union analysis serves the real and the paired blocks
+    assert rep.min_re_lambda == pytest.approx(float(z[f"{name}_bsr_min_re_lambda"]), rel=1e-10)
+
+
+def test_bs_real_matches_oracle_on_graded_mesh(cuda_ok):
+    # odd N_t on a graded mesh: a real eigenvalue among the 2 x 2 blocks, c2-like spatial pattern
+    from oracle import fd_oracle as orc
+    from paper_2008_01996_b200 import problems
+
+    system, _ = problems.build_system(mesh=("square", 24), n_t=13, rhs="seeded", j_max=50_000, grading=2.0)
+    sol, rep = solvers.solve_bs_real(system)
+    ref = orc.solve_bs_real(*orc.system_arrays(system))
+    assert rel_diff(sol.coefficients, ref) < 1e-10
+    assert orc.residual(*orc.system_arrays(system), sol.coefficients) < 1e-12

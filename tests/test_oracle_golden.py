@@ -1,10 +1,12 @@
 """The CPU oracle (oracle/fd_oracle.py) pinned against outputs of the
 reference package itself (tests/golden/*.npz, made by make_golden.py)."""
 
+import os
+
 import numpy as np
 import pytest
 
-from conftest import load_golden, rel_diff
+from conftest import GOLDEN, load_golden, rel_diff
 from oracle import fd_oracle as orc
 
 SMALL = ["lshape0", "odd", "random_11", "random_12", "random_13"]
@@ -26,6 +28,17 @@ def test_oracle_bs_complex_matches_reference(name):
     u = orc.solve_bs_complex(*orc.system_arrays(system))
     assert rel_diff(u, ref["bs"]) < 1e-12
     assert orc.residual(*orc.system_arrays(system), u) < 1e-12
+
+
+@pytest.mark.parametrize("name", SMALL + ["c1"])
+def test_oracle_bs_real_matches_reference(name):
+    # bsreal.npz: the reference's solve_bs_real on the same stored systems (make_golden_bsreal.py)
+    system, _ = load_golden(name)
+    ref = np.load(os.path.join(GOLDEN, "bsreal.npz"))
+    u = orc.solve_bs_real(*orc.system_arrays(system))
+    assert rel_diff(u, ref[f"{name}_bsr"]) < 1e-12
+    assert orc.residual(*orc.system_arrays(system), u) == pytest.approx(float(ref[f"{name}_bsr_residual"]),
+                                                                        rel=1e-3, abs=1e-15)
 
 
 @pytest.mark.parametrize("name", SMALL)
