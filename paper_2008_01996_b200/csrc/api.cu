@@ -1,4 +1,10 @@
 // C-ABI of libkhb200 (declared in include/khb200.h).
+#ifndef KH_DEFAULT_LANES
+#define KH_DEFAULT_LANES 2
+#endif
+#ifndef KH_DEFAULT_SOLVE_LANES
+#define KH_DEFAULT_SOLVE_LANES 2
+#endif
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,9 +151,21 @@ struct kh_plan {
   // side streams: the fused-front kernels of a level run there (one stream
   // per size class, so the classes overlap each other's tails), concurrently
   // with the large-front kernels on the caller's stream; levels are joined
-  cudaStream_t side[kSmallClasses] = {};
-  cudaEvent_t ev_main = nullptr, ev_side[kSmallClasses] = {};
-  cudaEvent_t ev_fwd = nullptr;  // large fronts' panels final (fused forward sweep may start)
+  // Shift lanes: a batch of shifts is split into n_lanes contiguous groups,
+  // each walking the tree on its own stream set (lane 0's main stream is the
+  // caller's): one lane's latency-bound kernels (pivot blocks, narrow-level
+  // solves, level tails) overlap the other lanes' throughput-bound ones.
+  struct Lane {
+    cudaStream_t main = nullptr;  // lanes >= 1 (owned); lane 0 runs on the caller's stream
+    cudaStream_t side[kSmallClasses] = {};
+    cudaEvent_t ev_main = nullptr, ev_side[kSmallClasses] = {};
+    cudaEvent_t ev_fwd = nullptr;   // large fronts' panels final (fused forward sweep may start)
+    cudaEvent_t ev_done = nullptr;  // the lane's work is queued up to here (joined by the caller's stream)
+  };
+  static constexpr int kMaxLanes = 4;
+  Lane lane[kMaxLanes];
+  int factor_lanes = 1, solve_lanes = 1;
+  cudaEvent_t ev_fork = nullptr;
   // optional per-level timing of the factorization (kh_plan_set_level_timing):
   // lvl_ev[i] recorded on the caller's stream before level depth - i and at the end
   bool level_timing = false;
@@ -205,34 +223,94 @@ namespace {
 void plan_release(kh_plan* p) {
   if (p->owned) cudaFree(p->owned);
   p->owned = nullptr;
-  if (p->ev_main) cudaEventDestroy(p->ev_main);
-  p->ev_main = nullptr;
-  if (p->ev_fwd) cudaEventDestroy(p->ev_fwd);
-  p->ev_fwd = nullptr;
   for (cudaEvent_t e : p->lvl_ev) cudaEventDestroy(e);
   p->lvl_ev.clear();
-  for (int c = 0; c < kSmallClasses; ++c) {
-    if (p->ev_side[c]) cudaEventDestroy(p->ev_side[c]);
-    if (p->side[c]) cudaStreamDestroy(p->side[c]);
-    p->ev_side[c] = nullptr;
-    p->side[c] = nullptr;
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  p->ev_fork = nullptr;
+  for (kh_plan::Lane& L : p->lane) {
+    for (cudaEvent_t* e : {&L.ev_main, &L.ev_fwd, &L.ev_done}) {
+      if (*e) cudaEventDestroy(*e);
+      *e = nullptr;
+    }
+    for (int c = 0; c < kSmallClasses; ++c) {
+      if (L.ev_side[c]) cudaEventDestroy(L.ev_side[c]);
+      if (L.side[c]) cudaStreamDestroy(L.side[c]);
+      L.ev_side[c] = nullptr;
+      L.side[c] = nullptr;
+    }
+    if (L.main) cudaStreamDestroy(L.main);
+    L.main = nullptr;
   }
 }
 
+cudaError_t lane_create(kh_plan::Lane& L, bool own_main) {
+  cudaError_t e = cudaSuccess;
+  if (own_main) e = cudaStreamCreateWithFlags(&L.main, cudaStreamNonBlocking);
+  for (int c = 0; c < kSmallClasses; ++c) {
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&L.side[c], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&L.ev_side[c], cudaEventDisableTiming);
+  }
+  for (cudaEvent_t* ev : {&L.ev_main, &L.ev_fwd, &L.ev_done})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  return e;
+}
+
+int env_lanes(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  const int n = v ? std::atoi(v) : dflt;
+  return std::min(std::max(n, 1), kh_plan::kMaxLanes);
+}
+
 // fork: the side streams start after the work queued so far on `st`
-cudaError_t fork_side(kh_plan* p, cudaStream_t st) {
-  cudaError_t e = cudaEventRecord(p->ev_main, st);
-  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(p->side[c], p->ev_main, 0);
+cudaError_t fork_side(kh_plan::Lane& L, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(L.ev_main, st);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(L.side[c], L.ev_main, 0);
   return e;
 }
 
 // join every way: the next level on any stream sees this level's results
-cudaError_t join_side(kh_plan* p, cudaStream_t st) {
+cudaError_t join_side(kh_plan::Lane& L, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaEventRecord(p->ev_side[c], p->side[c]);
-  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(st, p->ev_side[c], 0);
-  if (e == cudaSuccess) e = cudaEventRecord(p->ev_main, st);
-  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(p->side[c], p->ev_main, 0);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaEventRecord(L.ev_side[c], L.side[c]);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(st, L.ev_side[c], 0);
+  if (e == cudaSuccess) e = cudaEventRecord(L.ev_main, st);
+  for (int c = 0; c < kSmallClasses && e == cudaSuccess; ++c) e = cudaStreamWaitEvent(L.side[c], L.ev_main, 0);
+  return e;
+}
+
+// One contiguous group of a batch's shifts and the streams it runs on.
+struct LaneRun {
+  kh_plan::Lane* L;
+  cudaStream_t st;
+  int64_t off;  // first shift of the group inside the batch (index into the per-batch work buffers)
+  int32_t ns;
+};
+
+// Split ns shifts into at most `lanes` groups (multiples of 4 shifts: the
+// register-resident front kernels put four shifts of a front in one CTA) and
+// fork the extra lanes' streams off the caller's.
+cudaError_t lanes_begin(kh_plan* p, int lanes, int32_t ns, cudaStream_t st, std::vector<LaneRun>& runs) {
+  int32_t per = (ns + lanes - 1) / lanes;
+  per = (per + 3) & ~3;
+  runs.clear();
+  for (int32_t off = 0, l = 0; off < ns; off += per, ++l)
+    runs.push_back({&p->lane[l], l == 0 ? st : p->lane[l].main, off, std::min(per, ns - off)});
+  cudaError_t e = cudaSuccess;
+  if (runs.size() > 1) {
+    e = cudaEventRecord(p->ev_fork, st);
+    for (size_t l = 1; l < runs.size() && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(runs[l].st, p->ev_fork, 0);
+  }
+  for (size_t l = 0; l < runs.size() && e == cudaSuccess; ++l) e = fork_side(*runs[l].L, runs[l].st);
+  return e;
+}
+
+// The caller's stream waits for the extra lanes.
+cudaError_t lanes_end(cudaStream_t st, std::vector<LaneRun>& runs) {
+  cudaError_t e = cudaSuccess;
+  for (size_t l = 1; l < runs.size() && e == cudaSuccess; ++l) {
+    e = cudaEventRecord(runs[l].L->ev_done, runs[l].st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, runs[l].L->ev_done, 0);
+  }
   return e;
 }
 
@@ -810,12 +888,11 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
     e = cudaMalloc(reinterpret_cast<void**>(&p->owned), measure.off);
     C.base = p->owned;
   }
-  for (int c = 0; c < kSmallClasses; ++c) {
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side[c], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_side[c], cudaEventDisableTiming);
-  }
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_main, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fwd, cudaEventDisableTiming);
+  p->factor_lanes = env_lanes("KH_LANES", KH_DEFAULT_LANES);
+  p->solve_lanes = env_lanes("KH_SOLVE_LANES", KH_DEFAULT_SOLVE_LANES);
+  for (int l = 0; l < std::max(p->factor_lanes, p->solve_lanes) && e == cudaSuccess; ++l)
+    e = lane_create(p->lane[l], l > 0);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) {
     carve(p, S, X, C);
     auto up = [&](void* dst, const void* src, size_t bytes) {
@@ -873,8 +950,6 @@ namespace {
 int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_ri, cudaStream_t st, bool fwd) {
   KH_CUDA(cudaMemcpyAsync(p->lam, lambda_ri, nshift * 16, cudaMemcpyHostToDevice, st));
   const KhTree T = p->tree();
-  double2* panels = p->panels + slot0 * p->panel_total;
-  KH_CUDA(fork_side(p, st));
   if (p->level_timing && p->lvl_ev.size() < (size_t)p->depth + 2) {
     for (size_t i = p->lvl_ev.size(); i < (size_t)p->depth + 2; ++i) {
       cudaEvent_t e;
@@ -882,44 +957,56 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
       p->lvl_ev.push_back(e);
     }
   }
+  // per-level timing describes the single-lane schedule (levels of different lanes overlap otherwise)
+  std::vector<LaneRun> runs;
+  KH_CUDA(lanes_begin(p, p->level_timing ? 1 : p->factor_lanes, (int32_t)nshift, st, runs));
   for (int32_t d = p->depth; d >= 0; --d) {
     if (p->level_timing) KH_CUDA(cudaEventRecord(p->lvl_ev[p->depth - d], st));
     const int32_t* lev = p->level_fronts + p->level_off[d];
     const int32_t* co = p->classes(d);
-    double2 *uc = p->upd[d & 1], *uch = p->upd[(d + 1) & 1];
     const int64_t sc = p->upd_size[d & 1], sch = p->upd_size[(d + 1) & 1];
-    const int32_t ns = (int32_t)nshift;
-    const KhFwd fw{p->y, p->rupd[d & 1], p->rupd_size[d & 1], p->rupd[(d + 1) & 1], p->rupd_size[(d + 1) & 1]};
-    for (int c = 0; c < kSmallClasses; ++c) {
-      if (p->warp_mt[c] && !fwd)
-        KH_CUDA(kh_launch_warp_front(p->warp_mt[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                     uch, sch, p->minpiv_work, p->wdst, p->side[c]));
-      else
-        KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, p->lam, panels, uc, sc,
-                                       uch, sch, p->minpiv_work, p->side[c], fwd ? &fw : nullptr));
-    }
+    const int64_t rs = p->rupd_size[d & 1], rsh = p->rupd_size[(d + 1) & 1];
     const kh_plan::BigLevel& B = p->big[d];
-    KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, p->lam, panels, uch, sch, st));
-    for (int32_t sbi = 0; sbi < B.nsb; ++sbi) {
-      const kh_plan::SuperBlock& K = p->sbinfo[B.sb_off + sbi];
-      const int c0 = kh_piv_max() * sbi;
-      KH_CUDA(kh_launch_pivot_block(T, p->btasks + K.piv_off, K.piv_n, c0, ns, panels, p->minpiv_work, p->minv,
-                                    p->minv_size, st));
-      KH_CUDA(kh_launch_panel_solve(T, p->btasks + K.trsm_off, K.trsm_n, c0, ns, panels, p->minv, p->minv_size, st));
-      KH_CUDA(kh_launch_panel_update(T, p->btasks + K.upd_off, K.upd_n, c0, ns, panels, st));
+    for (const LaneRun& R : runs) {
+      kh_plan::Lane& L = *R.L;
+      const int32_t ns = R.ns;
+      double2* panels = p->panels + (slot0 + R.off) * p->panel_total;
+      double2 *uc = p->upd[d & 1] + R.off * sc, *uch = p->upd[(d + 1) & 1] + R.off * sch;
+      const double2* lam = p->lam + R.off;
+      double* minpiv = p->minpiv_work + R.off * p->nf;
+      double2* minv = p->minv + R.off * p->minv_size;
+      const KhFwd fw{p->y + R.off * p->n, p->rupd[d & 1] + R.off * rs, rs, p->rupd[(d + 1) & 1] + R.off * rsh, rsh};
+      for (int c = 0; c < kSmallClasses; ++c) {
+        if (p->warp_mt[c] && !fwd)
+          KH_CUDA(kh_launch_warp_front(p->warp_mt[c], T, lev + co[c], co[c + 1] - co[c], ns, lam, panels, uc, sc, uch,
+                                       sch, minpiv, p->wdst, L.side[c]));
+        else
+          KH_CUDA(kh_launch_factor_small(kClassMax[c], T, lev + co[c], co[c + 1] - co[c], ns, lam, panels, uc, sc,
+                                         uch, sch, minpiv, L.side[c], fwd ? &fw : nullptr));
+      }
+      KH_CUDA(kh_launch_big_assemble(T, p->btasks + B.asm_off, B.asm_n, ns, lam, panels, uch, sch, R.st));
+      for (int32_t sbi = 0; sbi < B.nsb; ++sbi) {
+        const kh_plan::SuperBlock& K = p->sbinfo[B.sb_off + sbi];
+        const int c0 = kh_piv_max() * sbi;
+        KH_CUDA(kh_launch_pivot_block(T, p->btasks + K.piv_off, K.piv_n, c0, ns, panels, minpiv, minv, p->minv_size,
+                                      R.st));
+        KH_CUDA(kh_launch_panel_solve(T, p->btasks + K.trsm_off, K.trsm_n, c0, ns, panels, minv, p->minv_size, R.st));
+        KH_CUDA(kh_launch_panel_update(T, p->btasks + K.upd_off, K.upd_n, c0, ns, panels, R.st));
+      }
+      if (fwd) {  // the level's large fronts: panels are final after their trsm;
+                  // their forward sweep runs on a side stream beside the Schur kernel
+        KH_CUDA(cudaEventRecord(L.ev_fwd, R.st));
+        KH_CUDA(cudaStreamWaitEvent(L.side[0], L.ev_fwd, 0));
+        KH_CUDA(kh_launch_fwd_level(T, lev + co[kSmallClasses], co[kSmallClasses + 1] - co[kSmallClasses], ns,
+                                    p->max_m, panels, fw.y, fw.ru_cur, fw.ru_stride_cur, fw.ru_child,
+                                    fw.ru_stride_child, L.side[0]));
+      }
+      KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
+                              sc, uch, sch, R.st));
+      KH_CUDA(join_side(L, R.st));
     }
-    if (fwd) {  // the level's large fronts: panels are final after their trsm;
-                // their forward sweep runs on a side stream beside the Schur kernel
-      KH_CUDA(cudaEventRecord(p->ev_fwd, st));
-      KH_CUDA(cudaStreamWaitEvent(p->side[0], p->ev_fwd, 0));
-      KH_CUDA(kh_launch_fwd_level(T, lev + co[kSmallClasses], co[kSmallClasses + 1] - co[kSmallClasses], ns,
-                                  p->max_m, panels, p->y, fw.ru_cur, fw.ru_stride_cur, fw.ru_child,
-                                  fw.ru_stride_child, p->side[0]));
-    }
-    KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
-                            sc, uch, sch, st));
-    KH_CUDA(join_side(p, st));
   }
+  KH_CUDA(lanes_end(st, runs));
   if (p->level_timing) KH_CUDA(cudaEventRecord(p->lvl_ev[p->depth + 1], st));
   KH_CUDA(kh_launch_rowreduce(p->minpiv_work, p->nf, (int32_t)nshift, 1, p->minpiv + slot0, st));
   KH_CUDA(kh_launch_shift_absmax_nnz(p->mv, p->av, p->nnz, (int32_t)nshift, p->lam, p->absmax_work,
@@ -934,22 +1021,48 @@ int check_batch(kh_plan* p, int64_t slot0, int64_t nshift) {
   return KH_OK;
 }
 
+// one level of the forward / backward sweep for one lane's shifts
+int solve_fwd_level(kh_plan* p, const KhTree& T, const LaneRun& R, int64_t slot0, int32_t d) {
+  constexpr int L = kSolveSmallClasses;  // fronts with m <= 64 use the warp-per-front kernels, the rest the CTA ones
+  const double2* panels = p->panels + (slot0 + R.off) * p->panel_total;
+  double2* y = p->y + R.off * p->n;
+  const int32_t* lev = p->level_fronts + p->level_off[d];
+  const int32_t* co = p->classes(d);
+  const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
+  double2 *rc = p->rupd[d & 1] + R.off * sc, *rch = p->rupd[(d + 1) & 1] + R.off * sch;
+  for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
+    KH_CUDA(kh_launch_fwd_small(T, lev + co[c], co[c + 1] - co[c], R.ns, panels, y, rc, sc, rch, sch,
+                                p->small_panel_max[L * d + c], R.L->side[c], kClassMax[c]));
+  KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], R.ns, p->max_m, panels, y, rc, sc, rch,
+                              sch, R.st, p->mid_panel_max[d], p->mid_m_max[d]));
+  KH_CUDA(join_side(*R.L, R.st));
+  return KH_OK;
+}
+
+int solve_bwd_level(kh_plan* p, const KhTree& T, const LaneRun& R, int64_t slot0, int32_t d) {
+  constexpr int L = kSolveSmallClasses;
+  const double2* panels = p->panels + (slot0 + R.off) * p->panel_total;
+  double2* y = p->y + R.off * p->n;
+  const int32_t* lev = p->level_fronts + p->level_off[d];
+  const int32_t* co = p->classes(d);
+  for (int c = 0; c < L; ++c)
+    KH_CUDA(kh_launch_bwd_small(T, lev + co[c], co[c + 1] - co[c], R.ns, panels, y, p->small_panel_max[L * d + c],
+                                R.L->side[c], kClassMax[c]));
+  KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], R.ns, p->max_p, p->max_m, panels, y,
+                              R.st, p->mid_panel_max[d], p->mid_m_max[d]));
+  KH_CUDA(join_side(*R.L, R.st));
+  return KH_OK;
+}
+
 // backward sweep from p->y (forward-solved) and the scatter to x
 int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* x_im, int64_t ldx, cudaStream_t st) {
   const KhTree T = p->tree();
-  const double2* panels = p->panels + slot0 * p->panel_total;
-  constexpr int L = kSolveSmallClasses;
-  KH_CUDA(fork_side(p, st));
-  for (int32_t d = 0; d <= p->depth; ++d) {
-    const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->classes(d);
-    for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
-      KH_CUDA(kh_launch_bwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y,
-                                  p->small_panel_max[L * d + c], p->side[c], kClassMax[c]));
-    KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_p, p->max_m, panels,
-                                p->y, st, p->mid_panel_max[d], p->mid_m_max[d]));
-    KH_CUDA(join_side(p, st));
-  }
+  std::vector<LaneRun> runs;
+  KH_CUDA(lanes_begin(p, p->solve_lanes, ns, st, runs));
+  for (int32_t d = 0; d <= p->depth; ++d)
+    for (const LaneRun& R : runs)
+      if (int rc = solve_bwd_level(p, T, R, slot0, d)) return rc;
+  KH_CUDA(lanes_end(st, runs));
   KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
   return KH_OK;
 }
@@ -1070,25 +1183,20 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   DeviceGuard dev_guard(p->device);
   KH_CUDA(dev_guard.err);
   const KhTree T = p->tree();
-  const double2* panels = p->panels + slot0 * p->panel_total;
   const int32_t ns = (int32_t)nshift;
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
-  KH_CUDA(fork_side(p, st));
-  // fronts with m <= 64 use the warp-per-front kernels, the rest the CTA ones
-  constexpr int L = kSolveSmallClasses;
-  for (int32_t d = p->depth; d >= 0; --d) {
-    const int32_t* lev = p->level_fronts + p->level_off[d];
-    const int32_t* co = p->classes(d);
-    double2 *rc = p->rupd[d & 1], *rch = p->rupd[(d + 1) & 1];
-    const int64_t sc = p->rupd_size[d & 1], sch = p->rupd_size[(d + 1) & 1];
-    for (int c = 0; c < L; ++c)  // one launch per class (its own shared-memory size), on its own side stream
-      KH_CUDA(kh_launch_fwd_small(T, lev + co[c], co[c + 1] - co[c], ns, panels, p->y, rc, sc, rch, sch,
-                                  p->small_panel_max[L * d + c], p->side[c], kClassMax[c]));
-    KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], ns, p->max_m, panels, p->y, rc, sc,
-                                rch, sch, st, p->mid_panel_max[d], p->mid_m_max[d]));
-    KH_CUDA(join_side(p, st));
-  }
-  return solve_bwd_impl(p, slot0, ns, x_re, x_im, ldx, st);
+  // each lane runs its forward sweep and goes straight into its backward sweep
+  std::vector<LaneRun> runs;
+  KH_CUDA(lanes_begin(p, p->solve_lanes, ns, st, runs));
+  for (int32_t d = p->depth; d >= 0; --d)
+    for (const LaneRun& R : runs)
+      if (int rc = solve_fwd_level(p, T, R, slot0, d)) return rc;
+  for (int32_t d = 0; d <= p->depth; ++d)
+    for (const LaneRun& R : runs)
+      if (int rc = solve_bwd_level(p, T, R, slot0, d)) return rc;
+  KH_CUDA(lanes_end(st, runs));
+  KH_CUDA(kh_launch_scatter_sol(p->n, ns, p->perm, p->y, x_re, x_im, ldx, st));
+  return KH_OK;
 }
 
 int kh_plan_residual_scale(kh_plan* p, int64_t nt, const double* Y, int64_t ldy, const double* F, int64_t ldf,
