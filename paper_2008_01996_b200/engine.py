@@ -204,6 +204,9 @@ class FDEngine:
             raise DimensionMismatch("spatial matrices must be square and of equal shape")
         self.n = M.shape[0]
         self.modal = modal
+        # optional hook on_iterate(U, fresh) of the refinement: called right after U
+        # received a correction (fresh=True) or lost it again (an undone step)
+        self.on_iterate = None
         self.n_t = modal.n_t
         self.n_k = modal.n_k
         self.sym = symbolic if symbolic is not None else sparse_direct.analyze((M + A).tocsr(), leaf_size)
@@ -474,10 +477,14 @@ class FDEngine:
         self.fd_apply(self.R, corr, accumulate=False)
         st = self._stream()
         _native.call("kh_daxpy", U.numel(), 1.0, corr.data_ptr(), U.data_ptr(), st)
+        if self.on_iterate is not None:
+            self.on_iterate(U, True)  # e.g. solve_fd starts the device-to-host copy beside the residual
         new = self._rel(self.residual(U, F, dd=dd))
         if not new < rel:
             # rounding floor reached: undo the step, keep the best iterate
             _native.call("kh_daxpy", U.numel(), -1.0, corr.data_ptr(), U.data_ptr(), st)
+            if self.on_iterate is not None:
+                self.on_iterate(U, False)  # U changed again: what was taken above is stale
             self.gpu_launches += 2
             return new, rel, False
         self.gpu_launches += 1

@@ -366,8 +366,13 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
             a0 = time.perf_counter()
             symbolic = sparse_direct.analyze(system.spatial.M_II, leaf_size, union_with=system.spatial.A_II)
             phases["analyze"] = time.perf_counter() - a0
-            aligned = (symbolic.align_values(system.spatial.M_II), symbolic.align_values(system.spatial.A_II))
-            sparse_direct.plan_bytes(symbolic, 1, 1)  # builds the launch schedule (cached on the symbolic)
+            # M_x and A_x aligned on the analyzed pattern and the launch schedule
+            # (cached on the symbolic), side by side: all three are native calls
+            with ThreadPoolExecutor(max_workers=2) as side:
+                fa = side.submit(symbolic.align_values, system.spatial.A_II)
+                fs = side.submit(sparse_direct.plan_bytes, symbolic, 1, 1)
+                aligned = (symbolic.align_values(system.spatial.M_II), fa.result())
+                fs.result()
             phases["aligned"] = time.perf_counter() - t0
             lam_ready.wait()
             if "stub" not in lam_box:  # the pencil failed on the main thread
@@ -464,10 +469,33 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
     report.fd_residual = rel
     # u += FD(f - K u): a step that does not help is undone; stagnation of the
     # fp64 residual above refine_tol switches to the compensated residual
+    # the device-to-host copy of an iterate starts right after its correction,
+    # on a second stream beside the residual that decides whether it is final
+    # (a later correction or an undone step supersedes the copy)
+    taken = {"host": None, "valid": False}
+    copy_stream = torch.cuda.Stream(dev)
+
+    def _take(Ucur, fresh):
+        taken["valid"] = fresh
+        if fresh:
+            if taken["host"] is None:
+                taken["host"] = torch.empty(Ucur.numel(), dtype=Ucur.dtype, pin_memory=True)
+            copy_stream.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(copy_stream):
+                taken["host"].copy_(Ucur.reshape(-1), non_blocking=True)
+
+    if os.environ.get("KH_D2H_OVERLAP", "1") != "0":
+        eng.on_iterate = _take
     rel, steps = eng.refine(U, F, rel, refine, refine_tol)
+    eng.on_iterate = None
     report.residual_mode = eng.residual_mode
     with nvtx.range("kh.solve_fd.d2h"):
-        coeffs = _to_host(U.reshape(-1))
+        if taken["valid"]:
+            copy_stream.synchronize()
+            coeffs = taken["host"].numpy()
+        else:
+            copy_stream.synchronize()  # a superseded copy must not outlive U
+            coeffs = _to_host(U.reshape(-1))
     report.t_refine = time.perf_counter() - t0
     report.refine_steps = steps
     report.residual = rel
