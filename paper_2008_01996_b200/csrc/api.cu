@@ -132,6 +132,7 @@ struct kh_plan {
   // per level: largest lower panel and m among the other fronts when they all
   // fit the bulk-copy staged solve kernels' shared memory (else 0)
   std::vector<int32_t> mid_panel_max, mid_m_max;
+  std::vector<int32_t> big_m_max;  // per level: largest m among the fronts with m > 64 (streamed solves' stage size)
   int32_t* tasks = nullptr;        // device (front, tile row, tile col) triples
   // large-front schedule: per level an assembly list and per 32-wide pivot
   // block the diag / left-looking / TRSM lists (offsets into btasks, int32s)
@@ -556,7 +557,7 @@ namespace {
 #endif
 
 struct Sched {
-  std::vector<int32_t> small_panel_max, mid_panel_max, mid_m_max;
+  std::vector<int32_t> small_panel_max, mid_panel_max, mid_m_max, big_m_max;
   std::vector<KhDevFront> df, lf_df;
   std::vector<KhKid> kids;
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
@@ -663,6 +664,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
     const bool fits = pm > 0 && pm + mm <= KH_MID_MAX_ENTRIES;
     X.mid_panel_max.push_back(fits ? pm : 0);
     X.mid_m_max.push_back(fits ? mm : 0);
+    X.big_m_max.push_back(mm);
   }
   X.lf_df.resize(X.lf.size());
   for (size_t i = 0; i < X.lf.size(); ++i) {
@@ -870,6 +872,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->small_panel_max = X.small_panel_max;
   p->mid_panel_max = X.mid_panel_max;
   p->mid_m_max = X.mid_m_max;
+  p->big_m_max = X.big_m_max;
   for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
   p->big = X.big;
   p->sbinfo = X.sbinfo;
@@ -999,7 +1002,7 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
         KH_CUDA(cudaStreamWaitEvent(L.side[0], L.ev_fwd, 0));
         KH_CUDA(kh_launch_fwd_level(T, lev + co[kSmallClasses], co[kSmallClasses + 1] - co[kSmallClasses], ns,
                                     p->max_m, panels, fw.y, fw.ru_cur, fw.ru_stride_cur, fw.ru_child,
-                                    fw.ru_stride_child, L.side[0]));
+                                    fw.ru_stride_child, L.side[0], 0, 0, p->big_m_max[d]));
       }
       KH_CUDA(kh_launch_schur(T, p->tasks + 3 * p->task_off[d], p->task_off[d + 1] - p->task_off[d], ns, panels, uc,
                               sc, uch, sch, R.st));
@@ -1034,7 +1037,7 @@ int solve_fwd_level(kh_plan* p, const KhTree& T, const LaneRun& R, int64_t slot0
     KH_CUDA(kh_launch_fwd_small(T, lev + co[c], co[c + 1] - co[c], R.ns, panels, y, rc, sc, rch, sch,
                                 p->small_panel_max[L * d + c], R.L->side[c], kClassMax[c]));
   KH_CUDA(kh_launch_fwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], R.ns, p->max_m, panels, y, rc, sc, rch,
-                              sch, R.st, p->mid_panel_max[d], p->mid_m_max[d]));
+                              sch, R.st, p->mid_panel_max[d], p->mid_m_max[d], p->big_m_max[d]));
   KH_CUDA(join_side(*R.L, R.st));
   return KH_OK;
 }
@@ -1049,7 +1052,7 @@ int solve_bwd_level(kh_plan* p, const KhTree& T, const LaneRun& R, int64_t slot0
     KH_CUDA(kh_launch_bwd_small(T, lev + co[c], co[c + 1] - co[c], R.ns, panels, y, p->small_panel_max[L * d + c],
                                 R.L->side[c], kClassMax[c]));
   KH_CUDA(kh_launch_bwd_level(T, lev + co[L], co[kSmallClasses + 1] - co[L], R.ns, p->max_p, p->max_m, panels, y,
-                              R.st, p->mid_panel_max[d], p->mid_m_max[d]));
+                              R.st, p->mid_panel_max[d], p->mid_m_max[d], p->big_m_max[d]));
   KH_CUDA(join_side(*R.L, R.st));
   return KH_OK;
 }

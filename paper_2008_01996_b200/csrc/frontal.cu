@@ -1911,6 +1911,216 @@ __global__ void __launch_bounds__(MID_NT) bwd_mid_tma_kernel(KhTree T, const int
   for (int k = tid; k < p; k += MID_NT) yy[k] = ts[k];
 }
 
+// ---- streamed solves of the fronts with m > 64 -----------------------------------
+// One CTA per (front, shift). The panel is consumed in blocks of wf <= ST_W
+// columns (as many as fit a stage of `stage` entries at the front's height),
+// rows kb..m-1 of each (one contiguous segment per column, so one bulk async
+// copy each), through a ring of `ns` shared-memory stages that the TMA engine
+// fills ahead of the arithmetic: the loads do not depend on the sweep, so up
+// to ns - 1 stages (tens of KB per SM) are in flight while a stage is
+// consumed, which is what an HBM-bound sweep needs; the level kernels above
+// take a dependent global round trip per 32-pivot block instead.
+//   forward, blocks ascending: warp 0 solves the block's w x w unit-lower
+//     system with shuffles, then thread-per-row x[r] -= sum_c L[r, c] x_c for
+//     all r below (a per-warp redundant block solve saves the barrier but
+//     saturates the shuffle pipe: 1800 cycles per stage, clock64 probe);
+//   backward, blocks descending: s_c = sum_{r > block} L[r, c] x[r] over ALL
+//     rows below the block (L11 and L21 alike: the column segments are
+//     contiguous), thread-per-row partial sums, warp transpose-reduction,
+//     fixed-order sum over the warps; then warp 0 finishes
+//     x_blk = L_blk^-T (y_blk / d - s).
+// Two CTA barriers per stage; results are deterministic (fixed row -> thread
+// map and reduction order).
+constexpr int ST_W = 8, ST_NT = 256, ST_NW = ST_NT / 32, ST_MAXS = 8;
+#ifdef KH_STREAM_TIMING
+// debug builds (profiles/probes/stream_timing.py): clock64 cycles of thread 0 of
+// fwd_stream_kernel summed over CTAs: [prologue, mbarrier waits, block solve, rows, barrier+issue, stages, CTAs]
+__device__ unsigned long long g_stphase[8];
+#define ST_LAP(i)                                                          \
+  if (tid == 0) {                                                          \
+    const long long t1_ = clock64();                                       \
+    atomicAdd(&g_stphase[i], (unsigned long long)(t1_ - tph_));            \
+    tph_ = t1_;                                                            \
+  }
+#else
+#define ST_LAP(i)
+#endif
+
+// columns per stage for a front of m rows
+KH_DEV int stream_width(int m, int stage) { return max(1, min(ST_W, stage / m)); }
+
+// stage `bi` (block of columns kb = wf bi ..) -> buf, by warp 0
+KH_DEV void stream_issue(const double2* P, int m, int p, int wf, int bi, double2* buf, uint64_t* bar, int lane) {
+  const int kb = wf * bi, w = min(wf, p - kb), rows = m - kb;
+  // the buffer was read through the generic proxy: order those reads before the async-proxy writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (lane == 0) mbar_arrive_expect_tx(bar, 16u * (uint32_t)(w * rows));
+  __syncwarp();
+  if (lane < w) bulk_g2s(buf + lane * rows, P + kb + (int64_t)(kb + lane) * m, 16u * (uint32_t)rows, bar);
+}
+
+__global__ void __launch_bounds__(ST_NT) fwd_stream_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                           const double2* __restrict__ panels, double2* y,
+                                                           double2* ru_cur, int64_t ru_stride_cur,
+                                                           const double2* __restrict__ ru_child,
+                                                           int64_t ru_stride_child, int32_t lvl_m, int32_t stage, int32_t ns) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[ST_MAXS];
+  __shared__ double2 xb[ST_W];                           // the current block's solution
+  double2* xs = reinterpret_cast<double2*>(smem_raw);  // lvl_m entries
+  double2* ring = xs + lvl_m;                            // ns stages of `stage` entries
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int b = blockIdx.y;
+  const int p = F.p, q = F.q, m = p + q;
+  KH_ASSERT(m <= lvl_m && ns <= ST_MAXS);
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yy = y + (int64_t)b * T.n + F.first;
+  double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
+  const int wf = stream_width(m, stage), nblk = (p + wf - 1) / wf;
+#ifdef KH_STREAM_TIMING
+  long long tph_ = clock64();
+  if (tid == 0) {
+    atomicAdd(&g_stphase[5], (unsigned long long)nblk);
+    atomicAdd(&g_stphase[6], 1ull);
+  }
+#endif
+  if (tid == 0) {
+    for (int i = 0; i < ns; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int s = 0; s < ns && s < nblk; ++s) stream_issue(P, m, p, wf, s, ring + s * stage, &full[s], lane);
+  // the front's rhs: pivot rows of y plus the children's updates (fixed child order)
+  const int nk = F.child_end - F.child_begin;
+  for (int r = tid; r < m; r += ST_NT) {
+    double2 v = r < p ? yy[r] : make_double2(0.0, 0.0);
+    for (int k = 0; k < nk; ++k) {
+      const KhKid C = T.kids[F.child_begin + k];
+      const int ci = T.cmap[C.cmap_begin + r];
+      if (ci >= 0) v = cadd(v, ru_child[(int64_t)b * ru_stride_child + C.rupd_off + ci]);
+    }
+    xs[r] = v;
+  }
+  __syncthreads();
+  ST_LAP(0)
+  const double2 z = make_double2(0.0, 0.0);
+  for (int s = 0; s < nblk; ++s) {
+    const int slot = s % ns;
+    const double2* buf = ring + slot * stage;
+    const int kb = wf * s, w = min(wf, p - kb), rows = m - kb;
+    mbar_wait(&full[slot], (uint32_t)((s / ns) & 1));
+    ST_LAP(1)
+    // the block's unit-lower solve by warp 0 (lane i owns row kb + i), published in xb
+    if (warp == 0) {
+      double2 xi = lane < w ? xs[kb + lane] : z;
+      double2 lk[ST_W];
+#pragma unroll
+      for (int k = 0; k < ST_W; ++k) lk[k] = (k < w && lane > k && lane < w) ? buf[k * rows + lane] : z;
+#pragma unroll
+      for (int k = 0; k < ST_W; ++k) xi = cfms(xi, lk[k], shfl2(xi, k));
+      if (lane < w) {
+        xb[lane] = xi;
+        yy[kb + lane] = xi;
+      }
+    }
+    __syncthreads();
+    double2 xc[ST_W];
+#pragma unroll
+    for (int c = 0; c < ST_W; ++c) xc[c] = c < w ? xb[c] : z;
+    ST_LAP(2)
+    for (int r = kb + w + tid; r < m; r += ST_NT) {
+      const double2* l = buf + (r - kb);
+      double2 a0 = z, a1 = z;
+#pragma unroll
+      for (int c = 0; c < ST_W; c += 2) {
+        if (c < w) a0 = cadd(a0, cmul(l[c * rows], xc[c]));
+        if (c + 1 < w) a1 = cadd(a1, cmul(l[(c + 1) * rows], xc[c + 1]));
+      }
+      xs[r] = csub(xs[r], cadd(a0, a1));
+    }
+    ST_LAP(3)
+    __syncthreads();  // stage consumed, xs updated
+    if (warp == 0 && s + ns < nblk) stream_issue(P, m, p, wf, s + ns, ring + slot * stage, &full[slot], lane);
+    ST_LAP(4)
+  }
+  for (int r = p + tid; r < m; r += ST_NT) ru[r - p] = xs[r];
+}
+
+__global__ void __launch_bounds__(ST_NT) bwd_stream_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
+                                                           const double2* __restrict__ panels, double2* y,
+                                                           int32_t lvl_m, int32_t stage, int32_t ns) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[ST_MAXS];
+  __shared__ double2 red[2][ST_NW][ST_W];
+  double2* xs = reinterpret_cast<double2*>(smem_raw);  // x: lvl_m entries (solution; update rows gathered)
+  double2* ys = xs + lvl_m;                              // y of the pivot rows (read-only): lvl_m entries
+  double2* ring = ys + lvl_m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const KhDevFront F = T.lf_fronts[(level_fronts - T.lf_base) + blockIdx.x];
+  const int b = blockIdx.y;
+  const int p = F.p, q = F.q, m = p + q;
+  KH_ASSERT(m <= lvl_m && ns <= ST_MAXS);
+  const double2* P = panels + (int64_t)b * T.panel_total + F.panel_off;
+  double2* yb = y + (int64_t)b * T.n;
+  double2* yy = yb + F.first;
+  const int64_t* urows = T.urows + F.rows_begin;
+  const int wf = stream_width(m, stage), nblk = (p + wf - 1) / wf;
+  if (tid == 0) {
+    for (int i = 0; i < ns; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int s = 0; s < ns && s < nblk; ++s)
+      stream_issue(P, m, p, wf, nblk - 1 - s, ring + s * stage, &full[s], lane);
+  for (int a = tid; a < q; a += ST_NT) xs[p + a] = yb[urows[a]];  // final: the ancestors are done
+  for (int k = tid; k < p; k += ST_NT) ys[k] = yy[k];
+  __syncthreads();
+  const double2 z = make_double2(0.0, 0.0);
+  for (int s = 0; s < nblk; ++s) {
+    const int slot = s % ns;
+    const double2* buf = ring + slot * stage;
+    const int kb = wf * (nblk - 1 - s), w = min(wf, p - kb), rows = m - kb;
+    mbar_wait(&full[slot], (uint32_t)((s / ns) & 1));
+    // s_c = sum over the rows below the block of L[r, c] x[r]
+    double2 acc[ST_W];
+#pragma unroll
+    for (int c = 0; c < ST_W; ++c) acc[c] = z;
+    for (int r = kb + w + tid; r < m; r += ST_NT) {
+      const double2 xr = xs[r];
+      const double2* l = buf + (r - kb);
+#pragma unroll
+      for (int c = 0; c < ST_W; ++c)
+        if (c < w) acc[c] = cadd(acc[c], cmul(l[c * rows], xr));
+    }
+    const double2 v = warp_sum8(acc, lane);
+    if ((lane & 3) == 0) red[s & 1][warp][((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = v;
+    __syncthreads();
+    // x_blk = L_blk^-T (y_blk / d - s) by warp 0: lane c owns column kb + c
+    if (warp == 0) {
+      double2 t = z;
+      double2 li[ST_W];
+#pragma unroll
+      for (int i = 1; i < ST_W; ++i) li[i] = (i < w && lane < i) ? buf[lane * rows + i] : z;  // L[kb + i, kb + lane]
+      if (lane < w) {
+        double2 sum = red[s & 1][0][lane];
+#pragma unroll
+        for (int wp = 1; wp < ST_NW; ++wp) sum = cadd(sum, red[s & 1][wp][lane]);
+        t = csub(cmul(ys[kb + lane], cinv(buf[lane * rows + lane])), sum);
+      }
+#pragma unroll
+      for (int i = ST_W - 1; i > 0; --i) t = cfms(t, li[i], shfl2(t, i));
+      if (lane < w) xs[kb + lane] = t;
+    }
+    __syncthreads();  // stage consumed, x_blk visible
+    if (warp == 0 && s + ns < nblk)
+      stream_issue(P, m, p, wf, nblk - 1 - (s + ns), ring + slot * stage, &full[slot], lane);
+  }
+  for (int k = tid; k < p; k += ST_NT) yy[k] = xs[k];
+}
+
 // ---- backward solve: x <- L^{-T} D^{-1} y, fronts top-down -------------------
 __global__ void __launch_bounds__(NT) bwd_level_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                        const double2* __restrict__ panels, double2* y) {
@@ -2136,11 +2346,75 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
   return max_m <= 32 ? run(bwd_small_tma_kernel<nw, 1>) : run(bwd_small_tma_kernel<nw, 2>);
 }
 
+#ifdef KH_STREAM_TIMING
+extern "C" int kh_debug_stream_cycles(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, g_stphase, sizeof(unsigned long long) * 8) != cudaSuccess) return 4;
+  static const unsigned long long zero[8] = {};
+  return cudaMemcpyToSymbol(g_stphase, zero, sizeof zero) == cudaSuccess ? 0 : 4;
+}
+#endif
+
+// stage size (entries) and ring depth of the streamed solves. A stage holds
+// up to ST_W columns of the level's tallest front, at most 24 KB (taller
+// fronts get fewer columns per stage). Wide levels (thousands of short
+// panels: the rhs gather in front of the sweep dominates a CTA's life) take a
+// ring of two, so that several CTAs per SM overlap each other; narrow levels
+// (the top of the tree: few CTAs, long panels) a ring of four.
+#ifndef KH_STREAM_STAGE_E
+#define KH_STREAM_STAGE_E 1536
+#endif
+#ifndef KH_STREAM_STAGES
+#define KH_STREAM_STAGES 4
+#endif
+#ifndef KH_STREAM_MIN_FRONTS
+#define KH_STREAM_MIN_FRONTS 12
+#endif
+#ifndef KH_STREAM_MAX_FRONTS
+#define KH_STREAM_MAX_FRONTS 64
+#endif
+#ifndef KH_STREAM_STAGES_WIDE
+#define KH_STREAM_STAGES_WIDE 2
+#endif
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+static int stream_stage_entries(int lvl_m) {
+  static const int e = env_int("KH_STREAM_STAGE_E", KH_STREAM_STAGE_E);
+  return std::max(std::min(e, ST_W * lvl_m), lvl_m);
+}
+static int stream_stages(int stage, int64_t ctas) {
+  static const int narrow = env_int("KH_STREAM_STAGES", KH_STREAM_STAGES);
+  static const int wide = env_int("KH_STREAM_STAGES_WIDE", KH_STREAM_STAGES_WIDE);
+  const int fit = (200 * 1024) / (16 * stage);
+  return std::max(2, std::min(std::min(ctas >= 148 * 4 ? wide : narrow, fit), ST_MAXS));
+}
+
+// streamed solves of the large fronts (KH_STREAM_SOLVE=0: the level / top / mid kernels)
+static bool stream_solves(int32_t nlev) {
+  static const bool on = [] {
+    const char* v = std::getenv("KH_STREAM_SOLVE");
+    return !v || std::atoi(v) != 0;
+  }();
+  static const int lo = [] { const char* v = std::getenv("KH_STREAM_MIN_FRONTS"); return v ? std::atoi(v) : KH_STREAM_MIN_FRONTS; }();
+  static const int hi = [] { const char* v = std::getenv("KH_STREAM_MAX_FRONTS"); return v ? std::atoi(v) : KH_STREAM_MAX_FRONTS; }();
+  return on && nlev >= lo && nlev <= hi;
+}
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
                                 int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
-                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m) {
+                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m, int32_t lvl_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
+  if (stream_solves(nlev) && lvl_m > 0) {
+    const int stage = stream_stage_entries(lvl_m), ns = stream_stages(stage, (int64_t)nlev * batch);
+    const int smem = 16 * (lvl_m + ns * stage);
+    cudaError_t e = kh_smem_optin((const void*)fwd_stream_kernel, smem);
+    if (e != cudaSuccess) return e;
+    fwd_stream_kernel<<<dim3(nlev, batch), ST_NT, smem, stream>>>(T, level_fronts, panels, y, ru_cur, ru_stride_cur,
+                                                                  ru_child, ru_stride_child, lvl_m, stage, ns);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   if (KH_MID_TMA && mid_panel > 0 && (int64_t)nlev * batch > kNarrowLevelCtas) {
     const int smem = 16 * (mid_panel + mid_m);
     cudaError_t e = kh_smem_optin((const void*)fwd_mid_tma_kernel, smem);
@@ -2168,8 +2442,17 @@ cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, in
 
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
-                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m) {
+                                cudaStream_t stream, int32_t mid_panel, int32_t mid_m, int32_t lvl_m) {
   if (nlev == 0 || batch == 0) return cudaSuccess;
+  if (stream_solves(nlev) && lvl_m > 0) {
+    const int stage = stream_stage_entries(lvl_m), ns = stream_stages(stage, (int64_t)nlev * batch);
+    const int smem = 16 * (2 * lvl_m + ns * stage);
+    cudaError_t e = kh_smem_optin((const void*)bwd_stream_kernel, smem);
+    if (e != cudaSuccess) return e;
+    bwd_stream_kernel<<<dim3(nlev, batch), ST_NT, smem, stream>>>(T, level_fronts, panels, y, lvl_m, stage, ns);
+    kh_note_launch();
+    return cudaGetLastError();
+  }
   const bool narrow = (int64_t)nlev * batch <= kNarrowLevelCtasBwd;
   if (KH_MID_TMA && mid_panel > 0 && !narrow) {
     const int smem = 16 * (mid_panel + mid_m);

@@ -86,7 +86,7 @@ cudaError_t kh_launch_sum_parts(int32_t g, const double* parts, int64_t len, dou
 cudaError_t kh_launch_fwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_m, const double2* panels, double2* y, double2* ru_cur,
                                 int64_t ru_stride_cur, const double2* ru_child, int64_t ru_stride_child,
-                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0);
+                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0, int32_t lvl_m = 0);
 // Level-synchronous kernels for the large fronts (see frontal.cu). Tasks are
 // (front, index) int32 pairs; schur tasks are (front, tile row, tile col).
 #ifndef KH_ASM_CHUNK_DEF
@@ -111,7 +111,7 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
                                 int32_t max_m = 64);
 cudaError_t kh_launch_bwd_level(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
                                 int32_t max_p, int32_t max_m, const double2* panels, double2* y,
-                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0);
+                                cudaStream_t stream, int32_t mid_panel = 0, int32_t mid_m = 0, int32_t lvl_m = 0);
 cudaError_t kh_launch_gather_rhs(int64_t n, int32_t batch, const int64_t* perm, const double* g_re,
                                  const double* g_im, int64_t ldg, double2* y, cudaStream_t stream);
 cudaError_t kh_launch_scatter_sol(int64_t n, int32_t batch, const int64_t* perm, const double2* y,
