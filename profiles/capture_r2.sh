@@ -13,10 +13,18 @@ for c in c1 c2 c5; do
   python bench.py --config $c --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; tail -n 1 gpurun_out/${T}_bench_$c.log > gpurun_out/${T}_bench_$c.json
 done
 timeout 1500 python bench.py --config c4 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_bench_c4.log 2>&1; tail -n 1 gpurun_out/${T}_bench_c4.log > gpurun_out/${T}_bench_c4.json
+# launch list of the default configuration (two shift lanes: every launch covers half the shifts)
 bash profiles/launch_list_dram.sh $T
-python profiles/level_breakdown.py gpurun_out/launches_dram_$T.csv > gpurun_out/${T}_level_breakdown.txt 2>&1
+# per-level breakdown, per-launch solve table and the ncu captures with one lane
+# (whole-batch launches, levels not interleaved)
+export KH_LANES=1 KH_SOLVE_LANES=1
+cp profiles/traffic.json gpurun_out/traffic_keep.json
+bash profiles/launch_list_dram.sh ${T}_1lane
+cp gpurun_out/traffic_keep.json profiles/traffic.json
+python profiles/level_breakdown.py gpurun_out/launches_dram_${T}_1lane.csv > gpurun_out/${T}_level_breakdown.txt 2>&1
+python profiles/solve_launches.py gpurun_out/launches_dram_${T}_1lane.csv > gpurun_out/${T}_solve_launches.md 2>&1
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-levels"
-for spec in "schur_update_kernel 11 schur" "warp_front_kernel<.int.6 7 wf6" "warp_front_kernel<.int.4 5 wf4" "front_kernel<.int.96 4 f96" "pivot_block_kernel 8 pivot" "panel_trsm_kernel 8 ptrsm" "bwd_small_tma 29 bwdsmall" "dgemm_kernel 8 dgemm"; do
+for spec in "schur_update_kernel 11 schur" "warp_front_kernel<.int.6 7 wf6" "warp_front_kernel<.int.5 7 wf5" "warp_front_kernel<.int.4 5 wf4" "front_kernel<.int.96 4 f96" "pivot_warp_kernel 12 pivot" "panel_trsm_kernel 12 ptrsm" "bwd_small_tma_kernel 66 bwdsmall" "fwd_stream_kernel 5 fwdstream" "dgemm_kernel 8 dgemm"; do
   set -- $spec
   timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$1" --launch-skip $2 -c 1 -f -o gpurun_out/ncu_${T}_$3 $B > gpurun_out/ncu_${T}_$3.log 2>&1
   python profiles/ncu_summary.py gpurun_out/ncu_${T}_$3.ncu-rep "$3 (c3, $B)" > gpurun_out/${T}_ncu_$3.txt 2>&1
