@@ -24,7 +24,8 @@ def load(path):
     return names, rows
 
 
-FACTOR_PREFIXES = ("factor_front_kernel", "big_", "schur_update_kernel", "shift_absmax", "rowreduce")
+FACTOR_PREFIXES = ("factor_front_kernel", "warp_front_kernel", "pivot_", "panel_", "big_", "schur_update_kernel",
+                   "shift_absmax", "rowreduce")
 
 
 def short(name):

@@ -195,6 +195,45 @@ def test_batched_shifts_match_superlu(cuda_ok, monkeypatch, mesh, small_max, lea
         assert np.linalg.norm(K @ X[:, k] - B[:, k]) / np.linalg.norm(B[:, k]) < 1e-12
 
 
+@pytest.mark.parametrize("ns", [1, 5, 9, 22])
+def test_shift_lanes_do_not_change_the_bits(cuda_ok, monkeypatch, ns):
+    """A batch walks the tree in 1..4 lanes of shifts on separate stream sets
+    (KH_LANES / KH_SOLVE_LANES, read at plan creation): ragged splits (lanes
+    of 4k shifts, a short last lane, fewer shifts than lanes) and every lane
+    count give bitwise the same solution, which matches SuperLU."""
+    import torch
+
+    from paper_2008_01996_b200 import fem, problems
+
+    ops = fem.assemble_p1(problems.spatial_mesh("square", 64))
+    M, A = ops.M_II.tocsr(), ops.A_II.tocsr()
+    n = M.shape[0]
+    rng = np.random.default_rng(11)
+    lam = rng.uniform(0.01, 3.0, ns) + 1j * rng.uniform(-40.0, 40.0, ns)
+    B = rng.standard_normal((n, ns)) + 1j * rng.standard_normal((n, ns))
+    sym = sd.analyze((M + A).tocsr())
+    mv, av = sym.align_values(M), sym.align_values(A)
+    st = _native.stream_handle()
+    out = {}
+    for fl, sl in [(1, 1), (2, 2), (3, 2), (4, 4), (2, 1)]:
+        monkeypatch.setenv("KH_LANES", str(fl))
+        monkeypatch.setenv("KH_SOLVE_LANES", str(sl))
+        plan = sd._Plan(sym, mv, av, ns, ns, torch.cuda.current_device())
+        plan.factor(0, lam, st)
+        plan.pivot_check(0, ns, st)
+        bre, bim = _dev(B.real.T), _dev(B.imag.T)
+        xre, xim = torch.empty_like(bre), torch.empty_like(bim)
+        plan.solve(0, ns, bre.data_ptr(), bim.data_ptr(), n, xre.data_ptr(), xim.data_ptr(), n, st)
+        out[(fl, sl)] = xre.cpu().numpy().T + 1j * xim.cpu().numpy().T
+        del plan
+    base = out[(1, 1)]
+    for key, X in out.items():
+        assert np.array_equal(X, base), key
+    for k in (0, ns - 1):
+        K = (M + lam[k] * A).astype(complex).tocsc()
+        assert np.linalg.norm(K @ base[:, k] - B[:, k]) / np.linalg.norm(B[:, k]) < 1e-12, k
+
+
 def test_many_shifts_wide_level_kernels(cuda_ok):
     """160 shifts in one batch: the large-front levels exceed the narrow-level
     CTA threshold, so the wide-level solve kernels run (the 9-shift cases above
