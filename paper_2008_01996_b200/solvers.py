@@ -40,6 +40,7 @@ from .errors import DefectivePencil, DimensionMismatch, ImaginaryResidueTooLarge
 FD_IMAG_TOL = 1e-6       # solvers.py:400
 DEFAULT_REFINE = 5  # upper bound; the stop rule ends c3 after 1 step, c4 after 3
 DEFAULT_REFINE_TOL = 1e-13
+SPECULATIVE_PLAN_MAX_NT = 512  # solve_fd builds the numeric plan before the eigenvalues exist up to this N_t
 
 
 @dataclass(frozen=True)
@@ -374,13 +375,36 @@ def solve_fd(system, pencil=None, threads=1, refine=DEFAULT_REFINE, refine_tol=D
                 aligned = (symbolic.align_values(system.spatial.M_II), fa.result())
                 fs.result()
             phases["aligned"] = time.perf_counter() - t0
+            eng = None
+            if not lam_ready.is_set() and nt <= SPECULATIVE_PLAN_MAX_NT:
+                # The shifts are not known yet: build the plan meanwhile for the
+                # mode count a pencil of conjugate pairs (plus one real
+                # eigenvalue when N_t is odd) has. It holds no shift data; if
+                # the count turns out different the plan is rebuilt below
+                # (only done for small pencils: there the host latency matters
+                # and a rebuilt workspace is cheap).
+                from .engine import ModalPlan
+
+                guess = (nt + 1) // 2
+                blank = ModalPlan(n_t=nt, lam=np.zeros(guess, dtype=np.complex128), weight=np.ones(guess),
+                                  n_pairs=nt // 2, n_single=nt % 2, w_in=None, w_out=None, kron_b=None)
+                with torch.cuda.device(dev), nvtx.range("kh.solve_fd.plan"):
+                    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, blank, device=dev,
+                                   leaf_size=leaf_size, max_batch=max_batch, keep_factors=keep_factors,
+                                   symbolic=symbolic, aligned=aligned)
+                phases["plan_early"] = time.perf_counter() - t0
             lam_ready.wait()
             if "stub" not in lam_box:  # the pencil failed on the main thread
                 return None
+            stub = lam_box["stub"]
             with torch.cuda.device(dev), nvtx.range("kh.solve_fd.plan"):
-                eng = FDEngine(system.spatial.M_II, system.spatial.A_II, lam_box["stub"], device=dev,
-                               leaf_size=leaf_size, max_batch=max_batch, keep_factors=keep_factors,
-                               symbolic=symbolic, aligned=aligned)
+                if eng is not None and eng.n_k == stub.n_k:
+                    eng.modal, eng.lam = stub, np.ascontiguousarray(stub.lam)
+                else:
+                    eng = None  # frees the speculative plan's workspace first
+                    eng = FDEngine(system.spatial.M_II, system.spatial.A_II, stub, device=dev,
+                                   leaf_size=leaf_size, max_batch=max_batch, keep_factors=keep_factors,
+                                   symbolic=symbolic, aligned=aligned)
                 phases["plan"] = time.perf_counter() - t0
                 phases["memplan"] = eng.t_memplan - t0
                 phases["plans_created"] = eng.t_plans - t0
