@@ -166,6 +166,10 @@ struct kh_plan {
   static constexpr int kMaxLanes = 4;
   Lane lane[kMaxLanes];
   int factor_lanes = 1, solve_lanes = 1;
+  // batches with fewer (front, shift) pairs than this run in one lane: on small
+  // problems (c1: 16 shifts of a 15 x 15 mesh) a second lane only doubles the launches
+  int64_t lane_min_work = 200000;
+  int lanes_for(int configured, int64_t nshift) const { return nshift * nf >= lane_min_work ? configured : 1; }
   cudaEvent_t ev_fork = nullptr;
   // optional per-level timing of the factorization (kh_plan_set_level_timing):
   // lvl_ev[i] recorded on the caller's stream before level depth - i and at the end
@@ -893,6 +897,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   }
   p->factor_lanes = env_lanes("KH_LANES", KH_DEFAULT_LANES);
   p->solve_lanes = env_lanes("KH_SOLVE_LANES", KH_DEFAULT_SOLVE_LANES);
+  if (const char* v = std::getenv("KH_LANES_MIN_WORK")) p->lane_min_work = std::atoll(v);
   for (int l = 0; l < std::max(p->factor_lanes, p->solve_lanes) && e == cudaSuccess; ++l)
     e = lane_create(p->lane[l], l > 0);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
@@ -962,7 +967,7 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
   }
   // per-level timing describes the single-lane schedule (levels of different lanes overlap otherwise)
   std::vector<LaneRun> runs;
-  KH_CUDA(lanes_begin(p, p->level_timing ? 1 : p->factor_lanes, (int32_t)nshift, st, runs));
+  KH_CUDA(lanes_begin(p, p->level_timing ? 1 : p->lanes_for(p->factor_lanes, nshift), (int32_t)nshift, st, runs));
   for (int32_t d = p->depth; d >= 0; --d) {
     if (p->level_timing) KH_CUDA(cudaEventRecord(p->lvl_ev[p->depth - d], st));
     const int32_t* lev = p->level_fronts + p->level_off[d];
@@ -1061,7 +1066,7 @@ int solve_bwd_level(kh_plan* p, const KhTree& T, const LaneRun& R, int64_t slot0
 int solve_bwd_impl(kh_plan* p, int64_t slot0, int32_t ns, double* x_re, double* x_im, int64_t ldx, cudaStream_t st) {
   const KhTree T = p->tree();
   std::vector<LaneRun> runs;
-  KH_CUDA(lanes_begin(p, p->solve_lanes, ns, st, runs));
+  KH_CUDA(lanes_begin(p, p->lanes_for(p->solve_lanes, ns), ns, st, runs));
   for (int32_t d = 0; d <= p->depth; ++d)
     for (const LaneRun& R : runs)
       if (int rc = solve_bwd_level(p, T, R, slot0, d)) return rc;
@@ -1190,7 +1195,7 @@ int kh_plan_solve(kh_plan* p, int64_t slot0, int64_t nshift, const double* b_re,
   KH_CUDA(kh_launch_gather_rhs(p->n, ns, p->perm, b_re, b_im, ldb, p->y, st));
   // each lane runs its forward sweep and goes straight into its backward sweep
   std::vector<LaneRun> runs;
-  KH_CUDA(lanes_begin(p, p->solve_lanes, ns, st, runs));
+  KH_CUDA(lanes_begin(p, p->lanes_for(p->solve_lanes, ns), ns, st, runs));
   for (int32_t d = p->depth; d >= 0; --d)
     for (const LaneRun& R : runs)
       if (int rc = solve_fwd_level(p, T, R, slot0, d)) return rc;
