@@ -97,11 +97,13 @@ constexpr int32_t kClassMax[kSmallClasses] = {32, 40, 48, 64, KH_CLASS4, 128};
 #ifndef KH_WARP_CLASSES
 #define KH_WARP_CLASSES 7
 #endif
-// the warp-per-front solve kernels take the classes with m <= 64
+// the warp-per-front solve kernels take the classes with m <= 96 (R = 1, 2, 2,
+// 2, 3 rows per lane); with 4 (m <= 64) the m <= 96 class goes through the CTA
+// kernels: 4.37 vs 4.17 ms per c3 solve
 #ifndef KH_SOLVE_SMALL_CLASSES
-#define KH_SOLVE_SMALL_CLASSES 4
+#define KH_SOLVE_SMALL_CLASSES 5
 #endif
-constexpr int kSolveSmallClasses = KH_SOLVE_SMALL_CLASSES;  // classes m <= 64: warp-per-front solves
+constexpr int kSolveSmallClasses = KH_SOLVE_SMALL_CLASSES;  // classes with warp-per-front solves
 constexpr int kClsStride = kSmallClasses + 2;
 constexpr int32_t kAbsmaxBlocks = 64;
 constexpr int32_t kResidualBlocks = 1184;  // 8 x 148 SMs

@@ -1511,16 +1511,16 @@ __global__ void __launch_bounds__(NT, 2) fwd_top_kernel(KhTree T, const int32_t*
   }
 }
 
-// ---- warp-per-front solves for fronts with m <= 64 ------------------------------
-// Lane l owns front rows l and l + 32. No block barriers: pivots are broadcast
+// ---- warp-per-front solves for fronts with m <= 32 R (R <= 4) -------------------
+// Lane l owns front rows l + 32 h. No block barriers: pivots are broadcast
 // with shuffles.
 constexpr int SOLVE_CH = 8;   // columns per warp_sum8 reduction (bwd)
 
 #ifndef KH_FWD_TMA_NW
 #define KH_FWD_TMA_NW 1
 #endif
-// R = 2: lanes own rows lane and lane + 32 (m <= 64); R = 1: m <= 32, one row
-// per lane (the m <= 32 class: no work on rows that cannot exist).
+// R rows per lane (rows lane + 32 h, h < R: m <= 32 R; one instantiation per
+// front class, so no work on rows that cannot exist).
 template <int NW, int R>
 __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const int32_t* __restrict__ level_fronts,
                                                                 int32_t nlev, const double2* __restrict__ panels,
@@ -1544,45 +1544,51 @@ __global__ void __launch_bounds__(32 * NW) fwd_small_tma_kernel(KhTree T, const 
     mbar_fence_init();
   }
   __syncwarp();
-  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 64);
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 32 * R);
   if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
   __syncwarp();
   for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
   double2* yy = y + (int64_t)b * T.n + F.first;
   double2* ru = ru_cur + (int64_t)b * ru_stride_cur + F.rupd_off;
-  const int r0 = lane, r1 = lane + 32;
   const double2 z = make_double2(0.0, 0.0);
-  double2 x0 = z, x1 = z;
-  KH_ASSERT(R == 2 || m <= 32);
+  double2 x[R];  // lane l owns front rows l + 32 h
+#pragma unroll
+  for (int h = 0; h < R; ++h) x[h] = z;
+  KH_ASSERT(m <= 32 * R);
   for (int c = F.child_begin; c < F.child_end; ++c) {
     const KhKid C = T.kids[c];
     const double2* rc = ru_child + (int64_t)b * ru_stride_child + C.rupd_off;
     const int32_t* cm = T.cmap + C.cmap_begin;
-    const int c0 = r0 < m ? cm[r0] : -1;
-    if (c0 >= 0) x0 = cadd(x0, rc[c0]);
-    if (R == 2) {
-      const int c1 = r1 < m ? cm[r1] : -1;
-      if (c1 >= 0) x1 = cadd(x1, rc[c1]);
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int r = lane + 32 * h;
+      const int ci = r < m ? cm[r] : -1;
+      if (ci >= 0) x[h] = cadd(x[h], rc[ci]);
     }
   }
-  if (r0 < p) x0 = cadd(x0, yy[r0]);
-  if (R == 2 && r1 < p) x1 = cadd(x1, yy[r1]);
+#pragma unroll
+  for (int h = 0; h < R; ++h)
+    if (lane + 32 * h < p) x[h] = cadd(x[h], yy[lane + 32 * h]);
   mbar_wait(br, 0);
   for (int k = 0; k < p; ++k) {
     const double2* col = Ls + cbase(k) - k;  // L[r, k] = col[r], r >= k
-    const double2 l0 = (r0 > k && r0 < m) ? col[r0] : z;
-    const double2 yk = shfl2(R == 1 || k < 32 ? x0 : x1, k & 31);
-    x0 = cfms(x0, l0, yk);
-    if (R == 2) {
-      const double2 l1 = (r1 > k && r1 < m) ? col[r1] : z;
-      x1 = cfms(x1, l1, yk);
+    double2 src = x[0];
+#pragma unroll
+    for (int h = 1; h < R; ++h)
+      if (k >= 32 * h) src = x[h];
+    const double2 yk = shfl2(src, k & 31);
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int r = lane + 32 * h;
+      const double2 l = (r > k && r < m) ? col[r] : z;
+      x[h] = cfms(x[h], l, yk);
     }
   }
-  if (r0 < p) yy[r0] = x0;
-  else if (r0 < m) ru[r0 - p] = x0;
-  if (R == 2) {
-    if (r1 < p) yy[r1] = x1;
-    else if (r1 < m) ru[r1 - p] = x1;
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int r = lane + 32 * h;
+    if (r < p) yy[r] = x[h];
+    else if (r < m) ru[r - p] = x[h];
   }
 }
 
@@ -1619,7 +1625,7 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
     mbar_fence_init();
   }
   __syncwarp();
-  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 64);
+  KH_ASSERT(p * m - (p * (p - 1)) / 2 <= maxe && m <= 32 * R);
   if (lane == 0) mbar_arrive_expect_tx(br, 16u * (uint32_t)(p * m - (p * (p - 1)) / 2));
   __syncwarp();
   for (int c = lane; c < p; c += 32) bulk_g2s(Ls + cbase(c), P + c + (int64_t)c * m, 16u * (uint32_t)(m - c), br);
@@ -1627,26 +1633,28 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
   double2* yy = yb + F.first;
   const int64_t* urows = T.urows + F.rows_begin;
   const double2 z = make_double2(0.0, 0.0);
-  const double2 xu0 = lane < q ? yb[urows[lane]] : z;
-  const double2 xu1 = R == 2 && lane + 32 < q ? yb[urows[lane + 32]] : z;
-  const int k0 = lane, k1 = lane + 32;
-  const double2 y0 = k0 < p ? yy[k0] : z, y1 = R == 2 && k1 < p ? yy[k1] : z;
-  KH_ASSERT(R == 2 || m <= 32);
+  double2 xu[R], yv[R], t[R];  // lane l: update rows / pivots l + 32 h
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    xu[h] = lane + 32 * h < q ? yb[urows[lane + 32 * h]] : z;
+    yv[h] = lane + 32 * h < p ? yy[lane + 32 * h] : z;
+    t[h] = z;
+  }
+  KH_ASSERT(m <= 32 * R);
   mbar_wait(br, 0);
-  double2 t0 = z, t1 = z;
   for (int kc = 0; kc < p; kc += SOLVE_CH) {
     double2 sv[SOLVE_CH];
 #pragma unroll
     for (int u = 0; u < SOLVE_CH; ++u) {
       const int k = kc + u;
       const double2* col = Ls + cbase(k) + (p - k);  // L21[:, k]
-      const double2 l0 = (k < p && lane < q) ? col[lane] : z;
-      if (R == 2) {
-        const double2 l1 = (k < p && lane + 32 < q) ? col[lane + 32] : z;
-        sv[u] = cadd(cmul(l0, xu0), cmul(l1, xu1));
-      } else {
-        sv[u] = cmul(l0, xu0);
+      double2 acc = z;
+#pragma unroll
+      for (int h = 0; h < R; ++h) {
+        const double2 l = (k < p && lane + 32 * h < q) ? col[lane + 32 * h] : z;
+        acc = h == 0 ? cmul(l, xu[0]) : cadd(acc, cmul(l, xu[h]));
       }
+      sv[u] = acc;
     }
     const double2 v = warp_sum8(sv, lane);
 #pragma unroll
@@ -1654,22 +1662,30 @@ __global__ void __launch_bounds__(32 * NW) bwd_small_tma_kernel(KhTree T, const 
       const int kk = lane + 32 * h, u = kk - kc;
       const int src = ((u >> 2) & 1) << 4 | ((u >> 1) & 1) << 3 | (u & 1) << 2;
       const double2 got = shfl2(v, src & 31);
-      if (u >= 0 && u < SOLVE_CH && kk < p) {
-        if (h == 0) t0 = got;
-        else t1 = got;
-      }
+      if (u >= 0 && u < SOLVE_CH && kk < p) t[h] = got;
     }
   }
-  if (k0 < p) t0 = csub(cmul(y0, cinv(Ls[cbase(k0)])), t0);
-  if (R == 2 && k1 < p) t1 = csub(cmul(y1, cinv(Ls[cbase(k1)])), t1);
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int k = lane + 32 * h;
+    if (k < p) t[h] = csub(cmul(yv[h], cinv(Ls[cbase(k)])), t[h]);
+  }
   // L11^T x = t bottom-up (column form: x_i final -> t_k -= L[i, k] x_i, k < i)
   for (int i = p - 1; i > 0; --i) {
-    const double2 xi = shfl2(R == 1 || i < 32 ? t0 : t1, i & 31);
-    if (k0 < i) t0 = cfms(t0, Ls[cbase(k0) + i - k0], xi);
-    if (R == 2 && k1 < i) t1 = cfms(t1, Ls[cbase(k1) + i - k1], xi);
+    double2 src = t[0];
+#pragma unroll
+    for (int h = 1; h < R; ++h)
+      if (i >= 32 * h) src = t[h];
+    const double2 xi = shfl2(src, i & 31);
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int k = lane + 32 * h;
+      if (k < i) t[h] = cfms(t[h], Ls[cbase(k) + i - k], xi);
+    }
   }
-  if (k0 < p) yy[k0] = t0;
-  if (R == 2 && k1 < p) yy[k1] = t1;
+#pragma unroll
+  for (int h = 0; h < R; ++h)
+    if (lane + 32 * h < p) yy[lane + 32 * h] = t[h];
 }
 
 // Backward solve of the large fronts of a narrow level (top of the tree):
@@ -2326,7 +2342,10 @@ cudaError_t kh_launch_fwd_small(const KhTree& T, const int32_t* level_fronts, in
     kh_note_launch();
     return cudaGetLastError();
   };
-  return max_m <= 32 ? run(fwd_small_tma_kernel<nw, 1>) : run(fwd_small_tma_kernel<nw, 2>);
+  if (max_m <= 32) return run(fwd_small_tma_kernel<nw, 1>);
+  if (max_m <= 64) return run(fwd_small_tma_kernel<nw, 2>);
+  if (max_m <= 96) return run(fwd_small_tma_kernel<nw, 3>);
+  return max_m <= 128 ? run(fwd_small_tma_kernel<nw, 4>) : cudaErrorInvalidValue;
 }
 
 cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, int32_t nlev, int32_t batch,
@@ -2343,7 +2362,10 @@ cudaError_t kh_launch_bwd_small(const KhTree& T, const int32_t* level_fronts, in
     kh_note_launch();
     return cudaGetLastError();
   };
-  return max_m <= 32 ? run(bwd_small_tma_kernel<nw, 1>) : run(bwd_small_tma_kernel<nw, 2>);
+  if (max_m <= 32) return run(bwd_small_tma_kernel<nw, 1>);
+  if (max_m <= 64) return run(bwd_small_tma_kernel<nw, 2>);
+  if (max_m <= 96) return run(bwd_small_tma_kernel<nw, 3>);
+  return max_m <= 128 ? run(bwd_small_tma_kernel<nw, 4>) : cudaErrorInvalidValue;
 }
 
 #ifdef KH_STREAM_TIMING
