@@ -97,11 +97,11 @@ constexpr int32_t kClassMax[kSmallClasses] = {32, 40, 48, 64, KH_CLASS4, 128};
 #ifndef KH_WARP_CLASSES
 #define KH_WARP_CLASSES 7
 #endif
-// the warp-per-front solve kernels take the classes with m <= 96 (R = 1, 2, 2,
-// 2, 3 rows per lane); with 4 (m <= 64) the m <= 96 class goes through the CTA
-// kernels: 4.37 vs 4.17 ms per c3 solve
+// the warp-per-front solve kernels take every class up to m <= 128 (R = 1, 2,
+// 2, 2, 3, 4 rows per lane); c3 solve with the classes up to 64 / 96 / 128:
+// 4.37 / 4.17 / 4.12 ms (the rest goes through the CTA kernels)
 #ifndef KH_SOLVE_SMALL_CLASSES
-#define KH_SOLVE_SMALL_CLASSES 5
+#define KH_SOLVE_SMALL_CLASSES 6
 #endif
 constexpr int kSolveSmallClasses = KH_SOLVE_SMALL_CLASSES;  // classes with warp-per-front solves
 constexpr int kClsStride = kSmallClasses + 2;
@@ -187,6 +187,7 @@ struct kh_plan {
   int32_t* wdst = nullptr;  // originals' slots in the warp-front kernels' dense image
   // per small class: register-resident warp kernel tile count (0: shared-memory kernel)
   int warp_mt[kSmallClasses] = {};
+  int n_fused = kSmallClasses;  // classes [0, n_fused) use the fused per-front factor kernels, the rest the large-front path
   int64_t *urows = nullptr, *orig_src = nullptr, *perm = nullptr, *indptr = nullptr, *indices = nullptr;
   double *mv = nullptr, *av = nullptr;
   double *om = nullptr, *oa = nullptr;  // values in front-original order (gathered on the device)
@@ -569,6 +570,7 @@ struct Sched {
   std::vector<int32_t> orig_dst;  // device copy: packed offsets for the fused-front classes
   std::vector<int32_t> wdst;      // warp-front image slots (-1 outside the warp classes)
   int warp_mt[kSmallClasses] = {};
+  int n_fused = kSmallClasses;  // classes factored by the fused per-front kernels (KH_SMALL_MAX)
   std::vector<int32_t> lf, level_off, cls_off, tasks, task_off, bt;
   std::vector<kh_plan::BigLevel> big;
   std::vector<kh_plan::SuperBlock> sbinfo;
@@ -605,17 +607,23 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   // super-block path for those fronts (c3 factorization 21.07 -> 20.70 ms)
   int small_max = 96;
   if (const char* env = std::getenv("KH_SMALL_MAX")) small_max = std::atoi(env);
+  // Front lists are always ordered by the size classes (the solves pick their
+  // kernels by class); the first n_fused classes are factored by the fused
+  // per-front kernels, the rest by the large-front path
+  int n_fused = 0;
+  while (n_fused < kSmallClasses && kClassMax[n_fused] <= small_max) ++n_fused;
+  X.n_fused = n_fused;
   auto front_class = [&](int32_t m) {
     for (int c = 0; c < kSmallClasses; ++c)
-      if (m <= kClassMax[c] && small_max >= kClassMax[c]) return c;
-    return kSmallClasses;  // large
+      if (m <= kClassMax[c]) return c;
+    return kSmallClasses;  // m > 128
   };
   // originals of fused fronts address the packed block-column layout directly
   X.orig_dst = S.orig_dst;
   for (int32_t f = 0; f < nf; ++f) {
     const kh::Front& F = S.fronts[f];
     const int32_t m = F.m();
-    if (front_class(m) >= kSmallClasses) continue;
+    if (front_class(m) >= n_fused) continue;
     for (int64_t e = F.orig_begin; e < F.orig_end; ++e) {
       const int32_t d = X.orig_dst[e], c = d / m, r = d - c * m;
       X.orig_dst[e] = kh_packed_col_base(m, c) + r;
@@ -626,12 +634,12 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   int warp_mask = KH_WARP_CLASSES;
   if (const char* env = std::getenv("KH_WARP_CLASSES")) warp_mask = std::atoi(env);
   for (int c = 0; c < kSmallClasses; ++c)
-    X.warp_mt[c] = ((warp_mask >> c) & 1) && kClassMax[c] <= 48 ? kClassMax[c] / 8 : 0;
+    X.warp_mt[c] = ((warp_mask >> c) & 1) && kClassMax[c] <= 48 && c < n_fused ? kClassMax[c] / 8 : 0;
   X.wdst.assign(S.orig_dst.size(), -1);
   for (int32_t f = 0; f < nf; ++f) {
     const kh::Front& F = S.fronts[f];
     const int32_t m = F.m(), c = front_class(m);
-    if (c >= kSmallClasses || !X.warp_mt[c]) continue;
+    if (c >= n_fused || !X.warp_mt[c]) continue;
     for (int64_t e = F.orig_begin; e < F.orig_end; ++e) {
       const int32_t d = S.orig_dst[e], cc = d / m, r = d - cc * m;
       X.wdst[e] = kh_warp_front_slot(m, F.p, r, cc);
@@ -684,7 +692,7 @@ void build_schedule(const kh::Symbolic& S, Sched& X) {
   }
   X.task_off.push_back(0);
   for (size_t d = 0; d < S.levels.size(); ++d) {
-    const int32_t first_large = X.level_off[d] + X.cls_off[kClsStride * d + kSmallClasses];
+    const int32_t first_large = X.level_off[d] + X.cls_off[kClsStride * d + n_fused];
     std::vector<int32_t> large(X.lf.begin() + first_large, X.lf.begin() + X.level_off[d + 1]);
     // Schur-update tasks: lower 64x64 tiles of U
     for (int32_t f : large) {
@@ -880,6 +888,7 @@ int kh_plan_create(const kh_symbolic* s, int device, const int64_t* indptr, cons
   p->mid_m_max = X.mid_m_max;
   p->big_m_max = X.big_m_max;
   for (int c = 0; c < kSmallClasses; ++c) p->warp_mt[c] = X.warp_mt[c];
+  p->n_fused = X.n_fused;
   p->big = X.big;
   p->sbinfo = X.sbinfo;
   p->minv_size = X.minv_size;
@@ -986,7 +995,7 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
       double* minpiv = p->minpiv_work + R.off * p->nf;
       double2* minv = p->minv + R.off * p->minv_size;
       const KhFwd fw{p->y + R.off * p->n, p->rupd[d & 1] + R.off * rs, rs, p->rupd[(d + 1) & 1] + R.off * rsh, rsh};
-      for (int c = 0; c < kSmallClasses; ++c) {
+      for (int c = 0; c < p->n_fused; ++c) {
         if (p->warp_mt[c] && !fwd)
           KH_CUDA(kh_launch_warp_front(p->warp_mt[c], T, lev + co[c], co[c + 1] - co[c], ns, lam, panels, uc, sc, uch,
                                        sch, minpiv, p->wdst, L.side[c]));
@@ -1007,7 +1016,7 @@ int factor_impl(kh_plan* p, int64_t slot0, int64_t nshift, const double* lambda_
                   // their forward sweep runs on a side stream beside the Schur kernel
         KH_CUDA(cudaEventRecord(L.ev_fwd, R.st));
         KH_CUDA(cudaStreamWaitEvent(L.side[0], L.ev_fwd, 0));
-        KH_CUDA(kh_launch_fwd_level(T, lev + co[kSmallClasses], co[kSmallClasses + 1] - co[kSmallClasses], ns,
+        KH_CUDA(kh_launch_fwd_level(T, lev + co[p->n_fused], co[kSmallClasses + 1] - co[p->n_fused], ns,
                                     p->max_m, panels, fw.y, fw.ru_cur, fw.ru_stride_cur, fw.ru_child,
                                     fw.ru_stride_child, L.side[0], 0, 0, p->big_m_max[d]));
       }
