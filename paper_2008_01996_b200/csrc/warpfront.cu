@@ -43,8 +43,11 @@
 
 namespace {
 
-constexpr int WF_WARPS = 4;  // shifts per CTA (one warp each)
-constexpr int WF_KMAP = 4;   // children whose pull maps are tabulated in shared memory
+#ifndef KH_WF_WARPS
+#define KH_WF_WARPS 4
+#endif
+constexpr int WF_WARPS = KH_WF_WARPS;  // shifts per CTA (one warp each)
+constexpr int WF_KMAP = WF_WARPS < 4 ? WF_WARPS : 4;  // children whose pull maps are tabulated in shared memory (by warp k)
 // packed (lower, by columns) update-block index in 32-bit arithmetic (q <= 64)
 KH_DEV int upk32(int q, int i, int j) { return i + j * (2 * q - j - 1) / 2; }
 // per-warp child staging buffer: packed lower triangle of a q <= 8 MT update
@@ -221,7 +224,7 @@ __device__ unsigned long long g_wphase[8 * 8];
 #endif
 
 template <int MT>
-__global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_kernel(
+__global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 12 : 8) / WF_WARPS) warp_front_kernel(
     KhTree T, const int32_t* __restrict__ level_fronts, const double2* __restrict__ lam, double2* panels,
     double2* upd_cur, int64_t upd_stride_cur, const double2* __restrict__ upd_child, int64_t upd_stride_child,
     double* minpiv, const int32_t* __restrict__ wdst, int32_t nshift) {
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(32 * WF_WARPS, (MT <= 5 ? 3 : 2)) warp_front_k
 // (j, j) the M_j fragments of the Gauss-Jordan inverse -- both are already in
 // the B-fragment layout in registers, so the image costs one store per value.
 template <int MT>
-__global__ void __launch_bounds__(32 * WF_WARPS, 2) pivot_warp_kernel(KhTree T, const int32_t* __restrict__ tasks,
+__global__ void __launch_bounds__(32 * WF_WARPS, 8 / WF_WARPS) pivot_warp_kernel(KhTree T, const int32_t* __restrict__ tasks,
                                                                      int c0, double2* panels, double* minpiv,
                                                                      double2* img, int64_t img_stride,
                                                                      int32_t nshift) {
